@@ -1,0 +1,164 @@
+/* detlsh_b200 — B200-native (sm_100a) DET-LSH index build and c^2-k-ANN query.
+ *
+ * This is the drop-in boundary: a C ABI (plain pointers and sizes, no torch or
+ * C++ types) over the CUDA implementation in paper_2406_10938_b200/csrc.  Each
+ * entry point names the reference interface it replaces (paths relative to
+ * /root/reference/proj).  The C++ facade in include/detlsh_b200.hpp restores
+ * the reference's own C++ signatures on top of it.
+ *
+ * Errors: every int-returning call returns DETLSH_OK (0) or a status code;
+ * the message is in detlsh_gpu_last_error() (thread-local).  Status codes map
+ * onto the reference's exception taxonomy:
+ *     DETLSH_E_INVALID  -> std::invalid_argument (index.cpp:17-23, 293-298)
+ *     DETLSH_E_CUDA     -> std::runtime_error (device failure / out of memory)
+ *     DETLSH_E_FORMAT   -> detlsh::FormatError (errors.hpp:19-28)
+ * No C++ exception ever crosses this boundary.
+ *
+ * Ownership: a detlsh_gpu_index owns its device buffers (dataset copy unless
+ * DETLSH_F_BORROW_DATA, hash family, breakpoint table, codes, trees).  Callers
+ * own every host buffer they pass.  An index is immutable after build; queries
+ * against one index may run concurrently from several host threads.
+ */
+#ifndef DETLSH_B200_H
+#define DETLSH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DETLSH_OK 0
+#define DETLSH_E_INVALID 1
+#define DETLSH_E_CUDA 2
+#define DETLSH_E_FORMAT 3
+
+/* flags */
+#define DETLSH_F_DEVICE_PTRS 0x1u  /* point / query / output pointers are device pointers */
+#define DETLSH_F_SAMPLE_GPU 0x2u   /* GPU-native breakpoint sample;
+                                      default is the reference-compatible sample */
+#define DETLSH_F_BORROW_DATA 0x4u  /* with DEVICE_PTRS: keep the caller's device dataset */
+#define DETLSH_F_NO_CODES 0x8u     /* drop the [L][n][K] code array after build */
+
+/* detlsh::LshParams (projection.hpp:79-92), same field order and meaning:
+ * beta <= 0 -> derived; r_min <= 0 -> estimated at build; epsilon/alpha1/
+ * alpha2 are outputs (filled by build). */
+typedef struct detlsh_params {
+    int32_t K, L;
+    double c, beta, epsilon, alpha1, alpha2;
+    int32_t n_regions;
+    double sample_fraction;
+    int32_t leaf_capacity;
+    double r_min;
+    int32_t k;
+} detlsh_params;
+
+typedef struct detlsh_gpu_index detlsh_gpu_index;
+typedef struct detlsh_gpu_tree detlsh_gpu_tree;
+
+/* ---- host-only numerics (no GPU needed) ---------------------------------- */
+
+/* candidate_budget (index.hpp:50, index.cpp:190-194). */
+uint64_t detlsh_candidate_budget(double beta, uint64_t n, int32_t k);
+/* derive_params (projection.hpp:75-77, projection.cpp:92-102); out4 =
+ * {alpha1, alpha2, epsilon, beta}. */
+int detlsh_derive_params(int32_t K, double c, int32_t L, double* out4);
+/* sample_hash_family (projection.hpp:30, projection.cpp:11-23); out [L][K][d]. */
+int detlsh_sample_hash_family(int32_t d, int32_t K, int32_t L, uint64_t seed, float* out);
+/* chi2_cdf / chi2_quantile (chi2.hpp:10-17). */
+double detlsh_chi2_cdf(double x, int32_t k);
+double detlsh_chi2_quantile(double alpha, int32_t k);
+
+int detlsh_device_count(void);
+const char* detlsh_gpu_last_error(void);
+const char* detlsh_version(void);
+
+/* ---- index build ----------------------------------------------------------- */
+
+/* build_index (index.hpp:39, index.cpp:212-218): points [n][d] fp32 row-major.
+ * params->epsilon/alpha1/alpha2/beta/r_min are written back as build derives
+ * them (the reference's DetIndex::params). */
+int detlsh_gpu_build(const float* points, uint64_t n, int32_t d, detlsh_params* params,
+                     uint64_t seed, int32_t device, uint32_t flags, detlsh_gpu_index** out);
+
+/* build_index_with_family (index.hpp:42-43, index.cpp:196-210): caller-supplied
+ * coefficients [L][K][d] (host memory); K and L come from the family. */
+int detlsh_gpu_build_with_family(const float* points, uint64_t n, int32_t d,
+                                 detlsh_params* params, const float* coeffs, int32_t K,
+                                 int32_t L, uint64_t family_seed, uint64_t seed, int32_t device,
+                                 uint32_t flags, detlsh_gpu_index** out);
+
+void detlsh_gpu_free(detlsh_gpu_index* index);
+
+/* ---- queries ------------------------------------------------------------------ */
+
+/* ck_ann (index.hpp:87, index.cpp:292-331), batched: nq queries [nq][d].
+ * Outputs row-major [nq][k]: ids (dataset positions) and exact distances,
+ * ascending by (distance, position); n_hits[q] <= k (the reference returns
+ * min(k, |S|) hits); radius_used[q] = r_min * c^t; cands_seen[q] = |S|.
+ * Any output pointer may be NULL.  stream: cudaStream_t or NULL (the index's
+ * own stream).  With DETLSH_F_DEVICE_PTRS all pointers are device pointers and
+ * the call is stream-ordered (returns once enqueued). */
+int detlsh_gpu_query(const detlsh_gpu_index* index, const float* queries, uint64_t nq,
+                     int32_t k, uint32_t flags, uint32_t* ids, double* dists, int32_t* n_hits,
+                     double* radius_used, uint64_t* cands_seen, void* stream);
+
+/* Multi-GPU merge: per-shard top-k lists gathered from `shards`
+ * ranks, layout [shards][nq][k] (dist, global id); writes the global top-k
+ * ascending by (dist, id).  Device pointers, stream-ordered. */
+int detlsh_gpu_merge_topk(const double* shard_dists, const uint64_t* shard_ids,
+                          const int32_t* shard_hits, int32_t shards, uint64_t nq, int32_t k,
+                          double* out_dists, uint64_t* out_ids, int32_t* out_hits,
+                          void* stream);
+
+/* ---- export (DetIndex fields, index.hpp:24-37) ------------------------------ */
+int detlsh_gpu_get_params(const detlsh_gpu_index* index, detlsh_params* out);
+uint64_t detlsh_gpu_n(const detlsh_gpu_index* index);
+int32_t detlsh_gpu_d(const detlsh_gpu_index* index);
+uint64_t detlsh_gpu_sample_size(const detlsh_gpu_index* index);
+int detlsh_gpu_export_family(const detlsh_gpu_index* index, float* out /* [L][K][d] */);
+int detlsh_gpu_export_table(const detlsh_gpu_index* index, float* out /* [L][K][N_r+1] */);
+int detlsh_gpu_export_codes(const detlsh_gpu_index* index, uint8_t* out /* [L][n][K] */);
+/* DeTree (de_tree.hpp:44-58) of tree `tree`, nodes in the reference's build
+ * order; positions concatenated leaf by leaf (ebegin/ecount index them). */
+int detlsh_gpu_tree_num_nodes(const detlsh_gpu_index* index, int32_t tree, uint64_t* out);
+int detlsh_gpu_export_tree(const detlsh_gpu_index* index, int32_t tree, int32_t* root_children,
+                           uint8_t* is_leaf, uint8_t* split_dim, int32_t* left, int32_t* right,
+                           uint8_t* bits, uint8_t* value, uint64_t* ebegin, uint32_t* ecount,
+                           uint32_t* positions);
+/* Per-stage device/host milliseconds of the last build (diagnostics):
+ * names written as a ';'-separated list into `names` (cap bytes). */
+int detlsh_gpu_build_timings(const detlsh_gpu_index* index, double* ms, int32_t cap,
+                             char* names, int32_t names_cap);
+
+/* ---- stage functions (reference stage API on the device) ------------------- */
+
+/* project_dataset (projection.hpp:58, projection.cpp:47-60): out [L][n][K]. */
+int detlsh_gpu_project(const float* coeffs, int32_t K, int32_t L, const float* points,
+                       uint64_t n, int32_t d, float* out, int32_t device, uint32_t flags);
+/* select_breakpoints (encoder.hpp:41-42, encoder.cpp:105-143): projected
+ * [L][n][K] -> table [L][K][N_r+1]. */
+int detlsh_gpu_select_breakpoints(const float* projected, uint64_t n, int32_t K, int32_t L,
+                                  int32_t n_regions, double sample_fraction, uint64_t seed,
+                                  float* table, uint64_t* sample_size, int32_t device,
+                                  uint32_t flags);
+/* encode_dataset (encoder.hpp:63, encoder.cpp:155-176): out [L][n][K] u8. */
+int detlsh_gpu_encode(const float* projected, uint64_t n, int32_t K, int32_t L,
+                      const float* table, int32_t n_regions, uint8_t* out, int32_t device,
+                      uint32_t flags);
+/* build_tree (de_tree.hpp:61, de_tree.cpp:133-152) from codes [L][n][K]. */
+int detlsh_gpu_build_tree(const uint8_t* codes, uint64_t n, int32_t K, int32_t L,
+                          int32_t n_regions, int32_t space, int32_t max_size, int32_t device,
+                          uint32_t flags, detlsh_gpu_tree** out);
+int detlsh_gpu_tree_nodes(const detlsh_gpu_tree* tree, uint64_t* out);
+int detlsh_gpu_tree_export(const detlsh_gpu_tree* tree, int32_t* root_children,
+                           uint8_t* is_leaf, uint8_t* split_dim, int32_t* left, int32_t* right,
+                           uint8_t* bits, uint8_t* value, uint64_t* ebegin, uint32_t* ecount,
+                           uint32_t* positions);
+void detlsh_gpu_tree_free(detlsh_gpu_tree* tree);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DETLSH_B200_H */

@@ -1,0 +1,386 @@
+"""Host-side mirror of the reference's C++ API for the DET-LSH hot path.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/detlsh/{index,projection,encoder,de_tree}.hpp:
+
+    build_index(data, params, seed)                 index.hpp:39
+    build_index_with_family(data, params, family, seed)   index.hpp:42-43
+    ck_ann(index, q, k) -> QueryResult              index.hpp:87
+    candidate_budget(beta, n, k)                    index.hpp:50
+    derive_params(K, c, L)                          projection.hpp:75-77
+    sample_hash_family(d, K, L, seed)               projection.hpp:30
+    project_dataset(family, data)                   projection.hpp:58
+    select_breakpoints(projected, n_regions, sample_fraction, seed)  encoder.hpp:41-42
+    encode_dataset(projected, table)                encoder.hpp:63
+    build_tree(encoded, space, max_size)            de_tree.hpp:61
+
+plus ``ck_ann_batch`` (the batched GPU entry point).  std::invalid_argument
+maps to ValueError; device failures to RuntimeError.  Every call goes through
+the C ABI (include/detlsh_b200.h) into the sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _lib
+from ._lib import F_BORROW_DATA, F_DEVICE_PTRS, F_NO_CODES, F_SAMPLE_GPU, Params, check
+
+SAMPLE_REFERENCE = "reference"
+SAMPLE_GPU = "gpu"
+
+
+@dataclass
+class LshParams:
+    """detlsh::LshParams (projection.hpp:79-92)."""
+
+    K: int = 16
+    L: int = 4
+    c: float = 1.5
+    beta: float = 0.0  # <= 0: derived at build
+    epsilon: float = 0.0
+    alpha1: float = 0.0
+    alpha2: float = 0.0
+    n_regions: int = 256
+    sample_fraction: float = 0.1
+    leaf_capacity: int = 128
+    r_min: float = 0.0  # <= 0: estimated at build
+    k: int = 50
+
+    def to_c(self) -> Params:
+        return Params(*[getattr(self, f.name) for f in fields(self)])
+
+    @staticmethod
+    def from_c(p: Params) -> "LshParams":
+        return LshParams(*[getattr(p, f.name) for f in fields(LshParams)])
+
+
+@dataclass
+class DerivedParams:
+    alpha1: float
+    alpha2: float
+    epsilon: float
+    beta: float
+
+
+@dataclass
+class QueryResult:
+    """detlsh::QueryResult (index.hpp:79-83)."""
+
+    hits: list = field(default_factory=list)  # [(position, distance)] ascending
+    radius_used: float = 0.0
+    candidates_seen: int = 0
+
+
+@dataclass
+class TreeExport:
+    """A DeTree (de_tree.hpp:44-58) flattened; nodes in the reference's build order."""
+
+    root_children: np.ndarray
+    is_leaf: np.ndarray
+    split_dim: np.ndarray
+    left: np.ndarray
+    right: np.ndarray
+    bits: np.ndarray
+    value: np.ndarray
+    ebegin: np.ndarray
+    ecount: np.ndarray
+    positions: np.ndarray
+
+
+def _ptr(a) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+def _is_cuda_tensor(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda"))
+
+
+def _as_host_f32(x, ndim=2) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    if a.ndim != ndim:
+        raise ValueError(f"expected a {ndim}-d array, got shape {a.shape}")
+    return a
+
+
+def candidate_budget(beta: float, n: int, k: int) -> int:
+    return int(_lib.load().detlsh_candidate_budget(beta, n, k))
+
+
+def derive_params(K: int, c: float, L: int) -> DerivedParams:
+    out = np.empty(4, np.float64)
+    check(_lib.load().detlsh_derive_params(K, c, L, _ptr(out)))
+    return DerivedParams(*map(float, out))
+
+
+def chi2_cdf(x: float, k: int) -> float:
+    return float(_lib.load().detlsh_chi2_cdf(x, k))
+
+
+def chi2_quantile(alpha: float, k: int) -> float:
+    return float(_lib.load().detlsh_chi2_quantile(alpha, k))
+
+
+def mix_seed(seed: int, stream: int) -> int:
+    """rng.hpp:56-61 (host arithmetic, for callers that derive stage seeds)."""
+    m = (1 << 64) - 1
+    z = (seed + 0x9E3779B97F4A7C15 * (stream + 1)) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def sample_hash_family(d: int, K: int, L: int, seed: int) -> np.ndarray:
+    out = np.empty((L, K, d), np.float32)
+    check(_lib.load().detlsh_sample_hash_family(d, K, L, seed, _ptr(out)))
+    return out
+
+
+def device_count() -> int:
+    return int(_lib.load().detlsh_device_count())
+
+
+class DetIndex:
+    """Assembled GPU index (detlsh::DetIndex, index.hpp:24-37).  Immutable after build."""
+
+    def __init__(self, handle, params: LshParams, n: int, d: int, device: int):
+        self._h = handle
+        self.params = params
+        self._n, self._d, self.device = n, d, device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().detlsh_gpu_free(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def n(self) -> int:
+        return self._n
+
+    def d(self) -> int:
+        return self._d
+
+    @property
+    def handle(self):
+        return self._h
+
+    def sample_size(self) -> int:
+        return int(_lib.load().detlsh_gpu_sample_size(self._h))
+
+    def table(self) -> np.ndarray:
+        p = self.params
+        out = np.empty((p.L, p.K, p.n_regions + 1), np.float32)
+        check(_lib.load().detlsh_gpu_export_table(self._h, _ptr(out)))
+        return out
+
+    def family(self) -> np.ndarray:
+        p = self.params
+        out = np.empty((p.L, p.K, self._d), np.float32)
+        check(_lib.load().detlsh_gpu_export_family(self._h, _ptr(out)))
+        return out
+
+    def codes(self) -> np.ndarray:
+        p = self.params
+        out = np.empty((p.L, self._n, p.K), np.uint8)
+        check(_lib.load().detlsh_gpu_export_codes(self._h, _ptr(out)))
+        return out
+
+    def tree(self, i: int) -> TreeExport:
+        lib = _lib.load()
+        nn = C.c_uint64(0)
+        check(lib.detlsh_gpu_tree_num_nodes(self._h, i, C.byref(nn)))
+        return _export_tree(lambda *a: lib.detlsh_gpu_export_tree(self._h, i, *a), self.params.K,
+                            nn.value, self._n)
+
+    def build_timings(self) -> dict:
+        ms = np.zeros(32, np.float64)
+        names = C.create_string_buffer(1024)
+        m = _lib.load().detlsh_gpu_build_timings(self._h, _ptr(ms), 32, names, 1024)
+        keys = names.value.decode().split(";") if m else []
+        return {k: float(v) for k, v in zip(keys, ms[:m])}
+
+    def project_query(self, q, space: int) -> np.ndarray:
+        """DetIndex::project_query (index.cpp:181-188) via the projection kernel."""
+        fam = self.family()[space:space + 1]
+        return project_dataset(fam, np.asarray(q, np.float32)[None, :], device=self.device)[0, 0]
+
+
+def _export_tree(fn, K, nn, n) -> TreeExport:
+    t = TreeExport(np.empty(1 << K, np.int32), np.empty(nn, np.uint8), np.empty(nn, np.uint8),
+                   np.empty(nn, np.int32), np.empty(nn, np.int32), np.empty((nn, K), np.uint8),
+                   np.empty((nn, K), np.uint8), np.empty(nn, np.uint64), np.empty(nn, np.uint32),
+                   np.empty(n, np.uint32))
+    check(fn(_ptr(t.root_children), _ptr(t.is_leaf), _ptr(t.split_dim), _ptr(t.left),
+             _ptr(t.right), _ptr(t.bits), _ptr(t.value), _ptr(t.ebegin), _ptr(t.ecount),
+             _ptr(t.positions)))
+    return t
+
+
+def _flags(sample: str) -> int:
+    if sample not in (SAMPLE_REFERENCE, SAMPLE_GPU):
+        raise ValueError(f"sample must be '{SAMPLE_REFERENCE}' or '{SAMPLE_GPU}'")
+    return F_SAMPLE_GPU if sample == SAMPLE_GPU else 0
+
+
+def build_index(data, params: LshParams | None = None, seed: int = 0, *, device: int = 0,
+                sample: str = SAMPLE_REFERENCE, borrow: bool = False,
+                keep_codes: bool = True) -> DetIndex:
+    """build_index (index.hpp:39).  `data` is an (n, d) float32 array or a CUDA tensor."""
+    params = params or LshParams()
+    cp = params.to_c()
+    h = C.c_void_p()
+    flags = _flags(sample) | (0 if keep_codes else F_NO_CODES)
+    if _is_cuda_tensor(data):
+        t = data.contiguous()
+        n, d = int(t.shape[0]), int(t.shape[1])
+        flags |= F_DEVICE_PTRS | (F_BORROW_DATA if borrow else 0)
+        dev = t.device.index if t.device.index is not None else device
+        check(_lib.load().detlsh_gpu_build(C.c_void_p(t.data_ptr()), n, d, C.byref(cp), seed, dev,
+                                           flags, C.byref(h)))
+        idx = DetIndex(h, LshParams.from_c(cp), n, d, dev)
+        if borrow:
+            idx._keepalive = t
+        return idx
+    a = _as_host_f32(data)
+    n, d = a.shape
+    check(_lib.load().detlsh_gpu_build(_ptr(a), n, d, C.byref(cp), seed, device, flags,
+                                       C.byref(h)))
+    return DetIndex(h, LshParams.from_c(cp), n, d, device)
+
+
+def build_index_with_family(data, params: LshParams, family: np.ndarray, seed: int = 0, *,
+                            family_seed: int = 0, device: int = 0,
+                            sample: str = SAMPLE_REFERENCE) -> DetIndex:
+    """build_index_with_family (index.hpp:42-43): the family's d/K/L win."""
+    a = _as_host_f32(data)
+    fam = np.ascontiguousarray(family, np.float32)
+    L, K, d = fam.shape
+    if d != a.shape[1]:
+        raise ValueError("build_index: family dimension does not match the dataset")
+    cp = params.to_c()
+    h = C.c_void_p()
+    check(_lib.load().detlsh_gpu_build_with_family(_ptr(a), a.shape[0], d, C.byref(cp), _ptr(fam),
+                                                   K, L, family_seed, seed, device,
+                                                   _flags(sample), C.byref(h)))
+    return DetIndex(h, LshParams.from_c(cp), a.shape[0], d, device)
+
+
+@dataclass
+class BatchResult:
+    ids: np.ndarray        # [nq][k] u32
+    dists: np.ndarray      # [nq][k] f64
+    n_hits: np.ndarray     # [nq] i32
+    radius_used: np.ndarray  # [nq] f64
+    candidates_seen: np.ndarray  # [nq] u64
+
+    def result(self, i: int) -> QueryResult:
+        m = int(self.n_hits[i])
+        return QueryResult([(int(p), float(v)) for p, v in zip(self.ids[i, :m], self.dists[i, :m])],
+                           float(self.radius_used[i]), int(self.candidates_seen[i]))
+
+
+def ck_ann_batch(index: DetIndex, queries, k: int, *, stream=None) -> BatchResult:
+    """Batched ck_ann over host queries [nq][d] (outputs on the host)."""
+    Q = _as_host_f32(queries)
+    if Q.shape[1] != index.d():
+        raise ValueError("ck_ann: query dimension mismatch")
+    nq = Q.shape[0]
+    out = BatchResult(np.zeros((nq, k), np.uint32), np.zeros((nq, k), np.float64),
+                      np.zeros(nq, np.int32), np.zeros(nq, np.float64), np.zeros(nq, np.uint64))
+    check(_lib.load().detlsh_gpu_query(index.handle, _ptr(Q), nq, k, 0, _ptr(out.ids),
+                                       _ptr(out.dists), _ptr(out.n_hits), _ptr(out.radius_used),
+                                       _ptr(out.candidates_seen), stream))
+    return out
+
+
+def ck_ann_device(index: DetIndex, queries, k: int, ids, dists, n_hits=None, radius=None,
+                  cands=None, stream=None) -> None:
+    """Batched ck_ann on device tensors (stream-ordered, no host copies)."""
+    def p(t):
+        return C.c_void_p(t.data_ptr()) if t is not None else None
+    if queries.shape[1] != index.d():
+        raise ValueError("ck_ann: query dimension mismatch")
+    check(_lib.load().detlsh_gpu_query(index.handle, p(queries), int(queries.shape[0]), k,
+                                       F_DEVICE_PTRS, p(ids), p(dists), p(n_hits), p(radius),
+                                       p(cands), stream))
+
+
+def ck_ann(index: DetIndex, q, k: int) -> QueryResult:
+    """ck_ann (index.hpp:87, index.cpp:292-331) for one query."""
+    qa = np.asarray(q, np.float32).reshape(1, -1)
+    if qa.shape[1] != index.d():
+        raise ValueError("ck_ann: query dimension mismatch")
+    return ck_ann_batch(index, qa, k).result(0)
+
+
+def merge_topk_device(shard_dists, shard_ids, shard_hits, k: int, out_dists, out_ids, out_hits,
+                      stream=None) -> None:
+    """Merge per-shard top-k lists ([shards][nq][k], device tensors) into the global top-k."""
+    shards, nq = int(shard_dists.shape[0]), int(shard_dists.shape[1])
+    check(_lib.load().detlsh_gpu_merge_topk(
+        C.c_void_p(shard_dists.data_ptr()), C.c_void_p(shard_ids.data_ptr()),
+        C.c_void_p(shard_hits.data_ptr()), shards, nq, k, C.c_void_p(out_dists.data_ptr()),
+        C.c_void_p(out_ids.data_ptr()), C.c_void_p(out_hits.data_ptr()), stream))
+
+
+# ---- stage functions ----------------------------------------------------------------
+
+def project_dataset(family: np.ndarray, data, *, device: int = 0) -> np.ndarray:
+    """project_dataset (projection.hpp:58) -> [L][n][K] fp32, bit-exact."""
+    fam = np.ascontiguousarray(family, np.float32)
+    L, K, d = fam.shape
+    a = _as_host_f32(data)
+    if a.shape[1] != d:
+        raise ValueError("project_dataset: dataset dimension mismatch")
+    out = np.empty((L, a.shape[0], K), np.float32)
+    check(_lib.load().detlsh_gpu_project(_ptr(fam), K, L, _ptr(a), a.shape[0], d, _ptr(out),
+                                         device, 0))
+    return out
+
+
+def select_breakpoints(projected: np.ndarray, n_regions: int, sample_fraction: float, seed: int,
+                       *, device: int = 0, sample: str = SAMPLE_REFERENCE) -> np.ndarray:
+    """select_breakpoints (encoder.hpp:41-42) -> [L][K][n_regions+1]."""
+    pr = np.ascontiguousarray(projected, np.float32)
+    L, n, K = pr.shape
+    out = np.empty((L, K, n_regions + 1), np.float32)
+    ns = C.c_uint64(0)
+    check(_lib.load().detlsh_gpu_select_breakpoints(_ptr(pr), n, K, L, n_regions, sample_fraction,
+                                                    seed, _ptr(out), C.byref(ns), device,
+                                                    _flags(sample)))
+    return out
+
+
+def encode_dataset(projected: np.ndarray, table: np.ndarray, *, device: int = 0) -> np.ndarray:
+    """encode_dataset (encoder.hpp:63) -> [L][n][K] u8."""
+    pr = np.ascontiguousarray(projected, np.float32)
+    tb = np.ascontiguousarray(table, np.float32)
+    L, n, K = pr.shape
+    if tb.shape[:2] != (L, K):
+        raise ValueError("encode_dataset: table shape does not match projected dataset")
+    out = np.empty((L, n, K), np.uint8)
+    check(_lib.load().detlsh_gpu_encode(_ptr(pr), n, K, L, _ptr(tb), tb.shape[2] - 1, _ptr(out),
+                                        device, 0))
+    return out
+
+
+def build_tree(encoded: np.ndarray, space: int, max_size: int, n_regions: int = 256, *,
+               device: int = 0) -> TreeExport:
+    """build_tree (de_tree.hpp:61) on the GPU, exported in the reference layout."""
+    enc = np.ascontiguousarray(encoded, np.uint8)
+    L, n, K = enc.shape
+    lib = _lib.load()
+    h = C.c_void_p()
+    check(lib.detlsh_gpu_build_tree(_ptr(enc), n, K, L, n_regions, space, max_size, device, 0,
+                                    C.byref(h)))
+    try:
+        nn = C.c_uint64(0)
+        check(lib.detlsh_gpu_tree_nodes(h, C.byref(nn)))
+        return _export_tree(lambda *a: lib.detlsh_gpu_tree_export(h, *a), K, nn.value, n)
+    finally:
+        lib.detlsh_gpu_tree_free(h)

@@ -1,0 +1,266 @@
+// Host determinism core — see host_core.hpp.
+#include "host_core.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <stdexcept>
+
+namespace detlsh_b200 {
+
+double Rng::normal() {
+    if (have_spare_) {
+        have_spare_ = false;
+        return spare_;
+    }
+    double u1;
+    do {
+        u1 = real01();
+    } while (u1 <= 0.0);
+    const double u2 = real01();
+    const double mag = std::sqrt(-2.0 * std::log(u1));
+    const double ang = 2.0 * 3.141592653589793 * u2;
+    spare_ = mag * std::sin(ang);
+    have_spare_ = true;
+    return mag * std::cos(ang);
+}
+
+uint64_t mix_seed(uint64_t seed, uint64_t stream) {
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (stream + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// ---- chi^2 (chi2.cpp:12-107) ------------------------------------------------
+namespace {
+double series_p(double a, double x) {
+    double ap = a, sum = 1.0 / a, del = sum;
+    for (int i = 0; i < 1000; ++i) {
+        ap += 1.0;
+        del *= x / ap;
+        sum += del;
+        if (std::fabs(del) < std::fabs(sum) * 1e-16) break;
+    }
+    return sum * std::exp(-x + a * std::log(x) - std::lgamma(a));
+}
+double contfrac_q(double a, double x) {
+    constexpr double tiny = 1e-300;
+    double b = x + 1.0 - a, c = 1.0 / tiny, d = 1.0 / b, h = d;
+    for (int i = 1; i <= 1000; ++i) {
+        const double an = -static_cast<double>(i) * (static_cast<double>(i) - a);
+        b += 2.0;
+        d = an * d + b;
+        if (std::fabs(d) < tiny) d = tiny;
+        c = b + an / c;
+        if (std::fabs(c) < tiny) c = tiny;
+        d = 1.0 / d;
+        const double del = d * c;
+        h *= del;
+        if (std::fabs(del - 1.0) < 1e-16) break;
+    }
+    return std::exp(-x + a * std::log(x) - std::lgamma(a)) * h;
+}
+}  // namespace
+
+double regularized_gamma_p(double a, double x) {
+    if (a <= 0.0) throw std::invalid_argument("regularized_gamma_p: a must be positive");
+    if (x < 0.0) throw std::invalid_argument("regularized_gamma_p: x must be non-negative");
+    if (x == 0.0) return 0.0;
+    return x < a + 1.0 ? series_p(a, x) : 1.0 - contfrac_q(a, x);
+}
+
+double chi2_cdf(double x, int k) {
+    if (k < 1) throw std::invalid_argument("chi2_cdf: k must be positive");
+    return x <= 0.0 ? 0.0 : regularized_gamma_p(0.5 * k, 0.5 * x);
+}
+
+double chi2_pdf(double x, int k) {
+    if (k < 1) throw std::invalid_argument("chi2_pdf: k must be positive");
+    if (x <= 0.0) return 0.0;
+    const double hk = 0.5 * k;
+    return std::exp((hk - 1.0) * std::log(x) - 0.5 * x - hk * 0.6931471805599453 -
+                    std::lgamma(hk));
+}
+
+double chi2_quantile(double alpha, int k) {
+    if (k < 1) throw std::invalid_argument("chi2_quantile: k must be positive");
+    if (!(alpha > 0.0) || alpha > 1.0)
+        throw std::invalid_argument("chi2_quantile: alpha must lie in (0, 1]");
+    if (alpha == 1.0) return 0.0;
+    const double target = 1.0 - alpha;
+    double lo = 0.0;
+    double hi = static_cast<double>(k) + 10.0 * std::sqrt(2.0 * k) + 10.0;
+    for (int i = 0; i < 200 && chi2_cdf(hi, k) < target; ++i) hi *= 2.0;
+    for (int i = 0; i < 200; ++i) {
+        const double mid = 0.5 * (lo + hi);
+        if (mid == lo || mid == hi) break;
+        (chi2_cdf(mid, k) < target ? lo : hi) = mid;
+    }
+    double x = 0.5 * (lo + hi);
+    for (int i = 0; i < 32; ++i) {
+        const double f = chi2_cdf(x, k) - target;
+        if (std::fabs(f) < 1e-12) break;
+        const double df = chi2_pdf(x, k);
+        if (df <= 0.0) break;
+        const double nx = x - f / df;
+        if (nx <= lo || nx >= hi) break;
+        x = nx;
+    }
+    return x;
+}
+
+Derived derive_params(int K, double c, int L) {
+    if (K < 1 || L < 1) throw std::invalid_argument("derive_params: K, L must be positive");
+    if (!(c > 1.0)) throw std::invalid_argument("derive_params: c must exceed 1");
+    Derived p;
+    p.alpha1 = std::exp(-1.0 / static_cast<double>(L));
+    const double eps_sq = chi2_quantile(p.alpha1, K);
+    p.epsilon = std::sqrt(eps_sq);
+    p.alpha2 = 1.0 - chi2_cdf(eps_sq / (c * c), K);
+    p.beta = 2.0 * (1.0 - std::pow(p.alpha2, static_cast<double>(L)));
+    return p;
+}
+
+uint64_t candidate_budget(double beta, uint64_t n, int k) {
+    const double raw = std::max(0.0, beta) * static_cast<double>(n) + static_cast<double>(k);
+    const auto b = static_cast<uint64_t>(std::ceil(raw));
+    return std::min<uint64_t>(b, n);
+}
+
+void sample_hash_family(int d, int K, int L, uint64_t seed, float* out) {
+    if (d < 1 || K < 1 || L < 1)
+        throw std::invalid_argument("sample_hash_family: d, K, L must be positive");
+    Rng rng(seed);
+    const size_t total = static_cast<size_t>(L) * K * d;
+    for (size_t i = 0; i < total; ++i) out[i] = static_cast<float>(rng.normal());
+}
+
+// ---- breakpoint replay (encoder.cpp:14-103) ---------------------------------
+namespace {
+
+// Median-of-three around a seeded pick, sentinel Hoare scan; one bounded()
+// draw per call.  Returns the pivot's sorted position.
+size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
+    const size_t len = hi - lo;
+    const size_t mid = lo + len / 2;
+    std::swap(a[mid], a[lo + rng.bounded(len)]);
+    if (a[mid] < a[lo]) std::swap(a[lo], a[mid]);
+    if (a[hi - 1] < a[lo]) std::swap(a[lo], a[hi - 1]);
+    if (a[hi - 1] < a[mid]) std::swap(a[mid], a[hi - 1]);
+    std::swap(a[mid], a[lo + 1]);
+    const float pv = a[lo + 1];
+    size_t i = lo + 1, j = hi - 1;
+    for (;;) {
+        while (a[++i] < pv) {
+        }
+        while (a[--j] > pv) {
+        }
+        if (i >= j) break;
+        std::swap(a[i], a[j]);
+    }
+    std::swap(a[lo + 1], a[j]);
+    return j;
+}
+
+void small_sort(float* a, size_t lo, size_t hi) {
+    for (size_t i = lo + 1; i < hi; ++i) {
+        const float v = a[i];
+        size_t j = i;
+        for (; j > lo && a[j - 1] > v; --j) a[j] = a[j - 1];
+        a[j] = v;
+    }
+}
+
+}  // namespace
+
+void select_row_breakpoints(float* a, uint64_t n_s, int n_regions, Rng& rng, float* row_out,
+                            uint64_t* draws) {
+    const size_t span = n_s / static_cast<size_t>(n_regions);
+    const size_t nt = static_cast<size_t>(n_regions) - 1;
+    // target t sits at rank span*(t+1)-1; work items are (lo, hi, tlo, thi)
+    struct Item {
+        size_t lo, hi, tlo, thi;
+    };
+    std::vector<Item> stack;
+    stack.reserve(256);
+    stack.push_back({0, n_s, 0, nt});
+    auto target = [span](size_t t) { return span * (t + 1) - 1; };
+    uint64_t nd = 0;
+    while (!stack.empty()) {
+        const Item it = stack.back();
+        stack.pop_back();
+        if (it.tlo >= it.thi) continue;
+        if (it.hi - it.lo <= 8) {
+            small_sort(a, it.lo, it.hi);
+            continue;
+        }
+        const size_t p = hoare_partition(a, it.lo, it.hi, rng);
+        ++nd;
+        // targets are an arithmetic progression: count those below / at p
+        size_t below = it.tlo, above;
+        {
+            size_t lo = it.tlo, hi = it.thi;
+            while (lo < hi) {
+                const size_t m = lo + (hi - lo) / 2;
+                if (target(m) < p) lo = m + 1; else hi = m;
+            }
+            below = lo;
+            hi = it.thi;
+            while (lo < hi) {
+                const size_t m = lo + (hi - lo) / 2;
+                if (target(m) <= p) lo = m + 1; else hi = m;
+            }
+            above = lo;
+        }
+        stack.push_back({it.lo, p, it.tlo, below});
+        stack.push_back({p + 1, it.hi, above, it.thi});
+    }
+    for (size_t t = 0; t < nt; ++t) row_out[t + 1] = a[target(t)];
+    row_out[0] = *std::min_element(a, a + target(0) + 1);
+    row_out[n_regions] = *std::max_element(a + target(nt - 1), a + n_s);
+    if (draws) *draws += nd;
+}
+
+RefSampler::RefSampler(uint64_t n, uint64_t n_s, int n_regions, uint64_t seed)
+    : n_(n), n_s_(n_s), n_regions_(n_regions), rng_(seed), idx_(n), sample_idx_(n_s) {
+    std::iota(idx_.begin(), idx_.end(), 0u);
+}
+
+const std::vector<uint32_t>& RefSampler::next_space_indices() {
+    for (uint64_t t = 0; t < n_s_; ++t) {
+        const uint64_t s = t + rng_.bounded(n_ - t);
+        std::swap(idx_[t], idx_[s]);
+    }
+    std::copy(idx_.begin(), idx_.begin() + static_cast<ptrdiff_t>(n_s_), sample_idx_.begin());
+    return sample_idx_;
+}
+
+void RefSampler::select_row(float* sample, float* row_out) {
+    select_row_breakpoints(sample, n_s_, n_regions_, rng_, row_out, &draws_);
+}
+
+double rmin_from_order_stats(const std::vector<double>& T, double guess, double epsilon,
+                             double c) {
+    std::vector<double> results;
+    results.reserve(T.size());
+    double start = guess;
+    for (const double tp : T) {
+        const auto reaches = [&](double r) { return tp <= epsilon * r; };
+        double r = start;
+        if (reaches(r)) {
+            for (int i = 0; i < 200 && r / c > 0.0 && reaches(r / c); ++i) r /= c;
+        } else {
+            for (int i = 0; i < 200; ++i) {
+                r *= c;
+                if (reaches(r)) break;
+            }
+        }
+        results.push_back(r);
+        start = r;
+    }
+    std::sort(results.begin(), results.end());
+    return results[(results.size() - 1) / 2];
+}
+
+}  // namespace detlsh_b200

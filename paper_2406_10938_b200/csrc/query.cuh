@@ -1,0 +1,66 @@
+// Batched c^2-k-ANN query (ck_ann, index.cpp:292-331) on the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace detlsh_b200 {
+
+struct QTree {
+    const uint32_t* leaf_node;
+    const uint32_t* leaf_begin;
+    const uint32_t* leaf_count;
+    const uint8_t* leaf_box;
+    const uint32_t* perm;
+    uint32_t num_leaves;
+};
+
+struct QueryPlan {
+    // index
+    const float* data;  // [n][d]
+    uint64_t n;
+    int d, K, L, NR;
+    const float* table;   // [L][K][NR+1]
+    const QTree* trees;   // device array [L]
+    double eps, c, r_min;
+    uint64_t budget;
+    int k;
+    uint32_t max_leaves;  // max num_leaves over trees
+    // batch
+    const float* q;      // [nq][d]
+    const float* qproj;  // [L][nq][K]
+    uint64_t nq;
+    // outputs ([nq][k] / [nq])
+    uint32_t* ids;
+    double* dists;
+    int32_t* n_hits;
+    double* radius;
+    uint64_t* cands;
+};
+
+constexpr int kQueryThreads = 256;
+constexpr int kTopCap = 1024;                      // top-k staging buffer
+constexpr int kFastMaxK = kTopCap - kQueryThreads;  // k handled by the fast path
+
+// Launch the batched query: fast path for every query (budget fills in tree 0,
+// round 0, no dedup needed), then the general path for the rest.  Scratch is
+// owned by the caller-provided QueryScratch (grown on demand).
+struct QueryScratch {
+    DevBuf<uint8_t> fast;  // per-CTA leaf item lists + candidate positions
+    DevBuf<uint8_t> slow;  // per-slot bitmap + members
+    DevBuf<uint32_t> slow_list;
+    DevBuf<uint32_t> counters;
+    size_t fast_slots = 0, slow_slots = 0;
+};
+
+void run_query_batch(const QueryPlan& plan, QueryScratch& scratch, int device, cudaStream_t s);
+
+// k-way merge of per-shard top-k lists: [shards][nq][k] -> [nq][k].
+void launch_merge_topk(const double* sd, const uint64_t* sid, const int32_t* sh, int shards,
+                       uint64_t nq, int k, double* od, uint64_t* oid, int32_t* oh,
+                       cudaStream_t s);
+
+}  // namespace detlsh_b200

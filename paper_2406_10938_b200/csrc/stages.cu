@@ -1,0 +1,405 @@
+// Build-stage kernels: exact projection, sample gather, GPU-native sample,
+// order-statistic breakpoints, encoding and the r_min order statistics.
+#include <algorithm>
+#include <vector>
+
+#include "primitives.cuh"
+#include "stages.cuh"
+
+namespace detlsh_b200 {
+
+int lk_padded(int LK) { return (LK + 63) / 64 * 64; }
+
+namespace {
+
+__global__ void coeffs_t_kernel(const float* __restrict__ c, int LK, int d, int LKp,
+                                double* __restrict__ out) {
+    const int64_t total = static_cast<int64_t>(d) * LKp;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int t = static_cast<int>(i / LKp), j = static_cast<int>(i % LKp);
+        out[i] = j < LK ? static_cast<double>(c[static_cast<int64_t>(j) * d + t]) : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Exact projection.  CTA = 256 threads = 64 point-lanes x 4 output groups;
+// each thread owns 2 points (p, p+64) x 16 outputs -> 32 fp64 accumulators.
+// Dims are streamed in chunks of 32 through shared memory: the point chunk as
+// fp32 (padded rows, conflict-free), the coefficient chunk pre-widened to
+// fp64 and read as warp-wide broadcasts.  The accumulation order is t = 0..d-1
+// for every output, exactly as project_point_into (projection.cpp:31-37).
+// ---------------------------------------------------------------------------
+constexpr int kPT = 128;  // points per tile
+constexpr int kDC = 32;   // dims per chunk
+constexpr int kJB = 16;   // outputs per thread
+
+__global__ void __launch_bounds__(256) project_exact_kernel(
+    const float* __restrict__ pts, uint64_t n, int d, const double* __restrict__ ct, int LK,
+    int LKp, int K, float* __restrict__ out) {
+    __shared__ float sx[kPT][kDC + 1];
+    __shared__ __align__(16) double sa[kDC][64];
+    const int tid = threadIdx.x;
+    const int p = tid & 63, g = tid >> 6;
+    const uint64_t tiles = (n + kPT - 1) / kPT;
+    for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const uint64_t z0 = tile * kPT;
+        for (int jp = 0; jp < LKp; jp += 64) {
+            double acc0[kJB], acc1[kJB];
+#pragma unroll
+            for (int j = 0; j < kJB; ++j) acc0[j] = acc1[j] = 0.0;
+            for (int t0 = 0; t0 < d; t0 += kDC) {
+                __syncthreads();
+                // points: kPT x kDC floats, coalesced along t
+                for (int i = tid; i < kPT * kDC; i += 256) {
+                    const int pp = i / kDC, c = i % kDC;
+                    const uint64_t z = z0 + pp;
+                    const int t = t0 + c;
+                    sx[pp][c] = (z < n && t < d) ? pts[z * d + t] : 0.0f;
+                }
+                for (int i = tid; i < kDC * 64; i += 256) {
+                    const int c = i / 64, j = i % 64;
+                    const int t = t0 + c;
+                    sa[c][j] = t < d ? ct[static_cast<int64_t>(t) * LKp + jp + j] : 0.0;
+                }
+                __syncthreads();
+#pragma unroll 4
+                for (int c = 0; c < kDC; ++c) {
+                    const double x0 = static_cast<double>(sx[p][c]);
+                    const double x1 = static_cast<double>(sx[p + 64][c]);
+                    const double2* arow = reinterpret_cast<const double2*>(&sa[c][g * kJB]);
+#pragma unroll
+                    for (int j2 = 0; j2 < kJB / 2; ++j2) {
+                        const double2 a = arow[j2];
+                        acc0[2 * j2] = fma(a.x, x0, acc0[2 * j2]);
+                        acc0[2 * j2 + 1] = fma(a.y, x0, acc0[2 * j2 + 1]);
+                        acc1[2 * j2] = fma(a.x, x1, acc1[2 * j2]);
+                        acc1[2 * j2 + 1] = fma(a.y, x1, acc1[2 * j2 + 1]);
+                    }
+                }
+            }
+            // store: output j' = jp + g*16 + j  -> (space, dim) = divmod(j', K)
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const uint64_t z = z0 + p + half * 64;
+                if (z >= n) continue;
+                const double* acc = half ? acc1 : acc0;
+                const int jb = jp + g * kJB;
+                if (K == 16 && jb + kJB <= LK) {
+                    const int sp = jb / 16;
+                    float4* o = reinterpret_cast<float4*>(out + (static_cast<uint64_t>(sp) * n + z) * 16);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        o[q] = make_float4(static_cast<float>(acc[4 * q]), static_cast<float>(acc[4 * q + 1]),
+                                           static_cast<float>(acc[4 * q + 2]), static_cast<float>(acc[4 * q + 3]));
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kJB; ++j) {
+                        const int jj = jb + j;
+                        if (jj < LK) {
+                            const int sp = jj / K, dim = jj % K;
+                            out[(static_cast<uint64_t>(sp) * n + z) * K + dim] = static_cast<float>(acc[j]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+__global__ void gather_sample_kernel(const float* __restrict__ proj, const uint32_t* __restrict__ idx,
+                                     uint64_t n_s, int K, float* __restrict__ out) {
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n_s;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const float* row = proj + static_cast<uint64_t>(idx[t]) * K;
+        for (int j = 0; j < K; ++j) out[static_cast<uint64_t>(j) * n_s + t] = row[j];
+    }
+}
+
+// Keyed Feistel bijection on [0, 2^(2h)) with cycle walking into [0, n).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void feistel_sample_kernel(uint64_t n, uint64_t n_s, uint64_t key, int half_bits,
+                                      uint32_t* __restrict__ idx) {
+    const uint64_t mask = (1ULL << half_bits) - 1;
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n_s;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t v = t;
+        do {
+            uint64_t l = v >> half_bits, r = v & mask;
+#pragma unroll
+            for (int round = 0; round < 4; ++round) {
+                const uint64_t f = mix64(key + 0x9e3779b97f4a7c15ULL * (round + 1) + r) & mask;
+                const uint64_t nl = r;
+                r = l ^ f;
+                l = nl;
+            }
+            v = (l << half_bits) | r;
+        } while (v >= n);
+        idx[t] = static_cast<uint32_t>(v);
+    }
+}
+
+// float -> order-preserving u32
+__device__ __forceinline__ uint32_t fkey(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fval(uint32_t k) {
+    const uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    return __uint_as_float(u);
+}
+
+__global__ void order_keys_kernel(const float* __restrict__ rows, uint64_t total, uint64_t n_s,
+                                  uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / n_s;
+        keys[i] = (r << 32) | fkey(rows[i]);
+        vals[i] = 0;
+    }
+}
+
+__global__ void order_pick_kernel(const uint64_t* __restrict__ sorted, int R, uint64_t n_s,
+                                  int NR, float* __restrict__ table) {
+    const int r = blockIdx.x;
+    const uint64_t span = n_s / NR;
+    for (int b = threadIdx.x; b <= NR; b += blockDim.x) {
+        uint64_t rank;
+        if (b == 0) rank = 0;
+        else if (b == NR) rank = n_s - 1;
+        else rank = span * b - 1;
+        table[static_cast<uint64_t>(r) * (NR + 1) + b] =
+            fval(static_cast<uint32_t>(sorted[static_cast<uint64_t>(r) * n_s + rank]));
+    }
+}
+
+// Encode: one thread per (space, point); the space's K boundary rows sit in
+// shared memory; branchless lower_bound = #{b : row[b] < v}.
+__global__ void encode_kernel(const float* __restrict__ proj, uint64_t n, int K,
+                              const float* __restrict__ table, int NR, int steps,
+                              uint8_t* __restrict__ codes) {
+    extern __shared__ float srow[];  // [K][NR+1]
+    const int sp = blockIdx.y;
+    const int W = NR + 1;
+    for (int i = threadIdx.x; i < K * W; i += blockDim.x)
+        srow[i] = table[static_cast<uint64_t>(sp) * K * W + i];
+    __syncthreads();
+    const float* P = proj + static_cast<uint64_t>(sp) * n * K;
+    uint8_t* C = codes + static_cast<uint64_t>(sp) * n * K;
+    for (uint64_t z = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; z < n;
+         z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (K == 16) {
+            const float4* src = reinterpret_cast<const float4*>(P + z * 16);
+            float v[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float4 f = src[q];
+                v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+            }
+            uint32_t packed[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float* row = srow + j * W;
+                int pos = 0;
+                for (int s = steps; s; s >>= 1)
+                    if (pos + s <= W && row[pos + s - 1] < v[j]) pos += s;
+                int reg = pos - 1;
+                reg = reg < 0 ? 0 : (reg > NR - 1 ? NR - 1 : reg);
+                packed[j >> 2] |= static_cast<uint32_t>(reg) << (8 * (j & 3));
+            }
+            reinterpret_cast<uint4*>(C + z * 16)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        } else {
+            for (int j = 0; j < K; ++j) {
+                const float v = P[z * K + j];
+                const float* row = srow + j * W;
+                int pos = 0;
+                for (int s = steps; s; s >>= 1)
+                    if (pos + s <= W && row[pos + s - 1] < v) pos += s;
+                int reg = pos - 1;
+                reg = reg < 0 ? 0 : (reg > NR - 1 ? NR - 1 : reg);
+                C[z * K + j] = static_cast<uint8_t>(reg);
+            }
+        }
+    }
+}
+
+// D[p][z] = min over spaces of the exact projected l2 (dataset.hpp:23-34 over K floats).
+__global__ void rmin_dist_kernel(const float* __restrict__ proj, uint64_t n, int K, int L,
+                                 const float* __restrict__ probe_proj, int np,
+                                 double* __restrict__ D) {
+    extern __shared__ float spp[];  // [np][L][K]
+    for (int i = threadIdx.x; i < np * L * K; i += blockDim.x) spp[i] = probe_proj[i];
+    __syncthreads();
+    for (uint64_t z = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; z < n;
+         z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double best[16];
+        for (int p = 0; p < np; ++p) best[p] = __longlong_as_double(0x7ff0000000000000LL);
+        for (int i = 0; i < L; ++i) {
+            float x[kMaxK];
+            const float* row = proj + (static_cast<uint64_t>(i) * n + z) * K;
+            for (int j = 0; j < K; ++j) x[j] = row[j];
+            for (int p = 0; p < np; ++p) {
+                const float* q = spp + (p * L + i) * K;
+                double acc = 0.0;
+                for (int j = 0; j < K; ++j) {
+                    const double diff = __dsub_rn(static_cast<double>(q[j]), static_cast<double>(x[j]));
+                    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                }
+                const double dist = __dsqrt_rn(acc);
+                best[p] = dist < best[p] ? dist : best[p];
+            }
+        }
+        for (int p = 0; p < np; ++p) D[static_cast<uint64_t>(p) * n + z] = best[p];
+    }
+}
+
+// Multi-pass 16-bit-digit rank selection over non-negative doubles (bit
+// patterns order like the values).  hist: [np][65536].
+__global__ void select_hist_kernel(const double* __restrict__ D, uint64_t n, int np,
+                                   const uint64_t* __restrict__ prefix, int shift,
+                                   uint32_t* __restrict__ hist) {
+    const int p = blockIdx.y;
+    const uint64_t pre = prefix[p];
+    const uint64_t hi_mask = shift + 16 >= 64 ? 0 : (~0ULL << (shift + 16));
+    const double* Dp = D + static_cast<uint64_t>(p) * n;
+    for (uint64_t z = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; z < n;
+         z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t b = static_cast<uint64_t>(__double_as_longlong(Dp[z]));
+        if ((b & hi_mask) == (pre & hi_mask))
+            atomicAdd(&hist[static_cast<uint64_t>(p) * 65536 + ((b >> shift) & 0xffff)], 1u);
+    }
+}
+
+__global__ void select_pick_kernel(uint32_t* __restrict__ hist, uint64_t* __restrict__ prefix,
+                                   uint64_t* __restrict__ need, int shift) {
+    // one block (1024 threads) per probe: find the bin holding rank `need`
+    const int p = blockIdx.x;
+    uint32_t* h = hist + static_cast<uint64_t>(p) * 65536;
+    __shared__ uint64_t part[1024];
+    const int per = 64;
+    uint64_t s = 0;
+    for (int i = 0; i < per; ++i) s += h[threadIdx.x * per + i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t want = need[p], cum = 0;
+        int blk = 0;
+        for (; blk < 1024; ++blk) {
+            if (cum + part[blk] >= want) break;
+            cum += part[blk];
+        }
+        int bin = blk * per;
+        for (int i = 0; i < per; ++i, ++bin) {
+            const uint64_t c = h[bin];
+            if (cum + c >= want) break;
+            cum += c;
+        }
+        need[p] = want - cum;
+        prefix[p] |= static_cast<uint64_t>(bin) << shift;
+    }
+    __syncthreads();
+    for (int i = 0; i < per; ++i) h[threadIdx.x * per + i] = 0;
+}
+
+}  // namespace
+
+void prepare_coeffs_t(const float* d_coeffs, int LK, int d, double* d_ct, cudaStream_t s) {
+    const int LKp = lk_padded(LK);
+    const int64_t total = static_cast<int64_t>(d) * LKp;
+    coeffs_t_kernel<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 4096)), 256, 0, s>>>(
+        d_coeffs, LK, d, LKp, d_ct);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_project_exact(const float* d_points, uint64_t n, int d, const double* d_ct, int K,
+                          int L, float* d_out, cudaStream_t s) {
+    if (n == 0) return;
+    const int LK = K * L;
+    const uint64_t tiles = (n + kPT - 1) / kPT;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count(dev)) * 8);
+    project_exact_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_points, n, d, d_ct, LK,
+                                                                      lk_padded(LK), K, d_out);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
+                          float* d_out, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n_s + 255) / 256, 65535));
+    gather_sample_kernel<<<grid, 256, 0, s>>>(d_proj_space, d_idx, n_s, K, d_out);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_feistel_sample(uint64_t n, uint64_t n_s, uint64_t key, uint32_t* d_idx,
+                           cudaStream_t s) {
+    int bits = 1;
+    while ((1ULL << bits) < n) ++bits;
+    const int half = (bits + 1) / 2;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n_s + 255) / 256, 65535));
+    feistel_sample_kernel<<<grid, 256, 0, s>>>(n, n_s, key, half, d_idx);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_regions,
+                          float* d_table, cudaStream_t s) {
+    const uint64_t total = static_cast<uint64_t>(R) * n_s;
+    DevBuf<uint64_t> k0(total), k1(total);
+    DevBuf<uint32_t> v0(total), v1(total), tmp(radix_temp_elems(total));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 65535));
+    order_keys_kernel<<<grid, 256, 0, s>>>(d_rows, total, n_s, k0.get(), v0.get());
+    DETLSH_LAUNCH_CHECK();
+    int rbits = 0;
+    while ((1 << rbits) < R) ++rbits;
+    const bool flip = radix_sort_pairs<uint64_t>(k0.get(), v0.get(), k1.get(), v1.get(), total, 0,
+                                                 32 + ((rbits + 7) / 8) * 8, tmp.get(), s);
+    order_pick_kernel<<<R, 256, 0, s>>>(flip ? k1.get() : k0.get(), R, n_s, n_regions, d_table);
+    DETLSH_LAUNCH_CHECK();
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+}
+
+void launch_encode(const float* d_proj, uint64_t n, int K, int L, const float* d_table,
+                   int n_regions, uint8_t* d_codes, cudaStream_t s) {
+    if (n == 0) return;
+    int steps = 1;
+    while (steps * 2 <= n_regions + 1) steps *= 2;
+    const size_t smem = static_cast<size_t>(K) * (n_regions + 1) * sizeof(float);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned gx = static_cast<unsigned>(
+        std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8));
+    encode_kernel<<<dim3(gx, L), 256, smem, s>>>(d_proj, n, K, d_table, n_regions, steps, d_codes);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float* d_probe_proj,
+                      int np, uint64_t rank, double* d_D, uint32_t* d_hist, uint64_t* h_T_bits,
+                      cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned gx = static_cast<unsigned>(
+        std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8));
+    rmin_dist_kernel<<<gx, 256, static_cast<size_t>(np) * L * K * sizeof(float), s>>>(
+        d_proj, n, K, L, d_probe_proj, np, d_D);
+    DETLSH_LAUNCH_CHECK();
+    DevBuf<uint64_t> pre(np), need(np);
+    std::vector<uint64_t> h(np, rank);
+    DETLSH_CUDA(cudaMemsetAsync(pre.get(), 0, np * sizeof(uint64_t), s));
+    DETLSH_CUDA(cudaMemcpyAsync(need.get(), h.data(), np * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    DETLSH_CUDA(cudaMemsetAsync(d_hist, 0, static_cast<size_t>(np) * 65536 * sizeof(uint32_t), s));
+    for (int shift = 48; shift >= 0; shift -= 16) {
+        select_hist_kernel<<<dim3(gx, np), 256, 0, s>>>(d_D, n, np, pre.get(), shift, d_hist);
+        DETLSH_LAUNCH_CHECK();
+        select_pick_kernel<<<np, 1024, 0, s>>>(d_hist, pre.get(), need.get(), shift);
+        DETLSH_LAUNCH_CHECK();
+    }
+    DETLSH_CUDA(cudaMemcpyAsync(h_T_bits, pre.get(), np * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace detlsh_b200

@@ -1,0 +1,48 @@
+// Launchers for the build-stage kernels (stages.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace detlsh_b200 {
+
+// coeffs [L][K][d] fp32 -> transposed double [d][LKp] (LKp = LK rounded up to 64)
+int lk_padded(int LK);
+void prepare_coeffs_t(const float* d_coeffs, int LK, int d, double* d_coeffs_t, cudaStream_t s);
+
+// project_dataset (projection.cpp:47-60), exact: fp64 FMA chain in t order
+// (float x float is exact in double, so fma == mul+add), rounded once.
+// out [L][n][K] fp32.
+void launch_project_exact(const float* d_points, uint64_t n, int d, const double* d_coeffs_t,
+                          int K, int L, float* d_out, cudaStream_t s);
+
+// sample values: out[j][t] = proj[space][idx[t]][j]  (j < K, t < n_s)
+void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
+                          float* d_out, cudaStream_t s);
+
+// GPU-native sample indices for one space: first n_s values of a keyed
+// Feistel permutation of [0, n).
+void launch_feistel_sample(uint64_t n, uint64_t n_s, uint64_t key, uint32_t* d_idx,
+                           cudaStream_t s);
+
+// Exact order statistics per row (GPU sample mode): rows [R][n_s] (fp32),
+// writes table rows [R][NR+1]: row[0]=min, row[t]=sorted[span*t-1], row[NR]=max.
+void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_regions,
+                          float* d_table, cudaStream_t s);
+
+// encode_dataset (encoder.cpp:155-176): branchless lower_bound over the
+// N_r+1 boundaries staged in shared memory; out [L][n][K] u8.
+void launch_encode(const float* d_proj, uint64_t n, int K, int L, const float* d_table,
+                   int n_regions, uint8_t* d_codes, cudaStream_t s);
+
+// r_min support (index.cpp:33-136 restated as an order statistic):
+// D[p][z] = min_i l2_double(probe_proj[p][i], proj[i][z]); returns via d_T
+// the bits of the `rank`-th smallest (1-based) D per probe.
+void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float* d_probe_proj,
+                      int n_probes, uint64_t rank, double* d_D, uint32_t* d_hist,
+                      uint64_t* h_T_bits, cudaStream_t s);
+
+}  // namespace detlsh_b200

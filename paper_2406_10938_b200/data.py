@@ -1,0 +1,100 @@
+"""Seeded synthetic stand-ins for BASELINE.json's configs (none of the paper's
+datasets are in this environment).  Each generator returns (base, queries) as
+float32 arrays; queries are held out from the same distribution (the last nq
+rows of one draw).  numpy PCG64 streams make every byte reproducible.
+
+  C1  n=1e5, d=128: 100 centres U[0,100]^d, isotropic sigma=5, seed 1
+  C2  n=1e6, d=128: 0 w.p. 0.5 else min(255, geometric(p=0.05)), seed 2
+  C3  n=1e6, d=784: 28x28 grid, 3-6 blobs of radius 3-6, non-zeros U[1,255], seed 3
+  C4  n=1e7, d=96 : N(0,1) rows L2-normalised, seed 4
+  C5  n=1e8, d=128: as C2, seed 5 (generated in shards)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+CONFIGS = {
+    "c1": dict(n=100_000, d=128, nq=1_000, seed=1),
+    "c2": dict(n=1_000_000, d=128, nq=10_000, seed=2),
+    "c3": dict(n=1_000_000, d=784, nq=10_000, seed=3),
+    "c4": dict(n=10_000_000, d=96, nq=10_000, seed=4),
+    "c5": dict(n=100_000_000, d=128, nq=10_000, seed=5),
+}
+
+
+def mixture(total: int, d: int, seed: int, clusters: int = 100, lo: float = 0.0,
+            hi: float = 100.0, sigma: float = 5.0) -> np.ndarray:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    centres = rng.uniform(lo, hi, size=(clusters, d)).astype(np.float32)
+    pick = rng.integers(0, clusters, size=total)
+    out = np.empty((total, d), np.float32)
+    step = 1 << 16
+    for s in range(0, total, step):
+        e = min(total, s + step)
+        out[s:e] = centres[pick[s:e]] + rng.normal(0.0, sigma, size=(e - s, d)).astype(np.float32)
+    return out
+
+
+def sparse_geometric(total: int, d: int, seed: int, p: float = 0.05) -> np.ndarray:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = np.empty((total, d), np.float32)
+    step = 1 << 16
+    for s in range(0, total, step):
+        e = min(total, s + step)
+        zero = rng.random((e - s, d)) < 0.5
+        g = np.minimum(rng.geometric(p, size=(e - s, d)), 255)
+        out[s:e] = np.where(zero, 0, g).astype(np.float32)
+    return out
+
+
+def blobs784(total: int, seed: int) -> np.ndarray:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    yy, xx = np.mgrid[0:28, 0:28]
+    grid = np.stack([yy.ravel(), xx.ravel()], 1).astype(np.float32)  # [784, 2]
+    out = np.zeros((total, 784), np.float32)
+    step = 1 << 13
+    for s in range(0, total, step):
+        e = min(total, s + step)
+        m = e - s
+        nb = rng.integers(3, 7, size=m)
+        mask = np.zeros((m, 784), bool)
+        for b in range(6):
+            active = nb > b
+            ctr = rng.uniform(0, 27, size=(m, 2)).astype(np.float32)
+            rad = rng.uniform(3, 6, size=m).astype(np.float32)
+            d2 = ((grid[None, :, :] - ctr[:, None, :]) ** 2).sum(-1)
+            mask |= active[:, None] & (d2 < 0.5 * (rad ** 2)[:, None])
+        vals = rng.integers(1, 256, size=(m, 784)).astype(np.float32)
+        out[s:e] = np.where(mask, vals, 0.0)
+    return out
+
+
+def unit_gaussian(total: int, d: int, seed: int) -> np.ndarray:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    out = np.empty((total, d), np.float32)
+    step = 1 << 18
+    for s in range(0, total, step):
+        e = min(total, s + step)
+        x = rng.standard_normal((e - s, d), dtype=np.float32)
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        out[s:e] = x
+    return out
+
+
+def make(config: str, n: int | None = None, nq: int | None = None):
+    """(base [n][d], queries [nq][d]) for config c1..c5 (n/nq may be scaled down)."""
+    c = CONFIGS[config]
+    n = c["n"] if n is None else n
+    nq = c["nq"] if nq is None else nq
+    total = n + nq
+    if config == "c1":
+        allp = mixture(total, c["d"], c["seed"])
+    elif config in ("c2", "c5"):
+        allp = sparse_geometric(total, c["d"], c["seed"])
+    elif config == "c3":
+        allp = blobs784(total, c["seed"])
+    elif config == "c4":
+        allp = unit_gaussian(total, c["d"], c["seed"])
+    else:
+        raise ValueError(config)
+    return allp[:n], allp[n:]
