@@ -1,0 +1,503 @@
+#!/usr/bin/env python
+"""DET-LSH on B200: index build (Mpoints/s) + batched 50-NN queries (queries/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload: BASELINE.json configs[1] ("c2": n=1e6, d=128 sparse 8-bit integers,
+10,000 held-out queries, K=16, L=4, N_r=256, leaf 128, k=50, c=1.5, beta=0.1),
+synthetic (paper_2406_10938_b200/data.py).  One build step = build_index over
+the whole (per-rank) shard; one query step = the whole 10,000-query batch
+through ck_ann, merged across ranks.  `value` is the build rate; the query
+rate, recall and ratio are in "query".  Multi-GPU: point-sharded independent
+indexes, NCCL all-gather of per-shard top-k + GPU merge.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DE-Tree index build Mpoints/s; batched 50-NN queries/s at reference-matched recall"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--nq", type=int, default=None)
+    ap.add_argument("--k", type=int, default=50)
+    ap.add_argument("--beta", type=float, default=0.1)
+    ap.add_argument("--seed", type=int, default=2)
+    ap.add_argument("--sample", choices=["reference", "gpu"], default="reference",
+                    help="breakpoint sample mode of the headline build")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-queries", type=int, default=200)
+    ap.add_argument("--cpu-build-rows", type=int, default=250_000)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled with nvidia-smi during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# ground truth + quality metrics (measurement only, outside the timed region)
+# ---------------------------------------------------------------------------
+def exact_knn_gpu(base, Q, k, integer_data: bool):
+    """metrics.cpp:8-33 semantics: order by (dist^2, position)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dt = torch.float32 if integer_data else torch.float64
+    X = torch.from_numpy(base).cuda().to(dt)
+    xn = (X * X).sum(1)
+    ids = np.empty((Q.shape[0], k), np.int64)
+    dists = np.empty((Q.shape[0], k), np.float64)
+    step = 256
+    for s in range(0, Q.shape[0], step):
+        q = torch.from_numpy(Q[s:s + step]).cuda().to(dt)
+        D = (q * q).sum(1, keepdim=True) + xn[None, :] - 2.0 * (q @ X.T)
+        if integer_data:
+            D = torch.round(D)
+        D = D.clamp_min_(0)
+        kth = torch.kthvalue(D, k, dim=1).values
+        for i in range(q.shape[0]):
+            row = D[i]
+            t = kth[i]
+            less = torch.nonzero(row < t).flatten()
+            lv = row[less]
+            order = torch.argsort(lv, stable=True)  # positions ascending within ties
+            less = less[order]
+            eq = torch.nonzero(row == t).flatten()[: k - less.numel()]
+            sel = torch.cat([less, eq])
+            ids[s + i] = sel.cpu().numpy()
+            dists[s + i] = np.sqrt(row[sel].double().cpu().numpy())
+    return ids, dists
+
+
+def recall_ratio(res_ids, res_d, n_hits, gt_ids, gt_d, k):
+    """recall / overall_ratio as metrics.cpp:35-66."""
+    rec, rat = [], []
+    for i in range(res_ids.shape[0]):
+        m = int(n_hits[i])
+        rec.append(len(set(res_ids[i, :m].tolist()) & set(gt_ids[i].tolist())) / k)
+        s, cnt = 0.0, 0
+        for r in range(min(m, k)):
+            t, v = gt_d[i, r], res_d[i, r]
+            if t == 0.0:
+                if v == 0.0:
+                    s += 1.0
+                    cnt += 1
+                continue
+            s += v / t
+            cnt += 1
+        rat.append(1.0 if cnt == 0 else s / cnt)
+    return float(np.mean(rec)), float(np.mean(rat))
+
+
+# algorithmic bytes per launch; kernels without a model get null
+def algo_bytes(kernel, n, d, nq, budget, K, L):
+    if kernel == "project_exact":
+        return 4.0 * d * n  # one read of the fp32 shard (4d B/point)
+    if kernel == "query_fast":
+        return 4.0 * d * budget * nq  # every verified candidate row (4d B/candidate)
+    if kernel == "encode":
+        return 5.0 * L * K * n  # fp32 projections in, u8 codes out
+    return None
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# the reference arm: the reference's own CPU implementation
+# ---------------------------------------------------------------------------
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle.bindings import Oracle, ref_available, make_params
+    from paper_2406_10938_b200 import data as gen
+    kind = "reference" if ref_available() else "port"
+    orc = Oracle(kind)
+    cfg = args.config
+    base, Q = gen.make(cfg, nq=args.nq)
+    n, d = base.shape
+    cores = os.cpu_count() or 1
+    p = make_params(beta=args.beta, k=args.k)
+    rows = min(n, args.cpu_build_rows)
+    sub = np.ascontiguousarray(base[:rows])
+    # build: single thread (the reference is single-threaded by design)
+    times = []
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oi = orc.build_index(sub, p, args.seed)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+        del oi
+    build_s = float(np.mean(times))
+    build_rate = rows / build_s / 1e6
+    # queries: full-size index (built once, untimed), all host threads
+    full = orc.build_index(base, p, args.seed)
+    nqs = min(args.cpu_queries, Q.shape[0])
+    qtimes = []
+    for step in range(args.warmup + args.steps):
+        qs = Q[(step * nqs) % Q.shape[0]:][:nqs]
+        ids, ds, nh, rad, cs, secs = full.ck_ann_batch(qs, args.k, threads=cores)
+        if step >= args.warmup:
+            qtimes.append(secs)
+    q_rate = nqs / float(np.mean(qtimes))
+    integer = bool(np.all(base == np.round(base)) and base.min() >= 0 and base.max() <= 255)
+    gt_ids, gt_d = exact_knn_gpu_or_cpu(base, Q[:nqs], args.k, integer, orc)
+    ids, ds, nh, rad, cs, _ = full.ck_ann_batch(Q[:nqs], args.k, threads=cores)
+    rec, rat = recall_ratio(ids, ds, nh, gt_ids, gt_d, args.k)
+    sample = (f"build: first {rows} of {n} rows x {args.steps} steps, 1 thread; "
+              f"queries: {nqs} per step on the full n={n} index, {cores} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(build_rate, 6), "unit": "Mpoints/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(build_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg}: n={n}, d={d}, nq={Q.shape[0]}, K=16, L=4, N_r=256, "
+                               f"leaf=128, k={args.k}, c=1.5, beta={args.beta}",
+                   "parallelism": "cpu"},
+        "query": {"value": round(q_rate, 3), "unit": "queries/s", "recall": rec, "ratio": rat,
+                  "queries": nqs},
+        "cpu_baseline": {"value": round(build_rate, 6), "unit": "Mpoints/s", "cores": 1,
+                         "kind": kind, "sample": sample,
+                         "query": {"value": round(q_rate, 3), "unit": "queries/s",
+                                   "cores": cores}},
+        "e2e": {"value": round(build_rate, 6), "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def exact_knn_gpu_or_cpu(base, Q, k, integer, orc):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return exact_knn_gpu(base, Q, k, integer)
+    except Exception:
+        pass
+    return orc.brute_force_knn(base, Q, k)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def cpu_baseline(args, base, Q):
+    """The reference (oracle/_ref) on this box's host cores, bounded sample."""
+    from oracle.bindings import Oracle, ref_available, make_params
+    kind = "reference" if ref_available() else "port"
+    orc = Oracle(kind)
+    n = base.shape[0]
+    rows = min(n, args.cpu_build_rows)
+    p = make_params(beta=args.beta, k=args.k)
+    t0 = time.perf_counter()
+    orc.build_index(np.ascontiguousarray(base[:rows]), p, args.seed)
+    b = time.perf_counter() - t0
+    full = orc.build_index(base, p, args.seed)
+    cores = os.cpu_count() or 1
+    nqs = min(args.cpu_queries, Q.shape[0])
+    _, _, _, _, _, secs = full.ck_ann_batch(Q[:nqs], args.k, threads=cores)
+    return {"value": round(rows / b / 1e6, 6), "unit": "Mpoints/s", "cores": 1, "kind": kind,
+            "sample": f"build_index on the first {rows} rows (1 thread); ck_ann on {nqs} "
+                      f"queries against the full n={n} index ({cores} threads)",
+            "query": {"value": round(nqs / secs, 3), "unit": "queries/s", "cores": cores}}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2406_10938_b200 as D
+    from paper_2406_10938_b200 import data as gen
+    from paper_2406_10938_b200.shard import gather_topk, shard_bounds
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = D.load()
+    cfg = args.config
+    base, Q = gen.make(cfg, nq=args.nq)
+    n, d = base.shape
+    nq = Q.shape[0]
+    s0, s1 = shard_bounds(n, world, rank)
+    shard = np.ascontiguousarray(base[s0:s1])
+    n_loc = shard.shape[0]
+    params = D.LshParams(beta=args.beta, k=args.k)
+    k = args.k
+    dev_shard = torch.from_numpy(shard).cuda()
+    dev_Q = torch.from_numpy(Q).cuda()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps):
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = None
+        for _ in range(steps):
+            out = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return e0.elapsed_time(e1) / steps, out
+
+    # ---------------- build ----------------
+    def build():
+        return D.build_index(dev_shard, params, seed=args.seed, sample=args.sample, borrow=True,
+                             keep_codes=False)
+
+    for _ in range(args.warmup):
+        idx = build()
+    del idx
+    clocks = ClockSampler(local)
+    clocks.start()
+    lc0 = lib.detlsh_launch_count()
+    lib.detlsh_profile_enable(1)
+    build_ms, idx = timed(build, args.steps)
+    lib.detlsh_profile_enable(0)
+    build_launches = (lib.detlsh_launch_count() - lc0) / args.steps
+    prof_build = collect_profile(lib)
+    build_ms = max_over_ranks(build_ms)
+    stage_ms = idx.build_timings()
+
+    # ---------------- queries ----------------
+    ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
+    dists = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+    hits = torch.empty(nq, dtype=torch.int32, device="cuda")
+    rad = torch.empty(nq, dtype=torch.float64, device="cuda")
+    cands = torch.empty(nq, dtype=torch.int64, device="cuda")
+    if world > 1:
+        g_d = torch.empty((world, nq, k), dtype=torch.float64, device="cuda")
+        g_i = torch.empty((world, nq, k), dtype=torch.int64, device="cuda")
+        g_h = torch.empty((world, nq), dtype=torch.int32, device="cuda")
+        m_d = torch.empty((nq, k), dtype=torch.float64, device="cuda")
+        m_i = torch.empty((nq, k), dtype=torch.int64, device="cuda")
+        m_h = torch.empty(nq, dtype=torch.int32, device="cuda")
+
+    def query():
+        D.ck_ann_device(idx, dev_Q, k, ids, dists, hits, rad, cands, stream=stream.cuda_stream)
+        if world == 1:
+            return ids, dists, hits
+        gid = ids.to(torch.int64) + s0  # global positions
+        gather_topk(dists, gid, hits, g_d, g_i, g_h)
+        D.merge_topk_device(g_d, g_i, g_h, k, m_d, m_i, m_h, stream=stream.cuda_stream)
+        return m_i, m_d, m_h
+
+    for _ in range(args.warmup):
+        query()
+    lc0 = lib.detlsh_launch_count()
+    lib.detlsh_profile_enable(1)
+    query_ms, (r_ids, r_d, r_h) = timed(query, args.steps)
+    lib.detlsh_profile_enable(0)
+    query_launches = (lib.detlsh_launch_count() - lc0) / args.steps
+    prof_query = collect_profile(lib)
+    query_ms = max_over_ranks(query_ms)
+    clk = clocks.stop()
+
+    # ---------------- end to end through the public API, host buffers ----------------
+    def e2e_build():
+        ix = D.build_index(shard, params, seed=args.seed, sample=args.sample, keep_codes=False)
+        _ = ix.params.r_min  # result read back (params travel D2H inside build)
+        return ix
+
+    e2e_build()
+    e2e_build_ms, ix2 = timed(e2e_build, max(1, args.steps))
+    e2e_build_ms = max_over_ranks(e2e_build_ms)
+    del ix2
+    Qpin = torch.from_numpy(Q).pin_memory().numpy()
+
+    def e2e_query():
+        res = D.ck_ann_batch(idx, Qpin, k)
+        if world > 1:
+            t = torch.from_numpy(res.ids.astype(np.int64) + s0).cuda()
+            td = torch.from_numpy(res.dists).cuda()
+            th = torch.from_numpy(res.n_hits).cuda()
+            gather_topk(td, t, th, g_d, g_i, g_h)
+            D.merge_topk_device(g_d, g_i, g_h, k, m_d, m_i, m_h, stream=stream.cuda_stream)
+            return m_i.cpu().numpy(), m_d.cpu().numpy()
+        return res.ids, res.dists
+
+    e2e_query()
+    e2e_query_ms, _ = timed(e2e_query, max(1, args.steps))
+    e2e_query_ms = max_over_ranks(e2e_query_ms)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- quality (merged results vs exact kNN) ----------------
+    integer = bool(np.all(base == np.round(base)) and base.min() >= 0 and base.max() <= 255)
+    out_ids = r_ids.cpu().numpy().astype(np.int64)
+    out_d = r_d.cpu().numpy()
+    out_h = r_h.cpu().numpy()
+    gt_ids, gt_d = exact_knn_gpu(base, Q, k, integer)
+    rec, rat = recall_ratio(out_ids, out_d, out_h, gt_ids, gt_d, k)
+
+    budget = D.candidate_budget(idx.params.beta, n_loc, k)
+    hbm, peak_kind = peaks()
+    build_roof = roofline(prof_build, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
+                          exclude=("query_fast", "query_slow"))
+    query_roof = roofline(prof_query, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
+                          only=("query_fast",))
+    value = n / (build_ms / 1e3) / 1e6
+    qps = nq / (query_ms / 1e3)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(build_ms, 3),
+        "higher_is_better": True, "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg}: n={n}, d={d}, nq={nq}, K=16, L=4, N_r=256, leaf=128, "
+                               f"k={k}, c=1.5, beta={args.beta}",
+                   "sample_mode": args.sample, "parallelism": f"point-shard x{world}",
+                   "l2": "inputs larger than L2 (dataset 512 MB, candidate rows 51 MB/query)"},
+        "query": {"value": round(qps, 2), "unit": "queries/s", "ms_per_step": round(query_ms, 3),
+                  "recall": round(rec, 6), "ratio": round(rat, 6), "gpu_launches": query_launches,
+                  "roofline": query_roof,
+                  "e2e": {"value": round(nq / (e2e_query_ms / 1e3), 2), "unit": "queries/s",
+                          "h2d_bytes_per_step": int(nq * d * 4),
+                          "d2h_bytes_per_step": int(nq * k * 12 + nq * 20)}},
+        "e2e": {"value": round(n / (e2e_build_ms / 1e3) / 1e6, 3), "unit": "Mpoints/s",
+                "h2d_bytes_per_step": int(n_loc * d * 4), "d2h_bytes_per_step": 96},
+        "gpu_launches": build_launches,
+        "roofline": build_roof,
+        "build_stages_ms": {k2: round(v, 3) for k2, v in stage_ms.items()},
+        "kernels_ms_per_step": {"build": {k2: round(v[0] / args.steps, 4) for k2, v in prof_build.items()},
+                                "query": {k2: round(v[0] / args.steps, 4) for k2, v in prof_query.items()}},
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args, base, Q)
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"error": str(e)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def collect_profile(lib):
+    import ctypes as C
+    names = C.create_string_buffer(4096)
+    ms = np.zeros(64, np.float64)
+    cnt = np.zeros(64, np.uint64)
+    m = lib.detlsh_profile_collect(names, 4096, C.c_void_p(ms.ctypes.data),
+                                   C.c_void_p(cnt.ctypes.data), 64)
+    keys = names.value.decode().split(";") if m else []
+    return {kk: (float(ms[i]), int(cnt[i])) for i, kk in enumerate(keys)}
+
+
+def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exclude=()):
+    items = [(kk, v) for kk, v in prof.items() if (only is None or kk in only) and kk not in exclude]
+    if not items:
+        return None
+    kern, (ms, launches) = max(items, key=lambda kv: kv[1][0])
+    per_launch_ms = ms / max(1, launches)
+    b = algo_bytes(kern, n, d, nq, budget, K, L)
+    total = sum(v[0] for v in prof.values() if v is not None)
+    out = {"kernel": kern, "bound": "hbm", "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+           "launch_ms": round(per_launch_ms, 4), "share_of_kernel_time": round(ms / total, 4) if total else None,
+           "traffic": None}
+    if b is None:
+        out.update({"achieved": None, "frac": None})
+    else:
+        ach = b / (per_launch_ms / 1e3) / 1e9
+        out.update({"achieved": round(ach, 2), "frac": round(ach / hbm, 5),
+                    "algorithmic_bytes": b})
+    return out
+
+
+if __name__ == "__main__":
+    main()

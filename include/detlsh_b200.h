@@ -74,6 +74,16 @@ int detlsh_device_count(void);
 const char* detlsh_gpu_last_error(void);
 const char* detlsh_version(void);
 
+/* ---- instrumentation -------------------------------------------------------- */
+/* Kernels this library has launched in this process (every launch site). */
+uint64_t detlsh_launch_count(void);
+/* Per-kernel CUDA-event timing on the launching stream (off by default). */
+void detlsh_profile_enable(int32_t on);
+/* Drains recorded events: up to cap entries of (total ms, launches); names
+ * ';'-separated into `names`.  Returns the number of entries. */
+int detlsh_profile_collect(char* names, int32_t names_cap, double* ms, uint64_t* launches,
+                           int32_t cap);
+
 /* ---- index build ----------------------------------------------------------- */
 
 /* build_index (index.hpp:39, index.cpp:212-218): points [n][d] fp32 row-major.

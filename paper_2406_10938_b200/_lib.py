@@ -69,6 +69,9 @@ def load() -> C.CDLL:
         "detlsh_device_count": ([], C.c_int),
         "detlsh_gpu_last_error": ([], C.c_char_p),
         "detlsh_version": ([], C.c_char_p),
+        "detlsh_launch_count": ([], u64),
+        "detlsh_profile_enable": ([i32], None),
+        "detlsh_profile_collect": ([C.c_char_p, i32, vp, vp, i32], C.c_int),
         "detlsh_gpu_build": ([vp, u64, i32, P, u64, i32, u32, C.POINTER(vp)], C.c_int),
         "detlsh_gpu_build_with_family": ([vp, u64, i32, P, vp, i32, i32, u64, u64, i32, u32,
                                           C.POINTER(vp)], C.c_int),

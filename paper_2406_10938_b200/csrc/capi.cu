@@ -458,6 +458,13 @@ double detlsh_chi2_quantile(double a, int32_t k) {
     }
 }
 
+uint64_t detlsh_launch_count(void) { return launch_count(); }
+void detlsh_profile_enable(int32_t on) { profile_enable(on != 0); }
+int detlsh_profile_collect(char* names, int32_t names_cap, double* ms, uint64_t* launches,
+                           int32_t cap) {
+    return profile_collect(names, names_cap, ms, launches, cap);
+}
+
 int detlsh_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {

@@ -8,6 +8,8 @@
 #include <string>
 #include <utility>
 
+#include "prof.cuh"
+
 namespace detlsh_b200 {
 
 // Maps onto DETLSH_E_INVALID (std::invalid_argument in the reference).
@@ -27,7 +29,11 @@ struct CudaError : std::runtime_error {
                                            " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
     } while (0)
 
-#define DETLSH_LAUNCH_CHECK() DETLSH_CUDA(cudaGetLastError())
+#define DETLSH_LAUNCH_CHECK()             \
+    do {                                    \
+        ::detlsh_b200::count_launch();      \
+        DETLSH_CUDA(cudaGetLastError());    \
+    } while (0)
 
 constexpr int kMaxK = 24;      // validate_params: K in [1, 24] (index.cpp:17)
 constexpr int kMaxRegions = 256;

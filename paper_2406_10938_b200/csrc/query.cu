@@ -714,6 +714,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         if (X.fast.size() < slots * fast_bytes) {
             X.fast.alloc(slots * fast_bytes);
         }
+        ProfScope ps("query_fast", s);
         query_fast_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
             P, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
         DETLSH_LAUNCH_CHECK();
@@ -731,6 +732,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         DETLSH_CUDA(cudaMemsetAsync(X.slow.get(), 0, slots * slow_bytes, s));
         X.slow_slots = slots;
     }
+    ProfScope ps("query_slow", s);
     query_slow_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
         P, slow_list, slow_count, X.slow.get(), slow_bytes);
     DETLSH_LAUNCH_CHECK();

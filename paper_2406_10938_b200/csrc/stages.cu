@@ -324,6 +324,7 @@ void launch_project_exact(const float* d_points, uint64_t n, int d, const double
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count(dev)) * 8);
+    ProfScope ps("project_exact", s);
     project_exact_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_points, n, d, d_ct, LK,
                                                                       lk_padded(LK), K, d_out);
     DETLSH_LAUNCH_CHECK();
@@ -332,6 +333,7 @@ void launch_project_exact(const float* d_points, uint64_t n, int d, const double
 void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
                           float* d_out, cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n_s + 255) / 256, 65535));
+    ProfScope ps("gather_sample", s);
     gather_sample_kernel<<<grid, 256, 0, s>>>(d_proj_space, d_idx, n_s, K, d_out);
     DETLSH_LAUNCH_CHECK();
 }
@@ -373,6 +375,7 @@ void launch_encode(const float* d_proj, uint64_t n, int K, int L, const float* d
     cudaGetDevice(&dev);
     const unsigned gx = static_cast<unsigned>(
         std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8));
+    ProfScope ps("encode", s);
     encode_kernel<<<dim3(gx, L), 256, smem, s>>>(d_proj, n, K, d_table, n_regions, steps, d_codes);
     DETLSH_LAUNCH_CHECK();
 }
@@ -384,6 +387,7 @@ void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float
     cudaGetDevice(&dev);
     const unsigned gx = static_cast<unsigned>(
         std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8));
+    ProfScope ps("rmin_dist", s);
     rmin_dist_kernel<<<gx, 256, static_cast<size_t>(np) * L * K * sizeof(float), s>>>(
         d_proj, n, K, L, d_probe_proj, np, d_D);
     DETLSH_LAUNCH_CHECK();

@@ -353,6 +353,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     DevBuf<uint32_t> k0(n), k1(n), v1(n), flags(n), ridx(n);
     T.perm.alloc(n);
     DevBuf<uint32_t> rtmp(std::max(radix_temp_elems(n), scan_temp_elems(n)));
+    ProfScope ps_sort("tree_slot_sort", s);
     slot_key_kernel<<<grid_for(n), 256, 0, s>>>(d_codes, n, K, sbits, k0.get(), T.perm.get());
     DETLSH_LAUNCH_CHECK();
     const bool flip = radix_sort_pairs<uint32_t>(k0.get(), T.perm.get(), k1.get(), v1.get(), n, 0,
@@ -398,6 +399,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
         B.grow(total + 2 * static_cast<size_t>(A), total, K, s);
         actB.grow(2 * static_cast<size_t>(A), 0, s);
         DETLSH_CUDA(cudaMemsetAsync(d_next_n, 0, 4, s));
+        ProfScope ps("tree_level_split", s);
         level_split_kernel<<<A, kLevelThreads, 0, s>>>(
             d_codes, K, sbits, cap, actA.get(), static_cast<uint32_t>(total), T.perm.get(),
             ptmp.get(), B.key.get(), B.begin.get(), B.count.get(), B.depth.get(), B.split.get(),
@@ -425,6 +427,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     DevBuf<uint32_t> stmp(radix_temp_elems(total) + scan_temp_elems(total));
     DETLSH_CUDA(cudaMemcpyAsync(ka.get(), B.key.get(), total * 8, cudaMemcpyDeviceToDevice, s));
     clamp_invalid_keys<<<grid_for(total), 256, 0, s>>>(ka.get(), total, invalid_key);
+    DETLSH_LAUNCH_CHECK();
     iota_kernel<<<grid_for(total), 256, 0, s>>>(va.get(), total);
     DETLSH_LAUNCH_CHECK();
     const bool f2 = radix_sort_pairs<uint64_t>(ka.get(), va.get(), kb.get(), vb.get(), total, 0,
