@@ -69,6 +69,12 @@ int detlsh_sample_hash_family(int32_t d, int32_t K, int32_t L, uint64_t seed, fl
 /* chi2_cdf / chi2_quantile (chi2.hpp:10-17). */
 double detlsh_chi2_cdf(double x, int32_t k);
 double detlsh_chi2_quantile(double alpha, int32_t k);
+/* select_row_breakpoints (encoder.hpp:36, encoder.cpp:57-103) as replayed by
+ * the host for the reference-compatible sample: reorders `sample` in place
+ * exactly as the reference does, writes n_regions+1 boundaries, and reports
+ * how many RNG draws (partition calls) it consumed from Rng(rng_seed). */
+int detlsh_select_row_breakpoints(float* sample, uint64_t n_s, int32_t n_regions,
+                                  uint64_t rng_seed, float* row, uint64_t* draws);
 
 int detlsh_device_count(void);
 const char* detlsh_gpu_last_error(void);

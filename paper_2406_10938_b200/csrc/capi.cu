@@ -12,6 +12,7 @@
 #include "../../include/detlsh_b200.h"
 #include "common.cuh"
 #include "host_core.hpp"
+#include "index.cuh"
 #include "query.cuh"
 #include "stages.cuh"
 #include "tree.cuh"
@@ -30,351 +31,6 @@ int sm_count(int device) {
 namespace {
 
 thread_local std::string g_last_error;
-
-using Clock = std::chrono::steady_clock;
-double ms_since(Clock::time_point t0) {
-    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
-}
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        DETLSH_CUDA(cudaGetDevice(&prev));
-        if (prev != dev) DETLSH_CUDA(cudaSetDevice(dev));
-    }
-    ~DeviceGuard() {
-        if (prev >= 0) cudaSetDevice(prev);
-    }
-};
-
-bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
-
-void validate(const detlsh_params& p, uint64_t n, int d) {
-    // validate_params (index.cpp:16-24) + stage preconditions
-    if (n == 0) throw InvalidArgument("build_index: empty dataset");
-    if (d < 1) throw InvalidArgument("build_index: d must be positive");
-    if (n > 0xffffffffULL) throw InvalidArgument("build_index: n must be < 2^32 (u32 positions)");
-    if (p.K < 1 || p.K > 24) throw InvalidArgument("build_index: K must lie in [1, 24]");
-    if (p.L < 1) throw InvalidArgument("build_index: L must be positive");
-    if (!(p.c > 1.0)) throw InvalidArgument("build_index: c must exceed 1");
-    if (p.leaf_capacity < 1) throw InvalidArgument("build_index: leaf_capacity must be positive");
-    if (!is_pow2(p.n_regions) || p.n_regions < 2 || p.n_regions > 256)
-        throw InvalidArgument("select_breakpoints: n_regions must be a power of two in [2, 256]");
-    if (!(p.sample_fraction > 0.0) || p.sample_fraction > 1.0)
-        throw InvalidArgument("select_breakpoints: sample_fraction must lie in (0, 1]");
-    uint64_t n_s = static_cast<uint64_t>(std::ceil(p.sample_fraction * static_cast<double>(n)));
-    n_s = std::max<uint64_t>(n_s, static_cast<uint64_t>(p.n_regions));
-    if (n_s > n) throw InvalidArgument("select_breakpoints: sample too small for region count");
-}
-
-uint64_t sample_size_for(double frac, uint64_t n, int NR) {
-    uint64_t n_s = static_cast<uint64_t>(std::ceil(frac * static_cast<double>(n)));
-    n_s = std::max<uint64_t>(n_s, static_cast<uint64_t>(NR));
-    if (n_s > n) throw InvalidArgument("select_breakpoints: sample too small for region count");
-    return n_s;
-}
-
-}  // namespace
-
-struct GpuIndex {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    detlsh_params params{};
-    uint64_t n = 0;
-    int d = 0;
-    uint64_t family_seed = 0, sample_size = 0;
-    bool sample_gpu = false;
-    const float* data = nullptr;  // device
-    DevBuf<float> data_buf;
-    std::vector<float> h_coeffs;  // [L][K][d]
-    DevBuf<float> coeffs;
-    DevBuf<double> coeffs_t;
-    DevBuf<float> table;
-    std::vector<float> h_table;
-    DevBuf<uint8_t> codes;
-    std::vector<std::unique_ptr<DevTree>> trees;
-    DevBuf<QTree> qtrees;
-    uint32_t max_leaves = 0;
-    QueryScratch scratch;
-    std::mutex qmu;
-    std::vector<std::pair<std::string, double>> timings;
-
-    ~GpuIndex() {
-        if (stream) cudaStreamDestroy(stream);
-    }
-};
-
-namespace {
-
-// Breakpoints in the reference-compatible mode: the host replays the shared
-// RNG stream (encoder.cpp:105-143) on exact sample values gathered on device.
-void breakpoints_ref(GpuIndex& X, const float* d_proj, uint64_t seed) {
-    const int K = X.params.K, L = X.params.L, NR = X.params.n_regions;
-    const uint64_t n = X.n, n_s = X.sample_size;
-    const size_t W = static_cast<size_t>(NR) + 1;
-    RefSampler sampler(n, n_s, NR, mix_seed(seed, kStreamBreakpoints));
-    DevBuf<uint32_t> d_idx(n_s);
-    DevBuf<float> d_sample(static_cast<size_t>(K) * n_s);
-    float* h_sample = nullptr;
-    DETLSH_CUDA(cudaMallocHost(&h_sample, static_cast<size_t>(K) * n_s * sizeof(float)));
-    std::unique_ptr<float, decltype(&cudaFreeHost)> guard(h_sample, &cudaFreeHost);
-    X.h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
-    for (int i = 0; i < L; ++i) {
-        const auto& idx = sampler.next_space_indices();
-        DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), idx.data(), n_s * 4, cudaMemcpyHostToDevice, X.stream));
-        launch_gather_sample(d_proj + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
-                             d_sample.get(), X.stream);
-        DETLSH_CUDA(cudaMemcpyAsync(h_sample, d_sample.get(), static_cast<size_t>(K) * n_s * 4,
-                                    cudaMemcpyDeviceToHost, X.stream));
-        DETLSH_CUDA(cudaStreamSynchronize(X.stream));
-        for (int j = 0; j < K; ++j)
-            sampler.select_row(h_sample + static_cast<size_t>(j) * n_s,
-                               X.h_table.data() + (static_cast<size_t>(i) * K + j) * W);
-    }
-    DETLSH_CUDA(cudaMemcpyAsync(X.table.get(), X.h_table.data(), X.h_table.size() * 4,
-                                cudaMemcpyHostToDevice, X.stream));
-}
-
-// GPU-native sample: per-space Feistel sample + exact order statistics.
-void breakpoints_gpu(GpuIndex& X, const float* d_proj, uint64_t seed) {
-    const int K = X.params.K, L = X.params.L, NR = X.params.n_regions;
-    const uint64_t n = X.n, n_s = X.sample_size;
-    DevBuf<uint32_t> d_idx(n_s);
-    DevBuf<float> rows(static_cast<size_t>(L) * K * n_s);
-    const uint64_t bseed = mix_seed(seed, kStreamBreakpoints);
-    for (int i = 0; i < L; ++i) {
-        launch_feistel_sample(n, n_s, mix_seed(bseed, static_cast<uint64_t>(i)), d_idx.get(), X.stream);
-        launch_gather_sample(d_proj + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
-                             rows.get() + static_cast<size_t>(i) * K * n_s, X.stream);
-    }
-    gpu_order_stat_table(rows.get(), L * K, n_s, NR, X.table.get(), X.stream);
-    X.h_table.resize(static_cast<size_t>(L) * K * (NR + 1));
-    DETLSH_CUDA(cudaMemcpyAsync(X.h_table.data(), X.table.get(), X.h_table.size() * 4,
-                                cudaMemcpyDeviceToHost, X.stream));
-}
-
-// r_min (index.cpp:75-136, 153-175) via per-probe order statistics.
-double estimate_rmin_gpu(GpuIndex& X, const float* d_proj, uint64_t seed) {
-    const int K = X.params.K, L = X.params.L;
-    const uint64_t n = X.n;
-    Rng rng(mix_seed(seed, kStreamProbes));
-    const int np = static_cast<int>(std::min<uint64_t>(10, n));
-    std::vector<uint64_t> pos(np);
-    for (int p = 0; p < np; ++p) pos[p] = rng.bounded(n);
-    DevBuf<float> probe(static_cast<size_t>(np) * L * K);
-    for (int p = 0; p < np; ++p)
-        for (int i = 0; i < L; ++i)
-            DETLSH_CUDA(cudaMemcpyAsync(probe.get() + (static_cast<size_t>(p) * L + i) * K,
-                                        d_proj + (static_cast<size_t>(i) * n + pos[p]) * K,
-                                        K * sizeof(float), cudaMemcpyDeviceToDevice, X.stream));
-    // initial guess: median pairwise distance of 32 strided points (space 0)
-    const uint64_t m = std::min<uint64_t>(32, n);
-    std::vector<float> sc(m * K);
-    for (uint64_t t = 0; t < m; ++t)
-        DETLSH_CUDA(cudaMemcpyAsync(sc.data() + t * K, d_proj + (t * n / m) * K, K * sizeof(float),
-                                    cudaMemcpyDeviceToHost, X.stream));
-    const uint64_t budget = candidate_budget(X.params.beta, n, X.params.k);
-    DevBuf<double> D(static_cast<size_t>(np) * n);
-    DevBuf<uint32_t> hist(static_cast<size_t>(np) * 65536);
-    std::vector<uint64_t> Tbits(np);
-    rmin_order_stats(d_proj, n, K, L, probe.get(), np, budget, D.get(), hist.get(), Tbits.data(),
-                     X.stream);
-    std::vector<double> pd;
-    pd.reserve(m * (m - 1) / 2);
-    for (uint64_t a = 0; a < m; ++a)
-        for (uint64_t b = a + 1; b < m; ++b) {
-            double acc = 0.0;
-            for (int j = 0; j < K; ++j) {
-                const double diff = static_cast<double>(sc[a * K + j]) - static_cast<double>(sc[b * K + j]);
-                acc += diff * diff;
-            }
-            pd.push_back(std::sqrt(acc));
-        }
-    double guess = 1.0;
-    if (!pd.empty()) {
-        std::nth_element(pd.begin(), pd.begin() + pd.size() / 2, pd.end());
-        const double med = pd[pd.size() / 2];
-        if (med > 0.0) guess = med / X.params.epsilon;
-    }
-    std::vector<double> T(np);
-    for (int p = 0; p < np; ++p) std::memcpy(&T[p], &Tbits[p], 8);
-    return rmin_from_order_stats(T, guess, X.params.epsilon, X.params.c);
-}
-
-std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int d,
-                                           detlsh_params* params, const float* coeffs_host,
-                                           uint64_t family_seed, uint64_t seed, int device,
-                                           uint32_t flags) {
-    if (!params) throw InvalidArgument("build_index: params is null");
-    if (!points) throw InvalidArgument("build_index: points is null");
-    validate(*params, n, d);
-    DeviceGuard dg(device);
-    auto X = std::make_unique<GpuIndex>();
-    X->device = device;
-    X->n = n;
-    X->d = d;
-    X->sample_gpu = (flags & DETLSH_F_SAMPLE_GPU) != 0;
-    DETLSH_CUDA(cudaStreamCreateWithFlags(&X->stream, cudaStreamNonBlocking));
-    cudaStream_t s = X->stream;
-    detlsh_params p = *params;
-    const auto t_all = Clock::now();
-    auto t0 = Clock::now();
-    // derived parameters (index.cpp:202-206)
-    const Derived der = derive_params(p.K, p.c, p.L);
-    p.alpha1 = der.alpha1;
-    p.alpha2 = der.alpha2;
-    p.epsilon = der.epsilon;
-    if (p.beta <= 0.0) p.beta = der.beta;
-    X->params = p;
-    const int K = p.K, L = p.L, NR = p.n_regions;
-    const int LK = K * L;
-    // hash family (projection.cpp:11-23), host, seeded stream 0
-    X->h_coeffs.resize(static_cast<size_t>(LK) * d);
-    if (coeffs_host) {
-        std::memcpy(X->h_coeffs.data(), coeffs_host, X->h_coeffs.size() * sizeof(float));
-        X->family_seed = family_seed;
-    } else {
-        X->family_seed = mix_seed(seed, kStreamFamily);
-        sample_hash_family(d, K, L, X->family_seed, X->h_coeffs.data());
-    }
-    X->timings.emplace_back("host_params_family", ms_since(t0));
-    t0 = Clock::now();
-    // dataset
-    if (flags & DETLSH_F_DEVICE_PTRS) {
-        if (flags & DETLSH_F_BORROW_DATA) {
-            X->data = points;
-        } else {
-            X->data_buf.alloc(n * static_cast<size_t>(d));
-            DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
-                                        cudaMemcpyDeviceToDevice, s));
-            X->data = X->data_buf.get();
-        }
-    } else {
-        X->data_buf.alloc(n * static_cast<size_t>(d));
-        DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
-                                    cudaMemcpyHostToDevice, s));
-        X->data = X->data_buf.get();
-    }
-    X->coeffs.alloc(X->h_coeffs.size());
-    DETLSH_CUDA(cudaMemcpyAsync(X->coeffs.get(), X->h_coeffs.data(), X->h_coeffs.size() * 4,
-                                cudaMemcpyHostToDevice, s));
-    X->coeffs_t.alloc(static_cast<size_t>(lk_padded(LK)) * d);
-    prepare_coeffs_t(X->coeffs.get(), LK, d, X->coeffs_t.get(), s);
-    DETLSH_CUDA(cudaStreamSynchronize(s));
-    X->timings.emplace_back("upload", ms_since(t0));
-    // projection (exact)
-    t0 = Clock::now();
-    DevBuf<float> proj(static_cast<size_t>(L) * n * K);
-    launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s);
-    DETLSH_CUDA(cudaStreamSynchronize(s));
-    X->timings.emplace_back("project", ms_since(t0));
-    // breakpoints
-    t0 = Clock::now();
-    X->sample_size = sample_size_for(p.sample_fraction, n, NR);
-    X->table.alloc(static_cast<size_t>(L) * K * (NR + 1));
-    if (X->sample_gpu) breakpoints_gpu(*X, proj.get(), seed);
-    else breakpoints_ref(*X, proj.get(), seed);
-    DETLSH_CUDA(cudaStreamSynchronize(s));
-    X->timings.emplace_back("breakpoints", ms_since(t0));
-    // encode
-    t0 = Clock::now();
-    X->codes.alloc(static_cast<size_t>(L) * n * K);
-    launch_encode(proj.get(), n, K, L, X->table.get(), NR, X->codes.get(), s);
-    DETLSH_CUDA(cudaStreamSynchronize(s));
-    X->timings.emplace_back("encode", ms_since(t0));
-    // trees
-    t0 = Clock::now();
-    std::vector<QTree> qt(L);
-    for (int i = 0; i < L; ++i) {
-        auto T = std::make_unique<DevTree>();
-        build_tree_gpu(X->codes.get() + static_cast<size_t>(i) * n * K, n, K, NR, i,
-                       p.leaf_capacity, *T, s);
-        qt[i] = QTree{T->leaf_node.get(), T->leaf_begin.get(), T->leaf_count.get(),
-                      T->leaf_box.get(), T->perm.get(), static_cast<uint32_t>(T->num_leaves)};
-        X->max_leaves = std::max<uint32_t>(X->max_leaves, static_cast<uint32_t>(T->num_leaves));
-        X->trees.push_back(std::move(T));
-    }
-    X->qtrees.alloc(L);
-    DETLSH_CUDA(cudaMemcpyAsync(X->qtrees.get(), qt.data(), L * sizeof(QTree), cudaMemcpyHostToDevice, s));
-    DETLSH_CUDA(cudaStreamSynchronize(s));
-    X->timings.emplace_back("trees", ms_since(t0));
-    // r_min
-    t0 = Clock::now();
-    if (X->params.r_min <= 0.0) X->params.r_min = estimate_rmin_gpu(*X, proj.get(), seed);
-    X->timings.emplace_back("rmin", ms_since(t0));
-    if (flags & DETLSH_F_NO_CODES) X->codes.release();
-    X->timings.emplace_back("total", ms_since(t_all));
-    *params = X->params;
-    return X;
-}
-
-void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t flags,
-                uint32_t* ids, double* dists, int32_t* n_hits, double* radius, uint64_t* cands,
-                cudaStream_t user_stream) {
-    if (k < 1 || static_cast<uint64_t>(k) > X.n) throw InvalidArgument("ck_ann: k must lie in [1, n]");
-    if (!(X.params.r_min > 0.0)) throw InvalidArgument("ck_ann: index has no initial radius");
-    if (nq == 0) return;
-    if (!queries) throw InvalidArgument("ck_ann: queries is null");
-    DeviceGuard dg(X.device);
-    std::lock_guard<std::mutex> lock(X.qmu);
-    cudaStream_t s = user_stream ? user_stream : X.stream;
-    const bool dev = (flags & DETLSH_F_DEVICE_PTRS) != 0;
-    const int K = X.params.K, L = X.params.L, d = X.d;
-    DevBuf<float> dq;
-    const float* q = queries;
-    if (!dev) {
-        dq.alloc(nq * static_cast<size_t>(d));
-        DETLSH_CUDA(cudaMemcpyAsync(dq.get(), queries, nq * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s));
-        q = dq.get();
-    }
-    DevBuf<float> qproj(static_cast<size_t>(L) * nq * K);
-    launch_project_exact(q, nq, d, X.coeffs_t.get(), K, L, qproj.get(), s);
-    DevBuf<uint32_t> o_ids;
-    DevBuf<double> o_d, o_r;
-    DevBuf<int32_t> o_h;
-    DevBuf<uint64_t> o_c;
-    QueryPlan P{};
-    P.data = X.data;
-    P.n = X.n;
-    P.d = d;
-    P.K = K;
-    P.L = L;
-    P.NR = X.params.n_regions;
-    P.table = X.table.get();
-    P.trees = X.qtrees.get();
-    P.eps = X.params.epsilon;
-    P.c = X.params.c;
-    P.r_min = X.params.r_min;
-    P.budget = candidate_budget(X.params.beta, X.n, k);
-    P.k = k;
-    P.max_leaves = X.max_leaves;
-    P.q = q;
-    P.qproj = qproj.get();
-    P.nq = nq;
-    if (dev) {
-        P.ids = ids;
-        P.dists = dists;
-        P.n_hits = n_hits;
-        P.radius = radius;
-        P.cands = cands;
-    } else {
-        if (ids) { o_ids.alloc(nq * k); P.ids = o_ids.get(); }
-        if (dists) { o_d.alloc(nq * k); P.dists = o_d.get(); }
-        if (n_hits) { o_h.alloc(nq); P.n_hits = o_h.get(); }
-        if (radius) { o_r.alloc(nq); P.radius = o_r.get(); }
-        if (cands) { o_c.alloc(nq); P.cands = o_c.get(); }
-    }
-    run_query_batch(P, X.scratch, X.device, s);
-    if (!dev) {
-        if (ids) DETLSH_CUDA(cudaMemcpyAsync(ids, P.ids, nq * k * 4, cudaMemcpyDeviceToHost, s));
-        if (dists) DETLSH_CUDA(cudaMemcpyAsync(dists, P.dists, nq * k * 8, cudaMemcpyDeviceToHost, s));
-        if (n_hits) DETLSH_CUDA(cudaMemcpyAsync(n_hits, P.n_hits, nq * 4, cudaMemcpyDeviceToHost, s));
-        if (radius) DETLSH_CUDA(cudaMemcpyAsync(radius, P.radius, nq * 8, cudaMemcpyDeviceToHost, s));
-        if (cands) DETLSH_CUDA(cudaMemcpyAsync(cands, P.cands, nq * 8, cudaMemcpyDeviceToHost, s));
-    }
-    // temporaries (query copy, projections, outputs) are freed on return
-    DETLSH_CUDA(cudaStreamSynchronize(s));
-}
 
 template <typename F>
 int guarded(F&& f) {
@@ -456,6 +112,20 @@ double detlsh_chi2_quantile(double a, int32_t k) {
     } catch (...) {
         return NAN;
     }
+}
+
+int detlsh_select_row_breakpoints(float* sample, uint64_t n_s, int32_t n_regions,
+                                  uint64_t rng_seed, float* row, uint64_t* draws) {
+    return guarded([&] {
+        if (!is_pow2(n_regions) || n_regions < 2)
+            throw InvalidArgument("select_row_breakpoints: n_regions must be a power of two >= 2");
+        if (n_s < static_cast<uint64_t>(n_regions))
+            throw InvalidArgument("select_row_breakpoints: sample smaller than region count");
+        Rng rng(rng_seed);
+        uint64_t nd = 0;
+        select_row_breakpoints(sample, n_s, n_regions, rng, row, &nd);
+        if (draws) *draws = nd;
+    });
 }
 
 uint64_t detlsh_launch_count(void) { return launch_count(); }
@@ -656,62 +326,59 @@ int detlsh_gpu_select_breakpoints(const float* projected, uint64_t n, int32_t K,
             throw InvalidArgument("select_breakpoints: sample_fraction must lie in (0, 1]");
         if (K < 1 || L < 1 || n == 0) throw InvalidArgument("select_breakpoints: bad shape");
         DeviceGuard dg(device);
+        ensure_mempool(device);
         const bool dev = flags & DETLSH_F_DEVICE_PTRS;
-        GpuIndex X;
-        X.device = device;
-        X.n = n;
-        X.params.K = K;
-        X.params.L = L;
-        X.params.n_regions = n_regions;
-        X.sample_gpu = flags & DETLSH_F_SAMPLE_GPU;
-        X.sample_size = sample_size_for(sample_fraction, n, n_regions);
-        DETLSH_CUDA(cudaStreamCreateWithFlags(&X.stream, cudaStreamNonBlocking));
+        const uint64_t n_s = sample_size_for(sample_fraction, n, n_regions);
+        OwnedStream os;  // declared before the buffers freed on it
+        os.create();
+        cudaStream_t st = os.s;
+        StreamScope sc(st);
         DevBuf<float> pr;
         const float* P = projected;
         const size_t total = static_cast<size_t>(L) * n * K;
         if (!dev) {
             pr.alloc(total);
-            to_device(pr.get(), projected, total * 4, false, X.stream);
+            to_device(pr.get(), projected, total * 4, false, st);
             P = pr.get();
         }
-        X.table.alloc(static_cast<size_t>(L) * K * (n_regions + 1));
+        const size_t W = static_cast<size_t>(n_regions) + 1;
+        DevBuf<float> d_table(static_cast<size_t>(L) * K * W);
         // `seed` is select_breakpoints' own seed argument (index.cpp passes
         // mix_seed(seed, 1)); the GPU-native mode derives one key per space.
-        if (X.sample_gpu) {
-            DevBuf<uint32_t> d_idx(X.sample_size);
-            DevBuf<float> rows(static_cast<size_t>(L) * K * X.sample_size);
+        if (flags & DETLSH_F_SAMPLE_GPU) {
+            DevBuf<uint32_t> d_idx(n_s);
+            DevBuf<float> rows(static_cast<size_t>(L) * K * n_s);
             for (int i = 0; i < L; ++i) {
-                launch_feistel_sample(n, X.sample_size, mix_seed(seed, static_cast<uint64_t>(i)),
-                                      d_idx.get(), X.stream);
-                launch_gather_sample(P + static_cast<size_t>(i) * n * K, d_idx.get(), X.sample_size,
-                                     K, rows.get() + static_cast<size_t>(i) * K * X.sample_size, X.stream);
+                launch_feistel_sample(n, n_s, mix_seed(seed, static_cast<uint64_t>(i)), d_idx.get(), st);
+                launch_gather_sample(P + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
+                                     rows.get() + static_cast<size_t>(i) * K * n_s, st);
             }
-            gpu_order_stat_table(rows.get(), L * K, X.sample_size, n_regions, X.table.get(), X.stream);
+            gpu_order_stat_table(rows.get(), L * K, n_s, n_regions, d_table.get(), st);
         } else {
-            const size_t W = static_cast<size_t>(n_regions) + 1;
-            RefSampler sampler(n, X.sample_size, n_regions, seed);
-            DevBuf<uint32_t> d_idx(X.sample_size);
-            DevBuf<float> d_sample(static_cast<size_t>(K) * X.sample_size);
-            std::vector<float> h_sample(static_cast<size_t>(K) * X.sample_size);
-            X.h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
+            RefSampler sampler(n, n_s, n_regions, seed);
+            DevBuf<uint32_t> d_idx(n_s);
+            DevBuf<float> d_sample(static_cast<size_t>(K) * n_s);
+            std::vector<float> h_sample(static_cast<size_t>(K) * n_s);
+            std::vector<float> h_table(static_cast<size_t>(L) * K * W, 0.0f);
             for (int i = 0; i < L; ++i) {
                 const auto& idx = sampler.next_space_indices();
-                DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), idx.data(), X.sample_size * 4, cudaMemcpyHostToDevice, X.stream));
-                launch_gather_sample(P + static_cast<size_t>(i) * n * K, d_idx.get(), X.sample_size, K,
-                                     d_sample.get(), X.stream);
+                DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), idx.data(), n_s * 4, cudaMemcpyHostToDevice, st));
+                launch_gather_sample(P + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
+                                     d_sample.get(), st);
                 DETLSH_CUDA(cudaMemcpyAsync(h_sample.data(), d_sample.get(), h_sample.size() * 4,
-                                            cudaMemcpyDeviceToHost, X.stream));
-                DETLSH_CUDA(cudaStreamSynchronize(X.stream));
+                                            cudaMemcpyDeviceToHost, st));
+                DETLSH_CUDA(cudaStreamSynchronize(st));
                 for (int j = 0; j < K; ++j)
-                    sampler.select_row(h_sample.data() + static_cast<size_t>(j) * X.sample_size,
-                                       X.h_table.data() + (static_cast<size_t>(i) * K + j) * W);
+                    sampler.select_row(h_sample.data() + static_cast<size_t>(j) * n_s,
+                                       h_table.data() + (static_cast<size_t>(i) * K + j) * W);
             }
-            DETLSH_CUDA(cudaMemcpyAsync(X.table.get(), X.h_table.data(), X.h_table.size() * 4,
-                                        cudaMemcpyHostToDevice, X.stream));
+            DETLSH_CUDA(cudaMemcpyAsync(d_table.get(), h_table.data(), h_table.size() * 4,
+                                        cudaMemcpyHostToDevice, st));
+            DETLSH_CUDA(cudaStreamSynchronize(st));
         }
-        from_device(table, X.table.get(), X.table.bytes(), dev, X.stream);
-        DETLSH_CUDA(cudaStreamSynchronize(X.stream));
-        if (sample_size) *sample_size = X.sample_size;
+        from_device(table, d_table.get(), d_table.bytes(), dev, st);
+        DETLSH_CUDA(cudaStreamSynchronize(st));
+        if (sample_size) *sample_size = n_s;
     });
 }
 

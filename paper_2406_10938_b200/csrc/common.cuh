@@ -38,7 +38,22 @@ struct CudaError : std::runtime_error {
 constexpr int kMaxK = 24;      // validate_params: K in [1, 24] (index.cpp:17)
 constexpr int kMaxRegions = 256;
 
-// Owning device buffer (cudaMalloc / cudaFree), movable.
+// Stream-ordered allocation.  Every DevBuf is allocated (cudaMallocAsync) and
+// freed (cudaFreeAsync) on the stream that is current for its thread when it
+// is allocated — set with StreamScope by every host function that launches
+// work — so buffers never need a device-wide cudaFree sync and concurrent
+// builds on several streams do not serialise.  The device's default memory
+// pool keeps freed blocks cached (release threshold raised at first use).
+cudaStream_t& alloc_stream();
+void ensure_mempool(int device);
+
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+    ~StreamScope() { alloc_stream() = prev; }
+};
+
+// Owning device buffer, movable.
 template <typename T>
 class DevBuf {
 public:
@@ -47,7 +62,7 @@ public:
     ~DevBuf() { release(); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) {
         o.p_ = nullptr;
         o.n_ = 0;
     }
@@ -56,6 +71,7 @@ public:
             release();
             p_ = o.p_;
             n_ = o.n_;
+            s_ = o.s_;
             o.p_ = nullptr;
             o.n_ = 0;
         }
@@ -63,22 +79,23 @@ public:
     }
     void alloc(size_t count) {
         release();
-        if (count) DETLSH_CUDA(cudaMalloc(&p_, count * sizeof(T)));
+        s_ = alloc_stream();
+        if (count) DETLSH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), count * sizeof(T), s_));
         n_ = count;
     }
-    // grow-only reallocation that keeps the first `keep` elements
+    // grow-only reallocation that keeps the first `keep` elements (stream-ordered)
     void grow(size_t count, size_t keep, cudaStream_t s) {
         if (count <= n_) return;
         T* np = nullptr;
-        DETLSH_CUDA(cudaMalloc(&np, count * sizeof(T)));
+        DETLSH_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&np), count * sizeof(T), s));
         if (keep && p_) DETLSH_CUDA(cudaMemcpyAsync(np, p_, keep * sizeof(T), cudaMemcpyDeviceToDevice, s));
-        DETLSH_CUDA(cudaStreamSynchronize(s));
-        release();
+        if (p_) cudaFreeAsync(p_, s);
         p_ = np;
         n_ = count;
+        s_ = s;
     }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) cudaFreeAsync(p_, s_);
         p_ = nullptr;
         n_ = 0;
     }
@@ -89,6 +106,25 @@ public:
 private:
     T* p_ = nullptr;
     size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+// Owned stream, synchronised and destroyed last (declare before the buffers
+// that are freed on it).
+struct OwnedStream {
+    cudaStream_t s = nullptr;
+    OwnedStream() = default;
+    OwnedStream(const OwnedStream&) = delete;
+    OwnedStream& operator=(const OwnedStream&) = delete;
+    void create() {
+        if (!s) DETLSH_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    }
+    ~OwnedStream() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
 };
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }

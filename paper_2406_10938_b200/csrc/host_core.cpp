@@ -139,6 +139,84 @@ void sample_hash_family(int d, int K, int L, uint64_t seed, float* out) {
 // ---- breakpoint replay (encoder.cpp:14-103) ---------------------------------
 namespace {
 
+// The sentinel scan-and-swap loop of partition_around (encoder.cpp:41-52):
+// a[lo+1] == pivot bounds the right scan, a[hi-1] >= pivot the left scan.
+size_t hoare_scan_simple(float* a, size_t lo, size_t hi, float pv) {
+    size_t i = lo + 1, j = hi - 1;
+    for (;;) {
+        while (a[++i] < pv) {
+        }
+        while (a[--j] > pv) {
+        }
+        if (i >= j) break;
+        std::swap(a[i], a[j]);
+    }
+    return j;
+}
+
+// The same loop, branch-light.  Hoare swaps the k-th left stopper (a >= pv,
+// ascending) with the k-th right stopper (a <= pv, descending) while they are
+// ordered; every position strictly between the current i and j still holds
+// its original value, so stoppers can be collected ahead of time in blocks
+// (cmov-style appends, no data-dependent branch per element).  Crossing rule,
+// derived from the sentinel loop: i' = next left stopper below j, else j;
+// j' = next right stopper at or above i', else i' - 1; stop when i' >= j'.
+// Buffered stoppers that fell outside (i, j) by the time they are consumed
+// are exactly the positions the sentinel loop would have crossed.
+size_t hoare_scan_blocked(float* a, size_t lo, size_t hi, float pv) {
+    constexpr int64_t B = 64;
+    int64_t lb[B], rb[B];
+    int ln = 0, lh = 0, rn = 0, rh = 0;
+    int64_t i = static_cast<int64_t>(lo) + 1, j = static_cast<int64_t>(hi) - 1;
+    int64_t lgen = i + 1, rgen = j - 1;
+    for (;;) {
+        int64_t in;
+        for (;;) {  // next left stopper in (i, j)
+            if (lh < ln) {
+                in = lb[lh++];
+                if (in >= j) in = j;
+                break;
+            }
+            if (lgen >= j) {
+                in = j;
+                break;
+            }
+            const int64_t end = std::min(lgen + B, j);
+            ln = 0;
+            lh = 0;
+            for (int64_t x = lgen; x < end; ++x) {
+                lb[ln] = x;
+                ln += a[x] >= pv;
+            }
+            lgen = end;
+        }
+        int64_t jn;
+        for (;;) {  // next right stopper in [in, j)
+            if (rh < rn) {
+                jn = rb[rh++];
+                if (jn < in) jn = in - 1;
+                break;
+            }
+            if (rgen < in) {
+                jn = in - 1;
+                break;
+            }
+            const int64_t end = std::max(rgen - B, in - 1);
+            rn = 0;
+            rh = 0;
+            for (int64_t y = rgen; y > end; --y) {
+                rb[rn] = y;
+                rn += a[y] <= pv;
+            }
+            rgen = end;
+        }
+        if (in >= jn) return static_cast<size_t>(jn);
+        std::swap(a[in], a[jn]);
+        i = in;
+        j = jn;
+    }
+}
+
 // Median-of-three around a seeded pick, sentinel Hoare scan; one bounded()
 // draw per call.  Returns the pivot's sorted position.
 size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
@@ -150,15 +228,7 @@ size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
     if (a[hi - 1] < a[mid]) std::swap(a[mid], a[hi - 1]);
     std::swap(a[mid], a[lo + 1]);
     const float pv = a[lo + 1];
-    size_t i = lo + 1, j = hi - 1;
-    for (;;) {
-        while (a[++i] < pv) {
-        }
-        while (a[--j] > pv) {
-        }
-        if (i >= j) break;
-        std::swap(a[i], a[j]);
-    }
+    const size_t j = len >= 32 ? hoare_scan_blocked(a, lo, hi, pv) : hoare_scan_simple(a, lo, hi, pv);
     std::swap(a[lo + 1], a[j]);
     return j;
 }

@@ -1,0 +1,399 @@
+// build_index (index.cpp:138-218) and batched ck_ann orchestration.
+//
+// Build pipeline (one index, one device):
+//   main stream : upload -> exact projection -> per space i: gather the sample,
+//                 host replay of the reference quickselects (RefSampler), upload
+//                 that space's boundary rows, record event e_i
+//   side[i]     : wait e_i -> encode space i -> DE-Tree i      (own host thread)
+//   side[L]     : r_min order statistics (needs projections only; own thread)
+// so the trees and r_min overlap the sequential host replay of later spaces.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <thread>
+
+#include "host_core.hpp"
+#include "index.cuh"
+#include "stages.cuh"
+
+namespace detlsh_b200 {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double ms_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// Runs fn on a host thread bound to `device`; the first exception is kept.
+class Worker {
+public:
+    template <typename F>
+    void run(int device, F fn) {
+        threads_.emplace_back([this, device, fn]() {
+            try {
+                DETLSH_CUDA(cudaSetDevice(device));
+                fn();
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!err_) err_ = std::current_exception();
+            }
+        });
+    }
+    void join() {
+        for (auto& t : threads_) t.join();
+        threads_.clear();
+        if (err_) std::rethrow_exception(err_);
+    }
+    ~Worker() {
+        for (auto& t : threads_)
+            if (t.joinable()) t.join();
+    }
+
+private:
+    std::vector<std::thread> threads_;
+    std::mutex mu_;
+    std::exception_ptr err_;
+};
+
+// GPU-native sample: per-space Feistel sample + exact order statistics.
+void breakpoints_gpu(GpuIndex& X, const float* d_proj, uint64_t seed, cudaStream_t s) {
+    const int K = X.params.K, L = X.params.L, NR = X.params.n_regions;
+    const uint64_t n = X.n, n_s = X.sample_size;
+    DevBuf<uint32_t> d_idx(n_s);
+    DevBuf<float> rows(static_cast<size_t>(L) * K * n_s);
+    const uint64_t bseed = mix_seed(seed, kStreamBreakpoints);
+    for (int i = 0; i < L; ++i) {
+        launch_feistel_sample(n, n_s, mix_seed(bseed, static_cast<uint64_t>(i)), d_idx.get(), s);
+        launch_gather_sample(d_proj + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
+                             rows.get() + static_cast<size_t>(i) * K * n_s, s);
+    }
+    gpu_order_stat_table(rows.get(), L * K, n_s, NR, X.table.get(), s);
+    X.h_table.resize(static_cast<size_t>(L) * K * (NR + 1));
+    DETLSH_CUDA(cudaMemcpyAsync(X.h_table.data(), X.table.get(), X.h_table.size() * 4,
+                                cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+}
+
+// r_min (index.cpp:75-136, 153-175) via per-probe order statistics.
+double estimate_rmin_gpu(GpuIndex& X, const float* d_proj, uint64_t seed, cudaStream_t s) {
+    StreamScope sc(s);
+    const int K = X.params.K, L = X.params.L;
+    const uint64_t n = X.n;
+    Rng rng(mix_seed(seed, kStreamProbes));
+    const int np = static_cast<int>(std::min<uint64_t>(10, n));
+    std::vector<uint64_t> pos(np);
+    for (int p = 0; p < np; ++p) pos[p] = rng.bounded(n);
+    DevBuf<float> probe(static_cast<size_t>(np) * L * K);
+    for (int p = 0; p < np; ++p)
+        for (int i = 0; i < L; ++i)
+            DETLSH_CUDA(cudaMemcpyAsync(probe.get() + (static_cast<size_t>(p) * L + i) * K,
+                                        d_proj + (static_cast<size_t>(i) * n + pos[p]) * K,
+                                        K * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    // initial guess: median pairwise distance of 32 strided points (space 0)
+    const uint64_t m = std::min<uint64_t>(32, n);
+    std::vector<float> sc_rows(m * K);
+    for (uint64_t t = 0; t < m; ++t)
+        DETLSH_CUDA(cudaMemcpyAsync(sc_rows.data() + t * K, d_proj + (t * n / m) * K,
+                                    K * sizeof(float), cudaMemcpyDeviceToHost, s));
+    const uint64_t budget = candidate_budget(X.params.beta, n, X.params.k);
+    DevBuf<double> D(static_cast<size_t>(np) * n);
+    DevBuf<uint32_t> hist(static_cast<size_t>(np) * 65536);
+    std::vector<uint64_t> Tbits(np);
+    rmin_order_stats(d_proj, n, K, L, probe.get(), np, budget, D.get(), hist.get(), Tbits.data(), s);
+    std::vector<double> pd;
+    pd.reserve(m * (m - 1) / 2);
+    for (uint64_t a = 0; a < m; ++a)
+        for (uint64_t b = a + 1; b < m; ++b) {
+            double acc = 0.0;
+            for (int j = 0; j < K; ++j) {
+                const double diff =
+                    static_cast<double>(sc_rows[a * K + j]) - static_cast<double>(sc_rows[b * K + j]);
+                acc += diff * diff;
+            }
+            pd.push_back(std::sqrt(acc));
+        }
+    double guess = 1.0;
+    if (!pd.empty()) {
+        std::nth_element(pd.begin(), pd.begin() + pd.size() / 2, pd.end());
+        const double med = pd[pd.size() / 2];
+        if (med > 0.0) guess = med / X.params.epsilon;
+    }
+    std::vector<double> T(np);
+    for (int p = 0; p < np; ++p) std::memcpy(&T[p], &Tbits[p], 8);
+    return rmin_from_order_stats(T, guess, X.params.epsilon, X.params.c);
+}
+
+}  // namespace
+
+DeviceGuard::DeviceGuard(int dev) {
+    DETLSH_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) DETLSH_CUDA(cudaSetDevice(dev));
+}
+DeviceGuard::~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+uint64_t sample_size_for(double frac, uint64_t n, int NR) {
+    uint64_t n_s = static_cast<uint64_t>(std::ceil(frac * static_cast<double>(n)));
+    n_s = std::max<uint64_t>(n_s, static_cast<uint64_t>(NR));
+    if (n_s > n) throw InvalidArgument("select_breakpoints: sample too small for region count");
+    return n_s;
+}
+
+void validate_params(const detlsh_params& p, uint64_t n, int d) {
+    // validate_params (index.cpp:16-24) + the stage preconditions build_index reaches
+    if (n == 0) throw InvalidArgument("build_index: empty dataset");
+    if (d < 1) throw InvalidArgument("build_index: d must be positive");
+    if (n > 0xffffffffULL) throw InvalidArgument("build_index: n must be < 2^32 (u32 positions)");
+    if (p.K < 1 || p.K > 24) throw InvalidArgument("build_index: K must lie in [1, 24]");
+    if (p.L < 1) throw InvalidArgument("build_index: L must be positive");
+    if (!(p.c > 1.0)) throw InvalidArgument("build_index: c must exceed 1");
+    if (p.leaf_capacity < 1) throw InvalidArgument("build_index: leaf_capacity must be positive");
+    if (!is_pow2(p.n_regions) || p.n_regions < 2 || p.n_regions > 256)
+        throw InvalidArgument("select_breakpoints: n_regions must be a power of two in [2, 256]");
+    if (!(p.sample_fraction > 0.0) || p.sample_fraction > 1.0)
+        throw InvalidArgument("select_breakpoints: sample_fraction must lie in (0, 1]");
+    sample_size_for(p.sample_fraction, n, p.n_regions);
+}
+
+std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int d,
+                                           detlsh_params* params, const float* coeffs_host,
+                                           uint64_t family_seed, uint64_t seed, int device,
+                                           uint32_t flags) {
+    if (!params) throw InvalidArgument("build_index: params is null");
+    if (!points) throw InvalidArgument("build_index: points is null");
+    validate_params(*params, n, d);
+    DeviceGuard dg(device);
+    ensure_mempool(device);
+    auto X = std::make_unique<GpuIndex>();
+    X->device = device;
+    X->n = n;
+    X->d = d;
+    X->sample_gpu = (flags & DETLSH_F_SAMPLE_GPU) != 0;
+    X->main.create();
+    cudaStream_t s = X->main.s;
+    StreamScope scope(s);
+    detlsh_params p = *params;
+    const auto t_all = Clock::now();
+    auto t0 = Clock::now();
+    // derived parameters (index.cpp:202-206)
+    const Derived der = derive_params(p.K, p.c, p.L);
+    p.alpha1 = der.alpha1;
+    p.alpha2 = der.alpha2;
+    p.epsilon = der.epsilon;
+    if (p.beta <= 0.0) p.beta = der.beta;
+    X->params = p;
+    const int K = p.K, L = p.L, NR = p.n_regions;
+    const int LK = K * L;
+    const size_t W = static_cast<size_t>(NR) + 1;
+    for (int i = 0; i <= L; ++i) {
+        X->side.push_back(std::make_unique<OwnedStream>());
+        X->side.back()->create();
+    }
+    // hash family (projection.cpp:11-23): host, seeded sub-stream 0
+    X->h_coeffs.resize(static_cast<size_t>(LK) * d);
+    if (coeffs_host) {
+        std::memcpy(X->h_coeffs.data(), coeffs_host, X->h_coeffs.size() * sizeof(float));
+        X->family_seed = family_seed;
+    } else {
+        X->family_seed = mix_seed(seed, kStreamFamily);
+        sample_hash_family(d, K, L, X->family_seed, X->h_coeffs.data());
+    }
+    X->timings.emplace_back("host_params_family", ms_since(t0));
+    t0 = Clock::now();
+    if ((flags & DETLSH_F_DEVICE_PTRS) && (flags & DETLSH_F_BORROW_DATA)) {
+        X->data = points;
+    } else {
+        X->data_buf.alloc(n * static_cast<size_t>(d));
+        DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
+                                    (flags & DETLSH_F_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice
+                                                                   : cudaMemcpyHostToDevice,
+                                    s));
+        X->data = X->data_buf.get();
+    }
+    X->coeffs.alloc(X->h_coeffs.size());
+    DETLSH_CUDA(cudaMemcpyAsync(X->coeffs.get(), X->h_coeffs.data(), X->h_coeffs.size() * 4,
+                                cudaMemcpyHostToDevice, s));
+    X->coeffs_t.alloc(static_cast<size_t>(lk_padded(LK)) * d);
+    prepare_coeffs_t(X->coeffs.get(), LK, d, X->coeffs_t.get(), s);
+    DevBuf<float> proj(static_cast<size_t>(L) * n * K);
+    X->sample_size = sample_size_for(p.sample_fraction, n, NR);
+    X->table.alloc(static_cast<size_t>(L) * K * W);
+    X->codes.alloc(static_cast<size_t>(L) * n * K);
+    X->trees.resize(L);
+    for (auto& t : X->trees) t = std::make_unique<DevTree>();
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    X->timings.emplace_back("upload", ms_since(t0));
+    // exact projection
+    t0 = Clock::now();
+    launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s);
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    X->timings.emplace_back("project", ms_since(t0));
+
+    Worker workers;
+    double rmin_ms = 0.0;
+    double r_min = X->params.r_min;
+    GpuIndex* Xp = X.get();
+    const float* d_proj = proj.get();
+    if (!(r_min > 0.0)) {
+        workers.run(device, [Xp, d_proj, seed, &r_min, &rmin_ms, L]() {
+            const auto ta = Clock::now();
+            r_min = estimate_rmin_gpu(*Xp, d_proj, seed, Xp->side[L]->s);
+            rmin_ms = ms_since(ta);
+        });
+    }
+    std::vector<cudaEvent_t> ready(L);
+    for (auto& e : ready) DETLSH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    struct EvGuard {
+        std::vector<cudaEvent_t>& v;
+        ~EvGuard() {
+            for (auto e : v) cudaEventDestroy(e);
+        }
+    } evg{ready};
+    const int cap = p.leaf_capacity;
+    auto launch_space = [&](int i) {
+        DETLSH_CUDA(cudaEventRecord(ready[i], s));
+        cudaEvent_t ev = ready[i];
+        workers.run(device, [Xp, d_proj, ev, i, n, K, NR, W, cap]() {
+            cudaStream_t ts = Xp->side[i]->s;
+            StreamScope sc(ts);
+            DETLSH_CUDA(cudaStreamWaitEvent(ts, ev, 0));
+            launch_encode(d_proj + static_cast<size_t>(i) * n * K, n, K, 1,
+                          Xp->table.get() + static_cast<size_t>(i) * K * W, NR,
+                          Xp->codes.get() + static_cast<size_t>(i) * n * K, ts);
+            build_tree_gpu(Xp->codes.get() + static_cast<size_t>(i) * n * K, n, K, NR, i, cap,
+                           *Xp->trees[i], ts);
+        });
+    };
+    // breakpoints
+    t0 = Clock::now();
+    if (X->sample_gpu) {
+        breakpoints_gpu(*X, d_proj, seed, s);
+        for (int i = 0; i < L; ++i) launch_space(i);
+    } else {
+        // reference-compatible sample: host replay of the shared RNG stream
+        // (encoder.cpp:105-143) on exact sample values gathered on the device
+        const uint64_t n_s = X->sample_size;
+        RefSampler sampler(n, n_s, NR, mix_seed(seed, kStreamBreakpoints));
+        DevBuf<uint32_t> d_idx(n_s);
+        DevBuf<float> d_sample(static_cast<size_t>(K) * n_s);
+        float* h_sample = nullptr;
+        DETLSH_CUDA(cudaMallocHost(&h_sample, static_cast<size_t>(K) * n_s * sizeof(float)));
+        std::unique_ptr<float, decltype(&cudaFreeHost)> hs_guard(h_sample, &cudaFreeHost);
+        X->h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
+        for (int i = 0; i < L; ++i) {
+            const auto& idx = sampler.next_space_indices();
+            DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), idx.data(), n_s * 4, cudaMemcpyHostToDevice, s));
+            launch_gather_sample(d_proj + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
+                                 d_sample.get(), s);
+            DETLSH_CUDA(cudaMemcpyAsync(h_sample, d_sample.get(), static_cast<size_t>(K) * n_s * 4,
+                                        cudaMemcpyDeviceToHost, s));
+            DETLSH_CUDA(cudaStreamSynchronize(s));
+            float* rows = X->h_table.data() + static_cast<size_t>(i) * K * W;
+            for (int j = 0; j < K; ++j)
+                sampler.select_row(h_sample + static_cast<size_t>(j) * n_s, rows + j * W);
+            DETLSH_CUDA(cudaMemcpyAsync(X->table.get() + static_cast<size_t>(i) * K * W, rows,
+                                        static_cast<size_t>(K) * W * 4, cudaMemcpyHostToDevice, s));
+            launch_space(i);
+        }
+    }
+    X->timings.emplace_back("breakpoints", ms_since(t0));
+    t0 = Clock::now();
+    workers.join();
+    X->timings.emplace_back("trees_rmin_tail", ms_since(t0));
+    double tree_ms = 0.0;
+    std::vector<QTree> qt(L);
+    for (int i = 0; i < L; ++i) {
+        const DevTree& T = *X->trees[i];
+        qt[i] = QTree{T.leaf_node.get(), T.leaf_begin.get(), T.leaf_count.get(), T.leaf_box.get(),
+                      T.perm.get(), static_cast<uint32_t>(T.num_leaves)};
+        X->max_leaves = std::max<uint32_t>(X->max_leaves, static_cast<uint32_t>(T.num_leaves));
+        tree_ms += T.build_ms;
+    }
+    X->qtrees.alloc(L);
+    DETLSH_CUDA(cudaMemcpyAsync(X->qtrees.get(), qt.data(), L * sizeof(QTree), cudaMemcpyHostToDevice, s));
+    X->params.r_min = r_min;
+    if (flags & DETLSH_F_NO_CODES) X->codes.release();
+    proj.release();
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    X->timings.emplace_back("trees_sum", tree_ms);
+    X->timings.emplace_back("rmin", rmin_ms);
+    X->timings.emplace_back("total", ms_since(t_all));
+    *params = X->params;
+    return X;
+}
+
+void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t flags,
+                uint32_t* ids, double* dists, int32_t* n_hits, double* radius, uint64_t* cands,
+                cudaStream_t user_stream) {
+    if (k < 1 || static_cast<uint64_t>(k) > X.n) throw InvalidArgument("ck_ann: k must lie in [1, n]");
+    if (!(X.params.r_min > 0.0)) throw InvalidArgument("ck_ann: index has no initial radius");
+    if (nq == 0) return;
+    if (!queries) throw InvalidArgument("ck_ann: queries is null");
+    DeviceGuard dg(X.device);
+    std::lock_guard<std::mutex> lock(X.qmu);
+    cudaStream_t s = user_stream ? user_stream : X.main.s;
+    StreamScope scope(s);
+    const bool dev = (flags & DETLSH_F_DEVICE_PTRS) != 0;
+    const int K = X.params.K, L = X.params.L, d = X.d;
+    DevBuf<float> dq;
+    const float* q = queries;
+    if (!dev) {
+        dq.alloc(nq * static_cast<size_t>(d));
+        DETLSH_CUDA(cudaMemcpyAsync(dq.get(), queries, nq * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s));
+        q = dq.get();
+    }
+    DevBuf<float> qproj(static_cast<size_t>(L) * nq * K);
+    launch_project_exact(q, nq, d, X.coeffs_t.get(), K, L, qproj.get(), s);
+    DevBuf<uint32_t> o_ids;
+    DevBuf<double> o_d, o_r;
+    DevBuf<int32_t> o_h;
+    DevBuf<uint64_t> o_c;
+    QueryPlan P{};
+    P.data = X.data;
+    P.n = X.n;
+    P.d = d;
+    P.K = K;
+    P.L = L;
+    P.NR = X.params.n_regions;
+    P.table = X.table.get();
+    P.trees = X.qtrees.get();
+    P.eps = X.params.epsilon;
+    P.c = X.params.c;
+    P.r_min = X.params.r_min;
+    P.budget = candidate_budget(X.params.beta, X.n, k);
+    P.k = k;
+    P.max_leaves = X.max_leaves;
+    P.q = q;
+    P.qproj = qproj.get();
+    P.nq = nq;
+    if (dev) {
+        P.ids = ids;
+        P.dists = dists;
+        P.n_hits = n_hits;
+        P.radius = radius;
+        P.cands = cands;
+    } else {
+        if (ids) { o_ids.alloc(nq * k); P.ids = o_ids.get(); }
+        if (dists) { o_d.alloc(nq * k); P.dists = o_d.get(); }
+        if (n_hits) { o_h.alloc(nq); P.n_hits = o_h.get(); }
+        if (radius) { o_r.alloc(nq); P.radius = o_r.get(); }
+        if (cands) { o_c.alloc(nq); P.cands = o_c.get(); }
+    }
+    run_query_batch(P, X.scratch, X.device, s, X.main.s);
+    if (!dev) {
+        if (ids) DETLSH_CUDA(cudaMemcpyAsync(ids, P.ids, nq * k * 4, cudaMemcpyDeviceToHost, s));
+        if (dists) DETLSH_CUDA(cudaMemcpyAsync(dists, P.dists, nq * k * 8, cudaMemcpyDeviceToHost, s));
+        if (n_hits) DETLSH_CUDA(cudaMemcpyAsync(n_hits, P.n_hits, nq * 4, cudaMemcpyDeviceToHost, s));
+        if (radius) DETLSH_CUDA(cudaMemcpyAsync(radius, P.radius, nq * 8, cudaMemcpyDeviceToHost, s));
+        if (cands) DETLSH_CUDA(cudaMemcpyAsync(cands, P.cands, nq * 8, cudaMemcpyDeviceToHost, s));
+    }
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace detlsh_b200

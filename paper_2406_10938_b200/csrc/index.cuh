@@ -1,0 +1,66 @@
+// The assembled GPU index (detlsh::DetIndex, index.hpp:24-37) and its
+// build / query orchestration.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/detlsh_b200.h"
+#include "common.cuh"
+#include "query.cuh"
+#include "tree.cuh"
+
+namespace detlsh_b200 {
+
+struct GpuIndex {
+    // streams first: members are destroyed in reverse order, so every buffer
+    // below is released (stream-ordered) before its stream goes away
+    OwnedStream main;
+    std::vector<std::unique_ptr<OwnedStream>> side;  // [0, L): trees, [L]: r_min
+    int device = 0;
+    detlsh_params params{};
+    uint64_t n = 0;
+    int d = 0;
+    uint64_t family_seed = 0, sample_size = 0;
+    bool sample_gpu = false;
+    const float* data = nullptr;  // device, [n][d]
+    DevBuf<float> data_buf;
+    std::vector<float> h_coeffs;  // [L][K][d]
+    DevBuf<float> coeffs;
+    DevBuf<double> coeffs_t;
+    DevBuf<float> table;
+    std::vector<float> h_table;
+    DevBuf<uint8_t> codes;
+    std::vector<std::unique_ptr<DevTree>> trees;
+    DevBuf<QTree> qtrees;
+    uint32_t max_leaves = 0;
+    QueryScratch scratch;
+    std::mutex qmu;
+    std::vector<std::pair<std::string, double>> timings;
+};
+
+std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int d,
+                                           detlsh_params* params, const float* coeffs_host,
+                                           uint64_t family_seed, uint64_t seed, int device,
+                                           uint32_t flags);
+
+void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t flags,
+                uint32_t* ids, double* dists, int32_t* n_hits, double* radius, uint64_t* cands,
+                cudaStream_t user_stream);
+
+void validate_params(const detlsh_params& p, uint64_t n, int d);
+uint64_t sample_size_for(double frac, uint64_t n, int NR);
+bool is_pow2(int v);
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev);
+    ~DeviceGuard();
+};
+
+}  // namespace detlsh_b200

@@ -696,14 +696,25 @@ __global__ void merge_topk_kernel(const double* __restrict__ sd, const uint64_t*
 
 }  // namespace
 
-void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream_t s) {
+void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream_t s,
+                     cudaStream_t alloc_s) {
     const int sms = sm_count(device);
     const size_t smem = smem_bytes(P.K, P.NR, P.d);
     if (smem > 220 * 1024) throw InvalidArgument("ck_ann: query dimension too large for the staging buffer");
     DETLSH_CUDA(cudaFuncSetAttribute(query_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (X.counters.size() < 4) X.counters.alloc(4);
-    if (X.slow_list.size() < P.nq) X.slow_list.alloc(P.nq);
+    // persistent scratch lives on the index's own stream (it outlives any
+    // caller stream); make it visible to `s` before use
+    auto grow_scratch = [&](auto& buf, size_t count) {
+        if (buf.size() >= count) return;
+        {
+            StreamScope sc(alloc_s);
+            buf.alloc(count);
+        }
+        DETLSH_CUDA(cudaStreamSynchronize(alloc_s));
+    };
+    grow_scratch(X.counters, 4);
+    grow_scratch(X.slow_list, P.nq);
     DETLSH_CUDA(cudaMemsetAsync(X.counters.get(), 0, 16, s));
     const size_t items = 3 * static_cast<size_t>(P.max_leaves) * sizeof(LeafItem);
     uint32_t slow_count = 0;
@@ -711,9 +722,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     if (P.k <= kFastMaxK) {
         const size_t fast_bytes = (items + 4 * static_cast<size_t>(P.max_leaves) + 4 * P.budget + 255) / 256 * 256;
         const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * 2);
-        if (X.fast.size() < slots * fast_bytes) {
-            X.fast.alloc(slots * fast_bytes);
-        }
+        grow_scratch(X.fast, slots * fast_bytes);
         ProfScope ps("query_fast", s);
         query_fast_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
             P, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
@@ -728,7 +737,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     const size_t slow_bytes = (items + 12 * P.budget + ((P.n + 31) / 32) * 4 + 255) / 256 * 256;
     const size_t slots = std::min<size_t>(slow_count, static_cast<size_t>(sms));
     if (X.slow_slots < slots || X.slow.size() < slots * slow_bytes) {
-        X.slow.alloc(slots * slow_bytes);
+        X.slow.release();
+        grow_scratch(X.slow, slots * slow_bytes);
         DETLSH_CUDA(cudaMemsetAsync(X.slow.get(), 0, slots * slow_bytes, s));
         X.slow_slots = slots;
     }

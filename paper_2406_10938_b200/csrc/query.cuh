@@ -56,7 +56,8 @@ struct QueryScratch {
     size_t fast_slots = 0, slow_slots = 0;
 };
 
-void run_query_batch(const QueryPlan& plan, QueryScratch& scratch, int device, cudaStream_t s);
+void run_query_batch(const QueryPlan& plan, QueryScratch& scratch, int device, cudaStream_t s,
+                     cudaStream_t alloc_s);
 
 // k-way merge of per-shard top-k lists: [shards][nq][k] -> [nq][k].
 void launch_merge_topk(const double* sd, const uint64_t* sid, const int32_t* sh, int shards,

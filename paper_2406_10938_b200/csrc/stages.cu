@@ -350,6 +350,7 @@ void launch_feistel_sample(uint64_t n, uint64_t n_s, uint64_t key, uint32_t* d_i
 
 void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_regions,
                           float* d_table, cudaStream_t s) {
+    StreamScope scope(s);
     const uint64_t total = static_cast<uint64_t>(R) * n_s;
     DevBuf<uint64_t> k0(total), k1(total);
     DevBuf<uint32_t> v0(total), v1(total), tmp(radix_temp_elems(total));
@@ -383,6 +384,7 @@ void launch_encode(const float* d_proj, uint64_t n, int K, int L, const float* d
 void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float* d_probe_proj,
                       int np, uint64_t rank, double* d_D, uint32_t* d_hist, uint64_t* h_T_bits,
                       cudaStream_t s) {
+    StreamScope scope(s);
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned gx = static_cast<unsigned>(

@@ -334,6 +334,7 @@ unsigned grid_for(uint64_t n, int threads = 256) {
 void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, int space,
                     int max_size, DevTree& T, cudaStream_t s) {
     const auto t0 = std::chrono::steady_clock::now();
+    StreamScope scope(s);
     if (max_size < 1) throw InvalidArgument("build_tree: max_size must be positive");
     if (K < 1 || K > kMaxK) throw InvalidArgument("build_tree: K must lie in [1, 24]");
     if (n_regions < 2 || (n_regions & (n_regions - 1)) || n_regions > kMaxRegions)
@@ -353,7 +354,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     DevBuf<uint32_t> k0(n), k1(n), v1(n), flags(n), ridx(n);
     T.perm.alloc(n);
     DevBuf<uint32_t> rtmp(std::max(radix_temp_elems(n), scan_temp_elems(n)));
-    ProfScope ps_sort("tree_slot_sort", s);
+    ProfScope ps_all("tree_build", s);
     slot_key_kernel<<<grid_for(n), 256, 0, s>>>(d_codes, n, K, sbits, k0.get(), T.perm.get());
     DETLSH_LAUNCH_CHECK();
     const bool flip = radix_sort_pairs<uint32_t>(k0.get(), T.perm.get(), k1.get(), v1.get(), n, 0,

@@ -59,3 +59,39 @@ def test_params_struct_layout_matches_header():
     # detlsh_params: int32 K, L; 5 doubles; int32; double; int32; double; int32
     assert ctypes.sizeof(D._lib.Params) == 88
     assert D._lib.Params.r_min.offset == 72
+
+
+def _select_row(sample, n_regions, seed):
+    s = np.array(sample, np.float32)
+    row = np.empty(n_regions + 1, np.float32)
+    dr = ctypes.c_uint64(0)
+    D._lib.check(D.load().detlsh_select_row_breakpoints(
+        ctypes.c_void_p(s.ctypes.data), len(s), n_regions, seed,
+        ctypes.c_void_p(row.ctypes.data), ctypes.byref(dr)))
+    return row, s, dr.value
+
+
+@pytest.mark.parametrize("trial", range(60))
+def test_host_replay_matches_oracle_partition_for_partition(port, trial):
+    """The blocked Hoare scan reproduces the reference's sentinel loop exactly:
+    same boundaries AND the same final arrangement (so the same later pivots)."""
+    g = np.random.Generator(np.random.PCG64(100 + trial))
+    n_regions = [2, 8, 16, 256][trial % 4]
+    n_s = int(n_regions + g.integers(0, [500, 5000, 60000][trial % 3]))
+    kind = trial % 5
+    if kind == 0:
+        s = g.normal(0, 1, n_s)
+    elif kind == 1:
+        s = g.integers(-3, 4, n_s)  # heavy duplicates
+    elif kind == 2:
+        s = np.sort(g.normal(0, 1, n_s))  # presorted
+    elif kind == 3:
+        s = np.full(n_s, 2.5)  # all equal
+    else:
+        s = np.sort(g.normal(0, 1, n_s))[::-1]  # reversed
+    s = s.astype(np.float32)
+    row, arr, draws = _select_row(s, n_regions, 77 + trial)
+    orow, oarr = port.select_row_breakpoints(s, n_regions, 77 + trial)
+    assert np.array_equal(row.view(np.uint32), orow.view(np.uint32))
+    assert np.array_equal(arr.view(np.uint32), oarr.view(np.uint32))
+    assert draws > 0 or n_s <= 8
