@@ -24,6 +24,7 @@ F_DEVICE_PTRS = 0x1
 F_SAMPLE_GPU = 0x2
 F_BORROW_DATA = 0x4
 F_NO_CODES = 0x8
+F_NO_U8 = 0x10
 
 
 class Params(C.Structure):

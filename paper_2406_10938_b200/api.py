@@ -26,7 +26,7 @@ from dataclasses import dataclass, field, fields
 import numpy as np
 
 from . import _lib
-from ._lib import F_BORROW_DATA, F_DEVICE_PTRS, F_NO_CODES, F_SAMPLE_GPU, Params, check
+from ._lib import F_BORROW_DATA, F_DEVICE_PTRS, F_NO_CODES, F_NO_U8, F_SAMPLE_GPU, Params, check
 
 SAMPLE_REFERENCE = "reference"
 SAMPLE_GPU = "gpu"
@@ -229,12 +229,12 @@ def _flags(sample: str) -> int:
 
 def build_index(data, params: LshParams | None = None, seed: int = 0, *, device: int = 0,
                 sample: str = SAMPLE_REFERENCE, borrow: bool = False,
-                keep_codes: bool = True) -> DetIndex:
+                keep_codes: bool = True, u8_rows: bool = True) -> DetIndex:
     """build_index (index.hpp:39).  `data` is an (n, d) float32 array or a CUDA tensor."""
     params = params or LshParams()
     cp = params.to_c()
     h = C.c_void_p()
-    flags = _flags(sample) | (0 if keep_codes else F_NO_CODES)
+    flags = _flags(sample) | (0 if keep_codes else F_NO_CODES) | (0 if u8_rows else F_NO_U8)
     if _is_cuda_tensor(data):
         t = data.contiguous()
         n, d = int(t.shape[0]), int(t.shape[1])

@@ -317,6 +317,18 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     }
     X->qtrees.alloc(L);
     DETLSH_CUDA(cudaMemcpyAsync(X->qtrees.get(), qt.data(), L * sizeof(QTree), cudaMemcpyHostToDevice, s));
+    // exact u8 verification rows, in tree-0 leaf order (query.cu)
+    t0 = Clock::now();
+    if (!(flags & DETLSH_F_NO_U8) && data_is_u8(X->data, n * static_cast<uint64_t>(d), s)) {
+        X->row_u8 = (d + 15) / 16 * 16;
+        const int chunks = X->row_u8 / 16;
+        int lpr = 1;
+        while (lpr < chunks && lpr < 32) lpr <<= 1;
+        X->u8_lpr = lpr;
+        X->data_u8.alloc(n * static_cast<size_t>(X->row_u8));
+        launch_pack_u8(X->data, X->trees[0]->perm.get(), n, d, X->row_u8, X->data_u8.get(), s);
+    }
+    X->timings.emplace_back("pack_u8", ms_since(t0));
     X->params.r_min = r_min;
     if (flags & DETLSH_F_NO_CODES) X->codes.release();
     proj.release();
@@ -363,6 +375,10 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     P.NR = X.params.n_regions;
     P.table = X.table.get();
     P.trees = X.qtrees.get();
+    P.perm0 = X.trees[0]->perm.get();
+    P.data_u8 = X.data_u8.get();
+    P.row_u8 = X.row_u8;
+    P.u8_lpr = X.u8_lpr;
     P.eps = X.params.epsilon;
     P.c = X.params.c;
     P.r_min = X.params.r_min;

@@ -36,6 +36,8 @@ struct GpuIndex {
     DevBuf<float> table;
     std::vector<float> h_table;
     DevBuf<uint8_t> codes;
+    DevBuf<uint8_t> data_u8;  // exact u8 rows in tree-0 leaf order (integral datasets)
+    int row_u8 = 0, u8_lpr = 0;
     std::vector<std::unique_ptr<DevTree>> trees;
     DevBuf<QTree> qtrees;
     uint32_t max_leaves = 0;

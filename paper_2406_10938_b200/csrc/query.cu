@@ -15,6 +15,14 @@
 // of its entries are taken: the emitted SET is identical, which is all the
 // top-k depends on.  Fast path (one CTA per query): tree 0, round 0, no dedup.
 // General path: bitmap dedup across trees and rounds, exact count_within.
+//
+// Exact verification, two data paths:
+//   * fp32 rows: sequential fp64 sum of (q_t - x_t)^2, one thread per row;
+//   * u8 rows (dataset and query integral in [0,255], detected at build /
+//     per query): int32 sum of squared byte differences (vabsdiffu4 + dp4a),
+//     rows stored in tree-0 leaf order so a leaf's candidates are contiguous.
+//     Every partial sum of the reference's double accumulation is then an
+//     exact integer < 2^53, so sqrt(double(int sum)) is bit-identical.
 #include <algorithm>
 
 #include "query.cuh"
@@ -22,6 +30,10 @@
 namespace detlsh_b200 {
 
 namespace {
+
+constexpr int kBatch = 1024;                    // candidates scored per block step
+constexpr int kTopCap = 2048;                   // staged (key, pos) entries
+static_assert(kFastMaxK == kTopCap - kBatch, "fast-path k bound");
 
 struct LeafItem {
     uint64_t mdb;  // mindist bits (non-negative double: bit order == value order)
@@ -35,57 +47,76 @@ __device__ __forceinline__ bool key_less(uint64_t am, uint32_t ai, uint64_t bm, 
     return am < bm || (am == bm && ai < bi);
 }
 
+// Shared memory: phase A (leaf scan) needs the penalty table, phase C (top-k)
+// the staging buffers; they share one region.
 struct Smem {
-    double* sq;       // [K][NR+1]
-    int* lbv;         // [K]  #{b : row[b] <  v}
-    int* ubv;         // [K]  #{b : row[b] <= v}
-    float* qv;        // [d]
-    float* qp;        // [K]
-    double* td;       // [kTopCap]
-    uint32_t* tp;     // [kTopCap]
+    double* sq;                // [K][NR+1]                       (phase A)
+    uint64_t* th;              // [kTopCap] top-k key hi           (phase C)
+    uint32_t* tl;              // [kTopCap] top-k key lo (position)
+    uint64_t* bh;              // [kBatch] batch key hi
+    uint32_t* bl;              // [kBatch] batch key lo
     unsigned long long* hist;  // [256]
-    unsigned long long* u64s;  // scratch scalars
+    unsigned long long* u64s;  // scalars
     uint32_t* u32s;
+    int* lbv;                  // [K]  #{b : row[b] <  v}
+    int* ubv;                  // [K]  #{b : row[b] <= v}
+    float* qp;                 // [K]
+    float* qv;                 // [d]
+    uint8_t* q8;               // [row_u8]
 };
 
-__device__ __forceinline__ Smem carve(uint8_t* base, int K, int NR, int d) {
-    Smem s;
+struct Carver {
+    uint8_t* base;
     size_t off = 0;
-    auto take = [&](size_t bytes, size_t align) {
+    __device__ uint8_t* take(size_t bytes, size_t align = 16) {
         off = (off + align - 1) / align * align;
         uint8_t* p = base + off;
         off += bytes;
         return p;
-    };
-    s.sq = reinterpret_cast<double*>(take(sizeof(double) * K * (NR + 1), 16));
-    s.td = reinterpret_cast<double*>(take(sizeof(double) * kTopCap, 16));
-    s.hist = reinterpret_cast<unsigned long long*>(take(8 * 256, 16));
-    s.u64s = reinterpret_cast<unsigned long long*>(take(8 * 16, 16));
-    s.tp = reinterpret_cast<uint32_t*>(take(4 * kTopCap, 16));
-    s.lbv = reinterpret_cast<int*>(take(4 * kMaxK, 16));
-    s.ubv = reinterpret_cast<int*>(take(4 * kMaxK, 16));
-    s.u32s = reinterpret_cast<uint32_t*>(take(4 * 16, 16));
-    s.qp = reinterpret_cast<float*>(take(4 * kMaxK, 16));
-    s.qv = reinterpret_cast<float*>(take(4 * static_cast<size_t>(d), 16));
+    }
+};
+
+__host__ __device__ inline size_t union_bytes(int K, int NR) {
+    const size_t a = sizeof(double) * K * (NR + 1);
+    const size_t c = (8 + 4) * static_cast<size_t>(kTopCap) + (8 + 4) * static_cast<size_t>(kBatch) + 64;
+    return (a > c ? a : c + 0) + 64;
+}
+
+__device__ __forceinline__ Smem carve(uint8_t* base, int K, int NR, int d, int row_u8) {
+    Carver c{base};
+    Smem s;
+    uint8_t* u = c.take(union_bytes(K, NR));
+    s.sq = reinterpret_cast<double*>(u);
+    s.th = reinterpret_cast<uint64_t*>(u);
+    s.bh = s.th + kTopCap;
+    s.tl = reinterpret_cast<uint32_t*>(s.bh + kBatch);
+    s.bl = s.tl + kTopCap;
+    s.hist = reinterpret_cast<unsigned long long*>(c.take(8 * 256));
+    s.u64s = reinterpret_cast<unsigned long long*>(c.take(8 * 16));
+    s.u32s = reinterpret_cast<uint32_t*>(c.take(4 * 16));
+    s.lbv = reinterpret_cast<int*>(c.take(4 * kMaxK));
+    s.ubv = reinterpret_cast<int*>(c.take(4 * kMaxK));
+    s.qp = reinterpret_cast<float*>(c.take(4 * kMaxK));
+    s.qv = reinterpret_cast<float*>(c.take(4 * static_cast<size_t>(d)));
+    s.q8 = c.take(static_cast<size_t>(row_u8) + 16);
     return s;
 }
 
-size_t smem_bytes(int K, int NR, int d) {
+size_t smem_bytes(int K, int NR, int d, int row_u8) {
     size_t off = 0;
-    auto take = [&](size_t bytes, size_t align) {
-        off = (off + align - 1) / align * align;
+    auto take = [&](size_t bytes) {
+        off = (off + 15) / 16 * 16;
         off += bytes;
     };
-    take(sizeof(double) * K * (NR + 1), 16);
-    take(sizeof(double) * kTopCap, 16);
-    take(8 * 256, 16);
-    take(8 * 16, 16);
-    take(4 * kTopCap, 16);
-    take(4 * kMaxK, 16);
-    take(4 * kMaxK, 16);
-    take(4 * 16, 16);
-    take(4 * kMaxK, 16);
-    take(4 * static_cast<size_t>(d), 16);
+    take(union_bytes(K, NR));
+    take(8 * 256);
+    take(8 * 16);
+    take(4 * 16);
+    take(4 * kMaxK);
+    take(4 * kMaxK);
+    take(4 * kMaxK);
+    take(4 * static_cast<size_t>(d));
+    take(static_cast<size_t>(row_u8) + 16);
     return off + 16;
 }
 
@@ -115,9 +146,9 @@ __device__ __forceinline__ double leaf_mindist(const QueryPlan& P, const QTree& 
                                                const Smem& S) {
     const uint8_t* box = T.leaf_box + static_cast<size_t>(li) * 64;
     uint4 raw[3];
-    raw[0] = reinterpret_cast<const uint4*>(box)[0];
-    raw[1] = reinterpret_cast<const uint4*>(box)[1];
-    if (P.K > 16) raw[2] = reinterpret_cast<const uint4*>(box)[2];
+    raw[0] = __ldg(reinterpret_cast<const uint4*>(box));
+    raw[1] = __ldg(reinterpret_cast<const uint4*>(box) + 1);
+    if (P.K > 16) raw[2] = __ldg(reinterpret_cast<const uint4*>(box) + 2);
     const uint8_t* b = reinterpret_cast<const uint8_t*>(raw);
     const int W = P.NR + 1;
     double acc = 0.0;
@@ -132,12 +163,13 @@ __device__ __forceinline__ double leaf_mindist(const QueryPlan& P, const QTree& 
     return __dsqrt_rn(acc);
 }
 
-// Exact original-space distance (dataset.hpp:23-34): sequential fp64 sum.
-__device__ __forceinline__ double l2_exact(const float* __restrict__ q, const float* __restrict__ x,
-                                           int d) {
+// Exact original-space squared distance (dataset.hpp:23-30): sequential fp64.
+__device__ __forceinline__ double l2sq_exact(const float* __restrict__ q, const float* __restrict__ x,
+                                             int d) {
     double acc = 0.0;
     if ((d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
         const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll 4
         for (int t = 0; t < d / 4; ++t) {
             const float4 xv = __ldg(x4 + t);
             const float* qq = q + 4 * t;
@@ -157,7 +189,11 @@ __device__ __forceinline__ double l2_exact(const float* __restrict__ q, const fl
             acc = __dadd_rn(acc, __dmul_rn(df, df));
         }
     }
-    return __dsqrt_rn(acc);
+    return acc;
+}
+
+__device__ __forceinline__ double l2_exact(const float* q, const float* x, int d) {
+    return __dsqrt_rn(l2sq_exact(q, x, d));
 }
 
 // Warp-aggregated append of `item` to list (counter in smem).
@@ -253,8 +289,7 @@ __device__ void weighted_select(LeafItem* A, uint32_t nA, uint64_t need, LeafIte
                 if (lane >= o) incl += t;
             }
             const unsigned long long excl = incl - part;
-            const bool here = excl < need && need <= incl;
-            if (here) {
+            if (excl < need && need <= incl) {
                 unsigned long long cum = excl;
                 int bin = lane * 8;
                 for (int b = 0; b < 8; ++b, ++bin) {
@@ -291,16 +326,14 @@ __device__ void weighted_select(LeafItem* A, uint32_t nA, uint64_t need, LeafIte
     __syncthreads();
 }
 
-// ---- block top-k over (dist, pos), ascending ---------------------------------
-__device__ __forceinline__ bool dp_less(double a, uint32_t ap, double b, uint32_t bp) {
-    return a < b || (a == b && ap < bp);
-}
-
+// ---- block top-k over (hi, lo) keys, ascending --------------------------------
+// hi = distance bits (non-negative double) or exact integer squared distance,
+// lo = dataset position: lexicographic order == the reference's (dist, pos).
 __device__ void topk_sort(const Smem& S) {
     const uint32_t cnt = S.u32s[4];
     for (uint32_t i = threadIdx.x + cnt; i < kTopCap; i += blockDim.x) {
-        S.td[i] = __longlong_as_double(0x7ff0000000000000LL);
-        S.tp[i] = 0xffffffffu;
+        S.th[i] = ~0ULL;
+        S.tl[i] = 0xffffffffu;
     }
     __syncthreads();
     for (int size = 2; size <= kTopCap; size <<= 1) {
@@ -309,13 +342,13 @@ __device__ void topk_sort(const Smem& S) {
                 const int lo = 2 * i - (i & (stride - 1));
                 const int hi = lo + stride;
                 const bool asc = (lo & size) == 0;
-                const double a = S.td[lo], b = S.td[hi];
-                const uint32_t ap = S.tp[lo], bp = S.tp[hi];
-                if (dp_less(b, bp, a, ap) == asc) {
-                    S.td[lo] = b;
-                    S.td[hi] = a;
-                    S.tp[lo] = bp;
-                    S.tp[hi] = ap;
+                const uint64_t a = S.th[lo], b = S.th[hi];
+                const uint32_t al = S.tl[lo], bl = S.tl[hi];
+                if (key_less(b, bl, a, al) == asc) {
+                    S.th[lo] = b;
+                    S.th[hi] = a;
+                    S.tl[lo] = bl;
+                    S.tl[hi] = al;
                 }
             }
             __syncthreads();
@@ -327,43 +360,53 @@ __device__ __forceinline__ void topk_init(const Smem& S) {
     if (threadIdx.x == 0) {
         S.u32s[4] = 0;  // count
         S.u32s[5] = 0;  // full
-        S.u32s[6] = 0;  // tau pos
-        S.u64s[2] = 0;  // tau dist bits
+        S.u32s[6] = 0;  // tau lo
+        S.u64s[2] = 0;  // tau hi
     }
     __syncthreads();
 }
 
-// Called by all threads; (valid, d, p) one candidate each.  Optional strict
-// lower bound (lbd, lbp) for chunked extraction of large k.
-__device__ void topk_push(const Smem& S, bool valid, double d, uint32_t p, int k) {
-    bool take = valid;
-    if (take && S.u32s[5]) {
-        const double td = __longlong_as_double(static_cast<long long>(S.u64s[2]));
-        take = dp_less(d, p, td, S.u32s[6]);
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, take);
-    if (m) {
-        const int lane = threadIdx.x & 31;
-        const int leader = __ffs(m) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(&S.u32s[4], static_cast<uint32_t>(__popc(m)));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (take) {
-            const uint32_t slot = base + __popc(m & ((1u << lane) - 1u));
-            S.td[slot] = d;
-            S.tp[slot] = p;
+// Stage the batch keys [0, nb) that beat the current k-th key; compact when
+// the staging area would overflow.  Called by all threads after the batch is
+// written (and synchronised).
+__device__ void topk_absorb(const Smem& S, uint32_t nb, int k) {
+    const bool full = S.u32s[5] != 0;
+    const uint64_t th = S.u64s[2];
+    const uint32_t tl = S.u32s[6];
+    const int lane = threadIdx.x & 31;
+    for (uint32_t base = 0; base < nb; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        bool take = false;
+        uint64_t h = 0;
+        uint32_t l = 0;
+        if (i < nb) {
+            h = S.bh[i];
+            l = S.bl[i];
+            take = !full || key_less(h, l, th, tl);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, take);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            uint32_t slot0 = 0;
+            if (lane == leader) slot0 = atomicAdd(&S.u32s[4], static_cast<uint32_t>(__popc(m)));
+            slot0 = __shfl_sync(0xffffffffu, slot0, leader);
+            if (take) {
+                const uint32_t slot = slot0 + __popc(m & ((1u << lane) - 1u));
+                S.th[slot] = h;
+                S.tl[slot] = l;
+            }
         }
     }
     __syncthreads();
-    if (S.u32s[4] > static_cast<uint32_t>(kTopCap - blockDim.x)) {
+    if (S.u32s[4] > static_cast<uint32_t>(kTopCap - kBatch)) {
         topk_sort(S);
         if (threadIdx.x == 0) {
             const uint32_t c = min(S.u32s[4], static_cast<uint32_t>(k));
             S.u32s[4] = c;
             if (c >= static_cast<uint32_t>(k)) {
                 S.u32s[5] = 1;
-                S.u64s[2] = static_cast<unsigned long long>(__double_as_longlong(S.td[k - 1]));
-                S.u32s[6] = S.tp[k - 1];
+                S.u64s[2] = S.th[k - 1];
+                S.u32s[6] = S.tl[k - 1];
             }
         }
         __syncthreads();
@@ -378,17 +421,21 @@ __device__ uint32_t topk_finish(const Smem& S, int k) {
     return c;
 }
 
+__device__ __forceinline__ uint32_t sqdiff4(uint32_t a, uint32_t b, uint32_t acc) {
+    const uint32_t d = __vabsdiffu4(a, b);
+    return __dp4a(d, d, acc);
+}
+
 // ---------------------------------------------------------------------------
 // Fast path: tree 0, round 0 fills the budget.
 // ---------------------------------------------------------------------------
 struct FastSlot {
     LeafItem *A, *B, *C;
     uint32_t* pre;
-    uint32_t* cand;
+    uint32_t* cand;  // candidate rows as tree-0 permutation indices
 };
 
-__device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl,
-                                              uint64_t budget) {
+__device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl) {
     uint8_t* p = base + static_cast<size_t>(blockIdx.x) * slot_bytes;
     FastSlot f;
     f.A = reinterpret_cast<LeafItem*>(p);
@@ -396,27 +443,110 @@ __device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, 
     f.C = f.B + maxl;
     f.pre = reinterpret_cast<uint32_t*>(f.C + maxl);
     f.cand = f.pre + maxl;
-    (void)budget;
     return f;
 }
 
-__device__ void load_query(const QueryPlan& P, uint64_t q, int tree, const Smem& S, bool vec) {
-    if (vec)
-        for (int t = threadIdx.x; t < P.d; t += blockDim.x) S.qv[t] = P.q[q * P.d + t];
+__device__ void load_query_proj(const QueryPlan& P, uint64_t q, int tree, const Smem& S) {
     for (int j = threadIdx.x; j < P.K; j += blockDim.x)
         S.qp[j] = P.qproj[(static_cast<uint64_t>(tree) * P.nq + q) * P.K + j];
     __syncthreads();
 }
 
+// Loads the query vector (fp32, and u8 when the index has u8 rows); returns
+// whether the u8 path is exact for this query (all values integral in [0,255]).
+__device__ bool load_query_vec(const QueryPlan& P, uint64_t q, const Smem& S) {
+    if (threadIdx.x == 0) S.u32s[9] = 1;
+    __syncthreads();
+    bool ok = true;
+    for (int t = threadIdx.x; t < P.d; t += blockDim.x) {
+        const float v = P.q[q * P.d + t];
+        S.qv[t] = v;
+        if (P.data_u8) {
+            const bool integral = v >= 0.0f && v <= 255.0f && v == floorf(v);
+            ok = ok && integral;
+            S.q8[t] = integral ? static_cast<uint8_t>(v) : 0;
+        }
+    }
+    if (P.data_u8)
+        for (int t = P.d + threadIdx.x; t < P.row_u8; t += blockDim.x) S.q8[t] = 0;
+    if (!ok) S.u32s[9] = 0;
+    __syncthreads();
+    const bool u8 = P.data_u8 != nullptr && S.u32s[9] != 0;
+    __syncthreads();
+    return u8;
+}
+
+// Scores candidates [base, base+nb) into the batch keys.
+__device__ void score_batch(const QueryPlan& P, const FastSlot& F, const Smem& S, uint32_t base,
+                            uint32_t nb, bool u8) {
+    if (u8) {
+        // LPR lanes per row, 16 B per lane-chunk; int32 exact squared distance
+        const int lpr = P.u8_lpr;
+        const int rpw = 32 / lpr;
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int sub = lane & (lpr - 1), rsub = lane / lpr;
+        const int chunks = P.row_u8 / 16;
+        const uint4* q4 = reinterpret_cast<const uint4*>(S.q8);
+        for (uint32_t r0 = warp * rpw; r0 < nb; r0 += (blockDim.x / 32) * rpw) {
+            const uint32_t r = r0 + rsub;
+            uint32_t acc = 0;
+            uint32_t pp = 0;
+            if (r < nb) {
+                pp = F.cand[base + r];
+                const uint4* row = reinterpret_cast<const uint4*>(P.data_u8 + static_cast<uint64_t>(pp) * P.row_u8);
+                for (int ch = sub; ch < chunks; ch += lpr) {
+                    const uint4 x = __ldg(row + ch);
+                    const uint4 qq = q4[ch];
+                    acc = sqdiff4(qq.x, x.x, acc);
+                    acc = sqdiff4(qq.y, x.y, acc);
+                    acc = sqdiff4(qq.z, x.z, acc);
+                    acc = sqdiff4(qq.w, x.w, acc);
+                }
+            }
+            for (int o = lpr >> 1; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (sub == 0 && r < nb) {
+                S.bh[r] = acc;
+                S.bl[r] = __ldg(P.perm0 + pp);
+            }
+        }
+    } else {
+        // one thread per row, two rows in flight per thread (independent fp64 chains)
+        for (uint32_t r = threadIdx.x; r < nb; r += 2 * blockDim.x) {
+            const uint32_t r2 = r + blockDim.x;
+            const uint32_t p1 = __ldg(P.perm0 + F.cand[base + r]);
+            const bool two = r2 < nb;
+            const uint32_t p2 = two ? __ldg(P.perm0 + F.cand[base + r2]) : p1;
+            const float* x1 = P.data + static_cast<uint64_t>(p1) * P.d;
+            const float* x2 = P.data + static_cast<uint64_t>(p2) * P.d;
+            double a1 = 0.0, a2 = 0.0;
+            for (int t = 0; t < P.d; ++t) {
+                const double qv = static_cast<double>(S.qv[t]);
+                const double d1 = __dsub_rn(qv, static_cast<double>(__ldg(x1 + t)));
+                const double d2 = __dsub_rn(qv, static_cast<double>(__ldg(x2 + t)));
+                a1 = __dadd_rn(a1, __dmul_rn(d1, d1));
+                a2 = __dadd_rn(a2, __dmul_rn(d2, d2));
+            }
+            S.bh[r] = static_cast<uint64_t>(__double_as_longlong(__dsqrt_rn(a1)));
+            S.bl[r] = p1;
+            if (two) {
+                S.bh[r2] = static_cast<uint64_t>(__double_as_longlong(__dsqrt_rn(a2)));
+                S.bl[r2] = p2;
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    const Smem S = carve(smem_raw, P.K, P.NR, P.d);
-    const FastSlot F = fast_slot(scratch, slot_bytes, P.max_leaves, P.budget);
+    const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
+    const FastSlot F = fast_slot(scratch, slot_bytes, P.max_leaves);
     const double radius = __dmul_rn(P.eps, P.r_min);
     const uint32_t B32 = static_cast<uint32_t>(P.budget);
+    const QTree T0 = P.trees[0];
     for (uint64_t q = blockIdx.x; q < P.nq; q += gridDim.x) {
-        load_query(P, q, 0, S, true);
+        const bool u8 = load_query_vec(P, q, S);
+        load_query_proj(P, q, 0, S);
         build_sq(P, 0, S);
         uint32_t nA;
         uint64_t W;
@@ -432,6 +562,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
         // exclusive prefix of the taken counts, in A order
         if (threadIdx.x == 0) S.u32s[3] = 0;
         __syncthreads();
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         for (uint32_t base = 0; base < nA; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
             uint32_t take = 0;
@@ -440,9 +571,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
                 if (key_less(it.mdb, it.id, kmdb, kid)) take = it.w;
                 else if (it.mdb == kmdb && it.id == kid) take = static_cast<uint32_t>(take_cut);
             }
-            // block exclusive scan
             uint32_t incl = take;
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += t;
@@ -460,37 +589,30 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
             if (threadIdx.x == 0) S.u32s[3] += tot;
             __syncthreads();
         }
-        // candidate positions, one warp per leaf (coalesced along the leaf)
-        {
-            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-            const QTree T = P.trees[0];
-            for (uint32_t i = warp; i < nA; i += kQueryThreads / 32) {
-                const LeafItem it = F.A[i];
-                uint32_t take = 0;
-                if (key_less(it.mdb, it.id, kmdb, kid)) take = it.w;
-                else if (it.mdb == kmdb && it.id == kid) take = static_cast<uint32_t>(take_cut);
-                const uint32_t dst = F.pre[i], src = T.leaf_begin[it.li];
-                for (uint32_t e = lane; e < take; e += 32) F.cand[dst + e] = T.perm[src + e];
-            }
+        // candidate rows (tree-0 permutation indices), one warp per leaf
+        for (uint32_t i = warp; i < nA; i += kQueryThreads / 32) {
+            const LeafItem it = F.A[i];
+            uint32_t take = 0;
+            if (key_less(it.mdb, it.id, kmdb, kid)) take = it.w;
+            else if (it.mdb == kmdb && it.id == kid) take = static_cast<uint32_t>(take_cut);
+            const uint32_t dst = F.pre[i], src = T0.leaf_begin[it.li];
+            for (uint32_t e = lane; e < take; e += 32) F.cand[dst + e] = src + e;
         }
         __syncthreads();
-        // exact verification + top-k
+        // exact verification + top-k (the penalty table region is reused)
         topk_init(S);
-        for (uint32_t c0 = 0; c0 < B32; c0 += blockDim.x) {
-            const uint32_t c = c0 + threadIdx.x;
-            double dist = 0.0;
-            uint32_t pos = 0;
-            const bool valid = c < B32;
-            if (valid) {
-                pos = F.cand[c];
-                dist = l2_exact(S.qv, P.data + static_cast<uint64_t>(pos) * P.d, P.d);
-            }
-            topk_push(S, valid, dist, pos, P.k);
+        for (uint32_t c0 = 0; c0 < B32; c0 += kBatch) {
+            const uint32_t nb = min(static_cast<uint32_t>(kBatch), B32 - c0);
+            score_batch(P, F, S, c0, nb, u8);
+            __syncthreads();
+            topk_absorb(S, nb, P.k);
         }
         const uint32_t nh = topk_finish(S, P.k);
         for (uint32_t t = threadIdx.x; t < nh; t += blockDim.x) {
-            if (P.ids) P.ids[q * P.k + t] = S.tp[t];
-            if (P.dists) P.dists[q * P.k + t] = S.td[t];
+            const uint64_t h = S.th[t];
+            const double dist = u8 ? __dsqrt_rn(static_cast<double>(h)) : __longlong_as_double(static_cast<long long>(h));
+            if (P.ids) P.ids[q * P.k + t] = S.tl[t];
+            if (P.dists) P.dists[q * P.k + t] = dist;
         }
         if (threadIdx.x == 0) {
             if (P.n_hits) P.n_hits[q] = static_cast<int32_t>(nh);
@@ -512,7 +634,7 @@ struct SlowSlot {
 };
 
 __device__ __forceinline__ SlowSlot slow_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl,
-                                              uint64_t n, uint64_t budget) {
+                                              uint64_t budget) {
     uint8_t* p = base + static_cast<size_t>(blockIdx.x) * slot_bytes;
     SlowSlot s;
     s.A = reinterpret_cast<LeafItem*>(p);
@@ -521,7 +643,6 @@ __device__ __forceinline__ SlowSlot slow_slot(uint8_t* base, size_t slot_bytes, 
     s.mdist = reinterpret_cast<double*>(s.C + maxl);
     s.mpos = reinterpret_cast<uint32_t*>(s.mdist + budget);
     s.bitmap = s.mpos + budget;
-    (void)n;
     return s;
 }
 
@@ -575,18 +696,18 @@ __device__ void emit_members(const QueryPlan& P, int tree, const LeafItem* A, ui
 __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
     QueryPlan P, const uint32_t* list, uint32_t count, uint8_t* scratch, size_t slot_bytes) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    const Smem S = carve(smem_raw, P.K, P.NR, P.d);
-    const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.n, P.budget);
+    const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
+    const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.budget);
     for (uint32_t qi = blockIdx.x; qi < count; qi += gridDim.x) {
         const uint64_t q = list ? list[qi] : qi;
         if (threadIdx.x == 0) S.u32s[7] = 0;  // |S|
         __syncthreads();
-        for (int t = threadIdx.x; t < P.d; t += blockDim.x) S.qv[t] = P.q[q * P.d + t];
+        load_query_vec(P, q, S);
         double r = P.r_min;
         bool done = false;
         for (;;) {
             for (int tree = 0; tree < P.L && !done; ++tree) {
-                load_query(P, q, tree, S, false);
+                load_query_proj(P, q, tree, S);
                 build_sq(P, tree, S);
                 const double radius = __dmul_rn(P.eps, r);
                 const uint32_t have = S.u32s[7];
@@ -620,34 +741,38 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
             if (enough) break;
             r = __dmul_rn(r, P.c);
         }
-        // top-k of the members, extracted in chunks (any k)
+        // top-k of the members, extracted kFastMaxK at a time (any k)
         const uint32_t msz = S.u32s[7];
         const uint32_t want = min(msz, static_cast<uint32_t>(P.k));
         uint32_t out = 0;
-        double lbd = -1.0;
-        uint32_t lbp = 0;
+        uint64_t lbh = 0;
+        uint32_t lbl = 0;
+        bool have_lb = false;
         while (out < want) {
             const int kk = static_cast<int>(min(want - out, static_cast<uint32_t>(kFastMaxK)));
             topk_init(S);
-            for (uint32_t c0 = 0; c0 < msz; c0 += blockDim.x) {
-                const uint32_t c = c0 + threadIdx.x;
-                bool valid = c < msz;
-                double dist = 0.0;
-                uint32_t pos = 0;
-                if (valid) {
-                    dist = L.mdist[c];
-                    pos = L.mpos[c];
-                    valid = dp_less(lbd, lbp, dist, pos);
+            for (uint32_t c0 = 0; c0 < msz; c0 += kBatch) {
+                const uint32_t nb = min(static_cast<uint32_t>(kBatch), msz - c0);
+                for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+                    const uint64_t h = static_cast<uint64_t>(__double_as_longlong(L.mdist[c0 + i]));
+                    const uint32_t l = L.mpos[c0 + i];
+                    const bool above = !have_lb || key_less(lbh, lbl, h, l);
+                    S.bh[i] = above ? h : ~0ULL;  // sentinels never beat a real key
+                    S.bl[i] = above ? l : 0xffffffffu;
                 }
-                topk_push(S, valid, dist, pos, kk);
+                __syncthreads();
+                topk_absorb(S, nb, kk);
             }
-            const uint32_t got = topk_finish(S, kk);
+            uint32_t got = topk_finish(S, kk);
+            // drop sentinel entries (only possible when fewer than kk remain)
+            while (got > 0 && S.th[got - 1] == ~0ULL && S.tl[got - 1] == 0xffffffffu) --got;
             for (uint32_t t = threadIdx.x; t < got; t += blockDim.x) {
-                if (P.ids) P.ids[q * P.k + out + t] = S.tp[t];
-                if (P.dists) P.dists[q * P.k + out + t] = S.td[t];
+                if (P.ids) P.ids[q * P.k + out + t] = S.tl[t];
+                if (P.dists) P.dists[q * P.k + out + t] = __longlong_as_double(static_cast<long long>(S.th[t]));
             }
-            lbd = S.td[got - 1];
-            lbp = S.tp[got - 1];
+            lbh = S.th[got - 1];
+            lbl = S.tl[got - 1];
+            have_lb = true;
             out += got;
             __syncthreads();
         }
@@ -699,7 +824,7 @@ __global__ void merge_topk_kernel(const double* __restrict__ sd, const uint64_t*
 void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream_t s,
                      cudaStream_t alloc_s) {
     const int sms = sm_count(device);
-    const size_t smem = smem_bytes(P.K, P.NR, P.d);
+    const size_t smem = smem_bytes(P.K, P.NR, P.d, P.row_u8);
     if (smem > 220 * 1024) throw InvalidArgument("ck_ann: query dimension too large for the staging buffer");
     DETLSH_CUDA(cudaFuncSetAttribute(query_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -720,8 +845,11 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     uint32_t slow_count = 0;
     const uint32_t* slow_list = X.slow_list.get();
     if (P.k <= kFastMaxK) {
+        int per_sm = 0;
+        DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, query_fast_kernel, kQueryThreads, smem));
+        per_sm = std::max(1, std::min(per_sm, 4));
         const size_t fast_bytes = (items + 4 * static_cast<size_t>(P.max_leaves) + 4 * P.budget + 255) / 256 * 256;
-        const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * 2);
+        const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
         grow_scratch(X.fast, slots * fast_bytes);
         ProfScope ps("query_fast", s);
         query_fast_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(

@@ -25,6 +25,10 @@ struct QueryPlan {
     int d, K, L, NR;
     const float* table;   // [L][K][NR+1]
     const QTree* trees;   // device array [L]
+    const uint32_t* perm0;   // tree 0 permutation (row index -> dataset position)
+    const uint8_t* data_u8;  // exact u8 rows in tree-0 order, or null
+    int row_u8;              // bytes per u8 row (d rounded up to 16)
+    int u8_lpr;              // lanes per u8 row (power of two <= 32)
     double eps, c, r_min;
     uint64_t budget;
     int k;
@@ -42,8 +46,7 @@ struct QueryPlan {
 };
 
 constexpr int kQueryThreads = 256;
-constexpr int kTopCap = 1024;                      // top-k staging buffer
-constexpr int kFastMaxK = kTopCap - kQueryThreads;  // k handled by the fast path
+constexpr int kFastMaxK = 1024;  // k handled by the fast path (larger k: general path)
 
 // Launch the batched query: fast path for every query (budget fills in tree 0,
 // round 0, no dedup needed), then the general path for the rest.  Scratch is

@@ -409,3 +409,61 @@ void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float
 }
 
 }  // namespace detlsh_b200
+
+namespace detlsh_b200 {
+namespace {
+
+__global__ void integral_u8_kernel(const float* __restrict__ x, uint64_t total,
+                                   unsigned int* __restrict__ bad) {
+    bool ok = true;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const float v = x[i];
+        ok = ok && v >= 0.0f && v <= 255.0f && v == floorf(v);
+    }
+    if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
+// out[p'] = u8(rows[perm[p']]), zero-padded to row_bytes (multiple of 16)
+__global__ void pack_u8_kernel(const float* __restrict__ x, const uint32_t* __restrict__ perm,
+                               uint64_t n, int d, int row_bytes, uint8_t* __restrict__ out) {
+    const uint64_t total = n * static_cast<uint64_t>(row_bytes);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t r = i / row_bytes;
+        const int t = static_cast<int>(i % row_bytes);
+        out[i] = t < d ? static_cast<uint8_t>(x[static_cast<uint64_t>(perm[r]) * d + t]) : 0;
+    }
+}
+
+}  // namespace
+
+bool data_is_u8(const float* d_x, uint64_t total, cudaStream_t s) {
+    StreamScope scope(s);
+    DevBuf<unsigned int> bad(1);
+    DETLSH_CUDA(cudaMemsetAsync(bad.get(), 0, 4, s));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8)));
+    integral_u8_kernel<<<grid, 256, 0, s>>>(d_x, total, bad.get());
+    DETLSH_LAUNCH_CHECK();
+    unsigned int h = 1;
+    DETLSH_CUDA(cudaMemcpyAsync(&h, bad.get(), 4, cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    return h == 0;
+}
+
+void launch_pack_u8(const float* d_x, const uint32_t* d_perm, uint64_t n, int d, int row_bytes,
+                    uint8_t* d_out, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t total = n * static_cast<uint64_t>(row_bytes);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 16)));
+    ProfScope ps("pack_u8", s);
+    pack_u8_kernel<<<grid, 256, 0, s>>>(d_x, d_perm, n, d, row_bytes, d_out);
+    DETLSH_LAUNCH_CHECK();
+}
+
+}  // namespace detlsh_b200

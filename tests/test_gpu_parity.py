@@ -218,3 +218,25 @@ def test_errors_map_to_reference_taxonomy(gpu):
         gpu.ck_ann(idx, np.zeros(8, np.float32), 0)
     with pytest.raises(ValueError):
         gpu.ck_ann(idx, np.zeros(8, np.float32), 101)
+
+
+@pytest.mark.parametrize("d", [128, 20, 784 // 8])
+def test_u8_rows_path_equals_fp64_path_and_oracle(gpu, port, d):
+    """Integral datasets use exact int32 distances on u8 rows; both verification
+    paths and the oracle must agree bit for bit, including a non-integral query
+    (per-query fallback to the fp64 path)."""
+    g = np.random.Generator(np.random.PCG64(d))
+    n = 6000
+    data = np.where(g.random((n, d)) < 0.5, 0, np.minimum(g.geometric(0.05, (n, d)), 255)).astype(np.float32)
+    Q = np.where(g.random((24, d)) < 0.5, 0, np.minimum(g.geometric(0.05, (24, d)), 255)).astype(np.float32)
+    Q[3] += 0.5  # not integral -> fp64 path for this query
+    Q[5, 0] = 300.0  # out of u8 range -> fp64 path
+    c = dict(K=16, L=4, n_regions=256, leaf_capacity=32, sample_fraction=0.1, beta=0.1, k=25)
+    a = gpu.build_index(data, _params(**c), seed=4)
+    b = gpu.build_index(data, _params(**c), seed=4, u8_rows=False)
+    ra, rb = gpu.ck_ann_batch(a, Q, 25), gpu.ck_ann_batch(b, Q, 25)
+    assert np.array_equal(ra.ids, rb.ids) and bits_equal(ra.dists, rb.dists)
+    oi = port.build_index(data, make_params(**c), 4)
+    for qi in range(Q.shape[0]):
+        ids, ds, rad, cs = oi.ck_ann(Q[qi], 25)
+        assert np.array_equal(ra.ids[qi], ids) and bits_equal(ra.dists[qi], ds)
