@@ -33,6 +33,7 @@ namespace {
 
 constexpr int kBatch = 1024;                    // candidates scored per block step
 constexpr int kTopCap = 2048;                   // staged (key, pos) entries
+constexpr int kBins = 1024;                     // mindist histogram bins (fast-path cut)
 static_assert(kFastMaxK == kTopCap - kBatch, "fast-path k bound");
 
 struct LeafItem {
@@ -56,6 +57,7 @@ struct Smem {
     uint64_t* bh;              // [kBatch] batch key hi
     uint32_t* bl;              // [kBatch] batch key lo
     unsigned long long* hist;  // [256]
+    uint32_t* bins;            // [kBins] leaf-weight histogram over mindist / radius
     unsigned long long* u64s;  // scalars
     uint32_t* u32s;
     int* lbv;                  // [K]  #{b : row[b] <  v}
@@ -92,6 +94,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base, int K, int NR, int d, int r
     s.tl = reinterpret_cast<uint32_t*>(s.bh + kBatch);
     s.bl = s.tl + kTopCap;
     s.hist = reinterpret_cast<unsigned long long*>(c.take(8 * 256));
+    s.bins = reinterpret_cast<uint32_t*>(c.take(4 * kBins));
     s.u64s = reinterpret_cast<unsigned long long*>(c.take(8 * 16));
     s.u32s = reinterpret_cast<uint32_t*>(c.take(4 * 16));
     s.lbv = reinterpret_cast<int*>(c.take(4 * kMaxK));
@@ -110,6 +113,7 @@ size_t smem_bytes(int K, int NR, int d, int row_u8) {
     };
     take(union_bytes(K, NR));
     take(8 * 256);
+    take(4 * kBins);
     take(8 * 16);
     take(4 * 16);
     take(4 * kMaxK);
@@ -211,6 +215,8 @@ __device__ __forceinline__ void warp_append(bool ok, const LeafItem& it, LeafIte
 
 // Scan every leaf of tree `tree`, appending those with mindist <= radius.
 // weight: leaf size, or (bitmap != null) the entries not yet in S.
+// Each appended item also records its histogram bin floor(md * kBins / radius)
+// (monotone in md) in `pad`, and its weight is added to S.bins.
 __device__ void scan_leaves(const QueryPlan& P, int tree, double radius, const Smem& S,
                             LeafItem* A, const uint32_t* bitmap, uint32_t& nA, uint64_t& W) {
     const QTree T = P.trees[tree];
@@ -218,6 +224,8 @@ __device__ void scan_leaves(const QueryPlan& P, int tree, double radius, const S
         S.u32s[0] = 0;
         S.u64s[0] = 0;
     }
+    for (int i = threadIdx.x; i < kBins; i += blockDim.x) S.bins[i] = 0;
+    const double scale = radius > 0.0 ? static_cast<double>(kBins) / radius : 0.0;
     __syncthreads();
     unsigned long long wsum = 0;
     const uint32_t nl = T.num_leaves;
@@ -244,8 +252,10 @@ __device__ void scan_leaves(const QueryPlan& P, int tree, double radius, const S
                     it.id = T.leaf_node[li];
                     it.w = w;
                     it.li = li;
-                    it.pad = 0;
+                    const double fb = __dmul_rn(md, scale);
+                    it.pad = fb >= static_cast<double>(kBins - 1) ? kBins - 1 : static_cast<uint32_t>(fb);
                     wsum += w;
+                    atomicAdd(&S.bins[it.pad], w);
                 }
             }
         }
@@ -556,20 +566,64 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
             __syncthreads();
             continue;
         }
-        uint64_t kmdb, take_cut;
-        uint32_t kid;
-        weighted_select(F.A, nA, P.budget, F.B, F.C, S, kmdb, kid, take_cut);
-        // exclusive prefix of the taken counts, in A order
-        if (threadIdx.x == 0) S.u32s[3] = 0;
-        __syncthreads();
+        // the budget trips inside histogram bin b* (bins are monotone in
+        // mindist); only that bin's leaves need the exact (mindist, id) order
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if (threadIdx.x < 32) {
+            constexpr int per = kBins / 32;
+            unsigned long long part = 0;
+            for (int b = 0; b < per; ++b) part += S.bins[lane * per + b];
+            unsigned long long incl = part;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const unsigned long long excl = incl - part;
+            if (excl < P.budget && P.budget <= incl) {
+                unsigned long long cum = excl;
+                int bin = lane * per;
+                for (int b = 0; b < per; ++b, ++bin) {
+                    const unsigned long long c = S.bins[bin];
+                    if (cum + c >= P.budget) break;
+                    cum += c;
+                }
+                S.u32s[2] = static_cast<uint32_t>(bin);
+                S.u64s[1] = P.budget - cum;
+            }
+            if (lane == 0) S.u32s[1] = 0;
+        }
+        __syncthreads();
+        const uint32_t bstar = S.u32s[2];
+        const uint64_t need_in_bin = S.u64s[1];
         for (uint32_t base = 0; base < nA; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
-            uint32_t take = 0;
+            bool ok = false;
+            LeafItem it;
+            if (i < nA) {
+                it = F.A[i];
+                ok = it.pad == bstar;
+            }
+            warp_append(ok, it, F.B, &S.u32s[1]);
+        }
+        __syncthreads();
+        uint64_t kmdb, take_cut;
+        uint32_t kid;
+        weighted_select(F.B, S.u32s[1], need_in_bin, F.C, F.B, S, kmdb, kid, take_cut);
+        // fused: exclusive prefix of the taken counts (A order) + candidate rows
+        // (tree-0 permutation indices; a leaf's rows are contiguous)
+        if (threadIdx.x == 0) S.u32s[3] = 0;
+        __syncthreads();
+        for (uint32_t base = 0; base < nA; base += blockDim.x) {
+            const uint32_t i = base + threadIdx.x;
+            uint32_t take = 0, src = 0;
             if (i < nA) {
                 const LeafItem it = F.A[i];
-                if (key_less(it.mdb, it.id, kmdb, kid)) take = it.w;
-                else if (it.mdb == kmdb && it.id == kid) take = static_cast<uint32_t>(take_cut);
+                if (it.pad < bstar) take = it.w;
+                else if (it.pad == bstar) {
+                    if (key_less(it.mdb, it.id, kmdb, kid)) take = it.w;
+                    else if (it.mdb == kmdb && it.id == kid) take = static_cast<uint32_t>(take_cut);
+                }
+                if (take) src = __ldg(T0.leaf_begin + it.li);
             }
             uint32_t incl = take;
             for (int o = 1; o < 32; o <<= 1) {
@@ -584,21 +638,12 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
                 if (w < warp) wpre += wt[w];
                 tot += wt[w];
             }
-            if (i < nA) F.pre[i] = S.u32s[3] + wpre + incl - take;
+            const uint32_t dst = S.u32s[3] + wpre + incl - take;
+            for (uint32_t e = 0; e < take; ++e) F.cand[dst + e] = src + e;
             __syncthreads();
             if (threadIdx.x == 0) S.u32s[3] += tot;
             __syncthreads();
         }
-        // candidate rows (tree-0 permutation indices), one warp per leaf
-        for (uint32_t i = warp; i < nA; i += kQueryThreads / 32) {
-            const LeafItem it = F.A[i];
-            uint32_t take = 0;
-            if (key_less(it.mdb, it.id, kmdb, kid)) take = it.w;
-            else if (it.mdb == kmdb && it.id == kid) take = static_cast<uint32_t>(take_cut);
-            const uint32_t dst = F.pre[i], src = T0.leaf_begin[it.li];
-            for (uint32_t e = lane; e < take; e += 32) F.cand[dst + e] = src + e;
-        }
-        __syncthreads();
         // exact verification + top-k (the penalty table region is reused)
         topk_init(S);
         for (uint32_t c0 = 0; c0 < B32; c0 += kBatch) {
