@@ -6,6 +6,8 @@
 #include <numeric>
 #include <stdexcept>
 
+#include <immintrin.h>
+
 namespace detlsh_b200 {
 
 double Rng::normal() {
@@ -217,6 +219,107 @@ size_t hoare_scan_blocked(float* a, size_t lo, size_t hi, float pv) {
     }
 }
 
+// AVX2 flavour of hoare_scan_blocked: the stopper lists are filled 8 floats at
+// a time (compare + movemask + a compress LUT); the pairing loop is unchanged,
+// so the swaps and the returned position are the same.
+struct CompressLut {
+    alignas(32) int32_t asc[256][8];
+    alignas(32) int32_t desc[256][8];
+    CompressLut() {
+        for (int m = 0; m < 256; ++m) {
+            int k = 0;
+            for (int b = 0; b < 8; ++b)
+                if ((m >> b) & 1) asc[m][k++] = b;
+            for (; k < 8; ++k) asc[m][k] = 0;
+            k = 0;
+            for (int b = 7; b >= 0; --b)
+                if ((m >> b) & 1) desc[m][k++] = b;
+            for (; k < 8; ++k) desc[m][k] = 0;
+        }
+    }
+};
+const CompressLut kLut;
+
+__attribute__((target("avx2,popcnt"))) size_t hoare_scan_avx2(float* a, size_t lo, size_t hi,
+                                                              float pv) {
+    constexpr int64_t B = 64;
+    alignas(32) int32_t lb[B + 8], rb[B + 8];
+    int ln = 0, lh = 0, rn = 0, rh = 0;
+    int64_t i = static_cast<int64_t>(lo) + 1, j = static_cast<int64_t>(hi) - 1;
+    int64_t lgen = i + 1, rgen = j - 1;
+    const __m256 vp = _mm256_set1_ps(pv);
+    for (;;) {
+        int64_t in;
+        for (;;) {  // next left stopper in (i, j)
+            if (lh < ln) {
+                in = lb[lh++];
+                if (in >= j) in = j;
+                break;
+            }
+            if (lgen >= j) {
+                in = j;
+                break;
+            }
+            const int64_t end = std::min(lgen + B, j);
+            ln = 0;
+            lh = 0;
+            int64_t x = lgen;
+            for (; x + 8 <= end; x += 8) {
+                const int m = _mm256_movemask_ps(_mm256_cmp_ps(_mm256_loadu_ps(a + x), vp, _CMP_GE_OQ));
+                const __m256i pos = _mm256_add_epi32(
+                    _mm256_load_si256(reinterpret_cast<const __m256i*>(kLut.asc[m])),
+                    _mm256_set1_epi32(static_cast<int32_t>(x)));
+                _mm256_storeu_si256(reinterpret_cast<__m256i*>(lb + ln), pos);
+                ln += __builtin_popcount(static_cast<unsigned>(m));
+            }
+            for (; x < end; ++x) {
+                lb[ln] = static_cast<int32_t>(x);
+                ln += a[x] >= pv;
+            }
+            lgen = end;
+        }
+        int64_t jn;
+        for (;;) {  // next right stopper in [in, j)
+            if (rh < rn) {
+                jn = rb[rh++];
+                if (jn < in) jn = in - 1;
+                break;
+            }
+            if (rgen < in) {
+                jn = in - 1;
+                break;
+            }
+            const int64_t end = std::max(rgen - B, in - 1);
+            rn = 0;
+            rh = 0;
+            int64_t y = rgen;
+            for (; y - 8 >= end; y -= 8) {
+                const int64_t b0 = y - 7;
+                const int m = _mm256_movemask_ps(_mm256_cmp_ps(_mm256_loadu_ps(a + b0), vp, _CMP_LE_OQ));
+                const __m256i pos = _mm256_add_epi32(
+                    _mm256_load_si256(reinterpret_cast<const __m256i*>(kLut.desc[m])),
+                    _mm256_set1_epi32(static_cast<int32_t>(b0)));
+                _mm256_storeu_si256(reinterpret_cast<__m256i*>(rb + rn), pos);
+                rn += __builtin_popcount(static_cast<unsigned>(m));
+            }
+            for (; y > end; --y) {
+                rb[rn] = static_cast<int32_t>(y);
+                rn += a[y] <= pv;
+            }
+            rgen = end;
+        }
+        if (in >= jn) return static_cast<size_t>(jn);
+        std::swap(a[in], a[jn]);
+        i = in;
+        j = jn;
+    }
+}
+
+bool have_avx2() {
+    static const bool v = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("popcnt");
+    return v;
+}
+
 // Median-of-three around a seeded pick, sentinel Hoare scan; one bounded()
 // draw per call.  Returns the pivot's sorted position.
 size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
@@ -228,7 +331,9 @@ size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
     if (a[hi - 1] < a[mid]) std::swap(a[mid], a[hi - 1]);
     std::swap(a[mid], a[lo + 1]);
     const float pv = a[lo + 1];
-    const size_t j = len >= 32 ? hoare_scan_blocked(a, lo, hi, pv) : hoare_scan_simple(a, lo, hi, pv);
+    const size_t j = len < 32      ? hoare_scan_simple(a, lo, hi, pv)
+                     : have_avx2() ? hoare_scan_avx2(a, lo, hi, pv)
+                                   : hoare_scan_blocked(a, lo, hi, pv);
     std::swap(a[lo + 1], a[j]);
     return j;
 }
