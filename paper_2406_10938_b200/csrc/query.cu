@@ -379,7 +379,9 @@ __device__ __forceinline__ void topk_init(const Smem& S) {
 // Stage the batch keys [0, nb) that beat the current k-th key; compact when
 // the staging area would overflow.  Called by all threads after the batch is
 // written (and synchronised).
-__device__ void topk_absorb(const Smem& S, uint32_t nb, int k) {
+// `row_to_pos` non-null: bl holds row indices that map to dataset positions
+// through it; the lookup is only done for keys that can still enter.
+__device__ void topk_absorb(const Smem& S, uint32_t nb, int k, const uint32_t* row_to_pos) {
     const bool full = S.u32s[5] != 0;
     const uint64_t th = S.u64s[2];
     const uint32_t tl = S.u32s[6];
@@ -392,7 +394,14 @@ __device__ void topk_absorb(const Smem& S, uint32_t nb, int k) {
         if (i < nb) {
             h = S.bh[i];
             l = S.bl[i];
-            take = !full || key_less(h, l, th, tl);
+            if (row_to_pos) {
+                if (!full || h <= th) {
+                    l = __ldg(row_to_pos + l);
+                    take = !full || key_less(h, l, th, tl);
+                }
+            } else {
+                take = !full || key_less(h, l, th, tl);
+            }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, take);
         if (m) {
@@ -490,33 +499,51 @@ __device__ bool load_query_vec(const QueryPlan& P, uint64_t q, const Smem& S) {
 __device__ void score_batch(const QueryPlan& P, const FastSlot& F, const Smem& S, uint32_t base,
                             uint32_t nb, bool u8) {
     if (u8) {
-        // LPR lanes per row, 16 B per lane-chunk; int32 exact squared distance
+        // LPR lanes per row, 16 B per lane-chunk; int32 exact squared distance.
+        // Candidate rows are staged in smem first, then every lane keeps kU
+        // row loads in flight.  bl holds the ROW index (tree-0 permutation
+        // index); topk_absorb maps it to the dataset position only for the
+        // rare keys that can enter the top-k.
+        constexpr int kU = 4;
+        for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) S.bl[i] = F.cand[base + i];
+        __syncthreads();
         const int lpr = P.u8_lpr;
         const int rpw = 32 / lpr;
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int sub = lane & (lpr - 1), rsub = lane / lpr;
         const int chunks = P.row_u8 / 16;
         const uint4* q4 = reinterpret_cast<const uint4*>(S.q8);
-        for (uint32_t r0 = warp * rpw; r0 < nb; r0 += (blockDim.x / 32) * rpw) {
-            const uint32_t r = r0 + rsub;
-            uint32_t acc = 0;
-            uint32_t pp = 0;
-            if (r < nb) {
-                pp = F.cand[base + r];
-                const uint4* row = reinterpret_cast<const uint4*>(P.data_u8 + static_cast<uint64_t>(pp) * P.row_u8);
-                for (int ch = sub; ch < chunks; ch += lpr) {
-                    const uint4 x = __ldg(row + ch);
+        const uint32_t step = (blockDim.x / 32) * rpw * kU;
+        for (uint32_t r0 = warp * rpw * kU; r0 < nb; r0 += step) {
+            uint32_t acc[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) acc[u] = 0;
+            for (int ch0 = 0; ch0 < chunks; ch0 += lpr) {
+                const int ch = ch0 + sub;
+                uint4 x[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const uint32_t r = r0 + u * rpw + rsub;
+                    x[u] = make_uint4(0, 0, 0, 0);
+                    if (r < nb && ch < chunks)
+                        x[u] = __ldg(reinterpret_cast<const uint4*>(P.data_u8 + static_cast<uint64_t>(S.bl[r]) * P.row_u8) + ch);
+                }
+                if (ch < chunks) {
                     const uint4 qq = q4[ch];
-                    acc = sqdiff4(qq.x, x.x, acc);
-                    acc = sqdiff4(qq.y, x.y, acc);
-                    acc = sqdiff4(qq.z, x.z, acc);
-                    acc = sqdiff4(qq.w, x.w, acc);
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        acc[u] = sqdiff4(qq.x, x[u].x, acc[u]);
+                        acc[u] = sqdiff4(qq.y, x[u].y, acc[u]);
+                        acc[u] = sqdiff4(qq.z, x[u].z, acc[u]);
+                        acc[u] = sqdiff4(qq.w, x[u].w, acc[u]);
+                    }
                 }
             }
-            for (int o = lpr >> 1; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (sub == 0 && r < nb) {
-                S.bh[r] = acc;
-                S.bl[r] = __ldg(P.perm0 + pp);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                for (int o = lpr >> 1; o; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+                const uint32_t r = r0 + u * rpw + rsub;
+                if (sub == 0 && r < nb) S.bh[r] = acc[u];
             }
         }
     } else {
@@ -606,9 +633,11 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
             warp_append(ok, it, F.B, &S.u32s[1]);
         }
         __syncthreads();
+        const uint32_t n_bin = S.u32s[1];  // weighted_select reuses this counter
+        __syncthreads();
         uint64_t kmdb, take_cut;
         uint32_t kid;
-        weighted_select(F.B, S.u32s[1], need_in_bin, F.C, F.B, S, kmdb, kid, take_cut);
+        weighted_select(F.B, n_bin, need_in_bin, F.C, F.B, S, kmdb, kid, take_cut);
         // fused: exclusive prefix of the taken counts (A order) + candidate rows
         // (tree-0 permutation indices; a leaf's rows are contiguous)
         if (threadIdx.x == 0) S.u32s[3] = 0;
@@ -650,7 +679,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
             const uint32_t nb = min(static_cast<uint32_t>(kBatch), B32 - c0);
             score_batch(P, F, S, c0, nb, u8);
             __syncthreads();
-            topk_absorb(S, nb, P.k);
+            topk_absorb(S, nb, P.k, u8 ? P.perm0 : nullptr);
         }
         const uint32_t nh = topk_finish(S, P.k);
         for (uint32_t t = threadIdx.x; t < nh; t += blockDim.x) {
@@ -806,7 +835,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
                     S.bl[i] = above ? l : 0xffffffffu;
                 }
                 __syncthreads();
-                topk_absorb(S, nb, kk);
+                topk_absorb(S, nb, kk, nullptr);
             }
             uint32_t got = topk_finish(S, kk);
             // drop sentinel entries (only possible when fewer than kk remain)
