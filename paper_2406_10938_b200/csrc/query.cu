@@ -148,21 +148,33 @@ __device__ void build_sq(const QueryPlan& P, int tree, const Smem& S) {
 
 __device__ __forceinline__ double leaf_mindist(const QueryPlan& P, const QTree& T, uint32_t li,
                                                const Smem& S) {
-    const uint8_t* box = T.leaf_box + static_cast<size_t>(li) * 64;
-    uint4 raw[3];
-    raw[0] = __ldg(reinterpret_cast<const uint4*>(box));
-    raw[1] = __ldg(reinterpret_cast<const uint4*>(box) + 1);
-    if (P.K > 16) raw[2] = __ldg(reinterpret_cast<const uint4*>(box) + 2);
-    const uint8_t* b = reinterpret_cast<const uint8_t*>(raw);
+    // box: per dim j, bytes (lo region, hi region) at 2j, 2j+1; kept in
+    // registers (byte extraction by shifts, fully unrolled)
+    const uint4* box = reinterpret_cast<const uint4*>(T.leaf_box + static_cast<size_t>(li) * 64);
+    uint32_t w[12];
+    {
+        const uint4 a = __ldg(box), b = __ldg(box + 1);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        if (P.K > 16) {
+            const uint4 c = __ldg(box + 2);
+            w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+        } else {
+            w[8] = w[9] = w[10] = w[11] = 0;
+        }
+    }
     const int W = P.NR + 1;
     double acc = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < P.K; ++j) {
-        const int lo = b[2 * j], hi = b[2 * j + 1];
-        double pen_sq = 0.0;
-        if (lo > 0 && lo >= S.ubv[j]) pen_sq = S.sq[j * W + lo];
-        else if (hi < P.NR - 1 && hi + 1 < S.lbv[j]) pen_sq = S.sq[j * W + hi + 1];
-        acc = __dadd_rn(acc, pen_sq);
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        if (j < P.K) {
+            const uint32_t half = w[j >> 1] >> ((j & 1) * 16);
+            const int lo = half & 0xff, hi = (half >> 8) & 0xff;
+            double pen_sq = 0.0;
+            if (lo > 0 && lo >= S.ubv[j]) pen_sq = S.sq[j * W + lo];
+            else if (hi < P.NR - 1 && hi + 1 < S.lbv[j]) pen_sq = S.sq[j * W + hi + 1];
+            acc = __dadd_rn(acc, pen_sq);
+        }
     }
     return __dsqrt_rn(acc);
 }
@@ -668,10 +680,17 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
                 tot += wt[w];
             }
             const uint32_t dst = S.u32s[3] + wpre + incl - take;
-            for (uint32_t e = 0; e < take; ++e) F.cand[dst + e] = src + e;
+            // guard: never write past the budget (an inconsistent cut is
+            // reported below instead of corrupting memory)
+            for (uint32_t e = 0; e < take && dst + e < B32; ++e) F.cand[dst + e] = src + e;
             __syncthreads();
             if (threadIdx.x == 0) S.u32s[3] += tot;
             __syncthreads();
+        }
+        if (S.u32s[3] != B32) {  // invariant: the cut emits exactly `budget` rows
+            if (threadIdx.x == 0) atomicOr(slow_n + 1, 1u);
+            __syncthreads();
+            continue;
         }
         // exact verification + top-k (the penalty table region is reused)
         topk_init(S);
@@ -929,8 +948,11 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         query_fast_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
             P, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
         DETLSH_LAUNCH_CHECK();
-        DETLSH_CUDA(cudaMemcpyAsync(&slow_count, X.counters.get(), 4, cudaMemcpyDeviceToHost, s));
+        uint32_t flags[2] = {0, 0};
+        DETLSH_CUDA(cudaMemcpyAsync(flags, X.counters.get(), 8, cudaMemcpyDeviceToHost, s));
         DETLSH_CUDA(cudaStreamSynchronize(s));
+        slow_count = flags[0];
+        if (flags[1]) throw CudaError("ck_ann: internal invariant violated (budget cut emitted != budget rows)");
     } else {
         slow_count = static_cast<uint32_t>(P.nq);
         slow_list = nullptr;  // every query takes the general path
