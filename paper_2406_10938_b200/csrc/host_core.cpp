@@ -249,6 +249,22 @@ __attribute__((target("avx2,popcnt"))) size_t hoare_scan_avx2(float* a, size_t l
     int64_t lgen = i + 1, rgen = j - 1;
     const __m256 vp = _mm256_set1_ps(pv);
     for (;;) {
+        // batch of ordered pairs straight from both buffers: L ascending, R
+        // descending, so L_t < R_t already implies L_t < j and R_t > i
+        {
+            const int avail = std::min(ln - lh, rn - rh);
+            int t = 0;
+            while (t < avail && lb[lh + t] < rb[rh + t]) {
+                std::swap(a[lb[lh + t]], a[rb[rh + t]]);
+                ++t;
+            }
+            if (t) {
+                i = lb[lh + t - 1];
+                j = rb[rh + t - 1];
+                lh += t;
+                rh += t;
+            }
+        }
         int64_t in;
         for (;;) {  // next left stopper in (i, j)
             if (lh < ln) {
@@ -403,9 +419,17 @@ RefSampler::RefSampler(uint64_t n, uint64_t n_s, int n_regions, uint64_t seed)
 }
 
 const std::vector<uint32_t>& RefSampler::next_space_indices() {
+    // Partial Fisher-Yates (encoder.cpp:133-134).  The swap targets depend only
+    // on the RNG stream, so they are drawn first (same draws, same order) and
+    // the random-access swaps then run with the targets prefetched ahead.
+    constexpr uint64_t kAhead = 16;
+    std::vector<uint32_t>& tgt = targets_;
+    tgt.resize(n_s_);
+    for (uint64_t t = 0; t < n_s_; ++t) tgt[t] = static_cast<uint32_t>(t + rng_.bounded(n_ - t));
+    uint32_t* idx = idx_.data();
     for (uint64_t t = 0; t < n_s_; ++t) {
-        const uint64_t s = t + rng_.bounded(n_ - t);
-        std::swap(idx_[t], idx_[s]);
+        if (t + kAhead < n_s_) __builtin_prefetch(idx + tgt[t + kAhead], 1);
+        std::swap(idx[t], idx[tgt[t]]);
     }
     std::copy(idx_.begin(), idx_.begin() + static_cast<ptrdiff_t>(n_s_), sample_idx_.begin());
     return sample_idx_;

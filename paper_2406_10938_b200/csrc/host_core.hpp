@@ -74,6 +74,7 @@ private:
     Rng rng_;
     std::vector<uint32_t> idx_;
     std::vector<uint32_t> sample_idx_;
+    std::vector<uint32_t> targets_;
     uint64_t draws_ = 0;
 };
 
