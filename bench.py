@@ -159,14 +159,33 @@ def recall_ratio(res_ids, res_d, n_hits, gt_ids, gt_d, k):
 
 
 # algorithmic bytes per launch; kernels without a model get null
-def algo_bytes(kernel, n, d, nq, budget, K, L):
+def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0):
     if kernel == "project_exact":
         return 4.0 * d * n  # one read of the fp32 shard (4d B/point)
     if kernel == "query_fast":
         return 4.0 * d * budget * nq  # every verified candidate row (4d B/candidate)
     if kernel == "encode":
-        return 5.0 * L * K * n  # fp32 projections in, u8 codes out
+        return 5.0 * K * n  # one space per launch: fp32 projections in, u8 codes out
+    if kernel == "tree_build":
+        return (K + 4.0) * n  # one tree: read its codes, write the leaf-order permutation
+    if kernel == "rmin_dist":
+        return (4.0 * L * K + 8.0 * 10) * n  # read projections, write 10 probe distances
+    if kernel == "pack_u8":
+        return (4.0 * d + row_u8) * n
     return None
+
+
+def ncu_traffic(kernel, units):
+    """dram__bytes_read+write for `kernel` from the committed ncu capture
+    (profiles/ncu_latest.json: bytes per unit), scaled to this launch."""
+    path = os.path.join(ROOT, "profiles", "ncu_latest.json")
+    try:
+        with open(path) as f:
+            table = json.load(f)
+        rec = table.get(kernel) or table[kernel + "_kernel"]
+        return rec["dram_bytes_per_unit"] * units, rec["source"]
+    except Exception:
+        return None, None
 
 
 def peaks():
@@ -350,6 +369,16 @@ def main():
     build_launches = (lib.detlsh_launch_count() - lc0) / args.steps
     prof_build = collect_profile(lib)
     build_ms = max_over_ranks(build_ms)
+    # the GPU-native breakpoint sample, reported beside the headline
+    other = "gpu" if args.sample == "reference" else "reference"
+
+    def build_other():
+        return D.build_index(dev_shard, params, seed=args.seed, sample=other, borrow=True,
+                             keep_codes=False)
+
+    build_other()
+    other_ms, _ = timed(build_other, args.steps)
+    other_ms = max_over_ranks(other_ms)
     stage_ms = idx.build_timings()
 
     # ---------------- queries ----------------
@@ -431,7 +460,11 @@ def main():
     build_roof = roofline(prof_build, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
                           exclude=("query_fast", "query_slow"))
     query_roof = roofline(prof_query, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
-                          only=("query_fast",))
+                          only=("query_fast",), row_u8=idx.row_u8())
+    # the reference arm scores its first cpu_queries queries: same subset here
+    m_ref = min(args.cpu_queries, nq)
+    rec_ref, rat_ref = recall_ratio(out_ids[:m_ref], out_d[:m_ref], out_h[:m_ref], gt_ids[:m_ref],
+                                    gt_d[:m_ref], k)
     value = n / (build_ms / 1e3) / 1e6
     qps = nq / (query_ms / 1e3)
     line = {
@@ -444,7 +477,9 @@ def main():
                    "sample_mode": args.sample, "parallelism": f"point-shard x{world}",
                    "l2": "inputs larger than L2 (dataset 512 MB, candidate rows 51 MB/query)"},
         "query": {"value": round(qps, 2), "unit": "queries/s", "ms_per_step": round(query_ms, 3),
-                  "recall": round(rec, 6), "ratio": round(rat, 6), "gpu_launches": query_launches,
+                  "recall": round(rec, 6), "ratio": round(rat, 6),
+                  "recall_on_reference_sample": round(rec_ref, 6),
+                  "ratio_on_reference_sample": round(rat_ref, 6), "gpu_launches": query_launches,
                   "roofline": query_roof,
                   "e2e": {"value": round(nq / (e2e_query_ms / 1e3), 2), "unit": "queries/s",
                           "h2d_bytes_per_step": int(nq * d * 4),
@@ -452,6 +487,10 @@ def main():
         "e2e": {"value": round(n / (e2e_build_ms / 1e3) / 1e6, 3), "unit": "Mpoints/s",
                 "h2d_bytes_per_step": int(n_loc * d * 4), "d2h_bytes_per_step": 96},
         "gpu_launches": build_launches,
+        "build_other_sample": {"sample_mode": other, "value": round(n / (other_ms / 1e3) / 1e6, 3),
+                               "unit": "Mpoints/s", "ms_per_step": round(other_ms, 3),
+                               "parity": "hybrid oracle (reference stage functions, same table)"
+                               if other == "gpu" else "bit-exact vs reference"},
         "roofline": build_roof,
         "build_stages_ms": {k2: round(v, 3) for k2, v in stage_ms.items()},
         "kernels_ms_per_step": {"build": {k2: round(v[0] / args.steps, 4) for k2, v in prof_build.items()},
@@ -479,23 +518,33 @@ def collect_profile(lib):
     return {kk: (float(ms[i]), int(cnt[i])) for i, kk in enumerate(keys)}
 
 
-def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exclude=()):
-    items = [(kk, v) for kk, v in prof.items() if (only is None or kk in only) and kk not in exclude]
+def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exclude=(),
+             row_u8=0):
+    # nested scopes (tree_level_split inside tree_build) are not separate work
+    items = [(kk, v) for kk, v in prof.items()
+             if (only is None or kk in only) and kk not in exclude and kk != "tree_level_split"]
     if not items:
         return None
     kern, (ms, launches) = max(items, key=lambda kv: kv[1][0])
     per_launch_ms = ms / max(1, launches)
-    b = algo_bytes(kern, n, d, nq, budget, K, L)
-    total = sum(v[0] for v in prof.values() if v is not None)
+    b = algo_bytes(kern, n, d, nq, budget, K, L, row_u8)
+    total = sum(v[0] for kk, v in prof.items() if kk != "tree_level_split")
+    units = nq if kern == "query_fast" else n
+    traffic, tsrc = ncu_traffic(kern, units)
     out = {"kernel": kern, "bound": "hbm", "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-           "launch_ms": round(per_launch_ms, 4), "share_of_kernel_time": round(ms / total, 4) if total else None,
-           "traffic": None}
+           "launch_ms": round(per_launch_ms, 4), "launches_per_step": launches / steps,
+           "share_of_kernel_time": round(ms / total, 4) if total else None,
+           "traffic": traffic, "traffic_source": tsrc}
     if b is None:
         out.update({"achieved": None, "frac": None})
     else:
         ach = b / (per_launch_ms / 1e3) / 1e9
         out.update({"achieved": round(ach, 2), "frac": round(ach / hbm, 5),
                     "algorithmic_bytes": b})
+        if kern == "query_fast" and row_u8:
+            b8 = float(row_u8) * budget * nq  # bytes the u8 rows actually hold
+            out["u8_rows"] = {"bytes": b8, "achieved": round(b8 / (per_launch_ms / 1e3) / 1e9, 2),
+                              "frac": round(b8 / (per_launch_ms / 1e3) / 1e9 / hbm, 5)}
     return out
 
 

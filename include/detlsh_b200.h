@@ -134,6 +134,8 @@ int detlsh_gpu_get_params(const detlsh_gpu_index* index, detlsh_params* out);
 uint64_t detlsh_gpu_n(const detlsh_gpu_index* index);
 int32_t detlsh_gpu_d(const detlsh_gpu_index* index);
 uint64_t detlsh_gpu_sample_size(const detlsh_gpu_index* index);
+/* Bytes per exact-u8 verification row (0 when the dataset is not integral in [0,255]). */
+int32_t detlsh_gpu_row_u8(const detlsh_gpu_index* index);
 int detlsh_gpu_export_family(const detlsh_gpu_index* index, float* out /* [L][K][d] */);
 int detlsh_gpu_export_table(const detlsh_gpu_index* index, float* out /* [L][K][N_r+1] */);
 int detlsh_gpu_export_codes(const detlsh_gpu_index* index, uint8_t* out /* [L][n][K] */);

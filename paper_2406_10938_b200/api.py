@@ -172,6 +172,10 @@ class DetIndex:
     def sample_size(self) -> int:
         return int(_lib.load().detlsh_gpu_sample_size(self._h))
 
+    def row_u8(self) -> int:
+        """Bytes per exact-u8 verification row (0: fp64 verification only)."""
+        return int(_lib.load().detlsh_gpu_row_u8(self._h))
+
     def table(self) -> np.ndarray:
         p = self.params
         out = np.empty((p.L, p.K, p.n_regions + 1), np.float32)

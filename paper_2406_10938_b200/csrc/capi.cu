@@ -202,6 +202,9 @@ int detlsh_gpu_get_params(const detlsh_gpu_index* index, detlsh_params* out) {
 }
 uint64_t detlsh_gpu_n(const detlsh_gpu_index* index) { return index ? index->impl->n : 0; }
 int32_t detlsh_gpu_d(const detlsh_gpu_index* index) { return index ? index->impl->d : 0; }
+int32_t detlsh_gpu_row_u8(const detlsh_gpu_index* index) {
+    return index ? index->impl->row_u8 : 0;
+}
 uint64_t detlsh_gpu_sample_size(const detlsh_gpu_index* index) {
     return index ? index->impl->sample_size : 0;
 }
