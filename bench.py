@@ -416,8 +416,10 @@ def main():
     clk = clocks.stop()
 
     # ---------------- end to end through the public API, host buffers ----------------
+    shard_pinned = torch.from_numpy(shard).pin_memory().numpy()  # host input, pinned
+
     def e2e_build():
-        ix = D.build_index(shard, params, seed=args.seed, sample=args.sample, keep_codes=False)
+        ix = D.build_index(shard_pinned, params, seed=args.seed, sample=args.sample, keep_codes=False)
         _ = ix.params.r_min  # result read back (params travel D2H inside build)
         return ix
 

@@ -58,6 +58,28 @@ private:
     std::exception_ptr err_;
 };
 
+// Per-thread pinned staging buffer, grown on demand and kept across builds
+// (cudaMallocHost costs milliseconds per call).
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+float* pinned_scratch(size_t bytes) {
+    thread_local PinnedBuf buf;
+    if (buf.bytes < bytes) {
+        if (buf.p) cudaFreeHost(buf.p);
+        buf.p = nullptr;
+        buf.bytes = 0;
+        DETLSH_CUDA(cudaMallocHost(&buf.p, bytes));
+        buf.bytes = bytes;
+    }
+    return static_cast<float*>(buf.p);
+}
+
 // GPU-native sample: per-space Feistel sample + exact order statistics.
 void breakpoints_gpu(GpuIndex& X, const float* d_proj, uint64_t seed, cudaStream_t s) {
     const int K = X.params.K, L = X.params.L, NR = X.params.n_regions;
@@ -282,9 +304,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         RefSampler sampler(n, n_s, NR, mix_seed(seed, kStreamBreakpoints));
         DevBuf<uint32_t> d_idx(n_s);
         DevBuf<float> d_sample(static_cast<size_t>(K) * n_s);
-        float* h_sample = nullptr;
-        DETLSH_CUDA(cudaMallocHost(&h_sample, static_cast<size_t>(K) * n_s * sizeof(float)));
-        std::unique_ptr<float, decltype(&cudaFreeHost)> hs_guard(h_sample, &cudaFreeHost);
+        float* h_sample = pinned_scratch(static_cast<size_t>(K) * n_s * sizeof(float));
         X->h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
         for (int i = 0; i < L; ++i) {
             const auto& idx = sampler.next_space_indices();

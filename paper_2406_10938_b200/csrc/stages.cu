@@ -229,81 +229,153 @@ __global__ void encode_kernel(const float* __restrict__ proj, uint64_t n, int K,
 }
 
 // D[p][z] = min over spaces of the exact projected l2 (dataset.hpp:23-34 over K floats).
-__global__ void rmin_dist_kernel(const float* __restrict__ proj, uint64_t n, int K, int L,
-                                 const float* __restrict__ probe_proj, int np,
-                                 double* __restrict__ D) {
+// D[p][z] = min over spaces of the exact projected l2 distance; since sqrt is
+// monotone, min_i sqrt(acc_i) == sqrt(min_i acc_i) bit for bit, so one sqrt
+// per probe.  Also tracks each probe's min / max bit pattern (doubles >= 0
+// order like their bits) to seed the range-narrowing select.
+constexpr int kMaxProbes = 10;
+
+template <int KT>
+__global__ void __launch_bounds__(256) rmin_dist_kernel(
+    const float* __restrict__ proj, uint64_t n, int K, int L, const float* __restrict__ probe_proj,
+    int np, double* __restrict__ D, unsigned long long* __restrict__ lo_bits,
+    unsigned long long* __restrict__ hi_bits) {
     extern __shared__ float spp[];  // [np][L][K]
     for (int i = threadIdx.x; i < np * L * K; i += blockDim.x) spp[i] = probe_proj[i];
     __syncthreads();
+    unsigned long long mn[kMaxProbes], mx[kMaxProbes];
+#pragma unroll
+    for (int p = 0; p < kMaxProbes; ++p) {
+        mn[p] = ~0ULL;
+        mx[p] = 0;
+    }
     for (uint64_t z = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; z < n;
          z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        double best[16];
-        for (int p = 0; p < np; ++p) best[p] = __longlong_as_double(0x7ff0000000000000LL);
+        double best[kMaxProbes];
+#pragma unroll
+        for (int p = 0; p < kMaxProbes; ++p) best[p] = __longlong_as_double(0x7ff0000000000000LL);
         for (int i = 0; i < L; ++i) {
-            float x[kMaxK];
+            float x[KT];
             const float* row = proj + (static_cast<uint64_t>(i) * n + z) * K;
-            for (int j = 0; j < K; ++j) x[j] = row[j];
-            for (int p = 0; p < np; ++p) {
-                const float* q = spp + (p * L + i) * K;
-                double acc = 0.0;
-                for (int j = 0; j < K; ++j) {
-                    const double diff = __dsub_rn(static_cast<double>(q[j]), static_cast<double>(x[j]));
-                    acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+            if (KT == 16 && K == 16) {
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(row) + q4);
+                    x[4 * q4] = v.x; x[4 * q4 + 1] = v.y; x[4 * q4 + 2] = v.z; x[4 * q4 + 3] = v.w;
                 }
-                const double dist = __dsqrt_rn(acc);
-                best[p] = dist < best[p] ? dist : best[p];
+            } else {
+#pragma unroll
+                for (int j = 0; j < KT; ++j) x[j] = j < K ? __ldg(row + j) : 0.0f;
+            }
+#pragma unroll
+            for (int p = 0; p < kMaxProbes; ++p) {
+                if (p < np) {
+                    const float* q = spp + (p * L + i) * K;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int j = 0; j < KT; ++j) {
+                        if (j < K) {
+                            const double diff = __dsub_rn(static_cast<double>(q[j]), static_cast<double>(x[j]));
+                            acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                        }
+                    }
+                    best[p] = acc < best[p] ? acc : best[p];
+                }
             }
         }
-        for (int p = 0; p < np; ++p) D[static_cast<uint64_t>(p) * n + z] = best[p];
+#pragma unroll
+        for (int p = 0; p < kMaxProbes; ++p) {
+            if (p < np) {
+                const double dist = __dsqrt_rn(best[p]);
+                D[static_cast<uint64_t>(p) * n + z] = dist;
+                const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(dist));
+                mn[p] = b < mn[p] ? b : mn[p];
+                mx[p] = b > mx[p] ? b : mx[p];
+            }
+        }
+    }
+#pragma unroll
+    for (int p = 0; p < kMaxProbes; ++p) {
+        if (p < np) {
+            unsigned long long a = mn[p], b = mx[p];
+            for (int o = 16; o; o >>= 1) {
+                const unsigned long long ta = __shfl_xor_sync(0xffffffffu, a, o);
+                const unsigned long long tb = __shfl_xor_sync(0xffffffffu, b, o);
+                a = ta < a ? ta : a;
+                b = tb > b ? tb : b;
+            }
+            if ((threadIdx.x & 31) == 0) {
+                atomicMin(lo_bits + p, a);
+                atomicMax(hi_bits + p, b);
+            }
+        }
     }
 }
 
-// Multi-pass 16-bit-digit rank selection over non-negative doubles (bit
-// patterns order like the values).  hist: [np][65536].
-__global__ void select_hist_kernel(const double* __restrict__ D, uint64_t n, int np,
-                                   const uint64_t* __restrict__ prefix, int shift,
-                                   uint32_t* __restrict__ hist) {
+// Exact rank selection by range narrowing: each pass histograms the bit
+// patterns in [lo, hi] into 2048 bins of width 2^shift (block-private smem
+// histograms), keeps the bin holding the wanted rank.  shift reaches 0 after
+// at most 6 passes, leaving lo == the exact order statistic.
+constexpr int kSelBins = 2048;
+
+__global__ void rmin_sel_init(const unsigned long long* lo, const unsigned long long* hi, int np,
+                              int* shift) {
+    const int p = threadIdx.x;
+    if (p < np) {
+        const unsigned long long span = hi[p] - lo[p];
+        const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+        shift[p] = bits > 11 ? bits - 11 : 0;
+    }
+}
+
+__global__ void rmin_sel_hist(const double* __restrict__ D, uint64_t n,
+                              const unsigned long long* __restrict__ lo, const int* __restrict__ shift,
+                              uint32_t* __restrict__ ghist) {
+    __shared__ uint32_t h[kSelBins];
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+    __syncthreads();
     const int p = blockIdx.y;
-    const uint64_t pre = prefix[p];
-    const uint64_t hi_mask = shift + 16 >= 64 ? 0 : (~0ULL << (shift + 16));
+    const unsigned long long L0 = lo[p];
+    const int sh = shift[p];
     const double* Dp = D + static_cast<uint64_t>(p) * n;
     for (uint64_t z = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; z < n;
          z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t b = static_cast<uint64_t>(__double_as_longlong(Dp[z]));
-        if ((b & hi_mask) == (pre & hi_mask))
-            atomicAdd(&hist[static_cast<uint64_t>(p) * 65536 + ((b >> shift) & 0xffff)], 1u);
+        const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(Dp[z]));
+        if (b >= L0) {
+            const unsigned long long off = (b - L0) >> sh;
+            if (off < kSelBins) atomicAdd(&h[off], 1u);
+        }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+        if (h[i]) atomicAdd(&ghist[static_cast<size_t>(p) * kSelBins + i], h[i]);
 }
 
-__global__ void select_pick_kernel(uint32_t* __restrict__ hist, uint64_t* __restrict__ prefix,
-                                   uint64_t* __restrict__ need, int shift) {
-    // one block (1024 threads) per probe: find the bin holding rank `need`
+__global__ void rmin_sel_pick(uint32_t* __restrict__ ghist, unsigned long long* lo,
+                              unsigned long long* hi, int* shift, uint64_t* need) {
     const int p = blockIdx.x;
-    uint32_t* h = hist + static_cast<uint64_t>(p) * 65536;
-    __shared__ uint64_t part[1024];
-    const int per = 64;
-    uint64_t s = 0;
-    for (int i = 0; i < per; ++i) s += h[threadIdx.x * per + i];
-    part[threadIdx.x] = s;
-    __syncthreads();
+    uint32_t* h = ghist + static_cast<size_t>(p) * kSelBins;
     if (threadIdx.x == 0) {
         uint64_t want = need[p], cum = 0;
-        int blk = 0;
-        for (; blk < 1024; ++blk) {
-            if (cum + part[blk] >= want) break;
-            cum += part[blk];
+        int bin = 0;
+        for (; bin < kSelBins; ++bin) {
+            if (cum + h[bin] >= want) break;
+            cum += h[bin];
         }
-        int bin = blk * per;
-        for (int i = 0; i < per; ++i, ++bin) {
-            const uint64_t c = h[bin];
-            if (cum + c >= want) break;
-            cum += c;
-        }
+        if (bin == kSelBins) bin = kSelBins - 1;  // unreachable: rank <= count in range
+        const int sh = shift[p];
+        const unsigned long long nlo = lo[p] + (static_cast<unsigned long long>(bin) << sh);
+        unsigned long long nhi = nlo + ((1ULL << sh) - 1);
+        if (nhi > hi[p] || nhi < nlo) nhi = hi[p];
         need[p] = want - cum;
-        prefix[p] |= static_cast<uint64_t>(bin) << shift;
+        lo[p] = nlo;
+        hi[p] = nhi;
+        const unsigned long long span = nhi - nlo;
+        const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+        shift[p] = bits > 11 ? bits - 11 : 0;
     }
     __syncthreads();
-    for (int i = 0; i < per; ++i) h[threadIdx.x * per + i] = 0;
+    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
 }
 
 }  // namespace
@@ -387,24 +459,36 @@ void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float
     StreamScope scope(s);
     int dev = 0;
     cudaGetDevice(&dev);
+    if (np > kMaxProbes) throw InvalidArgument("estimate_rmin: at most 10 probes");
     const unsigned gx = static_cast<unsigned>(
-        std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8));
-    ProfScope ps("rmin_dist", s);
-    rmin_dist_kernel<<<gx, 256, static_cast<size_t>(np) * L * K * sizeof(float), s>>>(
-        d_proj, n, K, L, d_probe_proj, np, d_D);
-    DETLSH_LAUNCH_CHECK();
-    DevBuf<uint64_t> pre(np), need(np);
+        std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8)));
+    DevBuf<unsigned long long> lo(np), hi(np);
+    DevBuf<uint64_t> need(np);
+    DevBuf<int> shift(np);
     std::vector<uint64_t> h(np, rank);
-    DETLSH_CUDA(cudaMemsetAsync(pre.get(), 0, np * sizeof(uint64_t), s));
+    DETLSH_CUDA(cudaMemsetAsync(lo.get(), 0xff, np * sizeof(unsigned long long), s));
+    DETLSH_CUDA(cudaMemsetAsync(hi.get(), 0, np * sizeof(unsigned long long), s));
     DETLSH_CUDA(cudaMemcpyAsync(need.get(), h.data(), np * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    DETLSH_CUDA(cudaMemsetAsync(d_hist, 0, static_cast<size_t>(np) * 65536 * sizeof(uint32_t), s));
-    for (int shift = 48; shift >= 0; shift -= 16) {
-        select_hist_kernel<<<dim3(gx, np), 256, 0, s>>>(d_D, n, np, pre.get(), shift, d_hist);
-        DETLSH_LAUNCH_CHECK();
-        select_pick_kernel<<<np, 1024, 0, s>>>(d_hist, pre.get(), need.get(), shift);
+    DETLSH_CUDA(cudaMemsetAsync(d_hist, 0, static_cast<size_t>(np) * kSelBins * sizeof(uint32_t), s));
+    {
+        ProfScope ps("rmin_dist", s);
+        const size_t smem = static_cast<size_t>(np) * L * K * sizeof(float);
+        if (K == 16)
+            rmin_dist_kernel<16><<<gx, 256, smem, s>>>(d_proj, n, K, L, d_probe_proj, np, d_D, lo.get(), hi.get());
+        else
+            rmin_dist_kernel<kMaxK><<<gx, 256, smem, s>>>(d_proj, n, K, L, d_probe_proj, np, d_D, lo.get(), hi.get());
         DETLSH_LAUNCH_CHECK();
     }
-    DETLSH_CUDA(cudaMemcpyAsync(h_T_bits, pre.get(), np * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    ProfScope ps("rmin_select", s);
+    rmin_sel_init<<<1, 32, 0, s>>>(lo.get(), hi.get(), np, shift.get());
+    DETLSH_LAUNCH_CHECK();
+    for (int pass = 0; pass < 6; ++pass) {  // 53-bit spans need at most 5 passes of 11 bits
+        rmin_sel_hist<<<dim3(gx, np), 256, 0, s>>>(d_D, n, lo.get(), shift.get(), d_hist);
+        DETLSH_LAUNCH_CHECK();
+        rmin_sel_pick<<<np, 256, 0, s>>>(d_hist, lo.get(), hi.get(), shift.get(), need.get());
+        DETLSH_LAUNCH_CHECK();
+    }
+    DETLSH_CUDA(cudaMemcpyAsync(h_T_bits, lo.get(), np * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     DETLSH_CUDA(cudaStreamSynchronize(s));
 }
 
