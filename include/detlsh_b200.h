@@ -90,6 +90,9 @@ void detlsh_profile_enable(int32_t on);
  * ';'-separated into `names`.  Returns the number of entries. */
 int detlsh_profile_collect(char* names, int32_t names_cap, double* ms, uint64_t* launches,
                            int32_t cap);
+/* SM cycles per phase of the last profiled query batch, summed over CTAs:
+ * setup, leaf scan, budget cut, candidate emission, verification+top-k, output. */
+void detlsh_query_phase_cycles(double* out6);
 
 /* ---- index build ----------------------------------------------------------- */
 

@@ -24,6 +24,7 @@
 //     Every partial sum of the reference's double accumulation is then an
 //     exact integer < 2^53, so sqrt(double(int sum)) is bit-identical.
 #include <algorithm>
+#include <mutex>
 
 #include "query.cuh"
 
@@ -177,6 +178,50 @@ __device__ __forceinline__ double leaf_mindist(const QueryPlan& P, const QTree& 
         }
     }
     return __dsqrt_rn(acc);
+}
+
+// Branchless, two-leaf-interleaved mindist for K <= 16 (the fast path's hot
+// loop): per dim the penalty index is selected without branches (both edge
+// candidates are valid table indices), the per-query thresholds live in
+// registers (lub[j] = lbv | ubv << 16), and two independent fp64 chains give
+// ILP.  Same operations in the same order as leaf_mindist.
+__device__ __forceinline__ void box_words(const QTree& T, uint32_t li, uint32_t (&w)[8]) {
+    const uint4* box = reinterpret_cast<const uint4*>(T.leaf_box + static_cast<size_t>(li) * 64);
+    const uint4 a = __ldg(box), b = __ldg(box + 1);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+}
+
+__device__ __forceinline__ double pen_sq16(const double* __restrict__ sqj, uint32_t half, uint32_t lub,
+                                           int NR) {
+    const int lo = half & 0xff, hi = (half >> 8) & 0xff;
+    const int lbv = lub & 0xffff, ubv = lub >> 16;
+    const bool use_lo = lo > 0 && lo >= ubv;
+    const bool use_hi = hi < NR - 1 && hi + 1 < lbv;
+    const double v = sqj[use_lo ? lo : hi + 1];
+    return (use_lo || use_hi) ? v : 0.0;
+}
+
+__device__ __forceinline__ void leaf_mindist2_k16(const QueryPlan& P, const QTree& T, uint32_t li0,
+                                                  uint32_t li1, const Smem& S, const uint32_t (&lub)[16],
+                                                  double& md0, double& md1) {
+    uint32_t w0[8], w1[8];
+    box_words(T, li0, w0);
+    box_words(T, li1, w1);
+    const int W = P.NR + 1;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j < P.K) {
+            const double* sqj = S.sq + j * W;
+            const uint32_t h0 = w0[j >> 1] >> ((j & 1) * 16);
+            const uint32_t h1 = w1[j >> 1] >> ((j & 1) * 16);
+            a0 = __dadd_rn(a0, pen_sq16(sqj, h0, lub[j], P.NR));
+            a1 = __dadd_rn(a1, pen_sq16(sqj, h1, lub[j], P.NR));
+        }
+    }
+    md0 = __dsqrt_rn(a0);
+    md1 = __dsqrt_rn(a1);
 }
 
 // Exact original-space squared distance (dataset.hpp:23-30): sequential fp64.
@@ -461,20 +506,29 @@ __device__ __forceinline__ uint32_t sqdiff4(uint32_t a, uint32_t b, uint32_t acc
 // Fast path: tree 0, round 0 fills the budget.
 // ---------------------------------------------------------------------------
 struct FastSlot {
-    LeafItem *A, *B, *C;
-    uint32_t* pre;
-    uint32_t* cand;  // candidate rows as tree-0 permutation indices
+    LeafItem *A, *B, *C;  // bin-b* items and the select's ping-pong buffers
+    uint32_t* full;       // leaves taken whole (leaf indices)
+    uint16_t* bin16;      // per-leaf histogram bin (0xffff: outside the radius)
+    uint32_t* cand;       // candidate rows as tree-0 permutation indices
 };
 
-__device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl) {
+__device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl,
+                                              uint64_t budget) {
     uint8_t* p = base + static_cast<size_t>(blockIdx.x) * slot_bytes;
     FastSlot f;
     f.A = reinterpret_cast<LeafItem*>(p);
     f.B = f.A + maxl;
     f.C = f.B + maxl;
-    f.pre = reinterpret_cast<uint32_t*>(f.C + maxl);
-    f.cand = f.pre + maxl;
+    f.full = reinterpret_cast<uint32_t*>(f.C + maxl);
+    f.cand = f.full + maxl;
+    f.bin16 = reinterpret_cast<uint16_t*>(f.cand + budget);
     return f;
+}
+
+size_t fast_slot_bytes(uint32_t maxl, uint64_t budget) {
+    const size_t b = 3 * static_cast<size_t>(maxl) * sizeof(LeafItem) + 4 * static_cast<size_t>(maxl) +
+                     4 * budget + 2 * static_cast<size_t>(maxl);
+    return (b + 255) / 256 * 256;
 }
 
 __device__ void load_query_proj(const QueryPlan& P, uint64_t q, int tree, const Smem& S) {
@@ -585,28 +639,77 @@ __device__ void score_batch(const QueryPlan& P, const FastSlot& F, const Smem& S
     }
 }
 
-__global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
+__global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
-    const FastSlot F = fast_slot(scratch, slot_bytes, P.max_leaves);
+    const FastSlot F = fast_slot(scratch, slot_bytes, P.max_leaves, P.budget);
     const double radius = __dmul_rn(P.eps, P.r_min);
     const uint32_t B32 = static_cast<uint32_t>(P.budget);
     const QTree T0 = P.trees[0];
+    long long t_prev = clock64();
+    auto phase = [&](int i) {  // per-phase cycle accounting (thread 0, optional)
+        if (P.phase_cycles && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(P.phase_cycles + i, static_cast<unsigned long long>(t - t_prev));
+            t_prev = t;
+        }
+    };
     for (uint64_t q = blockIdx.x; q < P.nq; q += gridDim.x) {
         const bool u8 = load_query_vec(P, q, S);
         load_query_proj(P, q, 0, S);
         build_sq(P, 0, S);
-        uint32_t nA;
-        uint64_t W;
-        scan_leaves(P, 0, radius, S, F.A, nullptr, nA, W);
+        phase(0);
+        // pass 1: exact mindist of every leaf -> weight histogram over bins
+        // monotone in mindist; each leaf's bin is kept (0xffff: outside)
+        const uint32_t nl = T0.num_leaves;
+        for (int i = threadIdx.x; i < kBins; i += blockDim.x) S.bins[i] = 0;
+        if (threadIdx.x == 0) S.u64s[0] = 0;
+        const double scale = radius > 0.0 ? static_cast<double>(kBins) / radius : 0.0;
+        __syncthreads();
+        {
+            unsigned long long wsum = 0;
+            auto record = [&](uint32_t li, double md) {
+                uint32_t b = 0xffff;
+                if (md <= radius) {
+                    const uint32_t cnt = __ldg(T0.leaf_count + li);
+                    const double fb = __dmul_rn(md, scale);
+                    b = fb >= static_cast<double>(kBins - 1) ? kBins - 1 : static_cast<uint32_t>(fb);
+                    wsum += cnt;
+                    atomicAdd(&S.bins[b], cnt);
+                }
+                F.bin16[li] = static_cast<uint16_t>(b);
+            };
+            if (P.K <= 16) {
+                uint32_t lub[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    lub[j] = j < P.K ? (static_cast<uint32_t>(S.lbv[j]) | (static_cast<uint32_t>(S.ubv[j]) << 16)) : 0u;
+                for (uint32_t li0 = threadIdx.x; li0 < nl; li0 += 2 * blockDim.x) {
+                    const uint32_t li1 = li0 + blockDim.x;
+                    double md0, md1;
+                    leaf_mindist2_k16(P, T0, li0, li1 < nl ? li1 : li0, S, lub, md0, md1);
+                    record(li0, md0);
+                    if (li1 < nl) record(li1, md1);
+                }
+            } else {
+                for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) record(li, leaf_mindist(P, T0, li, S));
+            }
+            for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+            if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&S.u64s[0], wsum);
+        }
+        __syncthreads();
+        const uint64_t W = S.u64s[0];
+        __syncthreads();
+        phase(1);
+        if (P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 7, static_cast<unsigned long long>(W));
         if (W < P.budget) {  // budget does not fill in tree 0 round 0
             if (threadIdx.x == 0) slow_list[atomicAdd(slow_n, 1u)] = static_cast<uint32_t>(q);
             __syncthreads();
             continue;
         }
-        // the budget trips inside histogram bin b* (bins are monotone in
-        // mindist); only that bin's leaves need the exact (mindist, id) order
+        // the budget trips inside bin b*: leaves of lower bins are taken whole,
+        // only b*'s leaves need the exact (mindist, node id) order
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         if (threadIdx.x < 32) {
             constexpr int per = kBins / 32;
@@ -629,42 +732,84 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
                 S.u32s[2] = static_cast<uint32_t>(bin);
                 S.u64s[1] = P.budget - cum;
             }
-            if (lane == 0) S.u32s[1] = 0;
+            if (lane == 0) {
+                S.u32s[0] = 0;  // whole-leaf list
+                S.u32s[1] = 0;  // bin-b* list
+            }
         }
         __syncthreads();
         const uint32_t bstar = S.u32s[2];
         const uint64_t need_in_bin = S.u64s[1];
-        for (uint32_t base = 0; base < nA; base += blockDim.x) {
-            const uint32_t i = base + threadIdx.x;
-            bool ok = false;
-            LeafItem it;
-            if (i < nA) {
-                it = F.A[i];
-                ok = it.pad == bstar;
+        // pass 2: collect (li of whole leaves) and (exact items of bin b*)
+        for (uint32_t base = 0; base < nl; base += blockDim.x) {
+            const uint32_t li = base + threadIdx.x;
+            uint16_t b = 0xffff;
+            if (li < nl) b = F.bin16[li];
+            const bool whole = b < bstar;
+            const uint32_t m = __ballot_sync(0xffffffffu, whole);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                uint32_t b0 = 0;
+                if (lane == leader) b0 = atomicAdd(&S.u32s[0], static_cast<uint32_t>(__popc(m)));
+                b0 = __shfl_sync(0xffffffffu, b0, leader);
+                if (whole) F.full[b0 + __popc(m & ((1u << lane) - 1u))] = li;
             }
-            warp_append(ok, it, F.B, &S.u32s[1]);
+            const bool atb = b == bstar;
+            LeafItem it;
+            if (atb) {
+                const double md = leaf_mindist(P, T0, li, S);
+                it.mdb = static_cast<uint64_t>(__double_as_longlong(md));
+                it.id = __ldg(T0.leaf_node + li);
+                it.w = __ldg(T0.leaf_count + li);
+                it.li = li;
+                it.pad = b;
+            }
+            warp_append(atb, it, F.B, &S.u32s[1]);
         }
         __syncthreads();
         const uint32_t n_bin = S.u32s[1];  // weighted_select reuses this counter
         __syncthreads();
         uint64_t kmdb, take_cut;
         uint32_t kid;
-        weighted_select(F.B, n_bin, need_in_bin, F.C, F.B, S, kmdb, kid, take_cut);
-        // fused: exclusive prefix of the taken counts (A order) + candidate rows
-        // (tree-0 permutation indices; a leaf's rows are contiguous)
+        weighted_select(F.B, n_bin, need_in_bin, F.C, F.A, S, kmdb, kid, take_cut);
+        // b* leaves ordered before the cut leaf are whole too; find the cut leaf
+        for (uint32_t base = 0; base < n_bin; base += blockDim.x) {
+            const uint32_t i = base + threadIdx.x;
+            bool before = false;
+            uint32_t li = 0;
+            if (i < n_bin) {
+                const LeafItem it = F.B[i];
+                li = it.li;
+                before = key_less(it.mdb, it.id, kmdb, kid);
+                if (it.mdb == kmdb && it.id == kid) S.u32s[10] = it.li;
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, before);
+            if (m) {
+                const int leader = __ffs(m) - 1;
+                uint32_t b0 = 0;
+                if (lane == leader) b0 = atomicAdd(&S.u32s[0], static_cast<uint32_t>(__popc(m)));
+                b0 = __shfl_sync(0xffffffffu, b0, leader);
+                if (before) F.full[b0 + __popc(m & ((1u << lane) - 1u))] = li;
+            }
+        }
+        __syncthreads();
+        const uint32_t n_full = S.u32s[0];
+        const uint32_t cut_li = S.u32s[10];
+        phase(2);
+        // emission: whole leaves (block prefix of their sizes, then one warp per
+        // leaf writes its contiguous row range), then the cut leaf's prefix
         if (threadIdx.x == 0) S.u32s[3] = 0;
         __syncthreads();
-        for (uint32_t base = 0; base < nA; base += blockDim.x) {
+        uint32_t* st_dst = S.tl;  // the top-k staging area is free until verification
+        uint32_t* st_src = S.tl + kQueryThreads;
+        uint32_t* st_take = S.tl + 2 * kQueryThreads;
+        for (uint32_t base = 0; base < n_full; base += blockDim.x) {
             const uint32_t i = base + threadIdx.x;
             uint32_t take = 0, src = 0;
-            if (i < nA) {
-                const LeafItem it = F.A[i];
-                if (it.pad < bstar) take = it.w;
-                else if (it.pad == bstar) {
-                    if (key_less(it.mdb, it.id, kmdb, kid)) take = it.w;
-                    else if (it.mdb == kmdb && it.id == kid) take = static_cast<uint32_t>(take_cut);
-                }
-                if (take) src = __ldg(T0.leaf_begin + it.li);
+            if (i < n_full) {
+                const uint32_t li = F.full[i];
+                take = __ldg(T0.leaf_count + li);
+                src = __ldg(T0.leaf_begin + li);
             }
             uint32_t incl = take;
             for (int o = 1; o < 32; o <<= 1) {
@@ -679,19 +824,31 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
                 if (w < warp) wpre += wt[w];
                 tot += wt[w];
             }
-            const uint32_t dst = S.u32s[3] + wpre + incl - take;
-            // guard: never write past the budget (an inconsistent cut is
-            // reported below instead of corrupting memory)
-            for (uint32_t e = 0; e < take && dst + e < B32; ++e) F.cand[dst + e] = src + e;
+            st_dst[threadIdx.x] = S.u32s[3] + wpre + incl - take;
+            st_src[threadIdx.x] = src;
+            st_take[threadIdx.x] = take;
+            __syncthreads();
+            for (int t = warp * 32; t < warp * 32 + 32; ++t) {
+                const uint32_t d0 = st_dst[t], s0 = st_src[t], tk = st_take[t];
+                for (uint32_t e = lane; e < tk && d0 + e < B32; e += 32) F.cand[d0 + e] = s0 + e;
+            }
             __syncthreads();
             if (threadIdx.x == 0) S.u32s[3] += tot;
             __syncthreads();
         }
-        if (S.u32s[3] != B32) {  // invariant: the cut emits exactly `budget` rows
+        {
+            const uint32_t d0 = S.u32s[3];
+            const uint32_t s0 = __ldg(T0.leaf_begin + cut_li);
+            for (uint32_t e = threadIdx.x; e < take_cut && d0 + e < B32; e += blockDim.x)
+                F.cand[d0 + e] = s0 + e;
+        }
+        if (S.u32s[3] + take_cut != B32) {  // invariant: exactly `budget` rows emitted
             if (threadIdx.x == 0) atomicOr(slow_n + 1, 1u);
             __syncthreads();
             continue;
         }
+        __syncthreads();
+        phase(3);
         // exact verification + top-k (the penalty table region is reused)
         topk_init(S);
         for (uint32_t c0 = 0; c0 < B32; c0 += kBatch) {
@@ -701,6 +858,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
             topk_absorb(S, nb, P.k, u8 ? P.perm0 : nullptr);
         }
         const uint32_t nh = topk_finish(S, P.k);
+        phase(4);
         for (uint32_t t = threadIdx.x; t < nh; t += blockDim.x) {
             const uint64_t h = S.th[t];
             const double dist = u8 ? __dsqrt_rn(static_cast<double>(h)) : __longlong_as_double(static_cast<long long>(h));
@@ -713,6 +871,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_fast_kernel(
             if (P.cands) P.cands[q] = P.budget;
         }
         __syncthreads();
+        phase(5);
     }
 }
 
@@ -912,7 +1071,15 @@ __global__ void merge_topk_kernel(const double* __restrict__ sd, const uint64_t*
     }
 }
 
+std::mutex g_phase_mu;
+double g_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
 }  // namespace
+
+void last_query_phases(double* out6) {
+    std::lock_guard<std::mutex> lk(g_phase_mu);
+    for (int i = 0; i < 8; ++i) out6[i] = g_phase[i];
+}
 
 void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream_t s,
                      cudaStream_t alloc_s) {
@@ -934,6 +1101,12 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     grow_scratch(X.counters, 4);
     grow_scratch(X.slow_list, P.nq);
     DETLSH_CUDA(cudaMemsetAsync(X.counters.get(), 0, 16, s));
+    QueryPlan Pp = P;
+    if (profiling_enabled()) {
+        grow_scratch(X.phases, 8);
+        DETLSH_CUDA(cudaMemsetAsync(X.phases.get(), 0, 8 * sizeof(unsigned long long), s));
+        Pp.phase_cycles = X.phases.get();
+    }
     const size_t items = 3 * static_cast<size_t>(P.max_leaves) * sizeof(LeafItem);
     uint32_t slow_count = 0;
     const uint32_t* slow_list = X.slow_list.get();
@@ -941,16 +1114,23 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         int per_sm = 0;
         DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, query_fast_kernel, kQueryThreads, smem));
         per_sm = std::max(1, std::min(per_sm, 4));
-        const size_t fast_bytes = (items + 4 * static_cast<size_t>(P.max_leaves) + 4 * P.budget + 255) / 256 * 256;
+        const size_t fast_bytes = fast_slot_bytes(P.max_leaves, P.budget);
         const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
         grow_scratch(X.fast, slots * fast_bytes);
         ProfScope ps("query_fast", s);
         query_fast_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
-            P, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
+            Pp, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
         DETLSH_LAUNCH_CHECK();
         uint32_t flags[2] = {0, 0};
         DETLSH_CUDA(cudaMemcpyAsync(flags, X.counters.get(), 8, cudaMemcpyDeviceToHost, s));
+        unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (Pp.phase_cycles)
+            DETLSH_CUDA(cudaMemcpyAsync(ph, Pp.phase_cycles, sizeof(ph), cudaMemcpyDeviceToHost, s));
         DETLSH_CUDA(cudaStreamSynchronize(s));
+        if (Pp.phase_cycles) {
+            std::lock_guard<std::mutex> lk(g_phase_mu);
+            for (int i = 0; i < 8; ++i) g_phase[i] = static_cast<double>(ph[i]);
+        }
         slow_count = flags[0];
         if (flags[1]) throw CudaError("ck_ann: internal invariant violated (budget cut emitted != budget rows)");
     } else {

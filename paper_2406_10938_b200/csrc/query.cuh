@@ -43,6 +43,9 @@ struct QueryPlan {
     int32_t* n_hits;
     double* radius;
     uint64_t* cands;
+    // optional: per-phase SM cycles of the fast path (setup, leaf scan, cut,
+    // emission, verification+top-k, output), summed over CTAs
+    unsigned long long* phase_cycles;
 };
 
 constexpr int kQueryThreads = 256;
@@ -56,8 +59,13 @@ struct QueryScratch {
     DevBuf<uint8_t> slow;  // per-slot bitmap + members
     DevBuf<uint32_t> slow_list;
     DevBuf<uint32_t> counters;
+    DevBuf<unsigned long long> phases;  // [6] fast-path phase cycles (profiling only)
     size_t fast_slots = 0, slow_slots = 0;
 };
+
+// Phase cycles of the last profiled fast-path launch (setup, leaf scan, cut,
+// emission, verification+top-k, output), summed over CTAs.
+void last_query_phases(double* out6);
 
 void run_query_batch(const QueryPlan& plan, QueryScratch& scratch, int device, cudaStream_t s,
                      cudaStream_t alloc_s);
