@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <mutex>
 
+#include "primitives.cuh"
 #include "query.cuh"
 
 namespace detlsh_b200 {
@@ -570,7 +571,7 @@ __device__ void score_batch(const QueryPlan& P, const FastSlot& F, const Smem& S
         // row loads in flight.  bl holds the ROW index (tree-0 permutation
         // index); topk_absorb maps it to the dataset position only for the
         // rare keys that can enter the top-k.
-        constexpr int kU = 4;
+        constexpr int kU = 8;
         for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) S.bl[i] = F.cand[base + i];
         __syncthreads();
         const int lpr = P.u8_lpr;
@@ -655,7 +656,8 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             t_prev = t;
         }
     };
-    for (uint64_t q = blockIdx.x; q < P.nq; q += gridDim.x) {
+    for (uint64_t qs = blockIdx.x; qs < P.nq; qs += gridDim.x) {
+        const uint64_t q = P.order ? P.order[qs] : qs;
         const bool u8 = load_query_vec(P, q, S);
         load_query_proj(P, q, 0, S);
         build_sq(P, 0, S);
@@ -1071,6 +1073,34 @@ __global__ void merge_topk_kernel(const double* __restrict__ sd, const uint64_t*
     }
 }
 
+// Locality key of a query: the tree-0 path bits of its space-0 codes -- the
+// top bit of every dim (the root slot) above the second bit of every dim.
+// Sorting by it lets concurrently running CTAs share candidate rows in L2.
+__global__ void query_order_keys(const float* __restrict__ qproj0, uint64_t nq, int K,
+                                 const float* __restrict__ table0, int NR, int sbits,
+                                 uint32_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+    for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < nq;
+         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t top = 0, second = 0;
+        const int W = NR + 1;
+        for (int j = 0; j < K && j < 16; ++j) {
+            const float v = qproj0[q * K + j];
+            const float* row = table0 + static_cast<size_t>(j) * W;
+            int lo = 0, hi = W;  // lower_bound
+            while (lo < hi) {
+                const int m = (lo + hi) >> 1;
+                if (row[m] < v) lo = m + 1; else hi = m;
+            }
+            int reg = lo - 1;
+            reg = reg < 0 ? 0 : (reg > NR - 1 ? NR - 1 : reg);
+            top |= static_cast<uint32_t>((reg >> (sbits - 1)) & 1) << j;
+            if (sbits > 1) second |= static_cast<uint32_t>((reg >> (sbits - 2)) & 1) << j;
+        }
+        keys[q] = (top << 16) | second;
+        idx[q] = static_cast<uint32_t>(q);
+    }
+}
+
 std::mutex g_phase_mu;
 double g_phase[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 
@@ -1106,6 +1136,25 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         grow_scratch(X.phases, 8);
         DETLSH_CUDA(cudaMemsetAsync(X.phases.get(), 0, 8 * sizeof(unsigned long long), s));
         Pp.phase_cycles = X.phases.get();
+    }
+    // locality-aware processing order for large batches (results are written
+    // to each query's own slot, so the order is invisible to the caller)
+    DevBuf<uint32_t> ok0, ok1, ov0, ov1, otmp;  // freed stream-ordered after the kernels
+    if (P.nq >= 4096) {
+        const uint64_t nq = P.nq;
+        ok0.alloc(nq);
+        ok1.alloc(nq);
+        ov0.alloc(nq);
+        ov1.alloc(nq);
+        otmp.alloc(radix_temp_elems(nq));
+        int sbits = 0;
+        while ((1 << sbits) < P.NR) ++sbits;
+        const unsigned g = static_cast<unsigned>(std::min<uint64_t>((nq + 255) / 256, 4096));
+        query_order_keys<<<g, 256, 0, s>>>(P.qproj, nq, P.K, P.table, P.NR, sbits, ok0.get(), ov0.get());
+        DETLSH_LAUNCH_CHECK();
+        const bool flip = radix_sort_pairs<uint32_t>(ok0.get(), ov0.get(), ok1.get(), ov1.get(), nq, 0,
+                                                     32, otmp.get(), s);
+        Pp.order = flip ? ov1.get() : ov0.get();
     }
     const size_t items = 3 * static_cast<size_t>(P.max_leaves) * sizeof(LeafItem);
     uint32_t slow_count = 0;

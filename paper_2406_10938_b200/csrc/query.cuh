@@ -46,6 +46,8 @@ struct QueryPlan {
     // optional: per-phase SM cycles of the fast path (setup, leaf scan, cut,
     // emission, verification+top-k, output), summed over CTAs
     unsigned long long* phase_cycles;
+    // optional processing order (locality): processing slot i handles query order[i]
+    const uint32_t* order;
 };
 
 constexpr int kQueryThreads = 256;
