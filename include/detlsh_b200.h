@@ -90,6 +90,9 @@ void detlsh_profile_enable(int32_t on);
  * ';'-separated into `names`.  Returns the number of entries. */
 int detlsh_profile_collect(char* names, int32_t names_cap, double* ms, uint64_t* launches,
                            int32_t cap);
+/* Self-test of the tensor-core path: C[128][N] = A[128][K] . B[N][K]^T on one
+ * tcgen05 (kind::i8, u8 x u8 -> s32) tile; host pointers. */
+int detlsh_test_tc_gemm_u8(const uint8_t* A, const uint8_t* B, int32_t N, int32_t K, int32_t* C);
 /* SM cycles per phase of the last profiled query batch, summed over CTAs:
  * setup, leaf scan, budget cut, candidate emission, verification+top-k, output. */
 void detlsh_query_phase_cycles(double* out6);

@@ -73,6 +73,7 @@ def load() -> C.CDLL:
         "detlsh_select_row_breakpoints": ([vp, u64, i32, u64, vp, C.POINTER(u64)], C.c_int),
         "detlsh_launch_count": ([], u64),
         "detlsh_query_phase_cycles": ([vp], None),
+        "detlsh_test_tc_gemm_u8": ([vp, vp, i32, i32, vp], C.c_int),
         "detlsh_profile_enable": ([i32], None),
         "detlsh_profile_collect": ([C.c_char_p, i32, vp, vp, i32], C.c_int),
         "detlsh_gpu_build": ([vp, u64, i32, P, u64, i32, u32, C.POINTER(vp)], C.c_int),

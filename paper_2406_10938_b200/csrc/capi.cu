@@ -130,6 +130,9 @@ int detlsh_select_row_breakpoints(float* sample, uint64_t n_s, int32_t n_regions
 
 uint64_t detlsh_launch_count(void) { return launch_count(); }
 void detlsh_query_phase_cycles(double* out6) { last_query_phases(out6); }
+int detlsh_test_tc_gemm_u8(const uint8_t* A, const uint8_t* B, int32_t N, int32_t K, int32_t* C) {
+    return guarded([&] { tc_gemm_u8_test(A, B, N, K, C); });
+}
 void detlsh_profile_enable(int32_t on) { profile_enable(on != 0); }
 int detlsh_profile_collect(char* names, int32_t names_cap, double* ms, uint64_t* launches,
                            int32_t cap) {

@@ -65,6 +65,9 @@ struct QueryScratch {
     size_t fast_slots = 0, slow_slots = 0;
 };
 
+// tcgen05 kind::i8 self-test (tc_score.cu): C[128][N] = A[128][K] . B[N][K]^T.
+void tc_gemm_u8_test(const uint8_t* hA, const uint8_t* hB, int N, int K, int32_t* hC);
+
 // Phase cycles of the last profiled fast-path launch (setup, leaf scan, cut,
 // emission, verification+top-k, output), summed over CTAs.
 void last_query_phases(double* out6);
