@@ -41,6 +41,8 @@ extern "C" {
 #define DETLSH_F_BORROW_DATA 0x4u  /* with DEVICE_PTRS: keep the caller's device dataset */
 #define DETLSH_F_NO_CODES 0x8u     /* drop the [L][n][K] code array after build */
 #define DETLSH_F_NO_U8 0x10u       /* never use the exact u8 verification rows (fp64 path only) */
+#define DETLSH_F_NO_TC 0x20u       /* query: verify on the per-query gather path only (no
+                                      tcgen05 dataset-major scoring); results are identical */
 
 /* detlsh::LshParams (projection.hpp:79-92), same field order and meaning:
  * beta <= 0 -> derived; r_min <= 0 -> estimated at build; epsilon/alpha1/

@@ -25,6 +25,7 @@ F_SAMPLE_GPU = 0x2
 F_BORROW_DATA = 0x4
 F_NO_CODES = 0x8
 F_NO_U8 = 0x10
+F_NO_TC = 0x20
 
 
 class Params(C.Structure):

@@ -26,7 +26,8 @@ from dataclasses import dataclass, field, fields
 import numpy as np
 
 from . import _lib
-from ._lib import F_BORROW_DATA, F_DEVICE_PTRS, F_NO_CODES, F_NO_U8, F_SAMPLE_GPU, Params, check
+from ._lib import (F_BORROW_DATA, F_DEVICE_PTRS, F_NO_CODES, F_NO_TC, F_NO_U8, F_SAMPLE_GPU,
+                   Params, check)
 
 SAMPLE_REFERENCE = "reference"
 SAMPLE_GPU = "gpu"
@@ -288,29 +289,35 @@ class BatchResult:
                            float(self.radius_used[i]), int(self.candidates_seen[i]))
 
 
-def ck_ann_batch(index: DetIndex, queries, k: int, *, stream=None) -> BatchResult:
-    """Batched ck_ann over host queries [nq][d] (outputs on the host)."""
+def ck_ann_batch(index: DetIndex, queries, k: int, *, stream=None,
+                 tensor_cores: bool = True) -> BatchResult:
+    """Batched ck_ann over host queries [nq][d] (outputs on the host).
+
+    tensor_cores=False keeps verification on the per-query gather path (no
+    tcgen05 dataset-major scoring); the results are identical either way."""
     Q = _as_host_f32(queries)
     if Q.shape[1] != index.d():
         raise ValueError("ck_ann: query dimension mismatch")
     nq = Q.shape[0]
     out = BatchResult(np.zeros((nq, k), np.uint32), np.zeros((nq, k), np.float64),
                       np.zeros(nq, np.int32), np.zeros(nq, np.float64), np.zeros(nq, np.uint64))
-    check(_lib.load().detlsh_gpu_query(index.handle, _ptr(Q), nq, k, 0, _ptr(out.ids),
+    flags = 0 if tensor_cores else F_NO_TC
+    check(_lib.load().detlsh_gpu_query(index.handle, _ptr(Q), nq, k, flags, _ptr(out.ids),
                                        _ptr(out.dists), _ptr(out.n_hits), _ptr(out.radius_used),
                                        _ptr(out.candidates_seen), stream))
     return out
 
 
 def ck_ann_device(index: DetIndex, queries, k: int, ids, dists, n_hits=None, radius=None,
-                  cands=None, stream=None) -> None:
+                  cands=None, stream=None, tensor_cores: bool = True) -> None:
     """Batched ck_ann on device tensors (stream-ordered, no host copies)."""
     def p(t):
         return C.c_void_p(t.data_ptr()) if t is not None else None
     if queries.shape[1] != index.d():
         raise ValueError("ck_ann: query dimension mismatch")
+    flags = F_DEVICE_PTRS | (0 if tensor_cores else F_NO_TC)
     check(_lib.load().detlsh_gpu_query(index.handle, p(queries), int(queries.shape[0]), k,
-                                       F_DEVICE_PTRS, p(ids), p(dists), p(n_hits), p(radius),
+                                       flags, p(ids), p(dists), p(n_hits), p(radius),
                                        p(cands), stream))
 
 

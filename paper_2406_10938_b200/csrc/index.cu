@@ -340,13 +340,19 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     // exact u8 verification rows, in tree-0 leaf order (query.cu)
     t0 = Clock::now();
     if (!(flags & DETLSH_F_NO_U8) && data_is_u8(X->data, n * static_cast<uint64_t>(d), s)) {
-        X->row_u8 = (d + 15) / 16 * 16;
+        X->row_u8 = (d + 31) / 32 * 32;  // whole 32-byte MMA K steps
         const int chunks = X->row_u8 / 16;
         int lpr = 1;
         while (lpr < chunks && lpr < 32) lpr <<= 1;
         X->u8_lpr = lpr;
         X->data_u8.alloc(n * static_cast<size_t>(X->row_u8));
         launch_pack_u8(X->data, X->trees[0]->perm.get(), n, d, X->row_u8, X->data_u8.get(), s);
+        X->xn_u8.alloc(n);
+        launch_row_norms_u8(X->data_u8.get(), n, X->row_u8, X->xn_u8.get(), s);
+        if (X->row_u8 <= 256) {  // tensor-core verification operand tiles
+            X->data_tc.alloc((n + 127) / 128 * 128 * static_cast<uint64_t>(X->row_u8));
+            launch_pack_tc_tiles(X->data_u8.get(), n, X->row_u8, X->data_tc.get(), s);
+        }
     }
     X->timings.emplace_back("pack_u8", ms_since(t0));
     X->params.r_min = r_min;
@@ -397,6 +403,11 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     P.trees = X.qtrees.get();
     P.perm0 = X.trees[0]->perm.get();
     P.data_u8 = X.data_u8.get();
+    P.xn_u8 = X.xn_u8.get();
+    P.data_tc = X.data_tc.get();
+    P.q_begin = 0;
+    P.q_end = nq;
+    P.tc_allowed = (flags & DETLSH_F_NO_TC) ? 0 : 1;
     P.row_u8 = X.row_u8;
     P.u8_lpr = X.u8_lpr;
     P.eps = X.params.epsilon;

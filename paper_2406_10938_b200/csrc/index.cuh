@@ -37,6 +37,8 @@ struct GpuIndex {
     std::vector<float> h_table;
     DevBuf<uint8_t> codes;
     DevBuf<uint8_t> data_u8;  // exact u8 rows in tree-0 leaf order (integral datasets)
+    DevBuf<int32_t> xn_u8;    // |x|^2 of those rows (tensor-core verification)
+    DevBuf<uint8_t> data_tc;  // those rows as 128-row MMA operand tiles
     int row_u8 = 0, u8_lpr = 0;
     std::vector<std::unique_ptr<DevTree>> trees;
     DevBuf<QTree> qtrees;

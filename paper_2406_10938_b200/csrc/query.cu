@@ -24,6 +24,8 @@
 //     Every partial sum of the reference's double accumulation is then an
 //     exact integer < 2^53, so sqrt(double(int sum)) is bit-identical.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "primitives.cuh"
@@ -36,6 +38,8 @@ namespace {
 constexpr int kBatch = 1024;                    // candidates scored per block step
 constexpr int kTopCap = 2048;                   // staged (key, pos) entries
 constexpr int kBins = 1024;                     // mindist histogram bins (fast-path cut)
+constexpr uint32_t kTcMinBudget = 8192;         // tensor-core hand-off from this budget on
+constexpr uint32_t kTauRows = 512;              // min rows scored exactly to set tau^2
 static_assert(kFastMaxK == kTopCap - kBatch, "fast-path k bound");
 
 struct LeafItem {
@@ -640,6 +644,55 @@ __device__ void score_batch(const QueryPlan& P, const FastSlot& F, const Smem& S
     }
 }
 
+// Writes the rows of whole leaves `list[0..n)` (tree-0 permutation indices,
+// contiguous per leaf) to cand[0..): a block prefix over leaf sizes, then one
+// warp per leaf.  Returns the number of rows (writes beyond `cap` dropped).
+__device__ uint32_t emit_rows(const uint32_t* list, uint32_t n, const QTree& T0, uint32_t* cand,
+                              uint32_t cap, const Smem& S) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) S.u32s[3] = 0;
+    __syncthreads();
+    uint32_t* st_dst = S.tl;  // the top-k staging area is free outside verification
+    uint32_t* st_src = S.tl + kQueryThreads;
+    uint32_t* st_take = S.tl + 2 * kQueryThreads;
+    for (uint32_t base = 0; base < n; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        uint32_t take = 0, src = 0;
+        if (i < n) {
+            const uint32_t li = list[i];
+            take = __ldg(T0.leaf_count + li);
+            src = __ldg(T0.leaf_begin + li);
+        }
+        uint32_t incl = take;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        uint32_t* wt = reinterpret_cast<uint32_t*>(S.hist);
+        if (lane == 31) wt[warp] = incl;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+        for (int w = 0; w < kQueryThreads / 32; ++w) {
+            if (w < warp) wpre += wt[w];
+            tot += wt[w];
+        }
+        st_dst[threadIdx.x] = S.u32s[3] + wpre + incl - take;
+        st_src[threadIdx.x] = src;
+        st_take[threadIdx.x] = take;
+        __syncthreads();
+        for (int t = warp * 32; t < warp * 32 + 32; ++t) {
+            const uint32_t d0 = st_dst[t], s0 = st_src[t], tk = st_take[t];
+            for (uint32_t e = lane; e < tk && d0 + e < cap; e += 32) cand[d0 + e] = s0 + e;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) S.u32s[3] += tot;
+        __syncthreads();
+    }
+    const uint32_t total = S.u32s[3];
+    __syncthreads();
+    return total;
+}
+
 __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -656,7 +709,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             t_prev = t;
         }
     };
-    for (uint64_t qs = blockIdx.x; qs < P.nq; qs += gridDim.x) {
+    for (uint64_t qs = P.q_begin + blockIdx.x; qs < P.q_end; qs += gridDim.x) {
         const uint64_t q = P.order ? P.order[qs] : qs;
         const bool u8 = load_query_vec(P, q, S);
         load_query_proj(P, q, 0, S);
@@ -798,53 +851,112 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         const uint32_t n_full = S.u32s[0];
         const uint32_t cut_li = S.u32s[10];
         phase(2);
-        // emission: whole leaves (block prefix of their sizes, then one warp per
-        // leaf writes its contiguous row range), then the cut leaf's prefix
-        if (threadIdx.x == 0) S.u32s[3] = 0;
-        __syncthreads();
-        uint32_t* st_dst = S.tl;  // the top-k staging area is free until verification
-        uint32_t* st_src = S.tl + kQueryThreads;
-        uint32_t* st_take = S.tl + 2 * kQueryThreads;
-        for (uint32_t base = 0; base < n_full; base += blockDim.x) {
-            const uint32_t i = base + threadIdx.x;
-            uint32_t take = 0, src = 0;
-            if (i < n_full) {
-                const uint32_t li = F.full[i];
-                take = __ldg(T0.leaf_count + li);
-                src = __ldg(T0.leaf_begin + li);
-            }
-            uint32_t incl = take;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            uint32_t* wt = reinterpret_cast<uint32_t*>(S.hist);
-            if (lane == 31) wt[warp] = incl;
+        // ---- tensor-core hand-off (u8 rows): exact tau^2 from the nearest
+        // leaves, the candidate SET as a bitmap; tc_score_kernel verifies it
+        bool tc = P.tc_bm != nullptr && u8 && B32 >= kTcMinBudget;
+        if (tc) {
+            if (threadIdx.x == 0) S.u32s[11] = 0xffffffffu;
             __syncthreads();
-            uint32_t wpre = 0, tot = 0;
-            for (int w = 0; w < kQueryThreads / 32; ++w) {
-                if (w < warp) wpre += wt[w];
-                tot += wt[w];
-            }
-            st_dst[threadIdx.x] = S.u32s[3] + wpre + incl - take;
-            st_src[threadIdx.x] = src;
-            st_take[threadIdx.x] = take;
-            __syncthreads();
-            for (int t = warp * 32; t < warp * 32 + 32; ++t) {
-                const uint32_t d0 = st_dst[t], s0 = st_src[t], tk = st_take[t];
-                for (uint32_t e = lane; e < tk && d0 + e < B32; e += 32) F.cand[d0 + e] = s0 + e;
+            if (threadIdx.x < 32) {  // b_tau: first bin whose cumulative rows reach kTauRows
+                constexpr int per = kBins / 32;
+                unsigned long long part = 0;
+                for (int b = 0; b < per; ++b) part += S.bins[lane * per + b];
+                unsigned long long incl = part;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const unsigned long long excl = incl - part;
+                const unsigned long long want = P.tc_tau_rows;
+                if (excl < want && want <= incl) {
+                    unsigned long long cum = excl;
+                    int bin = lane * per;
+                    for (int b = 0; b < per; ++b, ++bin) {
+                        cum += S.bins[bin];
+                        if (cum >= want) break;
+                    }
+                    S.u32s[11] = static_cast<uint32_t>(bin);
+                }
+                if (lane == 0) S.u32s[12] = 0;
             }
             __syncthreads();
-            if (threadIdx.x == 0) S.u32s[3] += tot;
+            tc = S.u32s[11] < bstar;  // uniform
             __syncthreads();
         }
+        if (tc) {
+            const uint32_t b_tau = S.u32s[11];
+            uint32_t* tau_list = reinterpret_cast<uint32_t*>(F.A);
+            for (uint32_t base = 0; base < n_full; base += blockDim.x) {
+                const uint32_t i = base + threadIdx.x;
+                uint32_t li = 0;
+                bool in = false;
+                if (i < n_full) {
+                    li = F.full[i];
+                    in = F.bin16[li] <= b_tau;
+                }
+                const uint32_t m = __ballot_sync(0xffffffffu, in);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    uint32_t b0 = 0;
+                    if (lane == leader) b0 = atomicAdd(&S.u32s[12], static_cast<uint32_t>(__popc(m)));
+                    b0 = __shfl_sync(0xffffffffu, b0, leader);
+                    if (in) tau_list[b0 + __popc(m & ((1u << lane) - 1u))] = li;
+                }
+            }
+            __syncthreads();
+            const uint32_t n_tau = S.u32s[12];
+            __syncthreads();
+            const uint32_t nt = emit_rows(tau_list, n_tau, T0, F.cand, B32, S);
+            // exact k-th smallest dist^2 among those rows
+            topk_init(S);
+            for (uint32_t c0 = 0; c0 < nt; c0 += kBatch) {
+                const uint32_t nb = min(static_cast<uint32_t>(kBatch), nt - c0);
+                score_batch(P, F, S, c0, nb, true);
+                __syncthreads();
+                topk_absorb(S, nb, P.k, P.perm0);
+            }
+            const uint32_t have = topk_finish(S, P.k);
+            const int32_t tau2 = have >= static_cast<uint32_t>(P.k) ? static_cast<int32_t>(S.th[P.k - 1]) : 0x7fffffff;
+            // candidate bitmap: whole leaves + the cut leaf's prefix
+            uint32_t* bm = P.tc_bm + (qs - P.q_begin) * P.tc_W;
+            for (uint32_t i = threadIdx.x; i <= n_full; i += blockDim.x) {
+                uint32_t a0, a1;
+                if (i < n_full) {
+                    const uint32_t li = F.full[i];
+                    a0 = __ldg(T0.leaf_begin + li);
+                    a1 = a0 + __ldg(T0.leaf_count + li);
+                } else {
+                    a0 = __ldg(T0.leaf_begin + cut_li);
+                    a1 = a0 + static_cast<uint32_t>(take_cut);
+                }
+                for (uint32_t w = a0 >> 5; a0 < a1 && w <= (a1 - 1) >> 5; ++w) {
+                    const uint32_t lo = max(a0, w << 5), hi = min(a1, (w << 5) + 32);
+                    const uint32_t nbits = hi - lo;
+                    const uint32_t mask = (nbits == 32 ? 0xffffffffu : ((1u << nbits) - 1u)) << (lo & 31);
+                    atomicOr(bm + w, mask);
+                }
+                // (query tile, 128-row tile) occupancy: tc_score skips empty tiles
+                uint32_t* tm = P.tc_tmap + ((qs - P.q_begin) >> 8) * P.tc_TW;
+                for (uint32_t t = a0 >> 7; a0 < a1 && t <= (a1 - 1) >> 7; ++t) {
+                    const uint32_t bit = 1u << (t & 31);
+                    if (!(*reinterpret_cast<volatile uint32_t*>(tm + (t >> 5)) & bit)) atomicOr(tm + (t >> 5), bit);
+                }
+            }
+            if (threadIdx.x == 0) P.tc_tau2[qs - P.q_begin] = tau2;
+            __syncthreads();
+            phase(3);
+            continue;
+        }
+        // emission: whole leaves (block prefix of their sizes, then one warp per
+        // leaf writes its contiguous row range), then the cut leaf's prefix
+        const uint32_t n_whole_rows = emit_rows(F.full, n_full, T0, F.cand, B32, S);
         {
-            const uint32_t d0 = S.u32s[3];
+            const uint32_t d0 = n_whole_rows;
             const uint32_t s0 = __ldg(T0.leaf_begin + cut_li);
             for (uint32_t e = threadIdx.x; e < take_cut && d0 + e < B32; e += blockDim.x)
                 F.cand[d0 + e] = s0 + e;
         }
-        if (S.u32s[3] + take_cut != B32) {  // invariant: exactly `budget` rows emitted
+        if (n_whole_rows + take_cut != B32) {  // invariant: exactly `budget` rows emitted
             if (threadIdx.x == 0) atomicOr(slow_n + 1, 1u);
             __syncthreads();
             continue;
@@ -1166,10 +1278,122 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         const size_t fast_bytes = fast_slot_bytes(P.max_leaves, P.budget);
         const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
         grow_scratch(X.fast, slots * fast_bytes);
-        ProfScope ps("query_fast", s);
-        query_fast_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
-            Pp, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
-        DETLSH_LAUNCH_CHECK();
+        auto launch_fast = [&](const QueryPlan& Pc) {
+            const uint64_t m = Pc.q_end - Pc.q_begin;
+            if (m == 0) return;
+            ProfScope ps("query_fast", s);
+            query_fast_kernel<<<static_cast<unsigned>(std::min<uint64_t>(slots, m)), kQueryThreads, smem, s>>>(
+                Pc, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
+            DETLSH_LAUNCH_CHECK();
+        };
+        // u8 rows with a large budget: the plan kernel hands each query's
+        // candidate set to the tcgen05 dataset-major scorer (tc_score.cu)
+        // tau^2 = k-th smallest dist^2 over the rows of the nearest leaves.  If
+        // those rows were a uniform sample of the candidates, about
+        // k * budget / tau_rows candidates would pass it; size the sample so
+        // that is a quarter of the survivor staging buffer (nearest-leaf rows
+        // do better than uniform; measured on C2, 2x this sample trades 1 ms
+        // of plan for 2.5 ms of scoring), and keep the tensor-core path only
+        // where the sample is a small part of the budget.
+        const uint64_t tau_rows = std::max<uint64_t>(
+            std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + kTcFinishCap - 1) / kTcFinishCap);
+        Pp.tc_tau_rows = static_cast<uint32_t>(std::min<uint64_t>(tau_rows, 0xffffffffULL));
+        const bool tc_ok = P.tc_allowed && P.data_u8 && P.xn_u8 && P.data_tc && P.row_u8 % 32 == 0 &&
+                           P.row_u8 <= 256 && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
+                           2ULL * P.k <= kTcFinishCap && 8 * tau_rows <= P.budget;
+        DevBuf<uint32_t> over_list;
+        if (!tc_ok) {
+            launch_fast(Pp);
+        } else {
+            const uint64_t W = (P.n + 31) / 32;
+            const int R = P.row_u8;
+            // test hook: a smaller staging buffer forces the overflow re-run
+            uint32_t tc_cap = kTcFinishCap;
+            if (const char* e = std::getenv("DETLSH_TEST_TC_CAP"))
+                tc_cap = static_cast<uint32_t>(std::max(1L, std::min<long>(std::atol(e), kTcFinishCap)));
+            // bitmaps of one chunk of processing slots stay under ~2 GB
+            uint64_t chunk = (2ULL << 30) / (W * 4);
+            chunk = std::max<uint64_t>(256, chunk / 256 * 256);
+            chunk = std::min<uint64_t>(chunk, (P.nq + 255) / 256 * 256);
+            DevBuf<uint32_t> bm(chunk * W);
+            DevBuf<int32_t> tau2(chunk), qn(chunk);
+            DevBuf<uint32_t> surv_cnt(chunk);
+            DevBuf<uint8_t> q8(chunk * R);
+            DevBuf<uint64_t> surv(chunk * kTcFinishCap);
+            const uint32_t TW = static_cast<uint32_t>(((P.n + 127) / 128 + 31) / 32);
+            DevBuf<uint32_t> tmap(chunk / 256 * TW);
+            const uint64_t rec_cap = chunk * 8192;  // threshold passes staged per chunk
+            DevBuf<uint4> rec(rec_cap);
+            DevBuf<unsigned long long> rec_cnt(1);
+            over_list.alloc(P.nq);
+            for (uint64_t c0 = 0; c0 < P.nq; c0 += chunk) {
+                const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);
+                DETLSH_CUDA(cudaMemsetAsync(bm.get(), 0, m * W * 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(tau2.get(), 0xff, m * 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(surv_cnt.get(), 0, m * 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(tmap.get(), 0, (m + 255) / 256 * TW * 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + 3, 0, 4, s));
+                QueryPlan Pc = Pp;
+                Pc.q_begin = c0;
+                Pc.q_end = c0 + m;
+                Pc.tc_bm = bm.get();
+                Pc.tc_W = W;
+                Pc.tc_tau2 = tau2.get();
+                Pc.tc_tmap = tmap.get();
+                Pc.tc_TW = TW;
+                launch_fast(Pc);
+                launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, q8.get(), qn.get(), s);
+                TcScoreArgs a{};
+                a.rows = P.data_tc;
+                a.xn = P.xn_u8;
+                a.q8 = q8.get();
+                a.qn = qn.get();
+                a.tau2 = tau2.get();
+                a.bm = bm.get();
+                a.W = W;
+                a.n = P.n;
+                a.nq = m;
+                a.R = R;
+                a.surv_cnt = surv_cnt.get();
+                a.surv = surv.get();
+                a.cap = tc_cap;
+                a.order = Pp.order;
+                a.slot0 = c0;
+                a.tmap = tmap.get();
+                a.TW = TW;
+                a.work = X.counters.get() + 3;
+                a.rec = rec.get();
+                a.rec_cnt = rec_cnt.get();
+                a.rec_cap = rec_cap;
+                DETLSH_CUDA(cudaMemsetAsync(rec_cnt.get(), 0, 8, s));
+                launch_tc_score(a, device, s);
+                unsigned long long used = 0;
+                DETLSH_CUDA(cudaMemcpyAsync(&used, rec_cnt.get(), 8, cudaMemcpyDeviceToHost, s));
+                DETLSH_CUDA(cudaStreamSynchronize(s));
+                if (std::getenv("DETLSH_TC_DEBUG"))
+                    std::fprintf(stderr, "tc_score: %llu pass records reserved (cap %llu) for %llu queries\n", used,
+                                 static_cast<unsigned long long>(rec_cap), static_cast<unsigned long long>(m));
+                if (used > rec_cap) {  // pass list overflowed: this chunk takes the gather path
+                    QueryPlan Pg = Pp;
+                    Pg.q_begin = c0;
+                    Pg.q_end = c0 + m;
+                    launch_fast(Pg);
+                    continue;
+                }
+                launch_tc_finish(a, P.perm0, P.k, P.r_min, P.budget, P.ids, P.dists, P.n_hits, P.radius,
+                                 P.cands, over_list.get(), X.counters.get() + 2, s);
+            }
+            uint32_t n_over = 0;
+            DETLSH_CUDA(cudaMemcpyAsync(&n_over, X.counters.get() + 2, 4, cudaMemcpyDeviceToHost, s));
+            DETLSH_CUDA(cudaStreamSynchronize(s));
+            if (n_over) {  // survivors overflowed the staging buffer: gather path for those
+                QueryPlan Pc = Pp;
+                Pc.order = over_list.get();
+                Pc.q_begin = 0;
+                Pc.q_end = n_over;
+                launch_fast(Pc);
+            }
+        }
         uint32_t flags[2] = {0, 0};
         DETLSH_CUDA(cudaMemcpyAsync(flags, X.counters.get(), 8, cudaMemcpyDeviceToHost, s));
         unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};

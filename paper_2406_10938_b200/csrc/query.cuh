@@ -27,6 +27,8 @@ struct QueryPlan {
     const QTree* trees;   // device array [L]
     const uint32_t* perm0;   // tree 0 permutation (row index -> dataset position)
     const uint8_t* data_u8;  // exact u8 rows in tree-0 order, or null
+    const int32_t* xn_u8;    // |x|^2 of those rows
+    const uint8_t* data_tc;  // the same rows in MMA tiles (launch_pack_tc_tiles)
     int row_u8;              // bytes per u8 row (d rounded up to 16)
     int u8_lpr;              // lanes per u8 row (power of two <= 32)
     double eps, c, r_min;
@@ -48,6 +50,17 @@ struct QueryPlan {
     unsigned long long* phase_cycles;
     // optional processing order (locality): processing slot i handles query order[i]
     const uint32_t* order;
+    // processed range of processing slots [q_begin, q_end)
+    uint64_t q_begin, q_end;
+    // tensor-core verification hand-off (null: score every candidate here).
+    // Indexed by slot - q_begin: candidate bitmaps over tree-0 rows, tau^2.
+    uint32_t* tc_bm;
+    uint64_t tc_W;
+    int32_t* tc_tau2;
+    uint32_t* tc_tmap;  // [slot tiles of 256][tc_TW] bits over 128-row tiles
+    uint32_t tc_TW;
+    int tc_allowed;  // host-side switch (DETLSH_F_NO_TC clears it)
+    uint32_t tc_tau_rows;  // rows of the nearest leaves scored exactly for tau^2
 };
 
 constexpr int kQueryThreads = 256;
@@ -64,6 +77,44 @@ struct QueryScratch {
     DevBuf<unsigned long long> phases;  // [6] fast-path phase cycles (profiling only)
     size_t fast_slots = 0, slow_slots = 0;
 };
+
+// ---- tensor-core exact verification (tc_score.cu) ----
+constexpr uint32_t kTcFinishCap = 4096;  // survivors staged per query
+
+struct TcScoreArgs {
+    const uint8_t* rows;   // u8 rows, tree-0 order, packed by launch_pack_tc_tiles
+    const int32_t* xn;     // [n] |x|^2
+    const uint8_t* q8;     // [nq][R] u8 queries
+    const int32_t* qn;     // [nq] |q|^2
+    const int32_t* tau2;   // [nq] inclusive dist^2 threshold; < 0: not a TC query
+    const uint32_t* bm;    // [nq][W] candidate bits over tree-0 rows
+    uint64_t W;            // words per query bitmap
+    uint64_t n, nq;
+    int R;
+    uint32_t* surv_cnt;    // [nq]
+    uint64_t* surv;        // [nq][cap] (dist^2 << 32 | row)
+    uint32_t cap;
+    // slot s of this batch is query order[slot0 + s] (or slot0 + s)
+    const uint32_t* order;
+    uint64_t slot0;
+    const uint32_t* tmap;  // [query tiles][TW] occupied 128-row tiles
+    uint32_t TW;
+    uint32_t* work;        // unit counter (zeroed by the caller)
+    uint4* rec;            // threshold passes {row, slot, dist^2, 0}; row ~0u: padding
+    unsigned long long* rec_cnt;  // reserved records (zeroed by the caller)
+    uint64_t rec_cap;
+};
+
+size_t tc_score_smem(int R);
+void launch_tc_pack_queries(const float* q, const uint32_t* order, uint64_t slot0, uint64_t m, int d,
+                            int R, uint8_t* q8, int32_t* qn, cudaStream_t s);
+void launch_row_norms_u8(const uint8_t* rows, uint64_t n, int R, int32_t* xn, cudaStream_t s);
+// u8 rows -> 128-row tiles in the MMA operand layout ([ceil(n/128)][R/16][128][16] bytes)
+void launch_pack_tc_tiles(const uint8_t* rows, uint64_t n, int R, uint8_t* tiles, cudaStream_t s);
+void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s);
+void launch_tc_finish(const TcScoreArgs& a, const uint32_t* perm0, int k, double r_min,
+                      uint64_t budget, uint32_t* ids, double* dists, int32_t* n_hits, double* radius,
+                      uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, cudaStream_t s);
 
 // tcgen05 kind::i8 self-test (tc_score.cu): C[128][N] = A[128][K] . B[N][K]^T.
 void tc_gemm_u8_test(const uint8_t* hA, const uint8_t* hB, int N, int K, int32_t* hC);

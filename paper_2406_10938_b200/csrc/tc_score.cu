@@ -1,7 +1,10 @@
 // Tensor-core (tcgen05, kind::i8) building blocks for exact u8 verification.
 // tc_gemm_u8_test: one 128 x N x K tile, C = A . B^T, used by the tests to pin
 // the descriptor / TMEM plumbing before it is used in the query path.
+#include <algorithm>
+
 #include "common.cuh"
+#include "query.cuh"
 #include "umma.cuh"
 
 namespace detlsh_b200 {
@@ -64,7 +67,438 @@ __global__ void __launch_bounds__(128) tc_gemm_u8_test_kernel(const uint8_t* __r
     if (tid < 32) umma::tmem_free(tmem, 256);
 }
 
+// ---------------------------------------------------------------------------
+// Dataset-major exact verification for u8 data.
+//
+// For a batch of queries, the candidate SET of each query is a bitmap over the
+// rows in tree-0 order (written by the plan kernel).  This kernel streams row
+// tiles (128 rows) against query tiles (256 queries): one tcgen05 kind::i8
+// MMA chain per tile computes every dot product q.x exactly in s32 (TMEM),
+// then the epilogue keeps, for each (row, query) whose candidate bit is set,
+// dist^2 = |q|^2 + |x|^2 - 2 q.x (exact integers) if it is <= the query's
+// threshold tau^2 (the k-th smallest dist^2 of a subset of its candidates, so
+// every true top-k member survives).  tc_finish ranks the survivors by
+// (dist^2, position) exactly.
+// ---------------------------------------------------------------------------
+constexpr int kTcRows = 128;     // rows per tile (MMA M, TMEM lanes)
+constexpr int kTcQueries = 256;  // queries per tile (MMA N, TMEM columns)
+
+// Slot s of the batch <- query order[slot0 + s]: u8 row (non-integral values
+// become 0; such queries never take the tensor-core path) and |q|^2.
+__global__ void tc_pack_queries_kernel(const float* __restrict__ q, const uint32_t* __restrict__ order,
+                                       uint64_t slot0, uint64_t m, int d, int R,
+                                       uint8_t* __restrict__ q8, int32_t* __restrict__ qn) {
+    const int lane = threadIdx.x & 31;  // one warp per slot
+    for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
+         i += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t qi = order ? order[slot0 + i] : slot0 + i;
+        int32_t s = 0;
+        for (int t = lane; t < R; t += 32) {
+            uint8_t b = 0;
+            if (t < d) {
+                const float v = q[qi * d + t];
+                const bool integral = v >= 0.0f && v <= 255.0f && v == floorf(v);
+                b = integral ? static_cast<uint8_t>(v) : 0;
+            }
+            q8[i * R + t] = b;
+            s += static_cast<int32_t>(b) * b;
+        }
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) qn[i] = s;
+    }
+}
+
+__global__ void row_norms_u8_kernel(const uint8_t* __restrict__ rows, uint64_t n, int R,
+                                    int32_t* __restrict__ xn) {
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < n;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint4* p = reinterpret_cast<const uint4*>(rows + r * R);
+        uint32_t acc = 0;
+        for (int c = 0; c < R / 16; ++c) {
+            const uint4 v = __ldg(p + c);
+            acc = __dp4a(v.x, v.x, acc);
+            acc = __dp4a(v.y, v.y, acc);
+            acc = __dp4a(v.z, v.z, acc);
+            acc = __dp4a(v.w, v.w, acc);
+        }
+        xn[r] = static_cast<int32_t>(acc);
+    }
+}
+
+// Rows -> HBM tiles of 128 rows in the canonical no-swizzle K-major layout
+// (chunk kc of row r at kc * 2048 + r * 16), zero rows past n: one tile is one
+// contiguous 128 * R byte block, moved by a single bulk copy.
+__global__ void pack_tc_tiles_kernel(const uint8_t* __restrict__ rows, uint64_t n, int R,
+                                     uint8_t* __restrict__ tiles) {
+    const int kch = R / 16;
+    const uint64_t total = (n + kTcRows - 1) / kTcRows * kTcRows * kch;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        // i enumerates destination chunks in order: tile, kc, row
+        const uint64_t t = i / (static_cast<uint64_t>(kch) * kTcRows);
+        const uint32_t rem = static_cast<uint32_t>(i % (static_cast<uint64_t>(kch) * kTcRows));
+        const uint32_t kc = rem / kTcRows, r = rem % kTcRows;
+        const uint64_t row = t * kTcRows + r;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < n) v = __ldg(reinterpret_cast<const uint4*>(rows + row * R) + kc);
+        reinterpret_cast<uint4*>(tiles)[i] = v;
+    }
+}
+
+// Warp-specialised, persistent: warp 8 streams the occupied row tiles
+// (pre-tiled in HBM in the canonical no-swizzle K-major layout, one 1-D bulk
+// copy per tile) into a kTcStages ring; warp 9 issues the tcgen05 MMAs into one
+// of two TMEM accumulators (2 x 256 columns); warps 0-7 drain the other one.
+// Work units (query tile, row-tile range) are handed out dynamically; row
+// tiles holding no candidate of the query tile are skipped.  The epilogue is
+// branch-free: 2 q.x - (|q|^2 - tau^2) >= |x|^2 per element (IMAD + compare
+// into a mask); only columns where some lane passes are revisited, with
+// single-column TMEM loads, to consult the candidate bitmap.
+constexpr int kTcThreads = 320;  // 8 epilogue warps + producer + MMA issuer
+constexpr uint32_t kTcRecChunk = 1024;  // records reserved per warp at a time
+constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
+
+__device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 4u : 3u; }
+
+__device__ __forceinline__ uint32_t next_tile(const uint32_t* __restrict__ row, uint32_t t, uint32_t t1) {
+    while (t < t1) {
+        const uint32_t w = __ldg(row + (t >> 5)) >> (t & 31);
+        if (w) return min(t + __ffs(w) - 1, t1);
+        t = (t | 31) + 1;
+    }
+    return t1;
+}
+
+// A warp's next run of kTcRecChunk record slots; the unused tail of the old
+// run becomes padding.  (Called warp-uniformly.)
+__device__ __noinline__ void tc_reserve(uint4* rec, unsigned long long* rec_cnt, uint64_t rec_cap, uint64_t& next,
+                                        uint64_t& end, int lane) {
+    for (uint64_t x = next + lane; x < end && x < rec_cap; x += 32) rec[x] = make_uint4(0xffffffffu, 0, 0, 0);
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(rec_cnt, static_cast<unsigned long long>(kTcRecChunk));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    next = base;
+    end = base + kTcRecChunk;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, uint32_t n_rt, uint32_t n_qt,
+                                                                 uint32_t G) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ __align__(8) uint64_t full[4], empty[4], tfull[2], tempty[2];
+    __shared__ uint32_t tslot, unit_s;
+    const int R = a.R, kch = R / 16;
+    const uint32_t stages = tc_stages(R);
+    const uint32_t tile_bytes = static_cast<uint32_t>(kTcRows * R);
+    uint8_t* sB = sm;                                    // [256][R] core layout
+    uint8_t* sA = sB + kTcQueries * R;                   // [stages][128][R] core layout
+    int32_t* snh = reinterpret_cast<int32_t*>(sA + stages * tile_bytes);  // tau^2 - |q|^2
+    int32_t* sqn = snh + kTcQueries;
+    uint32_t* sstash = reinterpret_cast<uint32_t*>(sqn + kTcQueries);  // [8 warps][32 lanes][kTcStash]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        for (uint32_t s = 0; s < stages; ++s) {
+            umma::mbar_init(&full[s], 1);
+            umma::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            umma::mbar_init(&tfull[s], 1);
+            umma::mbar_init(&tempty[s], 8);
+        }
+        umma::fence_mbar_init();
+    }
+    if (warp == 9) umma::tmem_alloc(&tslot, 512);
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = tslot;
+    const uint32_t idesc = umma::idesc_u8_s32(kTcRows, kTcQueries);
+    const uint32_t units = n_qt * G;
+    uint32_t it = 0;  // tiles processed by this CTA so far (pipeline phases)
+    uint32_t loaded_qt = 0xffffffffu;
+    uint64_t res_next = 0, res_end = 0;  // this warp's reservation in a.rec
+    for (;;) {
+        if (tid == 0) unit_s = atomicAdd(a.work, 1u);
+        __syncthreads();
+        const uint32_t u = unit_s;
+        __syncthreads();  // unit_s is rewritten next iteration
+        if (u >= units) break;
+        const uint32_t qt = u / G, g = u % G;
+        const uint32_t rt0 = static_cast<uint32_t>(static_cast<uint64_t>(n_rt) * g / G);
+        const uint32_t rt1 = static_cast<uint32_t>(static_cast<uint64_t>(n_rt) * (g + 1) / G);
+        const uint32_t* trow = a.tmap + static_cast<uint64_t>(qt) * a.TW;
+        const uint64_t q0 = static_cast<uint64_t>(qt) * kTcQueries;
+        uint32_t ntiles = 0;  // occupied tiles of the unit (every role walks the same list)
+        for (uint32_t w = rt0 >> 5; w <= (rt1 - 1) >> 5; ++w) {
+            uint32_t x = __ldg(trow + w);
+            if (w == rt0 >> 5) x &= ~0u << (rt0 & 31);
+            if (w == (rt1 - 1) >> 5 && (rt1 & 31)) x &= (1u << (rt1 & 31)) - 1u;
+            ntiles += __popc(x);
+        }
+        if (ntiles == 0) continue;  // nothing to score (uniform)
+        if (qt != loaded_qt) {  // every MMA of the previous unit has completed (epilogue drained it)
+            for (int i = tid; i < kTcQueries * kch; i += blockDim.x) {
+                const int kc = i / kTcQueries, r = i % kTcQueries;
+                const uint64_t qq = q0 + r;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (qq < a.nq) v = __ldg(reinterpret_cast<const uint4*>(a.q8 + qq * R) + kc);
+                *reinterpret_cast<uint4*>(sB + umma::tile_off(r, kc, kTcQueries)) = v;
+            }
+            for (int r = tid; r < kTcQueries; r += blockDim.x) {
+                const uint64_t qq = q0 + r;
+                const int32_t t = qq < a.nq ? a.tau2[qq] : -1;
+                const int32_t qn = qq < a.nq ? a.qn[qq] : 0;
+                sqn[r] = qn;
+                snh[r] = t < 0 ? -0x40000000 : t - qn;  // -2^30: no row can pass
+            }
+            umma::fence_async_smem();
+            umma::fence_before_sync();
+            __syncthreads();
+            umma::fence_after_sync();
+            loaded_qt = qt;
+        }
+        if (warp == 8) {
+            if (lane == 0) {
+                for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
+                    const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
+                    umma::mbar_wait(&empty[s], ph ^ 1);
+                    umma::mbar_arrive_expect_tx(&full[s], tile_bytes);
+                    umma::bulk_g2s(sA + s * tile_bytes, a.rows + static_cast<uint64_t>(t) * tile_bytes, tile_bytes,
+                                   &full[s]);
+                }
+            }
+        } else if (warp == 9) {
+            if (lane == 0) {
+                for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
+                    const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
+                    const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+                    umma::mbar_wait(&tempty[acc], aph ^ 1);
+                    umma::mbar_wait(&full[s], ph);
+                    umma::fence_after_sync();
+                    const uint32_t a0 = umma::smem_u32(sA + s * tile_bytes), b0 = umma::smem_u32(sB);
+                    for (int k = 0; k < R / 32; ++k) {
+                        const uint64_t da = umma::smem_desc(a0 + 2 * k * kTcRows * 16, kTcRows * 16, 128);
+                        const uint64_t db = umma::smem_desc(b0 + 2 * k * kTcQueries * 16, kTcQueries * 16, 128);
+                        umma::mma_u8(tmem + acc * kTcQueries, da, db, idesc, k > 0 ? 1u : 0u);
+                    }
+                    umma::commit(&empty[s]);
+                    umma::commit(&tfull[acc]);
+                }
+            }
+        } else {
+            const int sub = warp & 3, half = warp >> 2;
+            const int row = sub * 32 + lane;
+            // candidate words of this warp's 32 rows for its 128 query columns
+            // (lane l holds columns 4l..4l+3), prefetched one tile ahead
+            auto load_words = [&](uint32_t t, uint32_t (&w)[4]) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint64_t qq = q0 + half * 128 + lane * 4 + e;
+                    const uint64_t word = static_cast<uint64_t>(t) * 4 + sub;
+                    w[e] = (qq < a.nq && word < a.W) ? __ldg(a.bm + qq * a.W + word) : 0u;
+                }
+            };
+            uint32_t pw[4], nw[4] = {0, 0, 0, 0};
+            load_words(next_tile(trow, rt0, rt1), pw);
+            const uint32_t lt_mask = (1u << lane) - 1u;
+            for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
+                const uint32_t i = it + j, acc = i & 1, aph = (i >> 1) & 1;
+                const uint64_t r = static_cast<uint64_t>(t) * kTcRows + row;
+                const int32_t xn = r < a.n ? __ldg(a.xn + r) : 0x7fffffff;  // padded rows never pass
+                const uint32_t tn = next_tile(trow, t + 1, rt1);
+                if (tn < rt1) load_words(tn, nw);  // next tile's words, in flight during this one
+                umma::mbar_wait(&tfull[acc], aph);
+                umma::fence_after_sync();
+                const uint32_t tbase = tmem + (static_cast<uint32_t>(sub * 32) << 16) + acc * kTcQueries;
+                for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 32) {
+                    uint32_t v[32];
+                    umma::tmem_ld32(tbase + c0, v);
+                    // threshold mask: bit e <=> 2 q.x + tau^2 - |q|^2 >= |x|^2
+                    uint32_t mask = 0;
+                    const int4* nh4 = reinterpret_cast<const int4*>(snh + c0);
+#pragma unroll
+                    for (int e4 = 0; e4 < 8; ++e4) {
+                        const int4 h = nh4[e4];
+                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 0]) + h.x >= xn) << (4 * e4 + 0);
+                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 1]) + h.y >= xn) << (4 * e4 + 1);
+                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 2]) + h.z >= xn) << (4 * e4 + 2);
+                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 3]) + h.w >= xn) << (4 * e4 + 3);
+                    }
+                    // rare: columns where some lane passed.  The chunk's values are
+                    // stashed in shared memory so this loop stays small and indexes
+                    // them dynamically; candidate (row, query, dist^2) records go to
+                    // a global list through a per-warp reservation (no round trip on
+                    // the critical path)
+                    uint32_t cols = __reduce_or_sync(0xffffffffu, mask);
+                    if (cols) {
+                        uint32_t* sv = sstash + (warp * 32 + lane) * kTcStash;
+#pragma unroll
+                        for (int e4 = 0; e4 < 8; ++e4)
+                            *reinterpret_cast<uint4*>(sv + 4 * e4) =
+                                make_uint4(v[4 * e4], v[4 * e4 + 1], v[4 * e4 + 2], v[4 * e4 + 3]);
+                        while (cols) {
+                            const int e = __ffs(cols) - 1;
+                            cols &= cols - 1;
+                            const int cr = c0 + e - half * 128;  // candidate word: lane cr/4 holds it
+                            const int sel = cr & 3;
+                            const uint32_t mine = sel == 0 ? pw[0] : sel == 1 ? pw[1] : sel == 2 ? pw[2] : pw[3];
+                            const uint32_t b = __ballot_sync(0xffffffffu, (mask >> e) & 1u) &
+                                               __shfl_sync(0xffffffffu, mine, cr >> 2);
+                            if (!b) continue;
+                            const uint32_t cnt = __popc(b);
+                            if (res_next + cnt > res_end) tc_reserve(a.rec, a.rec_cnt, a.rec_cap, res_next, res_end, lane);
+                            const uint64_t slot = res_next + __popc(b & lt_mask);
+                            res_next += cnt;
+                            if (((b >> lane) & 1u) && slot < a.rec_cap) {
+                                const int c = c0 + e;
+                                a.rec[slot] = make_uint4(static_cast<uint32_t>(r), static_cast<uint32_t>(q0 + c),
+                                                         static_cast<uint32_t>(sqn[c] + xn - 2 * static_cast<int32_t>(sv[e])), 0);
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+                umma::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) umma::mbar_arrive(&tempty[acc]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) pw[e] = nw[e];
+            }
+        }
+        it += ntiles;
+        umma::fence_before_sync();
+        __syncthreads();
+        umma::fence_after_sync();
+    }
+    for (uint64_t x = res_next + lane; x < res_end && x < a.rec_cap; x += 32) a.rec[x] = make_uint4(0xffffffffu, 0, 0, 0);
+    if (warp == 9) umma::tmem_free(tmem, 512);
+}
+
+// Candidate threshold passes -> per-query survivor lists.
+__global__ void tc_collect_kernel(TcScoreArgs a) {
+    const uint64_t total = min(static_cast<uint64_t>(*a.rec_cnt), a.rec_cap);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint4 e = a.rec[i];
+        if (e.x == 0xffffffffu) continue;
+        const uint32_t slot = atomicAdd(a.surv_cnt + e.y, 1u);
+        if (slot < a.cap) a.surv[static_cast<uint64_t>(e.y) * a.cap + slot] = (static_cast<uint64_t>(e.z) << 32) | e.x;
+    }
+}
+
+// Exact top-k of each TC query's survivors by (dist^2, dataset position).
+__global__ void __launch_bounds__(256) tc_finish_kernel(TcScoreArgs a, const uint32_t* __restrict__ perm0,
+                                                        int k, double r_min, uint64_t budget,
+                                                        uint32_t* ids, double* dists, int32_t* n_hits,
+                                                        double* radius, uint64_t* cands,
+                                                        uint32_t* overflow_list, uint32_t* overflow_n) {
+    __shared__ uint64_t key[kTcFinishCap];  // (d2 << 32) | position, sorted ascending
+    for (uint64_t slot = blockIdx.x; slot < a.nq; slot += gridDim.x) {
+        if (a.tau2[slot] < 0) continue;
+        const uint64_t q = a.order ? a.order[a.slot0 + slot] : a.slot0 + slot;
+        const uint32_t cnt = a.surv_cnt[slot];
+        if (cnt > a.cap) {  // threshold too loose for the staging buffer: rerun on the gather path
+            if (threadIdx.x == 0) overflow_list[atomicAdd(overflow_n, 1u)] = static_cast<uint32_t>(q);
+            continue;
+        }
+        uint32_t n2 = 64;  // sort width: power of two >= cnt
+        while (n2 < cnt) n2 <<= 1;
+        for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+            uint64_t kk = ~0ULL;
+            if (i < cnt) {
+                const uint64_t s = a.surv[slot * a.cap + i];
+                kk = (s & 0xffffffff00000000ULL) | __ldg(perm0 + static_cast<uint32_t>(s));
+            }
+            key[i] = kk;
+        }
+        __syncthreads();
+        for (uint32_t size = 2; size <= n2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+                    const int lo = 2 * i - (i & (stride - 1));
+                    const int hi = lo + stride;
+                    const bool asc = (lo & size) == 0;
+                    const uint64_t x = key[lo], y = key[hi];
+                    if ((y < x) == asc) {
+                        key[lo] = y;
+                        key[hi] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        const uint32_t nh = min(cnt, static_cast<uint32_t>(k));
+        for (uint32_t t = threadIdx.x; t < nh; t += blockDim.x) {
+            const uint64_t kk = key[t];
+            if (ids) ids[q * k + t] = static_cast<uint32_t>(kk);
+            if (dists) dists[q * k + t] = __dsqrt_rn(static_cast<double>(kk >> 32));
+        }
+        if (threadIdx.x == 0) {
+            if (n_hits) n_hits[q] = static_cast<int32_t>(nh);
+            if (radius) radius[q] = r_min;
+            if (cands) cands[q] = budget;
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace
+
+size_t tc_score_smem(int R) {
+    const size_t need = static_cast<size_t>(kTcQueries + (R <= 128 ? 4 : 3) * kTcRows) * R + 2 * kTcQueries * 4 +
+                        8 * 32 * kTcStash * 4 + 1024;
+    return std::max<size_t>(need, 120 * 1024);  // one CTA per SM: it owns all 512 TMEM columns
+}
+
+void launch_tc_pack_queries(const float* q, const uint32_t* order, uint64_t slot0, uint64_t m, int d,
+                            int R, uint8_t* q8, int32_t* qn, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((m * 32 + 255) / 256, 8192)));
+    tc_pack_queries_kernel<<<grid, 256, 0, s>>>(q, order, slot0, m, d, R, q8, qn);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_row_norms_u8(const uint8_t* rows, uint64_t n, int R, int32_t* xn, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 8192)));
+    row_norms_u8_kernel<<<grid, 256, 0, s>>>(rows, n, R, xn);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s) {
+    const uint32_t n_rt = static_cast<uint32_t>((a.n + kTcRows - 1) / kTcRows);
+    const uint32_t n_qt = static_cast<uint32_t>((a.nq + kTcQueries - 1) / kTcQueries);
+    const size_t smem = tc_score_smem(a.R);
+    DETLSH_CUDA(cudaFuncSetAttribute(tc_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    // persistent: one CTA per SM; work units = (query tile, row-tile range),
+    // about 8 per CTA, handed out by an atomic counter
+    const uint32_t sms = static_cast<uint32_t>(sm_count(device));
+    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>((n_rt + 7) / 8, (8 * sms + n_qt - 1) / n_qt));
+    const uint32_t grid = std::min<uint32_t>(sms, n_qt * G);
+    {
+        ProfScope ps("tc_score", s);
+        tc_score_kernel<<<grid, kTcThreads, smem, s>>>(a, n_rt, n_qt, G);
+        DETLSH_LAUNCH_CHECK();
+    }
+    ProfScope ps("tc_collect", s);
+    tc_collect_kernel<<<sms * 8, 256, 0, s>>>(a);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_pack_tc_tiles(const uint8_t* rows, uint64_t n, int R, uint8_t* tiles, cudaStream_t s) {
+    const uint64_t chunks = (n + kTcRows - 1) / kTcRows * kTcRows * (R / 16);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, 16384)));
+    pack_tc_tiles_kernel<<<grid, 256, 0, s>>>(rows, n, R, tiles);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_tc_finish(const TcScoreArgs& a, const uint32_t* perm0, int k, double r_min,
+                      uint64_t budget, uint32_t* ids, double* dists, int32_t* n_hits, double* radius,
+                      uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(a.nq, 4096)));
+    ProfScope ps("tc_finish", s);
+    tc_finish_kernel<<<grid, 256, 0, s>>>(a, perm0, k, r_min, budget, ids, dists, n_hits, radius, cands,
+                                          overflow_list, overflow_n);
+    DETLSH_LAUNCH_CHECK();
+}
 
 void tc_gemm_u8_test(const uint8_t* hA, const uint8_t* hB, int N, int K, int32_t* hC) {
     if (N < 32 || N > 256 || N % 32 || K < 32 || K > 256 || K % 32)

@@ -19,3 +19,54 @@ def test_tc_gemm_u8_exact(gpu, N, K):
     assert rc == 0, gpu.load().detlsh_gpu_last_error()
     want = A.astype(np.int64) @ B.astype(np.int64).T
     assert np.array_equal(Cm.astype(np.int64), want)
+
+
+def _scopes(lib):
+    names = C.create_string_buffer(4096)
+    ms = np.zeros(64, np.float64)
+    cnt = np.zeros(64, np.uint64)
+    m = lib.detlsh_profile_collect(names, 4096, C.c_void_p(ms.ctypes.data), C.c_void_p(cnt.ctypes.data), 64)
+    return names.value.decode().split(";")[:m]
+
+
+def _sparse_u8(g, n, d):
+    return np.where(g.random((n, d)) < 0.5, 0, np.minimum(g.geometric(0.05, (n, d)), 255)).astype(np.float32)
+
+
+@pytest.mark.parametrize("d,k,nq,cap", [(128, 50, 5000, None), (100, 100, 600, None),
+                                        (256, 20, 1500, None), (64, 30, 800, 120)])
+def test_tc_verification_equals_gather_path_and_oracle(gpu, port, monkeypatch, d, k, nq, cap):
+    """Dataset-major tcgen05 verification (u8 rows, budget >= 8192) returns the
+    same (position, distance) lists as the per-query gather path and as the
+    oracle, ties included (duplicated rows).  cap shrinks the survivor staging
+    buffer so that queries overflow it and take the re-run."""
+    from paper_2406_10938_b200 import LshParams
+    if cap is not None:
+        monkeypatch.setenv("DETLSH_TEST_TC_CAP", str(cap))
+    g = np.random.Generator(np.random.PCG64(d * 7 + k))
+    n = 120000
+    data = _sparse_u8(g, n, d)
+    data[n // 2: n // 2 + 500] = data[:500]  # exact duplicates -> distance ties
+    Q = np.concatenate([_sparse_u8(g, nq - 100, d), data[g.integers(0, n, 100)]])
+    Q[7] += 0.25  # non-integral -> fp64 gather path for this query
+    c = dict(K=16, L=4, n_regions=256, leaf_capacity=128, sample_fraction=0.1, beta=0.1, k=k)
+    idx = gpu.build_index(data, LshParams(**c), seed=11)
+    assert idx.row_u8() % 32 == 0
+    lib = gpu.load()
+    lib.detlsh_profile_enable(1)
+    ra = gpu.ck_ann_batch(idx, Q, k)
+    lib.detlsh_profile_enable(0)
+    assert "tc_score" in _scopes(lib), "tensor-core path not taken"
+    rb = gpu.ck_ann_batch(idx, Q, k, tensor_cores=False)
+    assert np.array_equal(ra.n_hits, rb.n_hits)
+    assert np.array_equal(ra.ids, rb.ids)
+    assert np.array_equal(ra.dists.view(np.uint64), rb.dists.view(np.uint64))
+    assert np.array_equal(ra.candidates_seen, rb.candidates_seen)
+    assert np.array_equal(ra.radius_used, rb.radius_used)
+    from oracle.bindings import make_params
+    oi = port.build_index(data, make_params(**c), 11)
+    for qi in list(range(0, nq, max(1, nq // 12))) + [7, nq - 1]:
+        ids, ds, rad, cs = oi.ck_ann(Q[qi], k)
+        assert np.array_equal(ra.ids[qi], ids), f"query {qi}"
+        assert np.array_equal(ra.dists[qi].view(np.uint64), np.asarray(ds).view(np.uint64)), f"query {qi}"
+        assert ra.radius_used[qi] == rad and int(ra.candidates_seen[qi]) == cs
