@@ -158,10 +158,20 @@ def recall_ratio(res_ids, res_d, n_hits, gt_ids, gt_d, k):
     return float(np.mean(rec)), float(np.mean(rat))
 
 
+def tc_tau_rows(k, budget):
+    """Rows the plan kernel scores exactly for tau^2 (query.cu run_query_batch)."""
+    return max(512, 2 * k, -(-4 * k * budget // 4096))
+
+
 # algorithmic bytes per launch (DESIGN.md §5); kernels without a model get null
-def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0):
+def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0, plan=None):
     if kernel == "project_exact":
         return 4.0 * d * n  # one read of the fp32 shard (SURVEY §8d: 4d B/point)
+    if kernel == "query_fast" and plan is not None:
+        # tensor-core hand-off: per query the plan kernel reads tree 0's leaf
+        # table (64 B box + 8 B begin/count per leaf), scores tau_rows u8 rows
+        # and writes the n-bit candidate bitmap
+        return (72.0 * plan["leaves"] + row_u8 * plan["tau_rows"] + n / 8.0) * nq
     if kernel == "query_fast":
         return 4.0 * d * budget * nq  # every verified candidate row (4d B/candidate)
     if kernel == "encode":
@@ -186,6 +196,14 @@ def ncu_traffic(kernel, units):
         return rec["dram_bytes_per_unit"] * units, rec["source"]
     except Exception:
         return None, None
+
+
+def peak_bf16():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0
 
 
 def peaks():
@@ -461,8 +479,10 @@ def main():
     hbm, peak_kind = peaks()
     build_roof = roofline(prof_build, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
                           exclude=("query_fast", "query_slow"))
+    plan = {"leaves": int(idx.tree(0).is_leaf.sum()), "tau_rows": tc_tau_rows(k, budget)}
     query_roof = roofline(prof_query, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
-                          only=("query_fast",), row_u8=idx.row_u8())
+                          only=("query_fast",), row_u8=idx.row_u8(), plan=plan)
+    query_roof_tc = roofline_tc(prof_query, args.steps, n_loc, nq, idx.row_u8(), peak_bf16())
     # the reference arm scores its first cpu_queries queries: same subset here
     m_ref = min(args.cpu_queries, nq)
     rec_ref, rat_ref = recall_ratio(out_ids[:m_ref], out_d[:m_ref], out_h[:m_ref], gt_ids[:m_ref],
@@ -482,7 +502,7 @@ def main():
                   "recall": round(rec, 6), "ratio": round(rat, 6),
                   "recall_on_reference_sample": round(rec_ref, 6),
                   "ratio_on_reference_sample": round(rat_ref, 6), "gpu_launches": query_launches,
-                  "roofline": query_roof,
+                  "roofline": query_roof, "roofline_tc": query_roof_tc,
                   "e2e": {"value": round(nq / (e2e_query_ms / 1e3), 2), "unit": "queries/s",
                           "h2d_bytes_per_step": int(nq * d * 4),
                           "d2h_bytes_per_step": int(nq * k * 12 + nq * 20)}},
@@ -520,8 +540,24 @@ def collect_profile(lib):
     return {kk: (float(ms[i]), int(cnt[i])) for i, kk in enumerate(keys)}
 
 
+def roofline_tc(prof, steps, n, nq, row_u8, peak_bf16):
+    """tcgen05 scorer: every (row, query) dot product, 2 * R int8 ops each, on the
+    tensor pipe.  Peak: dense int8 = 2x dense bf16 on sm_100, so 2x the measured
+    bf16 burst figure (MEASURED_PEAKS.json)."""
+    if "tc_score" not in prof or not row_u8:
+        return None
+    ms, launches = prof["tc_score"]
+    per_launch_ms = ms / max(1, launches)
+    ops = 2.0 * row_u8 * n * nq / max(1, launches / steps)
+    ach = ops / (per_launch_ms / 1e3) / 1e12
+    peak = 2.0 * peak_bf16
+    return {"kernel": "tc_score", "bound": "tensor", "unit": "TOPS", "achieved": round(ach, 2),
+            "peak": round(peak, 1), "peak_kind": "2x measured bf16 burst (dense int8)",
+            "frac": round(ach / peak, 5), "launch_ms": round(per_launch_ms, 4), "int8_ops": ops}
+
+
 def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exclude=(),
-             row_u8=0):
+             row_u8=0, plan=None):
     # nested scopes (tree_level_split inside tree_build) are not separate work
     items = [(kk, v) for kk, v in prof.items()
              if (only is None or kk in only) and kk not in exclude and kk != "tree_level_split"]
@@ -529,7 +565,9 @@ def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exc
         return None
     kern, (ms, launches) = max(items, key=lambda kv: kv[1][0])
     per_launch_ms = ms / max(1, launches)
-    b = algo_bytes(kern, n, d, nq, budget, K, L, row_u8)
+    if kern == "query_fast" and "tc_score" not in prof:
+        plan = None  # no tensor-core hand-off in this run: the kernel verified everything
+    b = algo_bytes(kern, n, d, nq, budget, K, L, row_u8, plan)
     total = sum(v[0] for kk, v in prof.items() if kk != "tree_level_split")
     units = nq if kern == "query_fast" else n
     traffic, tsrc = ncu_traffic(kern, units)
@@ -543,7 +581,9 @@ def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exc
         ach = b / (per_launch_ms / 1e3) / 1e9
         out.update({"achieved": round(ach, 2), "frac": round(ach / hbm, 5),
                     "algorithmic_bytes": b})
-        if kern == "query_fast" and row_u8:
+        if plan is not None:
+            out["model"] = "plan kernel (tc hand-off): 72 B/leaf x tree-0 leaves + R x tau_rows + n/8 per query"
+        if kern == "query_fast" and row_u8 and plan is None:
             b8 = float(row_u8) * budget * nq  # bytes the u8 rows actually hold
             out["u8_rows"] = {"bytes": b8, "achieved": round(b8 / (per_launch_ms / 1e3) / 1e9, 2),
                               "frac": round(b8 / (per_launch_ms / 1e3) / 1e9 / hbm, 5)}
