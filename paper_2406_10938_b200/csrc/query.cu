@@ -38,6 +38,7 @@ namespace {
 constexpr int kBatch = 1024;                    // candidates scored per block step
 constexpr int kTopCap = 2048;                   // staged (key, pos) entries
 constexpr int kBins = 1024;                     // mindist histogram bins (fast-path cut)
+constexpr int kFine = kBins * 32;               // approximate round: fine bins kept per leaf
 constexpr uint32_t kTcMinBudget = 8192;         // tensor-core hand-off from this budget on
 constexpr uint32_t kTauRows = 512;              // min rows scored exactly to set tau^2
 static_assert(kFastMaxK == kTopCap - kBatch, "fast-path k bound");
@@ -58,6 +59,7 @@ __device__ __forceinline__ bool key_less(uint64_t am, uint32_t ai, uint64_t bm, 
 // the staging buffers; they share one region.
 struct Smem {
     double* sq;                // [K][NR+1]                       (phase A)
+    float* sq32;               // [K][NR+1] fp32 copy (approximate leaf scan)
     uint64_t* th;              // [kTopCap] top-k key hi           (phase C)
     uint32_t* tl;              // [kTopCap] top-k key lo (position)
     uint64_t* bh;              // [kBatch] batch key hi
@@ -99,6 +101,7 @@ __device__ __forceinline__ Smem carve(uint8_t* base, int K, int NR, int d, int r
     s.bh = s.th + kTopCap;
     s.tl = reinterpret_cast<uint32_t*>(s.bh + kBatch);
     s.bl = s.tl + kTopCap;
+    s.sq32 = reinterpret_cast<float*>(c.take(4 * static_cast<size_t>(K) * (NR + 1)));
     s.hist = reinterpret_cast<unsigned long long*>(c.take(8 * 256));
     s.bins = reinterpret_cast<uint32_t*>(c.take(4 * kBins));
     s.u64s = reinterpret_cast<unsigned long long*>(c.take(8 * 16));
@@ -118,6 +121,7 @@ size_t smem_bytes(int K, int NR, int d, int row_u8) {
         off += bytes;
     };
     take(union_bytes(K, NR));
+    take(4 * static_cast<size_t>(K) * (NR + 1));
     take(8 * 256);
     take(4 * kBins);
     take(8 * 16);
@@ -146,6 +150,7 @@ __device__ void build_sq(const QueryPlan& P, int tree, const Smem& S) {
         const float v = S.qp[j];
         const double D = __dsub_rn(static_cast<double>(row), static_cast<double>(v));
         S.sq[i] = __dmul_rn(D, D);
+        S.sq32[i] = __double2float_rn(S.sq[i]);
         if (row < v) atomicAdd(&S.lbv[j], 1);
         if (row <= v) atomicAdd(&S.ubv[j], 1);
     }
@@ -207,6 +212,15 @@ __device__ __forceinline__ double pen_sq16(const double* __restrict__ sqj, uint3
     return (use_lo || use_hi) ? v : 0.0;
 }
 
+__device__ __forceinline__ float pen_sq16f(const float* __restrict__ sqj, uint32_t half, uint32_t lub, int NR) {
+    const int lo = half & 0xff, hi = (half >> 8) & 0xff;
+    const int lbv = lub & 0xffff, ubv = lub >> 16;
+    const bool use_lo = lo > 0 && lo >= ubv;
+    const bool use_hi = hi < NR - 1 && hi + 1 < lbv;
+    const float v = sqj[use_lo ? lo : hi + 1];
+    return (use_lo || use_hi) ? v : 0.0f;
+}
+
 __device__ __forceinline__ void leaf_mindist2_k16(const QueryPlan& P, const QTree& T, uint32_t li0,
                                                   uint32_t li1, const Smem& S, const uint32_t (&lub)[16],
                                                   double& md0, double& md1) {
@@ -227,6 +241,38 @@ __device__ __forceinline__ void leaf_mindist2_k16(const QueryPlan& P, const QTre
     }
     md0 = __dsqrt_rn(a0);
     md1 = __dsqrt_rn(a1);
+}
+
+// Exact round: histogram bin of an exact mindist (0xffff: outside the radius).
+__device__ __forceinline__ uint32_t exact_bin(double md, double radius, double scale) {
+    if (!(md <= radius)) return 0xffffu;
+    const double fb = __dmul_rn(md, scale);
+    return fb >= static_cast<double>(kBins - 1) ? kBins - 1 : static_cast<uint32_t>(fb);
+}
+
+// Approximate round: the same penalty selection as leaf_mindist2_k16 with the
+// fp32 copy of the table, summed in fp32 in dimension order, no square root.
+// |result - exact squared mindist| <= (2K + 1) * 2^-24 * exact (+ denormal
+// rounding), which the caller's bound rel = (K + 2) * 2^-22 covers.
+__device__ __forceinline__ void leaf_a2_k16_f32(const QueryPlan& P, const QTree& T, uint32_t li0, uint32_t li1,
+                                                const Smem& S, const uint32_t (&lub)[16], float& a0, float& a1) {
+    uint32_t w0[8], w1[8];
+    box_words(T, li0, w0);
+    box_words(T, li1, w1);
+    const int W = P.NR + 1;
+    float s0 = 0.0f, s1 = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j < P.K) {
+            const float* sqj = S.sq32 + j * W;
+            const uint32_t h0 = w0[j >> 1] >> ((j & 1) * 16);
+            const uint32_t h1 = w1[j >> 1] >> ((j & 1) * 16);
+            s0 = __fadd_rn(s0, pen_sq16f(sqj, h0, lub[j], P.NR));
+            s1 = __fadd_rn(s1, pen_sq16f(sqj, h1, lub[j], P.NR));
+        }
+    }
+    a0 = s0;
+    a1 = s1;
 }
 
 // Exact original-space squared distance (dataset.hpp:23-30): sequential fp64.
@@ -513,7 +559,7 @@ __device__ __forceinline__ uint32_t sqdiff4(uint32_t a, uint32_t b, uint32_t acc
 struct FastSlot {
     LeafItem *A, *B, *C;  // bin-b* items and the select's ping-pong buffers
     uint32_t* full;       // leaves taken whole (leaf indices)
-    uint16_t* bin16;      // per-leaf histogram bin (0xffff: outside the radius)
+    uint16_t* bin16;      // per-leaf histogram bin (0xffff: outside the radius), 16-B aligned
     uint32_t* cand;       // candidate rows as tree-0 permutation indices
 };
 
@@ -526,13 +572,13 @@ __device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, 
     f.C = f.B + maxl;
     f.full = reinterpret_cast<uint32_t*>(f.C + maxl);
     f.cand = f.full + maxl;
-    f.bin16 = reinterpret_cast<uint16_t*>(f.cand + budget);
+    f.bin16 = reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(f.cand + budget) + 15) & ~uintptr_t(15));
     return f;
 }
 
 size_t fast_slot_bytes(uint32_t maxl, uint64_t budget) {
     const size_t b = 3 * static_cast<size_t>(maxl) * sizeof(LeafItem) + 4 * static_cast<size_t>(maxl) +
-                     4 * budget + 2 * static_cast<size_t>(maxl);
+                     4 * budget + 2 * (static_cast<size_t>(maxl) + 8) + 16;
     return (b + 255) / 256 * 256;
 }
 
@@ -693,6 +739,80 @@ __device__ uint32_t emit_rows(const uint32_t* list, uint32_t n, const QTree& T0,
     return total;
 }
 
+// Block-wide: the bin of hist[0..nbins) (nbins a multiple of blockDim.x) where
+// the running count reaches `need` (>= 1, <= total); *before = count below it.
+__device__ void select_count_bin(const uint32_t* hist, int nbins, uint32_t need, const Smem& S, uint32_t& bin,
+                                 uint32_t& before) {
+    const int per = nbins / blockDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t part = 0;
+    for (int b = 0; b < per; ++b) part += hist[threadIdx.x * per + b];
+    uint32_t incl = part;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    uint32_t* wt = reinterpret_cast<uint32_t*>(S.hist);
+    if (lane == 31) wt[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += wt[w];
+    incl += wpre;
+    const uint32_t excl = incl - part;
+    if (excl < need && need <= incl) {
+        uint32_t cum = excl;
+        int b = threadIdx.x * per;
+        for (int e = 0; e < per; ++e, ++b) {
+            const uint32_t c = hist[b];
+            if (cum + c >= need) break;
+            cum += c;
+        }
+        S.u32s[13] = static_cast<uint32_t>(b);
+        S.u32s[14] = cum;
+    }
+    __syncthreads();
+    bin = S.u32s[13];
+    before = S.u32s[14];
+    __syncthreads();
+}
+
+// Exact k-th smallest integer dist^2 over the u8 rows F.cand[0..nt) (tree-0
+// row indices; overwritten with their dist^2): two counting passes over
+// dist^2 >> s and its low s bits.  INT_MAX when nt < k.
+__device__ int32_t kth_dist2(const QueryPlan& P, const FastSlot& F, const Smem& S, uint32_t nt, int k) {
+    if (nt < static_cast<uint32_t>(k)) return 0x7fffffff;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(S.th);  // 4096 bins: top-k staging is idle here
+    int sh = 0;
+    while (((65025u * static_cast<uint32_t>(P.d)) >> sh) >= 4096u) ++sh;
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t c0 = 0; c0 < nt; c0 += kBatch) {
+        const uint32_t nb = min(static_cast<uint32_t>(kBatch), nt - c0);
+        score_batch(P, F, S, c0, nb, true);
+        __syncthreads();
+        for (uint32_t r = threadIdx.x; r < nb; r += blockDim.x) {
+            const uint32_t d2 = static_cast<uint32_t>(S.bh[r]);
+            F.cand[c0 + r] = d2;
+            atomicAdd(&hist[d2 >> sh], 1u);
+        }
+        __syncthreads();
+    }
+    uint32_t cb, before;
+    select_count_bin(hist, 4096, static_cast<uint32_t>(k), S, cb, before);
+    const int nfine = 1 << sh;
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+        const uint32_t d2 = F.cand[i];
+        if ((d2 >> sh) == cb) atomicAdd(&hist[d2 & (nfine - 1)], 1u);
+    }
+    __syncthreads();
+    uint32_t fb, before2;
+    select_count_bin(hist, nfine >= static_cast<int>(blockDim.x) ? nfine : static_cast<int>(blockDim.x),
+                     static_cast<uint32_t>(k) - before, S, fb, before2);
+    return static_cast<int32_t>((cb << sh) | fb);
+}
+
 __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -715,141 +835,249 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         load_query_proj(P, q, 0, S);
         build_sq(P, 0, S);
         phase(0);
-        // pass 1: exact mindist of every leaf -> weight histogram over bins
-        // monotone in mindist; each leaf's bin is kept (0xffff: outside)
+        // Leaf scan + budget cut.  Approximate round (K <= 16): fp32 squared
+        // mindists with a rigorous relative error bound `rel` bin the leaves;
+        // only leaves whose position against the crossing bin is ambiguous get
+        // exact fp64 mindists, and the exact cut is then checked to lie
+        // strictly between the leaves taken whole and the ones dropped.  Any
+        // doubt (crossing bin in the radius band, a check failing) re-runs the
+        // query in the exact round: exact mindist for every leaf.
         const uint32_t nl = T0.num_leaves;
-        for (int i = threadIdx.x; i < kBins; i += blockDim.x) S.bins[i] = 0;
-        if (threadIdx.x == 0) S.u64s[0] = 0;
-        const double scale = radius > 0.0 ? static_cast<double>(kBins) / radius : 0.0;
-        __syncthreads();
-        {
-            unsigned long long wsum = 0;
-            auto record = [&](uint32_t li, double md) {
-                uint32_t b = 0xffff;
-                if (md <= radius) {
-                    const uint32_t cnt = __ldg(T0.leaf_count + li);
-                    const double fb = __dmul_rn(md, scale);
-                    b = fb >= static_cast<double>(kBins - 1) ? kBins - 1 : static_cast<uint32_t>(fb);
-                    wsum += cnt;
-                    atomicAdd(&S.bins[b], cnt);
-                }
-                F.bin16[li] = static_cast<uint16_t>(b);
-            };
-            if (P.K <= 16) {
-                uint32_t lub[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    lub[j] = j < P.K ? (static_cast<uint32_t>(S.lbv[j]) | (static_cast<uint32_t>(S.ubv[j]) << 16)) : 0u;
-                for (uint32_t li0 = threadIdx.x; li0 < nl; li0 += 2 * blockDim.x) {
-                    const uint32_t li1 = li0 + blockDim.x;
-                    double md0, md1;
-                    leaf_mindist2_k16(P, T0, li0, li1 < nl ? li1 : li0, S, lub, md0, md1);
-                    record(li0, md0);
-                    if (li1 < nl) record(li1, md1);
-                }
-            } else {
-                for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) record(li, leaf_mindist(P, T0, li, S));
+        const double r2 = __dmul_rn(radius, radius);
+        const double rel = static_cast<double>(P.K + 2) * 0x1p-22;  // >= 2K ulp(fp32) of the sum
+        const double aabs = 1e-36;                                   // fp32 denormal rounding
+        const double r2_in = r2 * (1.0 - 1e-12), r2_out = r2 * (1.0 + 1e-12);
+        bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30;
+        const int lane = threadIdx.x & 31;
+        uint32_t n_full = 0, cut_li = 0, bstar = 0;
+        uint64_t take_cut = 0;
+        bool to_slow = false;
+        double scale = 0.0;
+        // approximate round: fine bin (kFine = 32 per histogram bin) of a leaf
+        // from its fp32 squared mindist; kFine-1: the radius band, 0xffff:
+        // certainly outside.  A fine bin is wider than the error margin
+        // (rel * kFine < 1), so only leaves in the fine bins next to the
+        // crossing bin's edges can be on the wrong side of them.
+        auto approx_bin = [&](float af) -> uint32_t {
+            const double a = static_cast<double>(af);
+            if (a * (1.0 + rel) + aabs < r2_in) {
+                const double fb = a * scale;
+                return fb >= static_cast<double>(kFine - 33) ? kFine - 33 : static_cast<uint32_t>(fb);
             }
-            for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
-            if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&S.u64s[0], wsum);
+            return a * (1.0 - rel) - aabs > r2_out ? 0xffffu : kFine - 1;
+        };
+        for (;;) {
+            for (int i = threadIdx.x; i < kBins; i += blockDim.x) S.bins[i] = 0;
+            if (threadIdx.x == 0) {
+                S.u64s[0] = 0;
+                S.u64s[2] = 0;  // W_D: weight taken whole (approximate round)
+                S.u64s[3] = 0;  // W_M: in-radius weight of the ambiguous leaves
+            }
+            scale = approx ? static_cast<double>(kFine) / r2
+                           : (radius > 0.0 ? static_cast<double>(kBins) / radius : 0.0);
+            __syncthreads();
+            // pass 1: every leaf of tree 0 -> weight histogram over bins
+            // monotone in mindist; the per-leaf key is kept for pass 2
+            {
+                unsigned long long wsum = 0;
+                auto record = [&](uint32_t li, uint32_t b) {
+                    if (b != 0xffffu) {
+                        const uint32_t cnt = __ldg(T0.leaf_count + li);
+                        wsum += cnt;
+                        atomicAdd(&S.bins[approx ? b >> 5 : b], cnt);
+                    }
+                    F.bin16[li] = static_cast<uint16_t>(b);
+                };
+                if (approx || P.K <= 16) {
+                    uint32_t lub[16];
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        lub[j] = j < P.K ? (static_cast<uint32_t>(S.lbv[j]) | (static_cast<uint32_t>(S.ubv[j]) << 16)) : 0u;
+                    for (uint32_t li0 = threadIdx.x; li0 < nl; li0 += 2 * blockDim.x) {
+                        const uint32_t li1 = li0 + blockDim.x;
+                        if (approx) {
+                            float a0, a1;
+                            leaf_a2_k16_f32(P, T0, li0, li1 < nl ? li1 : li0, S, lub, a0, a1);
+                            record(li0, approx_bin(a0));
+                            if (li1 < nl) record(li1, approx_bin(a1));
+                        } else {
+                            double md0, md1;
+                            leaf_mindist2_k16(P, T0, li0, li1 < nl ? li1 : li0, S, lub, md0, md1);
+                            const uint32_t b0 = exact_bin(md0, radius, scale), b1 = exact_bin(md1, radius, scale);
+                            record(li0, b0);
+                            if (li1 < nl) record(li1, b1);
+                        }
+                    }
+                } else {
+                    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) {
+                        record(li, exact_bin(leaf_mindist(P, T0, li, S), radius, scale));
+                    }
+                }
+                for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+                if (lane == 0 && wsum) atomicAdd(&S.u64s[0], wsum);
+            }
+            __syncthreads();
+            const uint64_t W = S.u64s[0];  // approximate round: an upper bound
+            __syncthreads();
+            phase(1);
+            if (W < P.budget) {  // budget does not fill in tree 0 round 0
+                to_slow = true;
+                break;
+            }
+            // the budget trips inside bin b*: leaves of lower bins are taken whole,
+            // only b*'s leaves need the exact (mindist, node id) order
+            if (threadIdx.x < 32) {
+                constexpr int per = kBins / 32;
+                unsigned long long part = 0;
+                for (int b = 0; b < per; ++b) part += S.bins[lane * per + b];
+                unsigned long long incl = part;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const unsigned long long excl = incl - part;
+                if (excl < P.budget && P.budget <= incl) {
+                    unsigned long long cum = excl;
+                    int bin = lane * per;
+                    for (int b = 0; b < per; ++b, ++bin) {
+                        const unsigned long long c = S.bins[bin];
+                        if (cum + c >= P.budget) break;
+                        cum += c;
+                    }
+                    S.u32s[2] = static_cast<uint32_t>(bin);
+                    S.u64s[1] = P.budget - cum;
+                }
+                if (lane == 0) {
+                    S.u32s[0] = 0;  // whole-leaf list
+                    S.u32s[1] = 0;  // ambiguous / bin-b* list
+                }
+            }
+            __syncthreads();
+            bstar = S.u32s[2];
+            if (approx && bstar == kBins - 1) {  // crossing in the radius band
+                approx = false;
+                __syncthreads();
+                continue;
+            }
+            const double lo_edge = approx ? static_cast<double>(bstar * 32) / scale : 0.0;
+            const double hi_edge = approx ? static_cast<double>((bstar + 1) * 32) / scale : 0.0;
+            const uint32_t lo_f = bstar * 32, hi_f = bstar * 32 + 31;  // b*'s fine bins
+            // pass 2: leaves taken whole -> F.full; ambiguous leaves (exact round:
+            // bin b*; approximate round: b*'s fine bins and the fine bin on
+            // either side) -> exact items in F.B.  Eight leaf bins per thread
+            // per step (one 16-byte load).
+            {
+                unsigned long long w_margin = 0, wm = 0;
+                const uint32_t nv = (nl + 7) / 8;
+                for (uint32_t vb = 0; vb < nv; vb += blockDim.x) {
+                    const uint32_t v = vb + threadIdx.x;
+                    uint4 pk = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                    if (v < nv) pk = reinterpret_cast<const uint4*>(F.bin16)[v];
+                    const uint32_t wds[4] = {pk.x, pk.y, pk.z, pk.w};
+                    uint32_t wmask = 0, amask = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        uint32_t b = (wds[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+                        if (v * 8 + e >= nl) b = 0xffffu;
+                        if (b == 0xffffu) continue;
+                        if (approx) {  // fine bins: certainly before / ambiguous / after
+                            if (b + 1 < lo_f) wmask |= 1u << e;
+                            else if (b <= hi_f + 1) amask |= 1u << e;
+                        } else {
+                            if (b < bstar) wmask |= 1u << e;
+                            else if (b == bstar) amask |= 1u << e;
+                        }
+                    }
+                    // whole leaves: warp-aggregated append
+                    const uint32_t cnt = __popc(wmask);
+                    uint32_t incl = cnt;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+                    uint32_t b0 = 0;
+                    if (lane == 31 && tot) b0 = atomicAdd(&S.u32s[0], tot);
+                    b0 = __shfl_sync(0xffffffffu, b0, 31) + incl - cnt;
+                    for (uint32_t m = wmask; m; m &= m - 1) F.full[b0++] = v * 8 + __ffs(m) - 1;
+                    // ambiguous leaves (a few hundred per query)
+                    for (uint32_t m = amask; m; m &= m - 1) {
+                        const uint32_t li = v * 8 + __ffs(m) - 1;
+                        const uint32_t w = __ldg(T0.leaf_count + li);
+                        if (approx && F.bin16[li] < lo_f) w_margin += w;  // counted below b* by the histogram
+                        const double md = leaf_mindist(P, T0, li, S);
+                        if (!(md <= radius)) continue;
+                        LeafItem it;
+                        it.mdb = static_cast<uint64_t>(__double_as_longlong(md));
+                        it.id = __ldg(T0.leaf_node + li);
+                        it.w = w;
+                        it.li = li;
+                        it.pad = 0;
+                        wm += w;
+                        F.B[atomicAdd(&S.u32s[1], 1u)] = it;
+                    }
+                }
+                for (int o = 16; o; o >>= 1) {
+                    w_margin += __shfl_xor_sync(0xffffffffu, w_margin, o);
+                    wm += __shfl_xor_sync(0xffffffffu, wm, o);
+                }
+                if (lane == 0 && w_margin) atomicAdd(&S.u64s[2], w_margin);
+                if (lane == 0 && wm) atomicAdd(&S.u64s[3], wm);
+            }
+            __syncthreads();
+            const uint32_t n_bin = S.u32s[1];  // weighted_select reuses this counter
+            // approximate round: weight taken whole = histogram weight below b*
+            // minus the margin leaves of bin b*-1 that turned out ambiguous
+            const uint64_t need = approx ? S.u64s[1] + S.u64s[2] : S.u64s[1];
+            const uint64_t w_whole = P.budget - need, w_amb = S.u64s[3];
+            __syncthreads();
+            if (approx && (need == 0 || need > w_amb)) {
+                approx = false;
+                continue;
+            }
+            uint64_t kmdb;
+            uint32_t kid;
+            weighted_select(F.B, n_bin, need, F.C, F.A, S, kmdb, kid, take_cut);
+            if (approx) {  // the cut must lie strictly between whole and dropped leaves
+                const double mdc = __longlong_as_double(static_cast<long long>(kmdb));
+                const bool lo_ok = w_whole == 0 || mdc > __dsqrt_rn(lo_edge);
+                const bool hi_ok = mdc < __dsqrt_rn(hi_edge);
+                if (!(lo_ok && hi_ok)) {
+                    approx = false;
+                    continue;
+                }
+            }
+            // ambiguous leaves ordered before the cut leaf are whole too; find the cut leaf
+            for (uint32_t base = 0; base < n_bin; base += blockDim.x) {
+                const uint32_t i = base + threadIdx.x;
+                bool before = false;
+                uint32_t li = 0;
+                if (i < n_bin) {
+                    const LeafItem it = F.B[i];
+                    li = it.li;
+                    before = key_less(it.mdb, it.id, kmdb, kid);
+                    if (it.mdb == kmdb && it.id == kid) S.u32s[10] = it.li;
+                }
+                const uint32_t m = __ballot_sync(0xffffffffu, before);
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    uint32_t b0 = 0;
+                    if (lane == leader) b0 = atomicAdd(&S.u32s[0], static_cast<uint32_t>(__popc(m)));
+                    b0 = __shfl_sync(0xffffffffu, b0, leader);
+                    if (before) F.full[b0 + __popc(m & ((1u << lane) - 1u))] = li;
+                }
+            }
+            __syncthreads();
+            n_full = S.u32s[0];
+            cut_li = S.u32s[10];
+            if (!approx && P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 6, 1ULL);
+            break;
         }
-        __syncthreads();
-        const uint64_t W = S.u64s[0];
-        __syncthreads();
-        phase(1);
-        if (P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 7, static_cast<unsigned long long>(W));
-        if (W < P.budget) {  // budget does not fill in tree 0 round 0
+        if (to_slow) {
             if (threadIdx.x == 0) slow_list[atomicAdd(slow_n, 1u)] = static_cast<uint32_t>(q);
             __syncthreads();
             continue;
         }
-        // the budget trips inside bin b*: leaves of lower bins are taken whole,
-        // only b*'s leaves need the exact (mindist, node id) order
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        if (threadIdx.x < 32) {
-            constexpr int per = kBins / 32;
-            unsigned long long part = 0;
-            for (int b = 0; b < per; ++b) part += S.bins[lane * per + b];
-            unsigned long long incl = part;
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            const unsigned long long excl = incl - part;
-            if (excl < P.budget && P.budget <= incl) {
-                unsigned long long cum = excl;
-                int bin = lane * per;
-                for (int b = 0; b < per; ++b, ++bin) {
-                    const unsigned long long c = S.bins[bin];
-                    if (cum + c >= P.budget) break;
-                    cum += c;
-                }
-                S.u32s[2] = static_cast<uint32_t>(bin);
-                S.u64s[1] = P.budget - cum;
-            }
-            if (lane == 0) {
-                S.u32s[0] = 0;  // whole-leaf list
-                S.u32s[1] = 0;  // bin-b* list
-            }
-        }
-        __syncthreads();
-        const uint32_t bstar = S.u32s[2];
-        const uint64_t need_in_bin = S.u64s[1];
-        // pass 2: collect (li of whole leaves) and (exact items of bin b*)
-        for (uint32_t base = 0; base < nl; base += blockDim.x) {
-            const uint32_t li = base + threadIdx.x;
-            uint16_t b = 0xffff;
-            if (li < nl) b = F.bin16[li];
-            const bool whole = b < bstar;
-            const uint32_t m = __ballot_sync(0xffffffffu, whole);
-            if (m) {
-                const int leader = __ffs(m) - 1;
-                uint32_t b0 = 0;
-                if (lane == leader) b0 = atomicAdd(&S.u32s[0], static_cast<uint32_t>(__popc(m)));
-                b0 = __shfl_sync(0xffffffffu, b0, leader);
-                if (whole) F.full[b0 + __popc(m & ((1u << lane) - 1u))] = li;
-            }
-            const bool atb = b == bstar;
-            LeafItem it;
-            if (atb) {
-                const double md = leaf_mindist(P, T0, li, S);
-                it.mdb = static_cast<uint64_t>(__double_as_longlong(md));
-                it.id = __ldg(T0.leaf_node + li);
-                it.w = __ldg(T0.leaf_count + li);
-                it.li = li;
-                it.pad = b;
-            }
-            warp_append(atb, it, F.B, &S.u32s[1]);
-        }
-        __syncthreads();
-        const uint32_t n_bin = S.u32s[1];  // weighted_select reuses this counter
-        __syncthreads();
-        uint64_t kmdb, take_cut;
-        uint32_t kid;
-        weighted_select(F.B, n_bin, need_in_bin, F.C, F.A, S, kmdb, kid, take_cut);
-        // b* leaves ordered before the cut leaf are whole too; find the cut leaf
-        for (uint32_t base = 0; base < n_bin; base += blockDim.x) {
-            const uint32_t i = base + threadIdx.x;
-            bool before = false;
-            uint32_t li = 0;
-            if (i < n_bin) {
-                const LeafItem it = F.B[i];
-                li = it.li;
-                before = key_less(it.mdb, it.id, kmdb, kid);
-                if (it.mdb == kmdb && it.id == kid) S.u32s[10] = it.li;
-            }
-            const uint32_t m = __ballot_sync(0xffffffffu, before);
-            if (m) {
-                const int leader = __ffs(m) - 1;
-                uint32_t b0 = 0;
-                if (lane == leader) b0 = atomicAdd(&S.u32s[0], static_cast<uint32_t>(__popc(m)));
-                b0 = __shfl_sync(0xffffffffu, b0, leader);
-                if (before) F.full[b0 + __popc(m & ((1u << lane) - 1u))] = li;
-            }
-        }
-        __syncthreads();
-        const uint32_t n_full = S.u32s[0];
-        const uint32_t cut_li = S.u32s[10];
         phase(2);
         // ---- tensor-core hand-off (u8 rows): exact tau^2 from the nearest
         // leaves, the candidate SET as a bitmap; tc_score_kernel verifies it
@@ -892,7 +1120,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                 bool in = false;
                 if (i < n_full) {
                     li = F.full[i];
-                    in = F.bin16[li] <= b_tau;
+                    in = (approx ? F.bin16[li] >> 5 : F.bin16[li]) <= b_tau;
                 }
                 const uint32_t m = __ballot_sync(0xffffffffu, in);
                 if (m) {
@@ -906,17 +1134,8 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             __syncthreads();
             const uint32_t n_tau = S.u32s[12];
             __syncthreads();
-            const uint32_t nt = emit_rows(tau_list, n_tau, T0, F.cand, B32, S);
-            // exact k-th smallest dist^2 among those rows
-            topk_init(S);
-            for (uint32_t c0 = 0; c0 < nt; c0 += kBatch) {
-                const uint32_t nb = min(static_cast<uint32_t>(kBatch), nt - c0);
-                score_batch(P, F, S, c0, nb, true);
-                __syncthreads();
-                topk_absorb(S, nb, P.k, P.perm0);
-            }
-            const uint32_t have = topk_finish(S, P.k);
-            const int32_t tau2 = have >= static_cast<uint32_t>(P.k) ? static_cast<int32_t>(S.th[P.k - 1]) : 0x7fffffff;
+            const uint32_t nt = min(emit_rows(tau_list, n_tau, T0, F.cand, B32, S), B32);
+            const int32_t tau2 = kth_dist2(P, F, S, nt, P.k);  // exact k-th smallest among those rows
             // candidate bitmap: whole leaves + the cut leaf's prefix
             uint32_t* bm = P.tc_bm + (qs - P.q_begin) * P.tc_W;
             for (uint32_t i = threadIdx.x; i <= n_full; i += blockDim.x) {

@@ -222,7 +222,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
         const uint32_t u = unit_s;
         __syncthreads();  // unit_s is rewritten next iteration
         if (u >= units) break;
-        const uint32_t qt = u / G, g = u % G;
+        // query-tile-minor: CTAs running at the same time stream the same row
+        // range for different query tiles, so each row tile comes from HBM once
+        const uint32_t qt = u % n_qt, g = u / n_qt;
         const uint32_t rt0 = static_cast<uint32_t>(static_cast<uint64_t>(n_rt) * g / G);
         const uint32_t rt1 = static_cast<uint32_t>(static_cast<uint64_t>(n_rt) * (g + 1) / G);
         const uint32_t* trow = a.tmap + static_cast<uint64_t>(qt) * a.TW;
