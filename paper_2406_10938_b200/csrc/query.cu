@@ -59,7 +59,8 @@ __device__ __forceinline__ bool key_less(uint64_t am, uint32_t ai, uint64_t bm, 
 // the staging buffers; they share one region.
 struct Smem {
     double* sq;                // [K][NR+1]                       (phase A)
-    float* sq32;               // [K][NR+1] fp32 copy (approximate leaf scan)
+    float* tlo;                // [K][NR] fast path: fp32 penalty if the box starts at region r
+    float* thi;                // [K][NR] fast path: fp32 penalty if the box ends at region r
     uint64_t* th;              // [kTopCap] top-k key hi           (phase C)
     uint32_t* tl;              // [kTopCap] top-k key lo (position)
     uint64_t* bh;              // [kBatch] batch key hi
@@ -97,11 +98,12 @@ __device__ __forceinline__ Smem carve(uint8_t* base, int K, int NR, int d, int r
     Smem s;
     uint8_t* u = c.take(union_bytes(K, NR));
     s.sq = reinterpret_cast<double*>(u);
+    s.tlo = reinterpret_cast<float*>(u);
+    s.thi = s.tlo + static_cast<size_t>(K) * NR;
     s.th = reinterpret_cast<uint64_t*>(u);
     s.bh = s.th + kTopCap;
     s.tl = reinterpret_cast<uint32_t*>(s.bh + kBatch);
     s.bl = s.tl + kTopCap;
-    s.sq32 = reinterpret_cast<float*>(c.take(4 * static_cast<size_t>(K) * (NR + 1)));
     s.hist = reinterpret_cast<unsigned long long*>(c.take(8 * 256));
     s.bins = reinterpret_cast<uint32_t*>(c.take(4 * kBins));
     s.u64s = reinterpret_cast<unsigned long long*>(c.take(8 * 16));
@@ -121,7 +123,6 @@ size_t smem_bytes(int K, int NR, int d, int row_u8) {
         off += bytes;
     };
     take(union_bytes(K, NR));
-    take(4 * static_cast<size_t>(K) * (NR + 1));
     take(8 * 256);
     take(4 * kBins);
     take(8 * 16);
@@ -150,11 +151,89 @@ __device__ void build_sq(const QueryPlan& P, int tree, const Smem& S) {
         const float v = S.qp[j];
         const double D = __dsub_rn(static_cast<double>(row), static_cast<double>(v));
         S.sq[i] = __dmul_rn(D, D);
-        S.sq32[i] = __double2float_rn(S.sq[i]);
         if (row < v) atomicAdd(&S.lbv[j], 1);
         if (row <= v) atomicAdd(&S.ubv[j], 1);
     }
     __syncthreads();
+}
+
+// Fast path, per (query, tree 0): the penalty of a box edge split by side, so
+// the scan needs no per-dimension branches: for a box [lo, hi] in dim j the
+// reference's penalty (de_tree.cpp:169-184) is tlo[j][lo] + thi[j][hi], at
+// most one of them non-zero:
+//   tlo[j][r] = pen(j, r)     if r > 0      and r >= ubv_j  (query below the box)
+//   thi[j][r] = pen(j, r + 1) if r < NR - 1 and r + 1 < lbv_j (query above it)
+// with pen(j, e) = (double(row_j[e]) - double(v_j))^2 rounded to fp32.
+__device__ void build_pen_tables(const QueryPlan& P, const Smem& S) {
+    const int W = P.NR + 1, NR = P.NR;
+    const float* tb = P.table;
+    for (int j = threadIdx.x; j < P.K; j += blockDim.x) {
+        S.lbv[j] = 0;
+        S.ubv[j] = 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P.K * W; i += blockDim.x) {
+        const int j = i / W;
+        const float row = tb[i], v = S.qp[j];
+        if (row < v) atomicAdd(&S.lbv[j], 1);
+        if (row <= v) atomicAdd(&S.ubv[j], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < P.K * NR; i += blockDim.x) {
+        const int j = i / NR, r = i % NR;
+        const double v = static_cast<double>(S.qp[j]);
+        float lo = 0.0f, hi = 0.0f;
+        if (r > 0 && r >= S.ubv[j]) {
+            const double D = __dsub_rn(static_cast<double>(tb[j * W + r]), v);
+            lo = __double2float_rn(__dmul_rn(D, D));
+        }
+        if (r < NR - 1 && r + 1 < S.lbv[j]) {
+            const double D = __dsub_rn(static_cast<double>(tb[j * W + r + 1]), v);
+            hi = __double2float_rn(__dmul_rn(D, D));
+        }
+        S.tlo[i] = lo;
+        S.thi[i] = hi;
+    }
+    __syncthreads();
+}
+
+// Exact mindist of tree-0 leaf li straight from the breakpoint table (no fp64
+// table in smem): the same operations in the same order as leaf_mindist.
+__device__ __forceinline__ double leaf_mindist_direct(const QueryPlan& P, const QTree& T, uint32_t li,
+                                                      const Smem& S) {
+    const uint4* box = reinterpret_cast<const uint4*>(T.leaf_box + static_cast<size_t>(li) * 64);
+    uint32_t w[12];
+    {
+        const uint4 a = __ldg(box), b = __ldg(box + 1);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+        if (P.K > 16) {
+            const uint4 c = __ldg(box + 2);
+            w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
+        } else {
+            w[8] = w[9] = w[10] = w[11] = 0;
+        }
+    }
+    const int W = P.NR + 1;
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        if (j < P.K) {
+            const uint32_t half = w[j >> 1] >> ((j & 1) * 16);
+            const int lo = half & 0xff, hi = (half >> 8) & 0xff;
+            int e = -1;
+            if (lo > 0 && lo >= S.ubv[j]) e = lo;
+            else if (hi < P.NR - 1 && hi + 1 < S.lbv[j]) e = hi + 1;
+            double pen_sq = 0.0;
+            if (e >= 0) {
+                const double D = __dsub_rn(static_cast<double>(__ldg(P.table + j * W + e)),
+                                           static_cast<double>(S.qp[j]));
+                pen_sq = __dmul_rn(D, D);
+            }
+            acc = __dadd_rn(acc, pen_sq);
+        }
+    }
+    return __dsqrt_rn(acc);
 }
 
 __device__ __forceinline__ double leaf_mindist(const QueryPlan& P, const QTree& T, uint32_t li,
@@ -212,15 +291,6 @@ __device__ __forceinline__ double pen_sq16(const double* __restrict__ sqj, uint3
     return (use_lo || use_hi) ? v : 0.0;
 }
 
-__device__ __forceinline__ float pen_sq16f(const float* __restrict__ sqj, uint32_t half, uint32_t lub, int NR) {
-    const int lo = half & 0xff, hi = (half >> 8) & 0xff;
-    const int lbv = lub & 0xffff, ubv = lub >> 16;
-    const bool use_lo = lo > 0 && lo >= ubv;
-    const bool use_hi = hi < NR - 1 && hi + 1 < lbv;
-    const float v = sqj[use_lo ? lo : hi + 1];
-    return (use_lo || use_hi) ? v : 0.0f;
-}
-
 __device__ __forceinline__ void leaf_mindist2_k16(const QueryPlan& P, const QTree& T, uint32_t li0,
                                                   uint32_t li1, const Smem& S, const uint32_t (&lub)[16],
                                                   double& md0, double& md1) {
@@ -250,25 +320,29 @@ __device__ __forceinline__ uint32_t exact_bin(double md, double radius, double s
     return fb >= static_cast<double>(kBins - 1) ? kBins - 1 : static_cast<uint32_t>(fb);
 }
 
-// Approximate round: the same penalty selection as leaf_mindist2_k16 with the
-// fp32 copy of the table, summed in fp32 in dimension order, no square root.
-// |result - exact squared mindist| <= (2K + 1) * 2^-24 * exact (+ denormal
-// rounding), which the caller's bound rel = (K + 2) * 2^-22 covers.
+// Approximate round: the reference's penalties rounded to fp32 (tlo/thi, at
+// most one non-zero per dimension, so tlo + thi is exact), summed in fp32 in
+// dimension order, no square root.  |result - exact squared mindist| <=
+// (2K + 1) * 2^-24 * exact (+ denormal rounding), which the caller's bound
+// rel = (K + 2) * 2^-22 covers.
 __device__ __forceinline__ void leaf_a2_k16_f32(const QueryPlan& P, const QTree& T, uint32_t li0, uint32_t li1,
-                                                const Smem& S, const uint32_t (&lub)[16], float& a0, float& a1) {
+                                                const Smem& S, float& a0, float& a1) {
     uint32_t w0[8], w1[8];
     box_words(T, li0, w0);
     box_words(T, li1, w1);
-    const int W = P.NR + 1;
+    const int NR = P.NR;
     float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j < P.K) {
-            const float* sqj = S.sq32 + j * W;
-            const uint32_t h0 = w0[j >> 1] >> ((j & 1) * 16);
-            const uint32_t h1 = w1[j >> 1] >> ((j & 1) * 16);
-            s0 = __fadd_rn(s0, pen_sq16f(sqj, h0, lub[j], P.NR));
-            s1 = __fadd_rn(s1, pen_sq16f(sqj, h1, lub[j], P.NR));
+            // byte offsets of lo / hi entries: one shift + one mask each
+            const char* tl = reinterpret_cast<const char*>(S.tlo + j * NR);
+            const char* th = reinterpret_cast<const char*>(S.thi + j * NR);
+            const int sl = (j & 1) * 16;
+            const uint32_t l0 = (w0[j >> 1] >> sl << 2) & 0x3fcu, u0 = (w0[j >> 1] >> (sl + 6)) & 0x3fcu;
+            const uint32_t l1 = (w1[j >> 1] >> sl << 2) & 0x3fcu, u1 = (w1[j >> 1] >> (sl + 6)) & 0x3fcu;
+            s0 = __fadd_rn(s0, __fadd_rn(*reinterpret_cast<const float*>(tl + l0), *reinterpret_cast<const float*>(th + u0)));
+            s1 = __fadd_rn(s1, __fadd_rn(*reinterpret_cast<const float*>(tl + l1), *reinterpret_cast<const float*>(th + u1)));
         }
     }
     a0 = s0;
@@ -833,7 +907,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         const uint64_t q = P.order ? P.order[qs] : qs;
         const bool u8 = load_query_vec(P, q, S);
         load_query_proj(P, q, 0, S);
-        build_sq(P, 0, S);
+        build_pen_tables(P, S);
         phase(0);
         // Leaf scan + budget cut.  Approximate round (K <= 16): fp32 squared
         // mindists with a rigorous relative error bound `rel` bin the leaves;
@@ -858,13 +932,19 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         // certainly outside.  A fine bin is wider than the error margin
         // (rel * kFine < 1), so only leaves in the fine bins next to the
         // crossing bin's edges can be on the wrong side of them.
-        auto approx_bin = [&](float af) -> uint32_t {
-            const double a = static_cast<double>(af);
-            if (a * (1.0 + rel) + aabs < r2_in) {
-                const double fb = a * scale;
-                return fb >= static_cast<double>(kFine - 33) ? kFine - 33 : static_cast<uint32_t>(fb);
+        // All in fp32: a < t_in  =>  a (1 + rel) + aabs < r2_in (threshold rounded
+        // down), a > t_out  =>  a (1 - rel) - aabs > r2_out (rounded up); the
+        // fine bin floor(a * scale_f) is within 2^-23 relative of a * scale,
+        // which the margin analysis absorbs ((rel + 2^-22) * kFine < 1).
+        const float t_in = __double2float_rd((r2_in - aabs) / (1.0 + rel));
+        const float t_out = __double2float_ru((r2_out + aabs) / (1.0 - rel));
+        float scale_f = 0.0f;
+        auto approx_bin = [&](float a) -> uint32_t {
+            if (a < t_in) {
+                const float fb = a * scale_f;
+                return fb >= static_cast<float>(kFine - 33) ? kFine - 33 : static_cast<uint32_t>(fb);
             }
-            return a * (1.0 - rel) - aabs > r2_out ? 0xffffu : kFine - 1;
+            return a > t_out ? 0xffffu : kFine - 1;
         };
         for (;;) {
             for (int i = threadIdx.x; i < kBins; i += blockDim.x) S.bins[i] = 0;
@@ -875,6 +955,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             }
             scale = approx ? static_cast<double>(kFine) / r2
                            : (radius > 0.0 ? static_cast<double>(kBins) / radius : 0.0);
+            scale_f = __double2float_rn(scale);
             __syncthreads();
             // pass 1: every leaf of tree 0 -> weight histogram over bins
             // monotone in mindist; the per-leaf key is kept for pass 2
@@ -888,30 +969,17 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                     }
                     F.bin16[li] = static_cast<uint16_t>(b);
                 };
-                if (approx || P.K <= 16) {
-                    uint32_t lub[16];
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        lub[j] = j < P.K ? (static_cast<uint32_t>(S.lbv[j]) | (static_cast<uint32_t>(S.ubv[j]) << 16)) : 0u;
+                if (approx) {
                     for (uint32_t li0 = threadIdx.x; li0 < nl; li0 += 2 * blockDim.x) {
                         const uint32_t li1 = li0 + blockDim.x;
-                        if (approx) {
-                            float a0, a1;
-                            leaf_a2_k16_f32(P, T0, li0, li1 < nl ? li1 : li0, S, lub, a0, a1);
-                            record(li0, approx_bin(a0));
-                            if (li1 < nl) record(li1, approx_bin(a1));
-                        } else {
-                            double md0, md1;
-                            leaf_mindist2_k16(P, T0, li0, li1 < nl ? li1 : li0, S, lub, md0, md1);
-                            const uint32_t b0 = exact_bin(md0, radius, scale), b1 = exact_bin(md1, radius, scale);
-                            record(li0, b0);
-                            if (li1 < nl) record(li1, b1);
-                        }
+                        float a0, a1;
+                        leaf_a2_k16_f32(P, T0, li0, li1 < nl ? li1 : li0, S, a0, a1);
+                        record(li0, approx_bin(a0));
+                        if (li1 < nl) record(li1, approx_bin(a1));
                     }
-                } else {
-                    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) {
-                        record(li, exact_bin(leaf_mindist(P, T0, li, S), radius, scale));
-                    }
+                } else {  // exact round (rare): exact mindists from the breakpoint table
+                    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x)
+                        record(li, exact_bin(leaf_mindist_direct(P, T0, li, S), radius, scale));
                 }
                 for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
                 if (lane == 0 && wsum) atomicAdd(&S.u64s[0], wsum);
@@ -1005,7 +1073,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                         const uint32_t li = v * 8 + __ffs(m) - 1;
                         const uint32_t w = __ldg(T0.leaf_count + li);
                         if (approx && F.bin16[li] < lo_f) w_margin += w;  // counted below b* by the histogram
-                        const double md = leaf_mindist(P, T0, li, S);
+                        const double md = leaf_mindist_direct(P, T0, li, S);
                         if (!(md <= radius)) continue;
                         LeafItem it;
                         it.mdb = static_cast<uint64_t>(__double_as_longlong(md));
