@@ -405,6 +405,9 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     P.data_u8 = X.data_u8.get();
     P.xn_u8 = X.xn_u8.get();
     P.data_tc = X.data_tc.get();
+    P.trees_num_leaves0 = static_cast<uint32_t>(X.trees[0]->num_leaves);
+    P.trees_leaf_begin0 = X.trees[0]->leaf_begin.get();
+    P.trees_leaf_count0 = X.trees[0]->leaf_count.get();
     P.q_begin = 0;
     P.q_end = nq;
     P.tc_allowed = (flags & DETLSH_F_NO_TC) ? 0 : 1;

@@ -518,6 +518,34 @@ __device__ void weighted_select(LeafItem* A, uint32_t nA, uint64_t need, LeafIte
     __syncthreads();
 }
 
+// weighted_select for n <= blockDim.x items: every thread ranks its item by
+// summing the weights of the smaller keys (n^2 / blockDim compares, no radix
+// passes).  The item list is read through L1 (every thread reads the same
+// entries in the same order).
+__device__ void small_weighted_select(const LeafItem* A, uint32_t n, uint64_t need, const Smem& S,
+                                      uint64_t& kmdb, uint32_t& kid, uint64_t& take_cut) {
+    const uint32_t i = threadIdx.x;
+    if (i < n) {
+        const LeafItem me = A[i];
+        uint64_t before = 0;
+        for (uint32_t j = 0; j < n; ++j) {
+            const uint64_t mj = __ldg(&A[j].mdb);
+            const uint32_t ij = __ldg(&A[j].id), wj = __ldg(&A[j].w);
+            if (key_less(mj, ij, me.mdb, me.id)) before += wj;
+        }
+        if (before < need && need <= before + me.w) {
+            S.u64s[4] = me.mdb;
+            S.u32s[12] = me.id;
+            S.u64s[5] = need - before;
+        }
+    }
+    __syncthreads();
+    kmdb = S.u64s[4];
+    kid = S.u32s[12];
+    take_cut = S.u64s[5];
+    __syncthreads();
+}
+
 // ---- block top-k over (hi, lo) keys, ascending --------------------------------
 // hi = distance bits (non-negative double) or exact integer squared distance,
 // lo = dataset position: lexicographic order == the reference's (dist, pos).
@@ -907,7 +935,6 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         const uint64_t q = P.order ? P.order[qs] : qs;
         const bool u8 = load_query_vec(P, q, S);
         load_query_proj(P, q, 0, S);
-        build_pen_tables(P, S);
         phase(0);
         // Leaf scan + budget cut.  Approximate round (K <= 16): fp32 squared
         // mindists with a rigorous relative error bound `rel` bin the leaves;
@@ -922,6 +949,8 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         const double aabs = 1e-36;                                   // fp32 denormal rounding
         const double r2_in = r2 * (1.0 - 1e-12), r2_out = r2 * (1.0 + 1e-12);
         bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30;
+        if (approx) build_pen_tables(P, S);
+        else build_sq(P, 0, S);
         const int lane = threadIdx.x & 31;
         uint32_t n_full = 0, cut_li = 0, bstar = 0;
         uint64_t take_cut = 0;
@@ -977,9 +1006,9 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                         record(li0, approx_bin(a0));
                         if (li1 < nl) record(li1, approx_bin(a1));
                     }
-                } else {  // exact round (rare): exact mindists from the breakpoint table
+                } else {  // exact round (rare): exact mindists (fp64 table built below)
                     for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x)
-                        record(li, exact_bin(leaf_mindist_direct(P, T0, li, S), radius, scale));
+                        record(li, exact_bin(leaf_mindist(P, T0, li, S), radius, scale));
                 }
                 for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
                 if (lane == 0 && wsum) atomicAdd(&S.u64s[0], wsum);
@@ -987,6 +1016,9 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             __syncthreads();
             const uint64_t W = S.u64s[0];  // approximate round: an upper bound
             __syncthreads();
+            // the fp32 side tables are dead now: the fp64 penalty table takes
+            // their place for the exact mindists of the ambiguous leaves
+            if (approx) build_sq(P, 0, S);
             phase(1);
             if (W < P.budget) {  // budget does not fill in tree 0 round 0
                 to_slow = true;
@@ -1016,13 +1048,15 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                     S.u64s[1] = P.budget - cum;
                 }
                 if (lane == 0) {
-                    S.u32s[0] = 0;  // whole-leaf list
-                    S.u32s[1] = 0;  // ambiguous / bin-b* list
+                    S.u32s[0] = 0;   // whole-leaf list
+                    S.u32s[1] = 0;   // ambiguous / bin-b* items
+                    S.u32s[15] = 0;  // ambiguous leaf indices
                 }
             }
             __syncthreads();
             bstar = S.u32s[2];
             if (approx && bstar == kBins - 1) {  // crossing in the radius band
+                if (P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 6, 1ULL);
                 approx = false;
                 __syncthreads();
                 continue;
@@ -1036,16 +1070,24 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             // per step (one 16-byte load).
             {
                 unsigned long long w_margin = 0, wm = 0;
-                const uint32_t nv = (nl + 7) / 8;
-                for (uint32_t vb = 0; vb < nv; vb += blockDim.x) {
-                    const uint32_t v = vb + threadIdx.x;
-                    uint4 pk = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-                    if (v < nv) pk = reinterpret_cast<const uint4*>(F.bin16)[v];
-                    const uint32_t wds[4] = {pk.x, pk.y, pk.z, pk.w};
+                uint32_t* amb_list = reinterpret_cast<uint32_t*>(F.C);  // free until the select
+                // 32 leaf bins per thread per step: four 16-byte loads in flight
+                const uint32_t nv = (nl + 7) / 8, nv4 = (nv + 3) / 4;
+                for (uint32_t vb = 0; vb < nv4; vb += blockDim.x) {
+                    const uint32_t v4 = vb + threadIdx.x;
+                    uint4 pk[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        pk[u] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+                        if (v4 * 4 + u < nv) pk[u] = reinterpret_cast<const uint4*>(F.bin16)[v4 * 4 + u];
+                    }
+                    const uint32_t v = v4 * 4;  // first 8-leaf vector of this thread
                     uint32_t wmask = 0, amask = 0;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        uint32_t b = (wds[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+                    for (int e = 0; e < 32; ++e) {
+                        const uint4& q4 = pk[e >> 3];
+                        const uint32_t wd = ((e >> 1) & 3) == 0 ? q4.x : ((e >> 1) & 3) == 1 ? q4.y : ((e >> 1) & 3) == 2 ? q4.z : q4.w;
+                        uint32_t b = (wd >> (16 * (e & 1))) & 0xffffu;
                         if (v * 8 + e >= nl) b = 0xffffu;
                         if (b == 0xffffu) continue;
                         if (approx) {  // fine bins: certainly before / ambiguous / after
@@ -1068,22 +1110,40 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                     if (lane == 31 && tot) b0 = atomicAdd(&S.u32s[0], tot);
                     b0 = __shfl_sync(0xffffffffu, b0, 31) + incl - cnt;
                     for (uint32_t m = wmask; m; m &= m - 1) F.full[b0++] = v * 8 + __ffs(m) - 1;
-                    // ambiguous leaves (a few hundred per query)
-                    for (uint32_t m = amask; m; m &= m - 1) {
-                        const uint32_t li = v * 8 + __ffs(m) - 1;
+                    // ambiguous leaves (a few hundred per query): listed, then
+                    // scored exactly below, one per thread
+                    const uint32_t acnt = __popc(amask);
+                    uint32_t ainc = acnt;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, ainc, o);
+                        if (lane >= o) ainc += t;
+                    }
+                    const uint32_t atot = __shfl_sync(0xffffffffu, ainc, 31);
+                    uint32_t a0 = 0;
+                    if (lane == 31 && atot) a0 = atomicAdd(&S.u32s[15], atot);
+                    a0 = __shfl_sync(0xffffffffu, a0, 31) + ainc - acnt;
+                    for (uint32_t m = amask; m; m &= m - 1) amb_list[a0++] = v * 8 + __ffs(m) - 1;
+                }
+                __syncthreads();
+                const uint32_t n_amb = S.u32s[15];
+                for (uint32_t base = 0; base < n_amb; base += blockDim.x) {
+                    const uint32_t i = base + threadIdx.x;
+                    bool ok = false;
+                    LeafItem it;
+                    if (i < n_amb) {
+                        const uint32_t li = amb_list[i];
                         const uint32_t w = __ldg(T0.leaf_count + li);
                         if (approx && F.bin16[li] < lo_f) w_margin += w;  // counted below b* by the histogram
-                        const double md = leaf_mindist_direct(P, T0, li, S);
-                        if (!(md <= radius)) continue;
-                        LeafItem it;
+                        const double md = leaf_mindist(P, T0, li, S);
+                        ok = md <= radius;
                         it.mdb = static_cast<uint64_t>(__double_as_longlong(md));
                         it.id = __ldg(T0.leaf_node + li);
                         it.w = w;
                         it.li = li;
                         it.pad = 0;
-                        wm += w;
-                        F.B[atomicAdd(&S.u32s[1], 1u)] = it;
+                        if (ok) wm += w;
                     }
+                    warp_append(ok, it, F.B, &S.u32s[1]);
                 }
                 for (int o = 16; o; o >>= 1) {
                     w_margin += __shfl_xor_sync(0xffffffffu, w_margin, o);
@@ -1100,17 +1160,23 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             const uint64_t w_whole = P.budget - need, w_amb = S.u64s[3];
             __syncthreads();
             if (approx && (need == 0 || need > w_amb)) {
+                if (P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 6, 1ULL);
                 approx = false;
                 continue;
             }
             uint64_t kmdb;
             uint32_t kid;
-            weighted_select(F.B, n_bin, need, F.C, F.A, S, kmdb, kid, take_cut);
+            if (n_bin <= static_cast<uint32_t>(blockDim.x))
+                small_weighted_select(F.B, n_bin, need, S, kmdb, kid, take_cut);
+            else
+                weighted_select(F.B, n_bin, need, F.C, F.A, S, kmdb, kid, take_cut);
+            if (P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 7, static_cast<unsigned long long>(n_bin));
             if (approx) {  // the cut must lie strictly between whole and dropped leaves
                 const double mdc = __longlong_as_double(static_cast<long long>(kmdb));
                 const bool lo_ok = w_whole == 0 || mdc > __dsqrt_rn(lo_edge);
                 const bool hi_ok = mdc < __dsqrt_rn(hi_edge);
                 if (!(lo_ok && hi_ok)) {
+                    if (P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 6, 1ULL);
                     approx = false;
                     continue;
                 }
@@ -1138,7 +1204,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             __syncthreads();
             n_full = S.u32s[0];
             cut_li = S.u32s[10];
-            if (!approx && P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 6, 1ULL);
+
             break;
         }
         if (to_slow) {
@@ -1148,8 +1214,8 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         }
         phase(2);
         // ---- tensor-core hand-off (u8 rows): exact tau^2 from the nearest
-        // leaves, the candidate SET as a bitmap; tc_score_kernel verifies it
-        bool tc = P.tc_bm != nullptr && u8 && B32 >= kTcMinBudget;
+        // leaves, the candidate SET as leaf flags; tc_score_kernel verifies it
+        bool tc = P.tc_flags != nullptr && u8 && B32 >= kTcMinBudget;
         if (tc) {
             if (threadIdx.x == 0) S.u32s[11] = 0xffffffffu;
             __syncthreads();
@@ -1204,30 +1270,30 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             __syncthreads();
             const uint32_t nt = min(emit_rows(tau_list, n_tau, T0, F.cand, B32, S), B32);
             const int32_t tau2 = kth_dist2(P, F, S, nt, P.k);  // exact k-th smallest among those rows
-            // candidate bitmap: whole leaves + the cut leaf's prefix
-            uint32_t* bm = P.tc_bm + (qs - P.q_begin) * P.tc_W;
-            for (uint32_t i = threadIdx.x; i <= n_full; i += blockDim.x) {
-                uint32_t a0, a1;
-                if (i < n_full) {
-                    const uint32_t li = F.full[i];
-                    a0 = __ldg(T0.leaf_begin + li);
-                    a1 = a0 + __ldg(T0.leaf_count + li);
-                } else {
-                    a0 = __ldg(T0.leaf_begin + cut_li);
-                    a1 = a0 + static_cast<uint32_t>(take_cut);
-                }
-                for (uint32_t w = a0 >> 5; a0 < a1 && w <= (a1 - 1) >> 5; ++w) {
-                    const uint32_t lo = max(a0, w << 5), hi = min(a1, (w << 5) + 32);
-                    const uint32_t nbits = hi - lo;
-                    const uint32_t mask = (nbits == 32 ? 0xffffffffu : ((1u << nbits) - 1u)) << (lo & 31);
-                    atomicOr(bm + w, mask);
-                }
-                // (query tile, 128-row tile) occupancy: tc_score skips empty tiles
-                uint32_t* tm = P.tc_tmap + ((qs - P.q_begin) >> 8) * P.tc_TW;
-                for (uint32_t t = a0 >> 7; a0 < a1 && t <= (a1 - 1) >> 7; ++t) {
-                    const uint32_t bit = 1u << (t & 31);
-                    if (!(*reinterpret_cast<volatile uint32_t*>(tm + (t >> 5)) & bit)) atomicOr(tm + (t >> 5), bit);
-                }
+            // candidate set: one flag bit per tree-0 leaf taken whole (built in
+            // smem when it fits, else with global atomics on the zeroed slot) +
+            // the cut leaf and the end row of its taken prefix; tc_expand turns
+            // them into the row bitmap tc_score reads
+            const uint64_t slot = qs - P.q_begin;
+            uint32_t* fl = P.tc_flags + slot * P.tc_LW;
+            const bool fl_smem = P.tc_LW * 4 <= union_bytes(P.K, P.NR) - 64;
+            uint32_t* sfl = reinterpret_cast<uint32_t*>(S.th);  // union: idle after kth_dist2
+            if (fl_smem) {
+                for (uint32_t w = threadIdx.x; w < P.tc_LW; w += blockDim.x) sfl[w] = 0;
+                __syncthreads();
+            }
+            for (uint32_t i = threadIdx.x; i < n_full; i += blockDim.x) {
+                const uint32_t li = F.full[i];
+                if (fl_smem) atomicOr(&sfl[li >> 5], 1u << (li & 31));
+                else atomicOr(&fl[li >> 5], 1u << (li & 31));
+            }
+            if (fl_smem) {
+                __syncthreads();
+                for (uint32_t w = threadIdx.x; w < P.tc_LW; w += blockDim.x) fl[w] = sfl[w];
+            }
+            if (threadIdx.x == 0) {
+                P.tc_cut[2 * slot] = cut_li;
+                P.tc_cut[2 * slot + 1] = __ldg(T0.leaf_begin + cut_li) + static_cast<uint32_t>(take_cut);
             }
             if (threadIdx.x == 0) P.tc_tau2[qs - P.q_begin] = tau2;
             __syncthreads();
@@ -1592,43 +1658,46 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         if (!tc_ok) {
             launch_fast(Pp);
         } else {
-            const uint64_t W = (P.n + 31) / 32;
             const int R = P.row_u8;
+            const uint32_t LW = (P.trees_num_leaves0 + 31) / 32;
+            const uint64_t W = (P.n + 31) / 32;
+            const uint32_t TW = static_cast<uint32_t>(((P.n + 127) / 128 + 31) / 32);
             // test hook: a smaller staging buffer forces the overflow re-run
             uint32_t tc_cap = kTcFinishCap;
             if (const char* e = std::getenv("DETLSH_TEST_TC_CAP"))
                 tc_cap = static_cast<uint32_t>(std::max(1L, std::min<long>(std::atol(e), kTcFinishCap)));
-            // bitmaps of one chunk of processing slots stay under ~2 GB
-            uint64_t chunk = (2ULL << 30) / (W * 4);
+            // per processing slot: leaf flags, row bitmap (n/8 bytes), survivors
+            // (32 KB), pass records (128 KB); a chunk stays under ~3 GB
+            uint64_t chunk = (3ULL << 30) / (W * 4 + 160 * 1024);
             chunk = std::max<uint64_t>(256, chunk / 256 * 256);
             chunk = std::min<uint64_t>(chunk, (P.nq + 255) / 256 * 256);
-            DevBuf<uint32_t> bm(chunk * W);
+            DevBuf<uint32_t> flags(chunk * LW), cut(chunk * 2), bm(chunk * W), tmap(chunk / 256 * TW);
             DevBuf<int32_t> tau2(chunk), qn(chunk);
             DevBuf<uint32_t> surv_cnt(chunk);
             DevBuf<uint8_t> q8(chunk * R);
             DevBuf<uint64_t> surv(chunk * kTcFinishCap);
-            const uint32_t TW = static_cast<uint32_t>(((P.n + 127) / 128 + 31) / 32);
-            DevBuf<uint32_t> tmap(chunk / 256 * TW);
-            const uint64_t rec_cap = chunk * 8192;  // threshold passes staged per chunk
+            const uint64_t rec_cap = chunk * 8192;  // candidate threshold passes staged per chunk
             DevBuf<uint4> rec(rec_cap);
             DevBuf<unsigned long long> rec_cnt(1);
             over_list.alloc(P.nq);
             for (uint64_t c0 = 0; c0 < P.nq; c0 += chunk) {
                 const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);
+                DETLSH_CUDA(cudaMemsetAsync(flags.get(), 0, m * LW * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(bm.get(), 0, m * W * 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(tmap.get(), 0xff, (m + 255) / 256 * TW * 4, s));  // no tile skipping
                 DETLSH_CUDA(cudaMemsetAsync(tau2.get(), 0xff, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(surv_cnt.get(), 0, m * 4, s));
-                DETLSH_CUDA(cudaMemsetAsync(tmap.get(), 0, (m + 255) / 256 * TW * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + 3, 0, 4, s));
                 QueryPlan Pc = Pp;
                 Pc.q_begin = c0;
                 Pc.q_end = c0 + m;
-                Pc.tc_bm = bm.get();
-                Pc.tc_W = W;
+                Pc.tc_flags = flags.get();
+                Pc.tc_LW = LW;
+                Pc.tc_cut = cut.get();
                 Pc.tc_tau2 = tau2.get();
-                Pc.tc_tmap = tmap.get();
-                Pc.tc_TW = TW;
                 launch_fast(Pc);
+                launch_tc_expand(flags.get(), LW, cut.get(), tau2.get(), m, P.trees_leaf_begin0, P.trees_leaf_count0,
+                                 P.trees_num_leaves0, bm.get(), W, s);
                 launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, q8.get(), qn.get(), s);
                 TcScoreArgs a{};
                 a.rows = P.data_tc;

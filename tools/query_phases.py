@@ -24,9 +24,10 @@ D.ck_ann_batch(idx, Q, 50)
 lib.detlsh_profile_enable(0)
 ph = np.zeros(8)
 lib.detlsh_query_phase_cycles(C.c_void_p(ph.ctypes.data))
-names = ["setup", "leaf_scan", "cut", "emission", "verify_topk", "output"]
+names = ["setup", "leaf_scan", "cut", "emission/tau+flags", "verify_topk", "output"]
 tot = ph[:6].sum()
 print(f"{cfg} nq={nq}: {nq/(t1-t0):.0f} q/s (unprofiled wall {1e3*(t1-t0):.1f} ms); "
-      f"leaves={idx.tree(0).is_leaf.sum()} in-radius leaves/query={ph[6]/nq:.0f} weight/query={ph[7]/nq:.0f}")
+      f"leaves={idx.tree(0).is_leaf.sum()} exact-round fallbacks={ph[6]:.0f} "
+      f"exactly scored leaves/query={ph[7]/nq:.0f}")
 for n_, v in zip(names, ph[:6]):
     print(f"  {n_:12s} {100*v/tot:5.1f}%  {v/nq/1e3:8.1f} kcycles/query (CTA thread-0 view)")
