@@ -331,7 +331,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     for (int i = 0; i < L; ++i) {
         const DevTree& T = *X->trees[i];
         qt[i] = QTree{T.leaf_node.get(), T.leaf_begin.get(), T.leaf_count.get(), T.leaf_box.get(),
-                      T.perm.get(), static_cast<uint32_t>(T.num_leaves)};
+                      T.leaf_cr.get(), T.perm.get(), static_cast<uint32_t>(T.num_leaves)};
         X->max_leaves = std::max<uint32_t>(X->max_leaves, static_cast<uint32_t>(T.num_leaves));
         tree_ms += T.build_ms;
     }

@@ -135,24 +135,38 @@ size_t smem_bytes(int K, int NR, int d, int row_u8) {
     return off + 16;
 }
 
+// lbv[j] = #{b : row_j[b] < v_j}, ubv[j] = #{b : row_j[b] <= v_j}: one warp per
+// dimension, lane-strided counts and a warp reduction (no contended atomics).
+__device__ void count_below(const float* tb, int K, int W, const Smem& S) {
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int j = threadIdx.x >> 5; j < K; j += nw) {
+        const float v = S.qp[j];
+        uint32_t lb = 0, ub = 0;
+        for (int b = lane; b < W; b += 32) {
+            const float row = tb[j * W + b];
+            lb += row < v;
+            ub += row <= v;
+        }
+        lb = __reduce_add_sync(0xffffffffu, lb);
+        ub = __reduce_add_sync(0xffffffffu, ub);
+        if (lane == 0) {
+            S.lbv[j] = static_cast<int>(lb);
+            S.ubv[j] = static_cast<int>(ub);
+        }
+    }
+    __syncthreads();
+}
+
 // Per (query, tree): squared edge penalties in fp64, exactly as mindist
 // (de_tree.cpp:169-184) forms them: pen = double(edge) - double(v), pen*pen.
 __device__ void build_sq(const QueryPlan& P, int tree, const Smem& S) {
     const int W = P.NR + 1;
     const float* tb = P.table + static_cast<size_t>(tree) * P.K * W;
-    for (int j = threadIdx.x; j < P.K; j += blockDim.x) {
-        S.lbv[j] = 0;
-        S.ubv[j] = 0;
-    }
-    __syncthreads();
+    count_below(tb, P.K, W, S);
     for (int i = threadIdx.x; i < P.K * W; i += blockDim.x) {
         const int j = i / W;
-        const float row = tb[i];
-        const float v = S.qp[j];
-        const double D = __dsub_rn(static_cast<double>(row), static_cast<double>(v));
+        const double D = __dsub_rn(static_cast<double>(tb[i]), static_cast<double>(S.qp[j]));
         S.sq[i] = __dmul_rn(D, D);
-        if (row < v) atomicAdd(&S.lbv[j], 1);
-        if (row <= v) atomicAdd(&S.ubv[j], 1);
     }
     __syncthreads();
 }
@@ -167,18 +181,7 @@ __device__ void build_sq(const QueryPlan& P, int tree, const Smem& S) {
 __device__ void build_pen_tables(const QueryPlan& P, const Smem& S) {
     const int W = P.NR + 1, NR = P.NR;
     const float* tb = P.table;
-    for (int j = threadIdx.x; j < P.K; j += blockDim.x) {
-        S.lbv[j] = 0;
-        S.ubv[j] = 0;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < P.K * W; i += blockDim.x) {
-        const int j = i / W;
-        const float row = tb[i], v = S.qp[j];
-        if (row < v) atomicAdd(&S.lbv[j], 1);
-        if (row <= v) atomicAdd(&S.ubv[j], 1);
-    }
-    __syncthreads();
+    count_below(tb, P.K, W, S);
     for (int i = threadIdx.x; i < P.K * NR; i += blockDim.x) {
         const int j = i / NR, r = i % NR;
         const double v = static_cast<double>(S.qp[j]);
@@ -193,6 +196,31 @@ __device__ void build_pen_tables(const QueryPlan& P, const Smem& S) {
         }
         S.tlo[i] = lo;
         S.thi[i] = hi;
+    }
+    __syncthreads();
+}
+
+// Per query, after build_pen_tables: the penalty of each half of each dim
+// (hp[j][b] for the box covering regions [b NR/2, (b+1) NR/2 - 1], the root
+// split) and their fp32 sums over dims 8c..8c+7 for every 8-bit half pattern
+// (tcd[c][x]); they live in the union right after tlo/thi (K <= 16).
+__device__ void build_half_tables(const QueryPlan& P, const Smem& S) {
+    const int NR = P.NR, H = NR / 2;
+    float* hp = S.tlo + 2 * P.K * NR;
+    float* tcd = hp + 2 * kMaxK;
+    for (int i = threadIdx.x; i < 2 * P.K; i += blockDim.x) {
+        const int j = i >> 1, b = i & 1;
+        hp[i] = __fadd_rn(S.tlo[j * NR + b * H], S.thi[j * NR + b * H + H - 1]);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+        const int c = i >> 8, x = i & 255;
+        float sum = 0.0f;
+        for (int t = 0; t < 8; ++t) {
+            const int j = 8 * c + t;
+            if (j < P.K) sum = __fadd_rn(sum, hp[2 * j + ((x >> t) & 1)]);
+        }
+        tcd[i] = sum;
     }
     __syncthreads();
 }
@@ -951,6 +979,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30;
         if (approx) build_pen_tables(P, S);
         else build_sq(P, 0, S);
+        if (approx) build_half_tables(P, S);
         const int lane = threadIdx.x & 31;
         uint32_t n_full = 0, cut_li = 0, bstar = 0;
         uint64_t take_cut = 0;
@@ -990,25 +1019,39 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             // monotone in mindist; the per-leaf key is kept for pass 2
             {
                 unsigned long long wsum = 0;
-                auto record = [&](uint32_t li, uint32_t b) {
+                auto record = [&](uint32_t li, uint32_t b, uint32_t cnt) {
                     if (b != 0xffffu) {
-                        const uint32_t cnt = __ldg(T0.leaf_count + li);
                         wsum += cnt;
                         atomicAdd(&S.bins[approx ? b >> 5 : b], cnt);
                     }
                     F.bin16[li] = static_cast<uint16_t>(b);
                 };
                 if (approx) {
-                    for (uint32_t li0 = threadIdx.x; li0 < nl; li0 += 2 * blockDim.x) {
-                        const uint32_t li1 = li0 + blockDim.x;
-                        float a0, a1;
-                        leaf_a2_k16_f32(P, T0, li0, li1 < nl ? li1 : li0, S, a0, a1);
-                        record(li0, approx_bin(a0));
-                        if (li1 < nl) record(li1, approx_bin(a1));
+                    // a leaf's box lies in one half of every dimension (the root
+                    // split), refined in a few: sum the half penalties by two
+                    // 8-dimension table lookups, then add the refinements
+                    const float* hp = S.tlo + 2 * P.K * P.NR;  // [K][2] half penalties
+                    const float* tcd = hp + 2 * kMaxK;          // [2][256] sums over 8 dims
+                    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) {
+                        const uint4 cr = __ldg(T0.leaf_cr + li);
+                        float a;
+                        if (cr.x >> 31) {  // the root is a leaf: no half
+                            float a1;
+                            leaf_a2_k16_f32(P, T0, li, li, S, a, a1);
+                        } else {
+                            a = __fadd_rn(tcd[cr.x & 0xffu], tcd[256 + ((cr.x >> 8) & 0xffu)]);
+                            for (uint32_t m = cr.y; m; m &= m - 1) {  // refined dims: + (box penalty - half penalty) >= 0
+                                const int j = __ffs(m) - 1;
+                                const uint32_t h = __ldg(reinterpret_cast<const uint16_t*>(T0.leaf_box + static_cast<size_t>(li) * 64) + j);
+                                const float pen = __fadd_rn(S.tlo[j * P.NR + (h & 0xffu)], S.thi[j * P.NR + (h >> 8)]);
+                                a = __fadd_rn(a, __fsub_rn(pen, hp[2 * j + ((cr.x >> j) & 1u)]));
+                            }
+                        }
+                        record(li, approx_bin(a), cr.z);
                     }
                 } else {  // exact round (rare): exact mindists (fp64 table built below)
                     for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x)
-                        record(li, exact_bin(leaf_mindist(P, T0, li, S), radius, scale));
+                        record(li, exact_bin(leaf_mindist(P, T0, li, S), radius, scale), __ldg(T0.leaf_count + li));
                 }
                 for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
                 if (lane == 0 && wsum) atomicAdd(&S.u64s[0], wsum);

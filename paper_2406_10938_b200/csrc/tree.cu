@@ -301,7 +301,7 @@ __global__ void leaves_kernel(uint64_t num_nodes, int K, int sbits,
                               const uint8_t* __restrict__ value, const uint32_t* __restrict__ node_begin,
                               const uint32_t* __restrict__ node_count, uint32_t* leaf_node,
                               uint32_t* leaf_begin, uint32_t* leaf_count, uint8_t* leaf_box,
-                              uint32_t* max_count) {
+                              uint4* leaf_cr, uint32_t* max_count) {
     for (uint64_t id = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; id < num_nodes;
          id += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         if (!leaf_flag[id]) continue;
@@ -311,6 +311,14 @@ __global__ void leaves_kernel(uint64_t num_nodes, int K, int sbits,
         leaf_count[li] = node_count[id];
         atomicMax(max_count, node_count[id]);
         uint8_t* box = leaf_box + static_cast<size_t>(li) * kBoxStride * 2;
+        uint32_t code = 0, refined = 0;
+        for (int j = 0; j < K; ++j) {
+            const int b = bits[id * K + j], v = value[id * K + j];
+            if (b == 0) code |= 1u << 31;
+            else code |= static_cast<uint32_t>((v >> (b - 1)) & 1) << j;
+            if (b != 1) refined |= 1u << j;
+        }
+        leaf_cr[li] = make_uint4(code, refined, node_count[id], 0u);
         for (int j = 0; j < kBoxStride; ++j) {
             if (j < K) {
                 const int b = bits[id * K + j], v = value[id * K + j];
@@ -469,11 +477,12 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     T.leaf_begin.alloc(nl);
     T.leaf_count.alloc(nl);
     T.leaf_box.alloc(static_cast<size_t>(nl) * kBoxStride * 2);
+    T.leaf_cr.alloc(nl);
     leaves_kernel<<<grid_for(valid), 256, 0, s>>>(valid, K, sbits, leaf_flag.get(), leaf_idx.get(),
                                                   T.bits.get(), T.value.get(), T.node_begin.get(),
                                                   T.node_count.get(), T.leaf_node.get(),
                                                   T.leaf_begin.get(), T.leaf_count.get(),
-                                                  T.leaf_box.get(), counters.get() + 1);
+                                                  T.leaf_box.get(), T.leaf_cr.get(), counters.get() + 1);
     DETLSH_LAUNCH_CHECK();
     uint32_t mx = 0;
     DETLSH_CUDA(cudaMemcpyAsync(&mx, counters.get() + 1, 4, cudaMemcpyDeviceToHost, s));
