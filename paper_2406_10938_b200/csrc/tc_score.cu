@@ -154,11 +154,15 @@ __global__ void pack_tc_tiles_kernel(const uint8_t* __restrict__ rows, uint64_t 
 // branch-free: 2 q.x - (|q|^2 - tau^2) >= |x|^2 per element (IMAD + compare
 // into a mask); only columns where some lane passes are revisited, with
 // single-column TMEM loads, to consult the candidate bitmap.
-constexpr int kTcThreads = 320;  // 8 epilogue warps + producer + MMA issuer
+constexpr int kEpiWarps = 16;                      // epilogue warps (4 per TMEM lane quarter)
+constexpr int kTcThreads = 32 * (kEpiWarps + 2);   // + producer + MMA issuer
+constexpr int kEpiCols = kTcQueries / (kEpiWarps / 4);  // query columns per epilogue warp
+constexpr int kEpiWords = kEpiCols / 32;           // candidate words per lane (columns per lane)
+constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr uint32_t kTcRecChunk = 1024;  // records reserved per warp at a time
 constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
 
-__device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 4u : 3u; }
+__device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 4u : 2u; }
 
 __device__ __forceinline__ uint32_t next_tile(const uint32_t* __restrict__ row, uint32_t t, uint32_t t1) {
     while (t < t1) {
@@ -193,7 +197,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
     uint8_t* sA = sB + kTcQueries * R;                   // [stages][128][R] core layout
     int32_t* snh = reinterpret_cast<int32_t*>(sA + stages * tile_bytes);  // tau^2 - |q|^2
     int32_t* sqn = snh + kTcQueries;
-    uint32_t* sstash = reinterpret_cast<uint32_t*>(sqn + kTcQueries);  // [8 warps][32 lanes][kTcStash]
+    uint32_t* sstash = reinterpret_cast<uint32_t*>(sqn + kTcQueries);  // [kEpiWarps][32 lanes][kTcStash]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         for (uint32_t s = 0; s < stages; ++s) {
@@ -202,11 +206,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
         }
         for (int s = 0; s < 2; ++s) {
             umma::mbar_init(&tfull[s], 1);
-            umma::mbar_init(&tempty[s], 8);
+            umma::mbar_init(&tempty[s], kEpiWarps);
         }
         umma::fence_mbar_init();
     }
-    if (warp == 9) umma::tmem_alloc(&tslot, 512);
+    if (warp == kMmaWarp) umma::tmem_alloc(&tslot, 512);
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             umma::fence_after_sync();
             loaded_qt = qt;
         }
-        if (warp == 8) {
+        if (warp == kProducerWarp) {
             if (lane == 0) {
                 for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
                     const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                                    &full[s]);
                 }
             }
-        } else if (warp == 9) {
+        } else if (warp == kMmaWarp) {
             if (lane == 0) {
                 for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
                     const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
@@ -287,19 +291,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                 }
             }
         } else {
-            const int sub = warp & 3, half = warp >> 2;
+            const int sub = warp & 3, part = warp >> 2;
             const int row = sub * 32 + lane;
-            // candidate words of this warp's 32 rows for its 128 query columns
-            // (lane l holds columns 4l..4l+3), prefetched one tile ahead
-            auto load_words = [&](uint32_t t, uint32_t (&w)[4]) {
+            const int cbeg = part * kEpiCols;  // this warp's query columns [cbeg, cbeg + kEpiCols)
+            // candidate words of this warp's 32 rows for its query columns (lane l
+            // holds columns cbeg + kEpiWords l ..), prefetched one tile ahead
+            auto load_words = [&](uint32_t t, uint32_t (&w)[kEpiWords]) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const uint64_t qq = q0 + half * 128 + lane * 4 + e;
+                for (int e = 0; e < kEpiWords; ++e) {
+                    const uint64_t qq = q0 + cbeg + lane * kEpiWords + e;
                     const uint64_t word = static_cast<uint64_t>(t) * 4 + sub;
                     w[e] = (qq < a.nq && word < a.W) ? __ldg(a.bm + qq * a.W + word) : 0u;
                 }
             };
-            uint32_t pw[4], nw[4] = {0, 0, 0, 0};
+            uint32_t pw[kEpiWords], nw[kEpiWords];
+#pragma unroll
+            for (int e = 0; e < kEpiWords; ++e) nw[e] = 0;
             load_words(next_tile(trow, rt0, rt1), pw);
             const uint32_t lt_mask = (1u << lane) - 1u;
             for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                 umma::mbar_wait(&tfull[acc], aph);
                 umma::fence_after_sync();
                 const uint32_t tbase = tmem + (static_cast<uint32_t>(sub * 32) << 16) + acc * kTcQueries;
-                for (int c0 = half * 128; c0 < half * 128 + 128; c0 += 32) {
+                for (int c0 = cbeg; c0 < cbeg + kEpiCols; c0 += 32) {
                     uint32_t v[32];
                     umma::tmem_ld32(tbase + c0, v);
                     // threshold mask: bit e <=> 2 q.x + tau^2 - |q|^2 >= |x|^2
@@ -340,11 +347,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                         while (cols) {
                             const int e = __ffs(cols) - 1;
                             cols &= cols - 1;
-                            const int cr = c0 + e - half * 128;  // candidate word: lane cr/4 holds it
-                            const int sel = cr & 3;
-                            const uint32_t mine = sel == 0 ? pw[0] : sel == 1 ? pw[1] : sel == 2 ? pw[2] : pw[3];
+                            const int cr = c0 + e - cbeg;  // candidate word: lane cr / kEpiWords holds it
+                            const int sel = cr % kEpiWords;
+                            uint32_t mine = pw[0];
+#pragma unroll
+                            for (int x = 1; x < kEpiWords; ++x) mine = sel == x ? pw[x] : mine;
                             const uint32_t b = __ballot_sync(0xffffffffu, (mask >> e) & 1u) &
-                                               __shfl_sync(0xffffffffu, mine, cr >> 2);
+                                               __shfl_sync(0xffffffffu, mine, cr / kEpiWords);
                             if (!b) continue;
                             const uint32_t cnt = __popc(b);
                             if (res_next + cnt > res_end) tc_reserve(a.rec, a.rec_cnt, a.rec_cap, res_next, res_end, lane);
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                 __syncwarp();
                 if (lane == 0) umma::mbar_arrive(&tempty[acc]);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) pw[e] = nw[e];
+                for (int e = 0; e < kEpiWords; ++e) pw[e] = nw[e];
             }
         }
         it += ntiles;
@@ -372,7 +381,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
         umma::fence_after_sync();
     }
     for (uint64_t x = res_next + lane; x < res_end && x < a.rec_cap; x += 32) a.rec[x] = make_uint4(0xffffffffu, 0, 0, 0);
-    if (warp == 9) umma::tmem_free(tmem, 512);
+    if (warp == kMmaWarp) umma::tmem_free(tmem, 512);
 }
 
 // Candidate threshold passes -> per-query survivor lists.
@@ -446,8 +455,8 @@ __global__ void __launch_bounds__(256) tc_finish_kernel(TcScoreArgs a, const uin
 }  // namespace
 
 size_t tc_score_smem(int R) {
-    const size_t need = static_cast<size_t>(kTcQueries + (R <= 128 ? 4 : 3) * kTcRows) * R + 2 * kTcQueries * 4 +
-                        8 * 32 * kTcStash * 4 + 1024;
+    const size_t need = static_cast<size_t>(kTcQueries + (R <= 128 ? 4 : 2) * kTcRows) * R + 2 * kTcQueries * 4 +
+                        kEpiWarps * 32 * kTcStash * 4 + 1024;
     return std::max<size_t>(need, 120 * 1024);  // one CTA per SM: it owns all 512 TMEM columns
 }
 
