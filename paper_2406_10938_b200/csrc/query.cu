@@ -1033,21 +1033,21 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                     const float* hp = S.tlo + 2 * P.K * P.NR;  // [K][2] half penalties
                     const float* tcd = hp + 2 * kMaxK;          // [2][256] sums over 8 dims
                     for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) {
-                        const uint4 cr = __ldg(T0.leaf_cr + li);
+                        const uint2 cr = __ldg(T0.leaf_cr + li);
                         float a;
-                        if (cr.x >> 31) {  // the root is a leaf: no half
+                        if (cr.x == 0xffffffffu) {  // no half form: every dimension from the box
                             float a1;
                             leaf_a2_k16_f32(P, T0, li, li, S, a, a1);
                         } else {
                             a = __fadd_rn(tcd[cr.x & 0xffu], tcd[256 + ((cr.x >> 8) & 0xffu)]);
-                            for (uint32_t m = cr.y; m; m &= m - 1) {  // refined dims: + (box penalty - half penalty) >= 0
+                            for (uint32_t m = cr.x >> 16; m; m &= m - 1) {  // refined dims: + (box penalty - half penalty) >= 0
                                 const int j = __ffs(m) - 1;
                                 const uint32_t h = __ldg(reinterpret_cast<const uint16_t*>(T0.leaf_box + static_cast<size_t>(li) * 64) + j);
                                 const float pen = __fadd_rn(S.tlo[j * P.NR + (h & 0xffu)], S.thi[j * P.NR + (h >> 8)]);
                                 a = __fadd_rn(a, __fsub_rn(pen, hp[2 * j + ((cr.x >> j) & 1u)]));
                             }
                         }
-                        record(li, approx_bin(a), cr.z);
+                        record(li, approx_bin(a), cr.y);
                     }
                 } else {  // exact round (rare): exact mindists (fp64 table built below)
                     for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x)

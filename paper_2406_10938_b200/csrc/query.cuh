@@ -14,7 +14,7 @@ struct QTree {
     const uint32_t* leaf_begin;
     const uint32_t* leaf_count;
     const uint8_t* leaf_box;
-    const uint4* leaf_cr;  // {half code, refined dims, count, 0} per leaf (tree.cuh)
+    const uint2* leaf_cr;  // {half code | refined dims << 16, count} per leaf (tree.cuh)
     const uint32_t* perm;
     uint32_t num_leaves;
 };

@@ -301,7 +301,7 @@ __global__ void leaves_kernel(uint64_t num_nodes, int K, int sbits,
                               const uint8_t* __restrict__ value, const uint32_t* __restrict__ node_begin,
                               const uint32_t* __restrict__ node_count, uint32_t* leaf_node,
                               uint32_t* leaf_begin, uint32_t* leaf_count, uint8_t* leaf_box,
-                              uint4* leaf_cr, uint32_t* max_count) {
+                              uint2* leaf_cr, uint32_t* max_count) {
     for (uint64_t id = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; id < num_nodes;
          id += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         if (!leaf_flag[id]) continue;
@@ -312,13 +312,14 @@ __global__ void leaves_kernel(uint64_t num_nodes, int K, int sbits,
         atomicMax(max_count, node_count[id]);
         uint8_t* box = leaf_box + static_cast<size_t>(li) * kBoxStride * 2;
         uint32_t code = 0, refined = 0;
+        bool half_form = K <= 16;
         for (int j = 0; j < K; ++j) {
             const int b = bits[id * K + j], v = value[id * K + j];
-            if (b == 0) code |= 1u << 31;
+            if (b == 0) half_form = false;
             else code |= static_cast<uint32_t>((v >> (b - 1)) & 1) << j;
             if (b != 1) refined |= 1u << j;
         }
-        leaf_cr[li] = make_uint4(code, refined, node_count[id], 0u);
+        leaf_cr[li] = make_uint2(half_form ? (code | refined << 16) : 0xffffffffu, node_count[id]);
         for (int j = 0; j < kBoxStride; ++j) {
             if (j < K) {
                 const int b = bits[id * K + j], v = value[id * K + j];

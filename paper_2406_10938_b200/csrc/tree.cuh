@@ -28,10 +28,11 @@ struct DevTree {
     // query-side leaf arrays, leaves in node-id order
     DevBuf<uint32_t> leaf_node, leaf_begin, leaf_count;
     DevBuf<uint8_t> leaf_box;  // [num_leaves][kBoxStride][2] (lo region, hi region)
-    // [num_leaves] {code, refined, count, 0}: bit j of code = the half (top
-    // region bit) dim j's box lies in; bit j of refined = the box is narrower
-    // than that half (bit 31 of code: the leaf is the root, no half at all)
-    DevBuf<uint4> leaf_cr;
+    // [num_leaves] {code | refined << 16, count} (K <= 16): bit j of code = the
+    // half (top region bit) dim j's box lies in; bit j of refined = the box is
+    // narrower than that half.  0xffffffff: no half form (the root leaf, or
+    // K > 16) -- the scan then takes the general per-dimension path.
+    DevBuf<uint2> leaf_cr;
     uint32_t max_leaf_count = 0;
     double build_ms = 0.0;
 };
