@@ -563,13 +563,13 @@ __device__ void small_weighted_select(const LeafItem* A, uint32_t n, uint64_t ne
         }
         if (before < need && need <= before + me.w) {
             S.u64s[4] = me.mdb;
-            S.u32s[12] = me.id;
+            S.u32s[13] = me.id;
             S.u64s[5] = need - before;
         }
     }
     __syncthreads();
     kmdb = S.u64s[4];
-    kid = S.u32s[12];
+    kid = S.u32s[13];
     take_cut = S.u64s[5];
     __syncthreads();
 }
@@ -689,6 +689,7 @@ __device__ __forceinline__ uint32_t sqdiff4(uint32_t a, uint32_t b, uint32_t acc
 struct FastSlot {
     LeafItem *A, *B, *C;  // bin-b* items and the select's ping-pong buffers
     uint32_t* full;       // leaves taken whole (leaf indices)
+    uint32_t* tau;        // whole leaves of the bins <= b_tau (tensor-core hand-off)
     uint16_t* bin16;      // per-leaf histogram bin (0xffff: outside the radius), 16-B aligned
     uint32_t* cand;       // candidate rows as tree-0 permutation indices
 };
@@ -701,13 +702,14 @@ __device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, 
     f.B = f.A + maxl;
     f.C = f.B + maxl;
     f.full = reinterpret_cast<uint32_t*>(f.C + maxl);
-    f.cand = f.full + maxl;
+    f.tau = f.full + maxl;
+    f.cand = f.tau + maxl;
     f.bin16 = reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(f.cand + budget) + 15) & ~uintptr_t(15));
     return f;
 }
 
 size_t fast_slot_bytes(uint32_t maxl, uint64_t budget) {
-    const size_t b = 3 * static_cast<size_t>(maxl) * sizeof(LeafItem) + 4 * static_cast<size_t>(maxl) +
+    const size_t b = 3 * static_cast<size_t>(maxl) * sizeof(LeafItem) + 8 * static_cast<size_t>(maxl) +
                      4 * budget + 2 * (static_cast<size_t>(maxl) + 8) + 16;
     return (b + 255) / 256 * 256;
 }
@@ -977,6 +979,8 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         const double aabs = 1e-36;                                   // fp32 denormal rounding
         const double r2_in = r2 * (1.0 - 1e-12), r2_out = r2 * (1.0 + 1e-12);
         bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30;
+        // tensor-core hand-off for this query (u8 rows, large budget)
+        const bool tc_eligible = P.tc_flags != nullptr && u8 && B32 >= kTcMinBudget;
         if (approx) build_pen_tables(P, S);
         else build_sq(P, 0, S);
         if (approx) build_half_tables(P, S);
@@ -1094,10 +1098,26 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                     S.u32s[0] = 0;   // whole-leaf list
                     S.u32s[1] = 0;   // ambiguous / bin-b* items
                     S.u32s[15] = 0;  // ambiguous leaf indices
+                    S.u32s[11] = 0xffffffffu;  // b_tau
+                    S.u32s[12] = 0;  // tau leaf list
+                }
+                if (tc_eligible) {  // b_tau: first bin whose cumulative rows reach tc_tau_rows
+                    const unsigned long long want = P.tc_tau_rows;
+                    if (excl < want && want <= incl) {
+                        unsigned long long cum = excl;
+                        int bin = lane * per;
+                        for (int b = 0; b < per; ++b, ++bin) {
+                            cum += S.bins[bin];
+                            if (cum >= want) break;
+                        }
+                        S.u32s[11] = static_cast<uint32_t>(bin);
+                    }
                 }
             }
             __syncthreads();
             bstar = S.u32s[2];
+            const bool do_tau = S.u32s[11] < bstar;  // tau leaves must be whole leaves
+            const uint32_t b_tau = S.u32s[11];
             if (approx && bstar == kBins - 1) {  // crossing in the radius band
                 if (P.phase_cycles && threadIdx.x == 0) atomicAdd(P.phase_cycles + 6, 1ULL);
                 approx = false;
@@ -1125,7 +1145,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                         if (v4 * 4 + u < nv) pk[u] = reinterpret_cast<const uint4*>(F.bin16)[v4 * 4 + u];
                     }
                     const uint32_t v = v4 * 4;  // first 8-leaf vector of this thread
-                    uint32_t wmask = 0, amask = 0;
+                    uint32_t wmask = 0, amask = 0, tmask = 0;
 #pragma unroll
                     for (int e = 0; e < 32; ++e) {
                         const uint4& q4 = pk[e >> 3];
@@ -1136,9 +1156,11 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                         if (approx) {  // fine bins: certainly before / ambiguous / after
                             if (b + 1 < lo_f) wmask |= 1u << e;
                             else if (b <= hi_f + 1) amask |= 1u << e;
+                            if (do_tau && b + 1 < lo_f && (b >> 5) <= b_tau) tmask |= 1u << e;
                         } else {
                             if (b < bstar) wmask |= 1u << e;
                             else if (b == bstar) amask |= 1u << e;
+                            if (do_tau && b < bstar && b <= b_tau) tmask |= 1u << e;
                         }
                     }
                     // whole leaves: warp-aggregated append
@@ -1153,6 +1175,19 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                     if (lane == 31 && tot) b0 = atomicAdd(&S.u32s[0], tot);
                     b0 = __shfl_sync(0xffffffffu, b0, 31) + incl - cnt;
                     for (uint32_t m = wmask; m; m &= m - 1) F.full[b0++] = v * 8 + __ffs(m) - 1;
+                    if (__any_sync(0xffffffffu, tmask != 0)) {  // tau leaves (nearest bins)
+                        const uint32_t tcnt = __popc(tmask);
+                        uint32_t tinc = tcnt;
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t t = __shfl_up_sync(0xffffffffu, tinc, o);
+                            if (lane >= o) tinc += t;
+                        }
+                        const uint32_t ttot = __shfl_sync(0xffffffffu, tinc, 31);
+                        uint32_t t0 = 0;
+                        if (lane == 31) t0 = atomicAdd(&S.u32s[12], ttot);
+                        t0 = __shfl_sync(0xffffffffu, t0, 31) + tinc - tcnt;
+                        for (uint32_t m = tmask; m; m &= m - 1) F.tau[t0++] = v * 8 + __ffs(m) - 1;
+                    }
                     // ambiguous leaves (a few hundred per query): listed, then
                     // scored exactly below, one per thread
                     const uint32_t acnt = __popc(amask);
@@ -1258,60 +1293,11 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         phase(2);
         // ---- tensor-core hand-off (u8 rows): exact tau^2 from the nearest
         // leaves, the candidate SET as leaf flags; tc_score_kernel verifies it
-        bool tc = P.tc_flags != nullptr && u8 && B32 >= kTcMinBudget;
+        const bool tc = tc_eligible && S.u32s[11] < bstar;  // b_tau found below the crossing bin
         if (tc) {
-            if (threadIdx.x == 0) S.u32s[11] = 0xffffffffu;
-            __syncthreads();
-            if (threadIdx.x < 32) {  // b_tau: first bin whose cumulative rows reach kTauRows
-                constexpr int per = kBins / 32;
-                unsigned long long part = 0;
-                for (int b = 0; b < per; ++b) part += S.bins[lane * per + b];
-                unsigned long long incl = part;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += t;
-                }
-                const unsigned long long excl = incl - part;
-                const unsigned long long want = P.tc_tau_rows;
-                if (excl < want && want <= incl) {
-                    unsigned long long cum = excl;
-                    int bin = lane * per;
-                    for (int b = 0; b < per; ++b, ++bin) {
-                        cum += S.bins[bin];
-                        if (cum >= want) break;
-                    }
-                    S.u32s[11] = static_cast<uint32_t>(bin);
-                }
-                if (lane == 0) S.u32s[12] = 0;
-            }
-            __syncthreads();
-            tc = S.u32s[11] < bstar;  // uniform
-            __syncthreads();
-        }
-        if (tc) {
-            const uint32_t b_tau = S.u32s[11];
-            uint32_t* tau_list = reinterpret_cast<uint32_t*>(F.A);
-            for (uint32_t base = 0; base < n_full; base += blockDim.x) {
-                const uint32_t i = base + threadIdx.x;
-                uint32_t li = 0;
-                bool in = false;
-                if (i < n_full) {
-                    li = F.full[i];
-                    in = (approx ? F.bin16[li] >> 5 : F.bin16[li]) <= b_tau;
-                }
-                const uint32_t m = __ballot_sync(0xffffffffu, in);
-                if (m) {
-                    const int leader = __ffs(m) - 1;
-                    uint32_t b0 = 0;
-                    if (lane == leader) b0 = atomicAdd(&S.u32s[12], static_cast<uint32_t>(__popc(m)));
-                    b0 = __shfl_sync(0xffffffffu, b0, leader);
-                    if (in) tau_list[b0 + __popc(m & ((1u << lane) - 1u))] = li;
-                }
-            }
-            __syncthreads();
             const uint32_t n_tau = S.u32s[12];
             __syncthreads();
-            const uint32_t nt = min(emit_rows(tau_list, n_tau, T0, F.cand, B32, S), B32);
+            const uint32_t nt = min(emit_rows(F.tau, n_tau, T0, F.cand, B32, S), B32);
             const int32_t tau2 = kth_dist2(P, F, S, nt, P.k);  // exact k-th smallest among those rows
             // candidate set: one flag bit per tree-0 leaf taken whole (built in
             // smem when it fits, else with global atomics on the zeroed slot) +
