@@ -978,7 +978,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
         const double rel = static_cast<double>(P.K + 2) * 0x1p-22;  // >= 2K ulp(fp32) of the sum
         const double aabs = 1e-36;                                   // fp32 denormal rounding
         const double r2_in = r2 * (1.0 - 1e-12), r2_out = r2 * (1.0 + 1e-12);
-        bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30;
+        bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30 && !P.force_exact;
         // tensor-core hand-off for this query (u8 rows, large budget)
         const bool tc_eligible = P.tc_flags != nullptr && u8 && B32 >= kTcMinBudget;
         if (approx) build_pen_tables(P, S);
@@ -1670,6 +1670,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         };
         // u8 rows with a large budget: the plan kernel hands each query's
         // candidate set to the tcgen05 dataset-major scorer (tc_score.cu)
+        // test hook: exact fp64 mindists for every leaf (no approximate round)
+        if (std::getenv("DETLSH_TEST_EXACT_SCAN")) Pp.force_exact = 1;
         // tau^2 = k-th smallest dist^2 over the rows of the nearest leaves.  If
         // those rows were a uniform sample of the candidates, about
         // k * budget / tau_rows candidates would pass it; size the sample so

@@ -64,6 +64,7 @@ struct QueryPlan {
     uint32_t* tc_cut;  // [slot][2]: cut leaf, end row of its taken prefix
     int32_t* tc_tau2;
     int tc_allowed;  // host-side switch (DETLSH_F_NO_TC clears it)
+    int force_exact;  // test hook: skip the approximate leaf scan
     uint32_t tc_tau_rows;  // rows of the nearest leaves scored exactly for tau^2
 };
 

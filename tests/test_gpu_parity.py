@@ -240,3 +240,43 @@ def test_u8_rows_path_equals_fp64_path_and_oracle(gpu, port, d):
     for qi in range(Q.shape[0]):
         ids, ds, rad, cs = oi.ck_ann(Q[qi], 25)
         assert np.array_equal(ra.ids[qi], ids) and bits_equal(ra.dists[qi], ds)
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=20000, d=64, K=16, L=4, n_regions=256, leaf_capacity=128, sample_fraction=0.1, beta=0.1, k=50),
+    dict(n=6000, d=24, K=12, L=2, n_regions=64, leaf_capacity=8, sample_fraction=0.5, beta=0.1, k=20),
+])
+def test_approximate_leaf_scan_equals_exact_scan(gpu, monkeypatch, case):
+    """The fp32 leaf scan (half-code tables, refined dims, margin classification)
+    must select exactly the leaves the all-fp64 scan selects."""
+    c = dict(case)
+    n, d = c.pop("n"), c.pop("d")
+    data = gaussian(n, d, n + 3, 1.3)
+    idx = gpu.build_index(data, _params(**c), seed=8)
+    Q = np.concatenate([gaussian(300, d, 9, 1.3), data[:: n // 50]])
+    ra = gpu.ck_ann_batch(idx, Q, c["k"])
+    monkeypatch.setenv("DETLSH_TEST_EXACT_SCAN", "1")
+    rb = gpu.ck_ann_batch(idx, Q, c["k"])
+    assert np.array_equal(ra.ids, rb.ids)
+    assert bits_equal(ra.dists, rb.dists)
+    assert np.array_equal(ra.candidates_seen, rb.candidates_seen)
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=3000, d=16, K=20, L=2, n_regions=16, leaf_capacity=16, sample_fraction=0.5, beta=0.1, k=10),
+    dict(n=100, d=8, K=6, L=2, n_regions=8, leaf_capacity=128, sample_fraction=1.0, beta=0.5, k=5),
+])
+def test_query_paths_without_half_form(gpu, port, case):
+    """K > 16 (no approximate scan) and a root-leaf tree (no half form) match the oracle."""
+    c = dict(case)
+    n, d = c.pop("n"), c.pop("d")
+    data = gaussian(n, d, n + 5, 1.0)
+    idx = gpu.build_index(data, _params(**c), seed=3)
+    oi = port.build_index(data, make_params(**c), 3)
+    Q = gaussian(20, d, 6, 1.0)
+    res = gpu.ck_ann_batch(idx, Q, c["k"])
+    for qi in range(Q.shape[0]):
+        ids, ds, rad, cs = oi.ck_ann(Q[qi], c["k"])
+        m = int(res.n_hits[qi])
+        assert np.array_equal(res.ids[qi, :m], ids), f"query {qi}"
+        assert bits_equal(res.dists[qi, :m], ds), f"query {qi}"
