@@ -154,6 +154,14 @@ int detlsh_gpu_export_tree(const detlsh_gpu_index* index, int32_t tree, int32_t*
                            uint8_t* is_leaf, uint8_t* split_dim, int32_t* left, int32_t* right,
                            uint8_t* bits, uint8_t* value, uint64_t* ebegin, uint32_t* ecount,
                            uint32_t* positions);
+/* detlsh::save_index (persist.hpp:17, persist.cpp:99-149): the DETL v1 byte
+ * stream of the index -- the same bytes the reference writes for the same
+ * build, so detlsh::load_index + ck_ann serve a GPU-built index.  *size gets
+ * the stream length; out (may be NULL) must hold cap >= *size bytes.  Entry
+ * symbols are recomputed on the GPU if the build dropped the codes; the
+ * dataset fingerprint (FNV-1a, dataset.cpp:22-30) is computed on the host. */
+int detlsh_gpu_save_detl(detlsh_gpu_index* index, uint8_t* out, uint64_t cap, uint64_t* size);
+
 /* Per-stage device/host milliseconds of the last build (diagnostics):
  * names written as a ';'-separated list into `names` (cap bytes). */
 int detlsh_gpu_build_timings(const detlsh_gpu_index* index, double* ms, int32_t cap,

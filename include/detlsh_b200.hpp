@@ -174,4 +174,15 @@ inline QueryResult ck_ann(const DetIndex& index, std::span<const float> q, int k
     return std::move(ck_ann_batch(index, q, k).front());
 }
 
+// save_index (persist.hpp:17): the DETL v1 bytes detlsh::save_index writes for
+// the same build; detlsh::load_index reads them back.
+inline std::vector<std::uint8_t> save_index(const DetIndex& index) {
+    auto* h = const_cast<detlsh_gpu_index*>(index.handle());
+    std::uint64_t size = 0;
+    detail::check(detlsh_gpu_save_detl(h, nullptr, 0, &size));
+    std::vector<std::uint8_t> bytes(size);
+    detail::check(detlsh_gpu_save_detl(h, bytes.data(), bytes.size(), &size));
+    return bytes;
+}
+
 }  // namespace detlsh_b200

@@ -141,6 +141,8 @@ class Oracle:
             self.f("index_save").restype = u64
             self.f("index_fingerprint").argtypes = [vp]
             self.f("index_fingerprint").restype = u64
+            self.f("index_load").argtypes = [vp, u64, vp, u64, i32]
+            self.f("index_load").restype = vp
 
     # ---- scalar helpers ------------------------------------------------------
     def mix_seed(self, seed, stream):
@@ -249,6 +251,13 @@ class Oracle:
         assert h, "oracle build failed"
         return OracleIndex(self, h, p, data)
 
+    def load_index(self, blob: bytes, data, params: Params):
+        """Reference only: detlsh::load_index (persist.cpp:157-246) of DETL v1 bytes."""
+        data = np.ascontiguousarray(data, np.float32)
+        buf = np.frombuffer(blob, np.uint8)
+        h = self.f("index_load")(_p(buf), len(blob), _p(data), data.shape[0], data.shape[1])
+        return OracleIndex(self, h, params, data) if h else None
+
     def brute_force_knn(self, data, Q, k):
         data = np.ascontiguousarray(data, np.float32)
         Q = np.ascontiguousarray(Q, np.float32)
@@ -330,6 +339,13 @@ class OracleIndex:
         t = tptr(self.h, i)
         nn = int(self.o.f("tree_num_nodes")(t))
         return _export(self.o.f("tree_export"), (t,), self.params.K, nn, self.n)
+
+    def save(self) -> bytes:
+        """Reference only: detlsh::save_index (persist.cpp:99-149) bytes."""
+        size = int(self.o.f("index_save")(self.h, None, 0))
+        buf = np.empty(size, np.uint8)
+        self.o.f("index_save")(self.h, _p(buf), size)
+        return buf.tobytes()
 
     def ck_ann(self, q, k):
         q = np.ascontiguousarray(q, np.float32)

@@ -483,4 +483,16 @@ uint64_t ref_index_save(void* h, uint8_t* out, uint64_t cap) {
     return b.size();
 }
 
+// detlsh::load_index (persist.cpp:157-246) of a DETL v1 byte stream against a
+// dataset; nullptr with the message in ref_last_error on FormatError.
+void* ref_index_load(const uint8_t* bytes, uint64_t size, const float* data, uint64_t n, int32_t d) {
+    try {
+        std::istringstream in(std::string(reinterpret_cast<const char*>(bytes), size), std::ios::binary);
+        return new RefIndex{load_index(in, make_dataset(data, n, d))};
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 }  // extern "C"

@@ -94,6 +94,7 @@ def load() -> C.CDLL:
         "detlsh_gpu_tree_num_nodes": ([vp, i32, C.POINTER(u64)], C.c_int),
         "detlsh_gpu_export_tree": ([vp, i32] + [vp] * 10, C.c_int),
         "detlsh_gpu_build_timings": ([vp, vp, i32, C.c_char_p, i32], C.c_int),
+        "detlsh_gpu_save_detl": ([vp, vp, u64, C.POINTER(u64)], C.c_int),
         "detlsh_gpu_project": ([vp, i32, i32, vp, u64, i32, vp, i32, u32], C.c_int),
         "detlsh_gpu_select_breakpoints": ([vp, u64, i32, i32, i32, dbl, u64, vp, C.POINTER(u64),
                                            i32, u32], C.c_int),

@@ -202,6 +202,20 @@ class DetIndex:
         return _export_tree(lambda *a: lib.detlsh_gpu_export_tree(self._h, i, *a), self.params.K,
                             nn.value, self._n)
 
+    def save_index(self, path: str | None = None) -> bytes:
+        """save_index (persist.hpp:17): the DETL v1 bytes the reference writes for
+        this index; also written to `path` when given."""
+        lib = _lib.load()
+        size = C.c_uint64(0)
+        check(lib.detlsh_gpu_save_detl(self._h, None, 0, C.byref(size)))
+        buf = np.empty(size.value, np.uint8)
+        check(lib.detlsh_gpu_save_detl(self._h, _ptr(buf), size.value, C.byref(size)))
+        b = buf.tobytes()
+        if path is not None:
+            with open(path, "wb") as f:
+                f.write(b)
+        return b
+
     def build_timings(self) -> dict:
         ms = np.zeros(32, np.float64)
         names = C.create_string_buffer(1024)

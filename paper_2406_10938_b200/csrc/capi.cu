@@ -276,6 +276,19 @@ int detlsh_gpu_export_tree(const detlsh_gpu_index* index, int32_t tree, int32_t*
     });
 }
 
+int detlsh_gpu_save_detl(detlsh_gpu_index* index, uint8_t* out, uint64_t cap, uint64_t* size) {
+    return guarded([&] {
+        GpuIndex& X = *index->impl;
+        std::lock_guard<std::mutex> lock(X.qmu);
+        const std::vector<uint8_t> b = save_detl(X);
+        if (size) *size = b.size();
+        if (out) {
+            if (cap < b.size()) throw InvalidArgument("save_index: output buffer too small");
+            std::memcpy(out, b.data(), b.size());
+        }
+    });
+}
+
 int detlsh_gpu_build_timings(const detlsh_gpu_index* index, double* ms, int32_t cap, char* names,
                              int32_t names_cap) {
     const auto& t = index->impl->timings;

@@ -58,6 +58,8 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
                 cudaStream_t user_stream);
 
 void validate_params(const detlsh_params& p, uint64_t n, int d);
+// DETL v1 byte stream of the index (persist.cu), identical to detlsh::save_index
+std::vector<uint8_t> save_detl(GpuIndex& X);
 uint64_t sample_size_for(double frac, uint64_t n, int NR);
 bool is_pow2(int v);
 

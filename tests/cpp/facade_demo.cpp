@@ -32,6 +32,9 @@ int main(int argc, char** argv) {
             for (std::size_t t = 0; t < r.hits.size(); ++t)
                 std::printf("%zu %zu %u %.17g\n", i, t, r.hits[t].first, r.hits[t].second);
         }
+        // save_index: DETL v1 bytes (the reference's persist format)
+        const auto blob = detlsh_b200::save_index(idx);
+        std::printf("detl %zu %c%c%c%c\n", blob.size(), blob[0], blob[1], blob[2], blob[3]);
         // the reference's precondition errors surface as std::invalid_argument
         try {
             detlsh_b200::ck_ann(idx, std::span<const float>(q.data(), d - 1), k);

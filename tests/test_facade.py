@@ -36,7 +36,9 @@ def test_facade_program_matches_oracle(port):
         subprocess.run(["make", "-s", "-C", CPP], check=True)
     out = subprocess.run([DEMO], check=True, capture_output=True, text=True).stdout.splitlines()
     r_min = float(out[0].split()[1])
-    rows = [tuple(x.split()) for x in out[1:]]
+    detl = [x.split() for x in out if x.startswith("detl ")]
+    assert detl and int(detl[0][1]) > 0 and detl[0][2] == "DETL"
+    rows = [tuple(x.split()) for x in out[1:] if not x.startswith("detl ")]
     base, Q = lcg_data(5000, 5, 24)
     oi = port.build_index(base, make_params(beta=0.1, k=7, leaf_capacity=32), 77)
     assert r_min == oi.params.r_min
