@@ -257,6 +257,19 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     DETLSH_CUDA(cudaStreamSynchronize(s));
     X->timings.emplace_back("project", ms_since(t0));
 
+    // exact u8 verification rows (integral datasets): decided now, packed in
+    // tree-0 leaf order by the space-0 worker right after tree 0 (query.cu)
+    t0 = Clock::now();
+    const bool want_u8 = !(flags & DETLSH_F_NO_U8) && data_is_u8(X->data, n * static_cast<uint64_t>(d), s);
+    if (want_u8) {
+        X->row_u8 = (d + 31) / 32 * 32;  // whole 32-byte MMA K steps
+        const int chunks = X->row_u8 / 16;
+        int lpr = 1;
+        while (lpr < chunks && lpr < 32) lpr <<= 1;
+        X->u8_lpr = lpr;
+    }
+    X->timings.emplace_back("u8_check", ms_since(t0));
+
     Worker workers;
     double rmin_ms = 0.0;
     double r_min = X->params.r_min;
@@ -281,7 +294,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     auto launch_space = [&](int i) {
         DETLSH_CUDA(cudaEventRecord(ready[i], s));
         cudaEvent_t ev = ready[i];
-        workers.run(device, [Xp, d_proj, ev, i, n, K, NR, W, cap]() {
+        workers.run(device, [Xp, d_proj, ev, i, n, K, NR, W, cap, want_u8]() {
             cudaStream_t ts = Xp->side[i]->s;
             StreamScope sc(ts);
             DETLSH_CUDA(cudaStreamWaitEvent(ts, ev, 0));
@@ -290,6 +303,18 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                           Xp->codes.get() + static_cast<size_t>(i) * n * K, ts);
             build_tree_gpu(Xp->codes.get() + static_cast<size_t>(i) * n * K, n, K, NR, i, cap,
                            *Xp->trees[i], ts);
+            if (i == 0 && want_u8) {  // overlaps the other trees
+                const int d = Xp->d, R = Xp->row_u8;
+                Xp->data_u8.alloc(n * static_cast<size_t>(R));
+                launch_pack_u8(Xp->data, Xp->trees[0]->perm.get(), n, d, R, Xp->data_u8.get(), ts);
+                Xp->xn_u8.alloc(n);
+                launch_row_norms_u8(Xp->data_u8.get(), n, R, Xp->xn_u8.get(), ts);
+                if (R <= 256) {  // tensor-core verification operand tiles
+                    Xp->data_tc.alloc((n + 127) / 128 * 128 * static_cast<uint64_t>(R));
+                    launch_pack_tc_tiles(Xp->data_u8.get(), n, R, Xp->data_tc.get(), ts);
+                }
+                DETLSH_CUDA(cudaStreamSynchronize(ts));
+            }
         });
     };
     // breakpoints
@@ -337,24 +362,6 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     }
     X->qtrees.alloc(L);
     DETLSH_CUDA(cudaMemcpyAsync(X->qtrees.get(), qt.data(), L * sizeof(QTree), cudaMemcpyHostToDevice, s));
-    // exact u8 verification rows, in tree-0 leaf order (query.cu)
-    t0 = Clock::now();
-    if (!(flags & DETLSH_F_NO_U8) && data_is_u8(X->data, n * static_cast<uint64_t>(d), s)) {
-        X->row_u8 = (d + 31) / 32 * 32;  // whole 32-byte MMA K steps
-        const int chunks = X->row_u8 / 16;
-        int lpr = 1;
-        while (lpr < chunks && lpr < 32) lpr <<= 1;
-        X->u8_lpr = lpr;
-        X->data_u8.alloc(n * static_cast<size_t>(X->row_u8));
-        launch_pack_u8(X->data, X->trees[0]->perm.get(), n, d, X->row_u8, X->data_u8.get(), s);
-        X->xn_u8.alloc(n);
-        launch_row_norms_u8(X->data_u8.get(), n, X->row_u8, X->xn_u8.get(), s);
-        if (X->row_u8 <= 256) {  // tensor-core verification operand tiles
-            X->data_tc.alloc((n + 127) / 128 * 128 * static_cast<uint64_t>(X->row_u8));
-            launch_pack_tc_tiles(X->data_u8.get(), n, X->row_u8, X->data_tc.get(), s);
-        }
-    }
-    X->timings.emplace_back("pack_u8", ms_since(t0));
     X->params.r_min = r_min;
     if (flags & DETLSH_F_NO_CODES) X->codes.release();
     proj.release();
