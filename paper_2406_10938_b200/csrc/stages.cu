@@ -107,6 +107,91 @@ __global__ void __launch_bounds__(256) project_exact_kernel(
     }
 }
 
+// The same contraction on the FP64 tensor cores: mma.sync m8n8k4 f64 chains
+// accumulate exactly as the sequential fma chain in k order (pinned on B200 by
+// tools/probes/dmma_order.cu, 0 mismatches in 128 000 dot products, and by the
+// projection parity tests), so k-steps issued in t order reproduce the
+// reference's double sum bit for bit.  Warp tile: 16 points x 64 outputs
+// (2 x 8 m8n8 tiles, 32 fp64 accumulators per lane); CTA tile 128 points.
+constexpr int kPS = 36;  // padded point row (floats): A-fragment loads hit 32 distinct banks
+constexpr int kAS = 72;  // padded coefficient row (doubles): B-fragment loads in 2 clean wavefronts
+
+__global__ void __launch_bounds__(256) project_dmma_kernel(
+    const float* __restrict__ pts, uint64_t n, int d, const double* __restrict__ ct, int LK,
+    int LKp, int K, float* __restrict__ out) {
+    __shared__ __align__(16) float sx[kPT][kPS];
+    __shared__ __align__(16) double sa[kDC][kAS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ar = lane >> 2, ac = lane & 3;  // fragment row / k-column
+    const uint64_t tiles = (n + kPT - 1) / kPT;
+    for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const uint64_t z0 = tile * kPT;
+        for (int jp = 0; jp < LKp; jp += 64) {
+            double acc[2][8][2];
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[m][j][0] = acc[m][j][1] = 0.0;
+            for (int t0 = 0; t0 < d; t0 += kDC) {
+                __syncthreads();
+                for (int i = tid; i < kPT * kDC; i += 256) {
+                    const int pp = i / kDC, c = i % kDC;
+                    const uint64_t z = z0 + pp;
+                    const int t = t0 + c;
+                    sx[pp][c] = (z < n && t < d) ? pts[z * d + t] : 0.0f;
+                }
+                for (int i = tid; i < kDC * 64; i += 256) {
+                    const int c = i / 64, j = i % 64;
+                    const int t = t0 + c;
+                    sa[c][j] = t < d ? ct[static_cast<int64_t>(t) * LKp + jp + j] : 0.0;
+                }
+                __syncthreads();
+                // past t = d - 1 the chunk is zero-padded: fma(0, 0, acc) == acc for every
+                // reachable acc (a chain started at +0 never holds -0 under round-to-nearest)
+                const int kmax = min(kDC, d - t0);
+                for (int c0 = 0; c0 < kmax; c0 += 4) {
+                    double a[2], b[8];
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) a[m] = static_cast<double>(sx[warp * 16 + m * 8 + ar][c0 + ac]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) b[j] = sa[c0 + ac][8 * j + ar];
+#pragma unroll
+                    for (int m = 0; m < 2; ++m)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                         : "+d"(acc[m][j][0]), "+d"(acc[m][j][1])
+                                         : "d"(a[m]), "d"(b[j]));
+                }
+            }
+            // D fragment: point warp*16 + m*8 + ar, outputs jp + 8j + 2ac + {0,1}
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                const uint64_t z = z0 + warp * 16 + m * 8 + ar;
+                if (z >= n) continue;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int jj = jp + 8 * j + 2 * ac;
+                    if (K % 2 == 0 && jj + 1 < LK && (jj % K) + 1 < K) {
+                        const int sp = jj / K, dim = jj % K;
+                        *reinterpret_cast<float2*>(out + (static_cast<uint64_t>(sp) * n + z) * K + dim) =
+                            make_float2(static_cast<float>(acc[m][j][0]), static_cast<float>(acc[m][j][1]));
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int jh = jj + h;
+                            if (jh < LK) {
+                                const int sp = jh / K, dim = jh % K;
+                                out[(static_cast<uint64_t>(sp) * n + z) * K + dim] = static_cast<float>(acc[m][j][h]);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
 __global__ void gather_sample_kernel(const float* __restrict__ proj, const uint32_t* __restrict__ idx,
                                      uint64_t n_s, int K, float* __restrict__ out) {
     for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n_s;
@@ -397,8 +482,8 @@ void launch_project_exact(const float* d_points, uint64_t n, int d, const double
     cudaGetDevice(&dev);
     const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count(dev)) * 8);
     ProfScope ps("project_exact", s);
-    project_exact_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_points, n, d, d_ct, LK,
-                                                                      lk_padded(LK), K, d_out);
+    project_dmma_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_points, n, d, d_ct, LK,
+                                                                     lk_padded(LK), K, d_out);
     DETLSH_LAUNCH_CHECK();
 }
 
