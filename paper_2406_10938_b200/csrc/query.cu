@@ -805,7 +805,34 @@ __device__ void score_batch(const QueryPlan& P, const FastSlot& F, const Smem& S
             const float* x1 = P.data + static_cast<uint64_t>(p1) * P.d;
             const float* x2 = P.data + static_cast<uint64_t>(p2) * P.d;
             double a1 = 0.0, a2 = 0.0;
-            for (int t = 0; t < P.d; ++t) {
+            int t = 0;
+            if ((P.d & 3) == 0) {
+                // 32 floats of each row in flight (8 x 16-byte loads per row) before
+                // the chain consumes them: one L1 miss per 128-byte line instead of
+                // one per element (thread-private rows would otherwise thrash L1)
+                for (; t + 32 <= P.d; t += 32) {
+                    float4 v1[8], v2[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        v1[u] = __ldg(reinterpret_cast<const float4*>(x1 + t) + u);
+                        v2[u] = __ldg(reinterpret_cast<const float4*>(x2 + t) + u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const float e1[4] = {v1[u].x, v1[u].y, v1[u].z, v1[u].w};
+                        const float e2[4] = {v2[u].x, v2[u].y, v2[u].z, v2[u].w};
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            const double qv = static_cast<double>(S.qv[t + 4 * u + w]);
+                            const double d1 = __dsub_rn(qv, static_cast<double>(e1[w]));
+                            const double d2 = __dsub_rn(qv, static_cast<double>(e2[w]));
+                            a1 = __dadd_rn(a1, __dmul_rn(d1, d1));
+                            a2 = __dadd_rn(a2, __dmul_rn(d2, d2));
+                        }
+                    }
+                }
+            }
+            for (; t < P.d; ++t) {
                 const double qv = static_cast<double>(S.qv[t]);
                 const double d1 = __dsub_rn(qv, static_cast<double>(__ldg(x1 + t)));
                 const double d2 = __dsub_rn(qv, static_cast<double>(__ldg(x2 + t)));
