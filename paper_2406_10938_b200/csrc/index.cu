@@ -314,6 +314,10 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                     launch_pack_tc_tiles(Xp->data_u8.get(), n, R, Xp->data_tc.get(), ts);
                 }
                 DETLSH_CUDA(cudaStreamSynchronize(ts));
+            } else if (i == 0) {  // fp32 rows in leaf order: contiguous per-leaf candidate reads
+                Xp->data_leaf.alloc(n * static_cast<size_t>(Xp->d));
+                launch_pack_f32(Xp->data, Xp->trees[0]->perm.get(), n, Xp->d, Xp->data_leaf.get(), ts);
+                DETLSH_CUDA(cudaStreamSynchronize(ts));
             }
         });
     };
@@ -412,6 +416,7 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     P.data_u8 = X.data_u8.get();
     P.xn_u8 = X.xn_u8.get();
     P.data_tc = X.data_tc.get();
+    P.data_leaf = X.data_leaf.get();
     P.trees_num_leaves0 = static_cast<uint32_t>(X.trees[0]->num_leaves);
     P.trees_leaf_begin0 = X.trees[0]->leaf_begin.get();
     P.trees_leaf_count0 = X.trees[0]->leaf_count.get();

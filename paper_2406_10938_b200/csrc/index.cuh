@@ -39,6 +39,7 @@ struct GpuIndex {
     DevBuf<uint8_t> data_u8;  // exact u8 rows in tree-0 leaf order (integral datasets)
     DevBuf<int32_t> xn_u8;    // |x|^2 of those rows (tensor-core verification)
     DevBuf<uint8_t> data_tc;  // those rows as 128-row MMA operand tiles
+    DevBuf<float> data_leaf;  // non-integral datasets: fp32 rows in tree-0 leaf order
     int row_u8 = 0, u8_lpr = 0;
     std::vector<std::unique_ptr<DevTree>> trees;
     DevBuf<QTree> qtrees;

@@ -799,11 +799,16 @@ __device__ void score_batch(const QueryPlan& P, const FastSlot& F, const Smem& S
         // one thread per row, two rows in flight per thread (independent fp64 chains)
         for (uint32_t r = threadIdx.x; r < nb; r += 2 * blockDim.x) {
             const uint32_t r2 = r + blockDim.x;
-            const uint32_t p1 = __ldg(P.perm0 + F.cand[base + r]);
+            // leaf-ordered rows when the index keeps them (contiguous per leaf;
+            // bl then holds the row and topk_absorb maps survivors to positions)
+            const bool leaf = P.data_leaf != nullptr;
+            const uint32_t c1 = F.cand[base + r];
             const bool two = r2 < nb;
-            const uint32_t p2 = two ? __ldg(P.perm0 + F.cand[base + r2]) : p1;
-            const float* x1 = P.data + static_cast<uint64_t>(p1) * P.d;
-            const float* x2 = P.data + static_cast<uint64_t>(p2) * P.d;
+            const uint32_t c2 = two ? F.cand[base + r2] : c1;
+            const uint32_t p1 = leaf ? c1 : __ldg(P.perm0 + c1);
+            const uint32_t p2 = leaf ? c2 : __ldg(P.perm0 + c2);
+            const float* x1 = (leaf ? P.data_leaf : P.data) + static_cast<uint64_t>(p1) * P.d;
+            const float* x2 = (leaf ? P.data_leaf : P.data) + static_cast<uint64_t>(p2) * P.d;
             double a1 = 0.0, a2 = 0.0;
             int t = 0;
             if ((P.d & 3) == 0) {
@@ -1378,7 +1383,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
             const uint32_t nb = min(static_cast<uint32_t>(kBatch), B32 - c0);
             score_batch(P, F, S, c0, nb, u8);
             __syncthreads();
-            topk_absorb(S, nb, P.k, u8 ? P.perm0 : nullptr);
+            topk_absorb(S, nb, P.k, (u8 || P.data_leaf) ? P.perm0 : nullptr);
         }
         const uint32_t nh = topk_finish(S, P.k);
         phase(4);

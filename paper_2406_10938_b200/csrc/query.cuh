@@ -30,6 +30,7 @@ struct QueryPlan {
     const uint8_t* data_u8;  // exact u8 rows in tree-0 order, or null
     const int32_t* xn_u8;    // |x|^2 of those rows
     const uint8_t* data_tc;  // the same rows in MMA tiles (launch_pack_tc_tiles)
+    const float* data_leaf;  // fp32 rows in tree-0 leaf order (non-integral datasets), or null
     int row_u8;              // bytes per u8 row (d rounded up to 16)
     int u8_lpr;              // lanes per u8 row (power of two <= 32)
     double eps, c, r_min;

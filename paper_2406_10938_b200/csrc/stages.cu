@@ -605,7 +605,34 @@ __global__ void pack_u8_kernel(const float* __restrict__ x, const uint32_t* __re
     }
 }
 
+// fp32 rows gathered into tree-0 leaf order (16-byte moves when d % 4 == 0).
+__global__ void pack_f32_kernel(const float* __restrict__ x, const uint32_t* __restrict__ perm, uint64_t n,
+                                int d, float* __restrict__ out) {
+    if ((d & 3) == 0) {
+        const int q4 = d / 4;
+        const uint64_t total = n * static_cast<uint64_t>(q4);
+        for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+             i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+            const uint64_t r = i / q4;
+            reinterpret_cast<float4*>(out)[i] =
+                __ldg(reinterpret_cast<const float4*>(x + static_cast<uint64_t>(perm[r]) * d) + (i % q4));
+        }
+        return;
+    }
+    const uint64_t total = n * static_cast<uint64_t>(d);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[i] = x[static_cast<uint64_t>(perm[i / d]) * d + i % d];
+}
+
 }  // namespace
+
+void launch_pack_f32(const float* d_x, const uint32_t* d_perm, uint64_t n, int d, float* d_out, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n * d / 4 + 255) / 256 + 1, 65535));
+    ProfScope ps("pack_f32", s);
+    pack_f32_kernel<<<grid, 256, 0, s>>>(d_x, d_perm, n, d, d_out);
+    DETLSH_LAUNCH_CHECK();
+}
 
 bool data_is_u8(const float* d_x, uint64_t total, cudaStream_t s) {
     StreamScope scope(s);

@@ -50,6 +50,8 @@ void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float
 namespace detlsh_b200 {
 // True when every value is an integer in [0, 255] (exact u8 verification path).
 bool data_is_u8(const float* d_x, uint64_t total, cudaStream_t s);
+// rows [perm[r]] -> out[r] (fp32, tree-0 leaf order)
+void launch_pack_f32(const float* d_x, const uint32_t* d_perm, uint64_t n, int d, float* d_out, cudaStream_t s);
 // Rows of d_x re-ordered by d_perm and narrowed to u8, row_bytes per row.
 void launch_pack_u8(const float* d_x, const uint32_t* d_perm, uint64_t n, int d, int row_bytes,
                     uint8_t* d_out, cudaStream_t s);
