@@ -65,6 +65,19 @@ class ClockSampler:
         self.thread = None
 
     def start(self):
+        # in-process NVML sampling (a light query every 100 ms); the nvidia-smi
+        # loop is the fallback (its driver calls can stall a host-sync-heavy build)
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.stop_flag = False
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -76,6 +89,20 @@ class ClockSampler:
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
 
+    def _poll(self):
+        nv = self.nvml
+        bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                ("sw_power_cap", 0x4)]
+        while not self.stop_flag:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+                self.rows.append([str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for _, b in bits])
+            except Exception:
+                pass
+            time.sleep(0.1)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
@@ -83,16 +110,21 @@ class ClockSampler:
                 self.rows.append(parts)
 
     def stop(self):
-        if self.proc is None:
-            return None
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        if self.thread:
+        if getattr(self, "nvml", None) is not None:
+            time.sleep(0.15)
+            self.stop_flag = True
             self.thread.join(timeout=2)
+        elif self.proc is None:
+            return None
+        else:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
         if not self.rows:
             return None
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -168,10 +200,10 @@ def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0, plan=None):
     if kernel == "project_exact":
         return 4.0 * d * n  # one read of the fp32 shard (4d B/point)
     if kernel == "query_fast" and plan is not None:
-        # tensor-core hand-off: per query the plan kernel reads tree 0's leaf
-        # table (64 B box + 8 B begin/count per leaf), scores tau_rows u8 rows
-        # and writes the n-bit candidate bitmap
-        return (72.0 * plan["leaves"] + row_u8 * plan["tau_rows"] + n / 8.0) * nq
+        # tensor-core hand-off: per query the plan kernel reads tree 0's 8-byte
+        # leaf records, writes and re-reads a 2-byte bin per leaf, scores
+        # tau_rows u8 rows and writes one flag bit per leaf
+        return (12.0 * plan["leaves"] + row_u8 * plan["tau_rows"] + plan["leaves"] / 8.0) * nq
     if kernel == "query_fast":
         return 4.0 * d * budget * nq  # every verified candidate row (4d B/candidate)
     if kernel == "encode":
@@ -479,10 +511,28 @@ def main():
     hbm, peak_kind = peaks()
     build_roof = roofline(prof_build, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
                           exclude=("query_fast", "query_slow"))
+    proj = prof_build.get("project_exact")
+    build_roof_proj = None
+    if proj:
+        pms = proj[0] / max(1, proj[1])
+        fl = 2.0 * n_loc * 16 * 4 * d
+        build_roof_proj = {"kernel": "project_exact", "bound": "fp64 tensor (mma.sync m8n8k4 f64)",
+                           "unit": "TFLOP/s", "achieved": round(fl / (pms / 1e3) / 1e12, 2), "peak": 45.0,
+                           "peak_kind": "nominal B200 FP64 tensor (blackwell guide); no measured FP64 peak",
+                           "frac": round(fl / (pms / 1e3) / 1e12 / 45.0, 4), "launch_ms": round(pms, 4)}
     plan = {"leaves": int(idx.tree(0).is_leaf.sum()), "tau_rows": tc_tau_rows(k, budget)}
     query_roof = roofline(prof_query, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
                           only=("query_fast",), row_u8=idx.row_u8(), plan=plan)
     query_roof_tc = roofline_tc(prof_query, args.steps, n_loc, nq, idx.row_u8(), peak_bf16())
+    step_ms = sum(v[0] for v in prof_query.values()) / args.steps
+    step_bytes = 4.0 * d * budget * nq  # candidates_seen x 4d per query
+    query_roof_step = {
+        "kernel": "query step (all query kernels)", "bound": "hbm", "unit": "GB/s", "peak": hbm,
+        "algorithmic_bytes": step_bytes, "step_kernel_ms": round(step_ms, 4),
+        "achieved": round(step_bytes / (step_ms / 1e3) / 1e9, 2),
+        "frac": round(step_bytes / (step_ms / 1e3) / 1e9 / hbm, 5),
+        "note": "SURVEY 8(d) bytes (4d per candidate); above 1 when candidates are verified "
+                "dataset-major on the tensor cores (each u8 row read once per 256-query tile)"}
     # the reference arm scores its first cpu_queries queries: same subset here
     m_ref = min(args.cpu_queries, nq)
     rec_ref, rat_ref = recall_ratio(out_ids[:m_ref], out_d[:m_ref], out_h[:m_ref], gt_ids[:m_ref],
@@ -502,7 +552,7 @@ def main():
                   "recall": round(rec, 6), "ratio": round(rat, 6),
                   "recall_on_reference_sample": round(rec_ref, 6),
                   "ratio_on_reference_sample": round(rat_ref, 6), "gpu_launches": query_launches,
-                  "roofline": query_roof, "roofline_tc": query_roof_tc,
+                  "roofline": query_roof, "roofline_tc": query_roof_tc, "roofline_step": query_roof_step,
                   "e2e": {"value": round(nq / (e2e_query_ms / 1e3), 2), "unit": "queries/s",
                           "h2d_bytes_per_step": int(nq * d * 4),
                           "d2h_bytes_per_step": int(nq * k * 12 + nq * 20)}},
@@ -514,6 +564,7 @@ def main():
                                "parity": "hybrid oracle (reference stage functions, same table)"
                                if other == "gpu" else "bit-exact vs reference"},
         "roofline": build_roof,
+        "roofline_projection": build_roof_proj,
         "build_stages_ms": {k2: round(v, 3) for k2, v in stage_ms.items()},
         "kernels_ms_per_step": {"build": {k2: round(v[0] / args.steps, 4) for k2, v in prof_build.items()},
                                 "query": {k2: round(v[0] / args.steps, 4) for k2, v in prof_query.items()}},
@@ -582,7 +633,7 @@ def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exc
         out.update({"achieved": round(ach, 2), "frac": round(ach / hbm, 5),
                     "algorithmic_bytes": b})
         if plan is not None:
-            out["model"] = "plan kernel (tc hand-off): 72 B/leaf x tree-0 leaves + R x tau_rows + n/8 per query"
+            out["model"] = "plan kernel (tc hand-off): 12 B/leaf x tree-0 leaves + R x tau_rows + leaves/8 per query"
         if kern == "query_fast" and row_u8 and plan is None:
             b8 = float(row_u8) * budget * nq  # bytes the u8 rows actually hold
             out["u8_rows"] = {"bytes": b8, "achieved": round(b8 / (per_launch_ms / 1e3) / 1e9, 2),
