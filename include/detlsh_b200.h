@@ -41,6 +41,8 @@ extern "C" {
 #define DETLSH_F_BORROW_DATA 0x4u  /* with DEVICE_PTRS: keep the caller's device dataset */
 #define DETLSH_F_NO_CODES 0x8u     /* drop the [L][n][K] code array after build */
 #define DETLSH_F_NO_U8 0x10u       /* never use the exact u8 verification rows (fp64 path only) */
+#define DETLSH_F_PAA 0x40u         /* build: the DET-ONLY variant (build_det_only_index,
+                                      index.cpp:220-232): PAA segment means, L = 1 */
 #define DETLSH_F_NO_TC 0x20u       /* query: verify on the per-query gather path only (no
                                       tcgen05 dataset-major scoring); results are identical */
 
@@ -128,6 +130,16 @@ void detlsh_gpu_free(detlsh_gpu_index* index);
 int detlsh_gpu_query(const detlsh_gpu_index* index, const float* queries, uint64_t nq,
                      int32_t k, uint32_t flags, uint32_t* ids, double* dists, int32_t* n_hits,
                      double* radius_used, uint64_t* cands_seen, void* stream);
+
+/* rc_ann (index.hpp, index.cpp:267-290), batched: for each query the closest
+ * candidate of one pass over the trees at radius epsilon * r (budget
+ * candidate_budget(beta, n, 1)); found[q] = 1 with (ids[q], dists[q]) when the
+ * budget was reached or that candidate lies within c * r, else found[q] = 0
+ * (the reference's std::nullopt).  r > 0 and c > 1, else DETLSH_E_INVALID.
+ * cands_seen may be NULL.  Pointer/stream conventions as detlsh_gpu_query. */
+int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint64_t nq, double r,
+                      double c, uint32_t flags, uint32_t* ids, double* dists, int32_t* found,
+                      uint64_t* cands_seen, void* stream);
 
 /* Multi-GPU merge: per-shard top-k lists gathered from `shards`
  * ranks, layout [shards][nq][k] (dist, global id); writes the global top-k

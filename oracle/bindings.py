@@ -143,6 +143,10 @@ class Oracle:
             self.f("index_fingerprint").restype = u64
             self.f("index_load").argtypes = [vp, u64, vp, u64, i32]
             self.f("index_load").restype = vp
+            self.f("build_det_only_index").argtypes = [vp, u64, i32, vp, u64]
+            self.f("build_det_only_index").restype = vp
+            self.f("rc_ann").argtypes = [vp, vp, dbl, dbl, vp, vp]
+            self.f("rc_ann").restype = i32
 
     # ---- scalar helpers ------------------------------------------------------
     def mix_seed(self, seed, stream):
@@ -251,6 +255,14 @@ class Oracle:
         assert h, "oracle build failed"
         return OracleIndex(self, h, p, data)
 
+    def build_det_only_index(self, data, params: Params, seed: int):
+        """Reference only: detlsh::build_det_only_index (index.cpp:220-232)."""
+        data = np.ascontiguousarray(data, np.float32)
+        p = Params.from_buffer_copy(params)
+        h = self.f("build_det_only_index")(_p(data), data.shape[0], data.shape[1], C.byref(p), seed)
+        assert h, "reference det-only build failed"
+        return OracleIndex(self, h, p, data)
+
     def load_index(self, blob: bytes, data, params: Params):
         """Reference only: detlsh::load_index (persist.cpp:157-246) of DETL v1 bytes."""
         data = np.ascontiguousarray(data, np.float32)
@@ -339,6 +351,15 @@ class OracleIndex:
         t = tptr(self.h, i)
         nn = int(self.o.f("tree_num_nodes")(t))
         return _export(self.o.f("tree_export"), (t,), self.params.K, nn, self.n)
+
+    def rc_ann(self, q, r, c):
+        """Reference only: detlsh::rc_ann -> (pos, dist) or None."""
+        q = np.ascontiguousarray(q, np.float32)
+        pos = C.c_uint32(0)
+        dist = C.c_double(0)
+        rc = self.o.f("rc_ann")(self.h, _p(q), r, c, C.byref(pos), C.byref(dist))
+        assert rc >= 0
+        return (pos.value, dist.value) if rc == 1 else None
 
     def save(self) -> bytes:
         """Reference only: detlsh::save_index (persist.cpp:99-149) bytes."""

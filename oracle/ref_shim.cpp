@@ -483,6 +483,33 @@ uint64_t ref_index_save(void* h, uint8_t* out, uint64_t cap) {
     return b.size();
 }
 
+// detlsh::build_det_only_index (index.cpp:220-232): PAA projection, L = 1.
+void* ref_build_det_only_index(const float* data, uint64_t n, int32_t d, ref_params* params, uint64_t seed) {
+    try {
+        auto* h = new RefIndex{build_det_only_index(make_dataset(data, n, d), to_lsh(params), seed)};
+        from_lsh(h->index.params, params);
+        return h;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// detlsh::rc_ann (index.cpp:267-290): 1 found / 0 none / -1 error.
+int ref_rc_ann(void* h, const float* q, double r, double c, uint32_t* pos, double* dist) {
+    try {
+        const auto& idx = static_cast<RefIndex*>(h)->index;
+        const auto best = rc_ann(idx, std::span<const float>(q, static_cast<size_t>(idx.d())), r, c);
+        if (!best) return 0;
+        *pos = best->first;
+        *dist = best->second;
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // detlsh::load_index (persist.cpp:157-246) of a DETL v1 byte stream against a
 // dataset; nullptr with the message in ref_last_error on FormatError.
 void* ref_index_load(const uint8_t* bytes, uint64_t size, const float* data, uint64_t n, int32_t d) {

@@ -14,8 +14,11 @@ from .api import (  # noqa: F401
     LshParams,
     QueryResult,
     TreeExport,
+    build_det_only_index,
     build_index,
     build_index_with_family,
+    rc_ann,
+    rc_ann_batch,
     build_tree,
     candidate_budget,
     chi2_cdf,

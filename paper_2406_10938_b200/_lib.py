@@ -26,6 +26,7 @@ F_BORROW_DATA = 0x4
 F_NO_CODES = 0x8
 F_NO_U8 = 0x10
 F_NO_TC = 0x20
+F_PAA = 0x40
 
 
 class Params(C.Structure):
@@ -82,6 +83,7 @@ def load() -> C.CDLL:
                                           C.POINTER(vp)], C.c_int),
         "detlsh_gpu_free": ([vp], None),
         "detlsh_gpu_query": ([vp, vp, u64, i32, u32, vp, vp, vp, vp, vp, vp], C.c_int),
+        "detlsh_gpu_rc_ann": ([vp, vp, u64, dbl, dbl, u32, vp, vp, vp, vp, vp], C.c_int),
         "detlsh_gpu_merge_topk": ([vp, vp, vp, i32, u64, i32, vp, vp, vp, vp], C.c_int),
         "detlsh_gpu_get_params": ([vp, P], C.c_int),
         "detlsh_gpu_n": ([vp], u64),

@@ -26,7 +26,7 @@ from dataclasses import dataclass, field, fields
 import numpy as np
 
 from . import _lib
-from ._lib import (F_BORROW_DATA, F_DEVICE_PTRS, F_NO_CODES, F_NO_TC, F_NO_U8, F_SAMPLE_GPU,
+from ._lib import (F_BORROW_DATA, F_DEVICE_PTRS, F_NO_CODES, F_NO_TC, F_NO_U8, F_PAA, F_SAMPLE_GPU,
                    Params, check)
 
 SAMPLE_REFERENCE = "reference"
@@ -333,6 +333,41 @@ def ck_ann_device(index: DetIndex, queries, k: int, ids, dists, n_hits=None, rad
     check(_lib.load().detlsh_gpu_query(index.handle, p(queries), int(queries.shape[0]), k,
                                        flags, p(ids), p(dists), p(n_hits), p(radius),
                                        p(cands), stream))
+
+
+def rc_ann_batch(index: DetIndex, queries, r: float, c: float):
+    """rc_ann (index.cpp:267-290) for a batch of host queries [nq][d]: returns
+    (ids [nq] u32, dists [nq] f64, found [nq] bool, candidates_seen [nq])."""
+    Q = _as_host_f32(queries)
+    if Q.shape[1] != index.d():
+        raise ValueError("rc_ann: query dimension mismatch")
+    nq = Q.shape[0]
+    ids = np.zeros(nq, np.uint32)
+    ds = np.zeros(nq, np.float64)
+    found = np.zeros(nq, np.int32)
+    cs = np.zeros(nq, np.uint64)
+    check(_lib.load().detlsh_gpu_rc_ann(index.handle, _ptr(Q), nq, float(r), float(c), 0, _ptr(ids),
+                                        _ptr(ds), _ptr(found), _ptr(cs), None))
+    return ids, ds, found.astype(bool), cs
+
+
+def rc_ann(index: DetIndex, q, r: float, c: float):
+    """rc_ann (index.hpp, index.cpp:267-290): (position, distance) or None."""
+    ids, ds, found, _ = rc_ann_batch(index, np.asarray(q, np.float32).reshape(1, -1), r, c)
+    return (int(ids[0]), float(ds[0])) if found[0] else None
+
+
+def build_det_only_index(data, params: LshParams | None = None, seed: int = 0, *, device: int = 0,
+                         sample: str = SAMPLE_REFERENCE) -> DetIndex:
+    """build_det_only_index (index.cpp:220-232): the DET-ONLY variant -- PAA
+    segment means (projection.cpp:62-90) as the single projected space (L = 1)."""
+    params = params or LshParams()
+    cp = params.to_c()
+    a = _as_host_f32(data)
+    h = C.c_void_p()
+    check(_lib.load().detlsh_gpu_build(_ptr(a), a.shape[0], a.shape[1], C.byref(cp), seed, device,
+                                       _flags(sample) | F_PAA, C.byref(h)))
+    return DetIndex(h, LshParams.from_c(cp), a.shape[0], a.shape[1], device)
 
 
 def ck_ann(index: DetIndex, q, k: int) -> QueryResult:

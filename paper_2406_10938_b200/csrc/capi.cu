@@ -192,6 +192,17 @@ int detlsh_gpu_query(const detlsh_gpu_index* index, const float* queries, uint64
     });
 }
 
+int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint64_t nq, double r,
+                      double c, uint32_t flags, uint32_t* ids, double* dists, int32_t* found,
+                      uint64_t* cands_seen, void* stream) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("rc_ann: index is null");
+        const RcArgs rc{r, c};
+        query_impl(*index->impl, queries, nq, 1, flags, ids, dists, found, nullptr, cands_seen,
+                   static_cast<cudaStream_t>(stream), &rc);
+    });
+}
+
 int detlsh_gpu_merge_topk(const double* shard_dists, const uint64_t* shard_ids,
                           const int32_t* shard_hits, int32_t shards, uint64_t nq, int32_t k,
                           double* out_dists, uint64_t* out_ids, int32_t* out_hits, void* stream) {

@@ -189,6 +189,12 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                                            uint32_t flags) {
     if (!params) throw InvalidArgument("build_index: params is null");
     if (!points) throw InvalidArgument("build_index: points is null");
+    const bool paa = (flags & DETLSH_F_PAA) != 0;
+    if (paa) {  // build_det_only_index (index.cpp:220-232)
+        if (coeffs_host) throw InvalidArgument("build_index: a hash family does not apply to PAA");
+        params->L = 1;
+        if (params->K > d) throw InvalidArgument("build_index: PAA requires K <= d");
+    }
     validate_params(*params, n, d);
     DeviceGuard dg(device);
     ensure_mempool(device);
@@ -197,6 +203,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     X->n = n;
     X->d = d;
     X->sample_gpu = (flags & DETLSH_F_SAMPLE_GPU) != 0;
+    X->paa = paa;
     X->main.create();
     cudaStream_t s = X->main.s;
     StreamScope scope(s);
@@ -217,9 +224,11 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         X->side.push_back(std::make_unique<OwnedStream>());
         X->side.back()->create();
     }
-    // hash family (projection.cpp:11-23): host, seeded sub-stream 0
-    X->h_coeffs.resize(static_cast<size_t>(LK) * d);
-    if (coeffs_host) {
+    // hash family (projection.cpp:11-23): host, seeded sub-stream 0 (none for PAA)
+    X->h_coeffs.resize(paa ? 0 : static_cast<size_t>(LK) * d);
+    if (paa) {
+        X->family_seed = 0;
+    } else if (coeffs_host) {
         std::memcpy(X->h_coeffs.data(), coeffs_host, X->h_coeffs.size() * sizeof(float));
         X->family_seed = family_seed;
     } else {
@@ -238,11 +247,13 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                                     s));
         X->data = X->data_buf.get();
     }
-    X->coeffs.alloc(X->h_coeffs.size());
-    DETLSH_CUDA(cudaMemcpyAsync(X->coeffs.get(), X->h_coeffs.data(), X->h_coeffs.size() * 4,
-                                cudaMemcpyHostToDevice, s));
-    X->coeffs_t.alloc(static_cast<size_t>(lk_padded(LK)) * d);
-    prepare_coeffs_t(X->coeffs.get(), LK, d, X->coeffs_t.get(), s);
+    if (!paa) {
+        X->coeffs.alloc(X->h_coeffs.size());
+        DETLSH_CUDA(cudaMemcpyAsync(X->coeffs.get(), X->h_coeffs.data(), X->h_coeffs.size() * 4,
+                                    cudaMemcpyHostToDevice, s));
+        X->coeffs_t.alloc(static_cast<size_t>(lk_padded(LK)) * d);
+        prepare_coeffs_t(X->coeffs.get(), LK, d, X->coeffs_t.get(), s);
+    }
     DevBuf<float> proj(static_cast<size_t>(L) * n * K);
     X->sample_size = sample_size_for(p.sample_fraction, n, NR);
     X->table.alloc(static_cast<size_t>(L) * K * W);
@@ -253,7 +264,8 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     X->timings.emplace_back("upload", ms_since(t0));
     // exact projection
     t0 = Clock::now();
-    launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s);
+    if (paa) launch_project_paa(X->data, n, d, K, proj.get(), s);
+    else launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s);
     DETLSH_CUDA(cudaStreamSynchronize(s));
     X->timings.emplace_back("project", ms_since(t0));
 
@@ -379,9 +391,15 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
 
 void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t flags,
                 uint32_t* ids, double* dists, int32_t* n_hits, double* radius, uint64_t* cands,
-                cudaStream_t user_stream) {
-    if (k < 1 || static_cast<uint64_t>(k) > X.n) throw InvalidArgument("ck_ann: k must lie in [1, n]");
-    if (!(X.params.r_min > 0.0)) throw InvalidArgument("ck_ann: index has no initial radius");
+                cudaStream_t user_stream, const RcArgs* rc) {
+    if (rc) {  // rc_ann (index.cpp:271-274)
+        if (!(rc->r > 0.0)) throw InvalidArgument("rc_ann: radius must be positive");
+        if (!(rc->c > 1.0)) throw InvalidArgument("rc_ann: c must exceed 1");
+        k = 1;
+    } else {
+        if (k < 1 || static_cast<uint64_t>(k) > X.n) throw InvalidArgument("ck_ann: k must lie in [1, n]");
+        if (!(X.params.r_min > 0.0)) throw InvalidArgument("ck_ann: index has no initial radius");
+    }
     if (nq == 0) return;
     if (!queries) throw InvalidArgument("ck_ann: queries is null");
     DeviceGuard dg(X.device);
@@ -398,7 +416,8 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
         q = dq.get();
     }
     DevBuf<float> qproj(static_cast<size_t>(L) * nq * K);
-    launch_project_exact(q, nq, d, X.coeffs_t.get(), K, L, qproj.get(), s);
+    if (X.paa) launch_project_paa(q, nq, d, K, qproj.get(), s);  // DetIndex::project_query (index.cpp:181-188)
+    else launch_project_exact(q, nq, d, X.coeffs_t.get(), K, L, qproj.get(), s);
     DevBuf<uint32_t> o_ids;
     DevBuf<double> o_d, o_r;
     DevBuf<int32_t> o_h;
@@ -426,8 +445,9 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     P.row_u8 = X.row_u8;
     P.u8_lpr = X.u8_lpr;
     P.eps = X.params.epsilon;
-    P.c = X.params.c;
-    P.r_min = X.params.r_min;
+    P.c = rc ? rc->c : X.params.c;
+    P.r_min = rc ? rc->r : X.params.r_min;
+    P.rc_mode = rc ? 1 : 0;
     P.budget = candidate_budget(X.params.beta, X.n, k);
     P.k = k;
     P.max_leaves = X.max_leaves;

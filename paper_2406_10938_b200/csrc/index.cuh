@@ -28,6 +28,7 @@ struct GpuIndex {
     int d = 0;
     uint64_t family_seed = 0, sample_size = 0;
     bool sample_gpu = false;
+    bool paa = false;  // DET-ONLY variant: PAA projection (projection.cpp:62-90), L = 1
     const float* data = nullptr;  // device, [n][d]
     DevBuf<float> data_buf;
     std::vector<float> h_coeffs;  // [L][K][d]
@@ -54,9 +55,16 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                                            uint64_t family_seed, uint64_t seed, int device,
                                            uint32_t flags);
 
+// rc_ann (index.cpp:267-290) instead of ck_ann: one pass over the trees at
+// radius eps * r with budget B(k = 1), then the closest candidate (n_hits 1) if
+// the budget was reached or it lies within c * r, else none (n_hits 0).
+struct RcArgs {
+    double r, c;
+};
+
 void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t flags,
                 uint32_t* ids, double* dists, int32_t* n_hits, double* radius, uint64_t* cands,
-                cudaStream_t user_stream);
+                cudaStream_t user_stream, const RcArgs* rc = nullptr);
 
 void validate_params(const detlsh_params& p, uint64_t n, int d);
 // DETL v1 byte stream of the index (persist.cu), identical to detlsh::save_index

@@ -94,11 +94,11 @@ std::vector<uint8_t> save_detl(GpuIndex& X) {
     o.scalar<int32_t>(p.leaf_capacity);
     o.scalar<double>(p.r_min);
     o.scalar<int32_t>(p.k);
-    o.scalar<uint8_t>(0);  // ProjectionKind::lsh (index.hpp:16-19)
-    o.scalar<uint64_t>(X.family_seed);
-    o.scalar<int32_t>(d);
-    o.scalar<int32_t>(K);
-    o.scalar<int32_t>(L);
+    o.scalar<uint8_t>(X.paa ? 1 : 0);  // ProjectionKind lsh / paa (index.hpp:16-19)
+    o.scalar<uint64_t>(X.family_seed);  // PAA: an empty HashFamily (all zero)
+    o.scalar<int32_t>(X.paa ? 0 : d);
+    o.scalar<int32_t>(X.paa ? 0 : K);
+    o.scalar<int32_t>(X.paa ? 0 : L);
     o.scalar<int32_t>(L);
     o.scalar<int32_t>(K);
     o.scalar<int32_t>(p.n_regions);
@@ -113,7 +113,8 @@ std::vector<uint8_t> save_detl(GpuIndex& X) {
     DevBuf<uint8_t> dcodes;
     if (!X.codes.get()) {
         proj.alloc(static_cast<size_t>(L) * n * K);
-        launch_project_exact(X.data, n, d, X.coeffs_t.get(), K, L, proj.get(), s);
+        if (X.paa) launch_project_paa(X.data, n, d, K, proj.get(), s);
+        else launch_project_exact(X.data, n, d, X.coeffs_t.get(), K, L, proj.get(), s);
         dcodes.alloc(static_cast<size_t>(L) * n * K);
         launch_encode(proj.get(), n, K, L, X.table.get(), p.n_regions, dcodes.get(), s);
     }

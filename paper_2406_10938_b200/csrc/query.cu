@@ -1505,7 +1505,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
                     emit_members(P, tree, L.A, nA, false, 0, 0, 0, L, S);
                 }
             }
-            if (done) break;
+            if (done || P.rc_mode) break;  // rc_ann: a single pass (index.cpp:278-289)
             // count_within(c * r) (index.cpp:244-249, 328)
             const double lim = __dmul_rn(P.c, r);
             const uint32_t msz = S.u32s[7];
@@ -1523,7 +1523,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
         }
         // top-k of the members, extracted kFastMaxK at a time (any k)
         const uint32_t msz = S.u32s[7];
-        const uint32_t want = min(msz, static_cast<uint32_t>(P.k));
+        uint32_t want = min(msz, static_cast<uint32_t>(P.k));
         uint32_t out = 0;
         uint64_t lbh = 0;
         uint32_t lbl = 0;
@@ -1556,6 +1556,10 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
             out += got;
             __syncthreads();
         }
+        // rc_ann: without the budget reached, the closest counts only within c * r
+        if (P.rc_mode && !done && want > 0 &&
+            !(__longlong_as_double(static_cast<long long>(lbh)) <= __dmul_rn(P.c, r)))
+            want = 0;
         if (threadIdx.x == 0) {
             if (P.n_hits) P.n_hits[q] = static_cast<int32_t>(want);
             if (P.radius) P.radius[q] = r;
@@ -1685,7 +1689,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     const size_t items = 3 * static_cast<size_t>(P.max_leaves) * sizeof(LeafItem);
     uint32_t slow_count = 0;
     const uint32_t* slow_list = X.slow_list.get();
-    if (P.k <= kFastMaxK) {
+    if (P.k <= kFastMaxK && !P.rc_mode) {
         int per_sm = 0;
         DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, query_fast_kernel, kQueryThreads, smem));
         per_sm = std::max(1, std::min(per_sm, 4));

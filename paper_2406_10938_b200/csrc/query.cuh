@@ -66,6 +66,7 @@ struct QueryPlan {
     int32_t* tc_tau2;
     int tc_allowed;  // host-side switch (DETLSH_F_NO_TC clears it)
     int force_exact;  // test hook: skip the approximate leaf scan
+    int rc_mode;      // rc_ann: one pass at radius eps * r_min (= r), k = 1, c * r acceptance
     uint32_t tc_tau_rows;  // rows of the nearest leaves scored exactly for tau^2
 };
 

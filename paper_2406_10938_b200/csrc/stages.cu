@@ -192,6 +192,22 @@ __global__ void __launch_bounds__(256) project_dmma_kernel(
     }
 }
 
+__global__ void project_paa_kernel(const float* __restrict__ pts, uint64_t n, int d, int K,
+                                   float* __restrict__ out) {
+    const int seg = d / K;
+    const uint64_t total = n * static_cast<uint64_t>(K);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t z = i / K;
+        const int j = static_cast<int>(i % K);
+        const int begin = j * seg, end = (j == K - 1) ? d : begin + seg;
+        const float* x = pts + z * d;
+        double sum = 0.0;
+        for (int t = begin; t < end; ++t) sum = __dadd_rn(sum, static_cast<double>(__ldg(x + t)));
+        out[i] = static_cast<float>(__ddiv_rn(sum, static_cast<double>(end - begin)));
+    }
+}
+
 __global__ void gather_sample_kernel(const float* __restrict__ proj, const uint32_t* __restrict__ idx,
                                      uint64_t n_s, int K, float* __restrict__ out) {
     for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n_s;
@@ -484,6 +500,13 @@ void launch_project_exact(const float* d_points, uint64_t n, int d, const double
     ProfScope ps("project_exact", s);
     project_dmma_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_points, n, d, d_ct, LK,
                                                                      lk_padded(LK), K, d_out);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* d_out, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n * K + 255) / 256, 65535)));
+    ProfScope ps("project_paa", s);
+    project_paa_kernel<<<grid, 256, 0, s>>>(d_points, n, d, K, d_out);
     DETLSH_LAUNCH_CHECK();
 }
 

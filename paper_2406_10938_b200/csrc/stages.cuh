@@ -19,6 +19,11 @@ void prepare_coeffs_t(const float* d_coeffs, int LK, int d, double* d_coeffs_t, 
 void launch_project_exact(const float* d_points, uint64_t n, int d, const double* d_coeffs_t,
                           int K, int L, float* d_out, cudaStream_t s);
 
+// paa_project_dataset (projection.cpp:62-90): out [1][n][K] fp32, segment j =
+// [j*(d/K), (j+1)*(d/K)) (the last takes the remainder), mean = sequential
+// double sum / length, rounded once to float.
+void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* d_out, cudaStream_t s);
+
 // sample values: out[j][t] = proj[space][idx[t]][j]  (j < K, t < n_s)
 void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
                           float* d_out, cudaStream_t s);
