@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -172,6 +173,25 @@ inline QueryResult ck_ann(const DetIndex& index, std::span<const float> q, int k
     if (q.size() != static_cast<std::size_t>(index.d()))
         throw std::invalid_argument("ck_ann: query dimension mismatch");
     return std::move(ck_ann_batch(index, q, k).front());
+}
+
+// build_det_only_index (index.cpp:220-232): PAA projection, L = 1.
+inline DetIndex build_det_only_index(std::span<const float> values, std::size_t n, int d, LshParams params,
+                                     std::uint64_t seed, int device = 0) {
+    return build_index(values, n, d, params, seed, device, DETLSH_F_PAA);
+}
+
+// rc_ann (index.cpp:267-290): the closest candidate, or nullopt.
+inline std::optional<std::pair<std::uint32_t, double>> rc_ann(const DetIndex& index, std::span<const float> q,
+                                                              double r, double c) {
+    if (q.size() != static_cast<std::size_t>(index.d()))
+        throw std::invalid_argument("rc_ann: query dimension mismatch");
+    std::uint32_t id = 0;
+    double dist = 0.0;
+    std::int32_t found = 0;
+    detail::check(detlsh_gpu_rc_ann(index.handle(), q.data(), 1, r, c, 0, &id, &dist, &found, nullptr, nullptr));
+    if (!found) return std::nullopt;
+    return std::make_pair(id, dist);
 }
 
 // save_index (persist.hpp:17): the DETL v1 bytes detlsh::save_index writes for
