@@ -141,6 +141,18 @@ int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint6
                       double c, uint32_t flags, uint32_t* ids, double* dists, int32_t* found,
                       uint64_t* cands_seen, void* stream);
 
+/* ---- vector files (io.hpp, io.cpp:28-85) ------------------------------------ */
+/* Shape of a .fvecs / .bvecs / .ivecs file (kind: 0 f32, 1 u8, 2 i32, from the
+ * extension as vec_element_from_path): every record header is validated.
+ * Errors: unknown extension -> DETLSH_E_INVALID; unreadable, truncated,
+ * non-positive or inconsistent dimension -> DETLSH_E_FORMAT (FormatError). */
+int detlsh_vectors_shape(const char* path, uint64_t* n, int32_t* d, int32_t* kind);
+/* read_vectors straight to device memory: `values` is a caller-owned device
+ * buffer [n][d] fp32 (n, d from detlsh_vectors_shape); the file streams through
+ * pinned chunks and u8 / i32 elements are widened to fp32 on the GPU. */
+int detlsh_gpu_read_vectors(const char* path, float* values, uint64_t n, int32_t d, int32_t device,
+                            void* stream);
+
 /* Multi-GPU merge: per-shard top-k lists gathered from `shards`
  * ranks, layout [shards][nq][k] (dist, global id); writes the global top-k
  * ascending by (dist, id).  Device pointers, stream-ordered. */

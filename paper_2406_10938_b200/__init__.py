@@ -19,6 +19,8 @@ from .api import (  # noqa: F401
     build_index_with_family,
     rc_ann,
     rc_ann_batch,
+    read_vectors_device,
+    vectors_shape,
     build_tree,
     candidate_budget,
     chi2_cdf,

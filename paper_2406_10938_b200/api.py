@@ -335,6 +335,27 @@ def ck_ann_device(index: DetIndex, queries, k: int, ids, dists, n_hits=None, rad
                                        p(cands), stream))
 
 
+def vectors_shape(path: str):
+    """(n, d, kind) of a .fvecs / .bvecs / .ivecs file (io.cpp:28-85 validation)."""
+    n = C.c_uint64(0)
+    d = C.c_int32(0)
+    kind = C.c_int32(0)
+    check(_lib.load().detlsh_vectors_shape(path.encode(), C.byref(n), C.byref(d), C.byref(kind)))
+    return n.value, d.value, ("f32", "u8", "i32")[kind.value]
+
+
+def read_vectors_device(path: str, device: int = 0):
+    """read_vectors (io.hpp) straight into a CUDA tensor [n][d] fp32: the file
+    streams through pinned chunks, u8 / i32 elements are widened on the GPU."""
+    import torch
+    n, d, _ = vectors_shape(path)
+    out = torch.empty((n, d), dtype=torch.float32, device=f"cuda:{device}")
+    if n:
+        check(_lib.load().detlsh_gpu_read_vectors(path.encode(), C.c_void_p(out.data_ptr()), n, d, device,
+                                                  None))
+    return out
+
+
 def rc_ann_batch(index: DetIndex, queries, r: float, c: float):
     """rc_ann (index.cpp:267-290) for a batch of host queries [nq][d]: returns
     (ids [nq] u32, dists [nq] f64, found [nq] bool, candidates_seen [nq])."""

@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "host_core.hpp"
 #include "index.cuh"
+#include "vecio.cuh"
 #include "query.cuh"
 #include "stages.cuh"
 #include "tree.cuh"
@@ -46,6 +47,9 @@ int guarded(F&& f) {
     } catch (const CudaError& e) {
         g_last_error = e.what();
         return DETLSH_E_CUDA;
+    } catch (const FormatError& e) {
+        g_last_error = e.what();
+        return DETLSH_E_FORMAT;
     } catch (const std::bad_alloc& e) {
         g_last_error = std::string("out of host memory: ") + e.what();
         return DETLSH_E_CUDA;
@@ -200,6 +204,24 @@ int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint6
         const RcArgs rc{r, c};
         query_impl(*index->impl, queries, nq, 1, flags, ids, dists, found, nullptr, cands_seen,
                    static_cast<cudaStream_t>(stream), &rc);
+    });
+}
+
+int detlsh_vectors_shape(const char* path, uint64_t* n, int32_t* d, int32_t* kind) {
+    return guarded([&] {
+        const int k = vec_kind_from_path(path);
+        int dd = 0;
+        vectors_shape(path, k, n, &dd);
+        *d = dd;
+        if (kind) *kind = k;
+    });
+}
+
+int detlsh_gpu_read_vectors(const char* path, float* values, uint64_t n, int32_t d, int32_t device,
+                            void* stream) {
+    return guarded([&] {
+        DeviceGuard dg(device);
+        read_vectors_into(path, vec_kind_from_path(path), values, n, d, static_cast<cudaStream_t>(stream));
     });
 }
 

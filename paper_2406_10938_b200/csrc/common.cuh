@@ -20,6 +20,10 @@ struct InvalidArgument : std::invalid_argument {
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+// Maps onto DETLSH_E_FORMAT (detlsh::FormatError, errors.hpp:19-28).
+struct FormatError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 #define DETLSH_CUDA(expr)                                                                     \
     do {                                                                                      \
