@@ -504,7 +504,11 @@ def main():
     out_ids = r_ids.cpu().numpy().astype(np.int64)
     out_d = r_d.cpu().numpy()
     out_h = r_h.cpu().numpy()
-    gt_ids, gt_d = exact_knn_gpu(base, Q, k, integer)
+    # exact ground truth with the library's brute_force_knn (metrics.cpp:8-33
+    # semantics); the squared k-th returned distance bounds each query's search
+    bound = np.where(out_h == k, out_d[:, k - 1] ** 2 * (1 + 1e-12), np.inf)
+    gt_ids, gt_d = D.brute_force_knn(base, Q, k, dist2_bound=bound)
+    gt_ids = gt_ids.astype(np.int64)
     rec, rat = recall_ratio(out_ids, out_d, out_h, gt_ids, gt_d, k)
 
     budget = D.candidate_budget(idx.params.beta, n_loc, k)

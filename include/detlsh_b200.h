@@ -141,6 +141,18 @@ int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint6
                       double c, uint32_t flags, uint32_t* ids, double* dists, int32_t* found,
                       uint64_t* cands_seen, void* stream);
 
+/* ---- exact ground truth ------------------------------------------------------- */
+/* brute_force_knn (metrics.hpp, metrics.cpp:8-33) on the GPU: for each query
+ * the k smallest l2_distance_sq (sequential fp64, dataset.hpp:23-30) over all
+ * n points, ordered by (dist^2, position); dists = sqrt(dist^2).  dist2_bound
+ * (optional, [nq], host or device) is an upper bound per query on the k-th
+ * smallest dist^2 (e.g. the squared k-th distance ck_ann returned); without
+ * it a strided sample sets the threshold.  Same answers either way.  k <= 1024.
+ * Pointers are device pointers with DETLSH_F_DEVICE_PTRS, else host. */
+int detlsh_gpu_brute_force_knn(const float* data, uint64_t n, int32_t d, const float* queries, uint64_t nq,
+                               int32_t k, const double* dist2_bound, uint32_t flags, uint32_t* ids,
+                               double* dists, int32_t device, void* stream);
+
 /* ---- vector files (io.hpp, io.cpp:28-85) ------------------------------------ */
 /* Shape of a .fvecs / .bvecs / .ivecs file (kind: 0 f32, 1 u8, 2 i32, from the
  * extension as vec_element_from_path): every record header is validated.

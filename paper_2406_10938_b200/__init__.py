@@ -14,6 +14,7 @@ from .api import (  # noqa: F401
     LshParams,
     QueryResult,
     TreeExport,
+    brute_force_knn,
     build_det_only_index,
     build_index,
     build_index_with_family,

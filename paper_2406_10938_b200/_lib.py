@@ -84,6 +84,7 @@ def load() -> C.CDLL:
         "detlsh_gpu_free": ([vp], None),
         "detlsh_gpu_query": ([vp, vp, u64, i32, u32, vp, vp, vp, vp, vp, vp], C.c_int),
         "detlsh_gpu_rc_ann": ([vp, vp, u64, dbl, dbl, u32, vp, vp, vp, vp, vp], C.c_int),
+        "detlsh_gpu_brute_force_knn": ([vp, u64, i32, vp, u64, i32, vp, u32, vp, vp, i32, vp], C.c_int),
         "detlsh_vectors_shape": ([C.c_char_p, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)], C.c_int),
         "detlsh_gpu_read_vectors": ([C.c_char_p, vp, u64, i32, i32, vp], C.c_int),
         "detlsh_gpu_merge_topk": ([vp, vp, vp, i32, u64, i32, vp, vp, vp, vp], C.c_int),

@@ -335,6 +335,26 @@ def ck_ann_device(index: DetIndex, queries, k: int, ids, dists, n_hits=None, rad
                                        p(cands), stream))
 
 
+def brute_force_knn(data, queries, k: int, *, dist2_bound=None, device: int = 0):
+    """brute_force_knn (metrics.cpp:8-33) on the GPU: (ids [nq][k], dists [nq][k])
+    ordered by (dist^2, position).  dist2_bound: optional per-query upper bound
+    on the k-th smallest dist^2 (e.g. the squared k-th ck_ann distance)."""
+    X = _as_host_f32(data)
+    Q = _as_host_f32(queries)
+    if Q.shape[1] != X.shape[1]:
+        raise ValueError("brute_force_knn: query dimension mismatch")
+    nq = Q.shape[0]
+    ids = np.zeros((nq, k), np.uint32)
+    ds = np.zeros((nq, k), np.float64)
+    b = None
+    if dist2_bound is not None:
+        bound = np.ascontiguousarray(dist2_bound, np.float64)
+        b = _ptr(bound)
+    check(_lib.load().detlsh_gpu_brute_force_knn(_ptr(X), X.shape[0], X.shape[1], _ptr(Q), nq, k, b, 0,
+                                                 _ptr(ids), _ptr(ds), device, None))
+    return ids, ds
+
+
 def vectors_shape(path: str):
     """(n, d, kind) of a .fvecs / .bvecs / .ivecs file (io.cpp:28-85 validation)."""
     n = C.c_uint64(0)

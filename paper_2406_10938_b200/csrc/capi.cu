@@ -14,6 +14,7 @@
 #include "host_core.hpp"
 #include "index.cuh"
 #include "vecio.cuh"
+#include "gt.cuh"
 #include "query.cuh"
 #include "stages.cuh"
 #include "tree.cuh"
@@ -204,6 +205,31 @@ int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint6
         const RcArgs rc{r, c};
         query_impl(*index->impl, queries, nq, 1, flags, ids, dists, found, nullptr, cands_seen,
                    static_cast<cudaStream_t>(stream), &rc);
+    });
+}
+
+int detlsh_gpu_brute_force_knn(const float* data, uint64_t n, int32_t d, const float* queries, uint64_t nq,
+                               int32_t k, const double* dist2_bound, uint32_t flags, uint32_t* ids,
+                               double* dists, int32_t device, void* stream) {
+    return guarded([&] {
+        if (!data || !queries || !ids || !dists) throw InvalidArgument("brute_force_knn: null pointer");
+        if (d < 1 || n == 0) throw InvalidArgument("brute_force_knn: empty dataset");
+        DeviceGuard dg(device);
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        StreamScope scope(s);
+        if (flags & DETLSH_F_DEVICE_PTRS) {
+            brute_force_knn_gpu(data, n, d, queries, nq, k, dist2_bound, ids, dists, device, s);
+            return;
+        }
+        DevBuf<float> X(n * static_cast<size_t>(d)), Q(nq * static_cast<size_t>(d));
+        DevBuf<uint32_t> oi(nq * static_cast<size_t>(k));
+        DevBuf<double> od(nq * static_cast<size_t>(k));
+        DETLSH_CUDA(cudaMemcpyAsync(X.get(), data, X.bytes(), cudaMemcpyHostToDevice, s));
+        DETLSH_CUDA(cudaMemcpyAsync(Q.get(), queries, Q.bytes(), cudaMemcpyHostToDevice, s));
+        brute_force_knn_gpu(X.get(), n, d, Q.get(), nq, k, dist2_bound, oi.get(), od.get(), device, s);
+        DETLSH_CUDA(cudaMemcpyAsync(ids, oi.get(), oi.bytes(), cudaMemcpyDeviceToHost, s));
+        DETLSH_CUDA(cudaMemcpyAsync(dists, od.get(), od.bytes(), cudaMemcpyDeviceToHost, s));
+        DETLSH_CUDA(cudaStreamSynchronize(s));
     });
 }
 
