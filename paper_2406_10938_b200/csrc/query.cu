@@ -1068,8 +1068,21 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                     // 8-dimension table lookups, then add the refinements
                     const float* hp = S.tlo + 2 * P.K * P.NR;  // [K][2] half penalties
                     const float* tcd = hp + 2 * kMaxK;          // [2][256] sums over 8 dims
-                    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) {
-                        const uint2 cr = __ldg(T0.leaf_cr + li);
+                    // four leaf records per thread in flight per step (the scan is
+                    // load-latency bound otherwise)
+                    constexpr int kU = 4;
+                    for (uint32_t l0 = threadIdx.x; l0 < nl; l0 += kU * blockDim.x) {
+                      uint2 crs[kU];
+#pragma unroll
+                      for (int u = 0; u < kU; ++u) {
+                          const uint32_t lu = l0 + u * blockDim.x;
+                          crs[u] = lu < nl ? __ldg(T0.leaf_cr + lu) : make_uint2(0u, 0u);
+                      }
+#pragma unroll
+                      for (int u = 0; u < kU; ++u) {
+                        const uint32_t li = l0 + u * blockDim.x;
+                        if (li >= nl) break;
+                        const uint2 cr = crs[u];
                         float a;
                         if (cr.x == 0xffffffffu) {  // no half form: every dimension from the box
                             float a1;
@@ -1084,6 +1097,7 @@ __global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
                             }
                         }
                         record(li, approx_bin(a), cr.y);
+                      }
                     }
                 } else {  // exact round (rare): exact mindists (fp64 table built below)
                     for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x)
