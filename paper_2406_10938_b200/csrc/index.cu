@@ -2,8 +2,9 @@
 //
 // Build pipeline (one index, one device):
 //   main stream : upload -> exact projection -> per space i: gather the sample,
-//                 host replay of the reference quickselects (RefSampler), upload
-//                 that space's boundary rows, record event e_i
+//                 GPU sort -> that space's boundary rows, record event e_i
+//   host        : replay of the reference quickselects of spaces 0..L-2
+//                 (RefSampler): their RNG draws pick the next space's sample
 //   side[i]     : wait e_i -> encode space i -> DE-Tree i      (own host thread)
 //   side[L]     : r_min order statistics (needs projections only; own thread)
 // so the trees and r_min overlap the sequential host replay of later spaces.
@@ -12,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <stdexcept>
 #include <thread>
 
 #include "host_core.hpp"
@@ -339,28 +341,86 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         breakpoints_gpu(*X, d_proj, seed, s);
         for (int i = 0; i < L; ++i) launch_space(i);
     } else {
-        // reference-compatible sample: host replay of the shared RNG stream
-        // (encoder.cpp:105-143) on exact sample values gathered on the device
+        // reference-compatible sample (encoder.cpp:105-143).  A boundary is an
+        // order statistic of the space's sample, whatever pivots the
+        // reference's quickselect draws, so the table rows come from a GPU
+        // sort of the gathered sample and space i's trees start at once.  The
+        // host replays the quickselects only because their draws advance the
+        // RNG that picks the NEXT space's sample: spaces 0..L-2 are replayed
+        // while the GPU encodes and builds, space L-1 not at all.  The one
+        // value an order statistic leaves open is the sign of a zero
+        // boundary (-0 == +0); those rows take the replayed value.
         const uint64_t n_s = X->sample_size;
         RefSampler sampler(n, n_s, NR, mix_seed(seed, kStreamBreakpoints));
         DevBuf<uint32_t> d_idx(n_s);
         DevBuf<float> d_sample(static_cast<size_t>(K) * n_s);
         float* h_sample = pinned_scratch(static_cast<size_t>(K) * n_s * sizeof(float));
-        X->h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
+        std::vector<float> h_rows(static_cast<size_t>(L) * K * W, 0.0f);  // replayed rows
+        cudaEvent_t copied;
+        DETLSH_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+        struct EvOne {
+            cudaEvent_t e;
+            ~EvOne() { cudaEventDestroy(e); }
+        } copied_guard{copied};
+        auto replay_space = [&](int i, int rows_needed) {
+            float* rows = h_rows.data() + static_cast<size_t>(i) * K * W;
+            for (int j = 0; j < rows_needed; ++j)
+                sampler.select_row(h_sample + static_cast<size_t>(j) * n_s, rows + j * W);
+        };
         for (int i = 0; i < L; ++i) {
             const auto& idx = sampler.next_space_indices();
             DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), idx.data(), n_s * 4, cudaMemcpyHostToDevice, s));
             launch_gather_sample(d_proj + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
                                  d_sample.get(), s);
+            const bool replay = i + 1 < L;
+            if (replay) {
+                DETLSH_CUDA(cudaMemcpyAsync(h_sample, d_sample.get(), static_cast<size_t>(K) * n_s * 4,
+                                            cudaMemcpyDeviceToHost, s));
+                DETLSH_CUDA(cudaEventRecord(copied, s));
+            }
+            gpu_order_stat_table(d_sample.get(), K, n_s, NR, X->table.get() + static_cast<size_t>(i) * K * W,
+                                 s, /*sync=*/false);
+            launch_space(i);
+            if (replay) {
+                DETLSH_CUDA(cudaEventSynchronize(copied));
+                replay_space(i, K);
+            }
+        }
+        X->h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
+        DETLSH_CUDA(cudaMemcpyAsync(X->h_table.data(), X->table.get(), X->h_table.size() * 4,
+                                    cudaMemcpyDeviceToHost, s));
+        DETLSH_CUDA(cudaStreamSynchronize(s));
+        // last space: replay only up to its last row holding a zero boundary
+        int last_zero = -1;
+        const size_t base = static_cast<size_t>(L - 1) * K * W;
+        for (int j = 0; j < K; ++j)
+            for (int b = 0; b < W; ++b)
+                if (X->h_table[base + static_cast<size_t>(j) * W + b] == 0.0f) last_zero = j;
+        if (last_zero >= 0) {
             DETLSH_CUDA(cudaMemcpyAsync(h_sample, d_sample.get(), static_cast<size_t>(K) * n_s * 4,
                                         cudaMemcpyDeviceToHost, s));
             DETLSH_CUDA(cudaStreamSynchronize(s));
-            float* rows = X->h_table.data() + static_cast<size_t>(i) * K * W;
-            for (int j = 0; j < K; ++j)
-                sampler.select_row(h_sample + static_cast<size_t>(j) * n_s, rows + j * W);
-            DETLSH_CUDA(cudaMemcpyAsync(X->table.get() + static_cast<size_t>(i) * K * W, rows,
-                                        static_cast<size_t>(K) * W * 4, cudaMemcpyHostToDevice, s));
-            launch_space(i);
+            replay_space(L - 1, last_zero + 1);
+        }
+        bool patched = false;
+        for (int i = 0; i < L; ++i) {
+            const int rows_known = i + 1 < L ? K : last_zero + 1;
+            for (int j = 0; j < rows_known; ++j)
+                for (int b = 0; b < W; ++b) {
+                    const size_t at = (static_cast<size_t>(i) * K + j) * W + b;
+                    const float g = X->h_table[at], h = h_rows[at];
+                    if (std::memcmp(&g, &h, 4) == 0) continue;
+                    if (!(g == 0.0f && h == 0.0f))
+                        throw std::runtime_error("breakpoints: GPU order statistic differs from the replay");
+                    X->h_table[at] = h;  // zero sign: the codes are unaffected (-0 == +0)
+                    patched = true;
+                }
+        }
+        if (patched) {
+            workers.join();  // encode read the table; patch only after it
+            DETLSH_CUDA(cudaMemcpyAsync(X->table.get(), X->h_table.data(), X->h_table.size() * 4,
+                                        cudaMemcpyHostToDevice, s));
+            DETLSH_CUDA(cudaStreamSynchronize(s));
         }
     }
     X->timings.emplace_back("breakpoints", ms_since(t0));

@@ -529,7 +529,7 @@ void launch_feistel_sample(uint64_t n, uint64_t n_s, uint64_t key, uint32_t* d_i
 }
 
 void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_regions,
-                          float* d_table, cudaStream_t s) {
+                          float* d_table, cudaStream_t s, bool sync) {
     StreamScope scope(s);
     const uint64_t total = static_cast<uint64_t>(R) * n_s;
     DevBuf<uint64_t> k0(total), k1(total);
@@ -543,7 +543,7 @@ void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_region
                                                  32 + ((rbits + 7) / 8) * 8, tmp.get(), s);
     order_pick_kernel<<<R, 256, 0, s>>>(flip ? k1.get() : k0.get(), R, n_s, n_regions, d_table);
     DETLSH_LAUNCH_CHECK();
-    DETLSH_CUDA(cudaStreamSynchronize(s));
+    if (sync) DETLSH_CUDA(cudaStreamSynchronize(s));
 }
 
 void launch_encode(const float* d_proj, uint64_t n, int K, int L, const float* d_table,

@@ -35,8 +35,9 @@ void launch_feistel_sample(uint64_t n, uint64_t n_s, uint64_t key, uint32_t* d_i
 
 // Exact order statistics per row (GPU sample mode): rows [R][n_s] (fp32),
 // writes table rows [R][NR+1]: row[0]=min, row[t]=sorted[span*t-1], row[NR]=max.
+// `sync` = false leaves the work queued on s (temporaries are stream-ordered).
 void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_regions,
-                          float* d_table, cudaStream_t s);
+                          float* d_table, cudaStream_t s, bool sync = true);
 
 // encode_dataset (encoder.cpp:155-176): branchless lower_bound over the
 // N_r+1 boundaries staged in shared memory; out [L][n][K] u8.

@@ -143,6 +143,25 @@ def test_build_index_and_queries(gpu, port, case):
         assert int(res.candidates_seen[qi]) == cs, f"query {qi} candidates"
 
 
+@pytest.mark.parametrize("L", [1, 3])
+def test_reference_sample_with_zero_boundaries(gpu, port, L):
+    """A third of the rows are all-zero, so many boundaries are exactly 0: the
+    table rows come from GPU order statistics, and zero boundaries take the
+    sign the reference's replayed quickselect leaves (incl. the last space,
+    which is otherwise not replayed)."""
+    n, d = 3000, 24
+    data = gaussian(n, d, 41, 2.0)
+    data[::3] = 0.0
+    c = dict(K=8, L=L, n_regions=64, leaf_capacity=32, sample_fraction=0.3, beta=0.1, k=10)
+    idx = gpu.build_index(data, _params(**c), seed=13)
+    oi = port.build_index(data, make_params(**c), 13)
+    t = np.asarray(idx.table())
+    assert (t == 0.0).sum() > 0
+    assert bits_equal(t, oi.table())
+    for i in range(L):
+        assert_tree_equal(idx.tree(i), oi.tree_export(i), f"tree {i}")
+
+
 def test_exhaustive_budget_is_brute_force_with_ties(gpu, port):
     """beta = 1 (test_query.cpp:342-396): the pipeline reduces to exact kNN incl. tie order."""
     g = np.random.Generator(np.random.PCG64(401))
