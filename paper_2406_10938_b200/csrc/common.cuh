@@ -50,6 +50,10 @@ constexpr int kMaxRegions = 256;
 // pool keeps freed blocks cached (release threshold raised at first use).
 cudaStream_t& alloc_stream();
 void ensure_mempool(int device);
+// Grows the pool in one mapping to hold `bytes` beyond what is in use, so a
+// build's many stream-ordered temporaries (several streams at once) do not
+// each map fresh memory the first times round.
+void reserve_mempool(int device, size_t bytes, cudaStream_t s);
 
 struct StreamScope {
     cudaStream_t prev;

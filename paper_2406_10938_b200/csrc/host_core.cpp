@@ -487,6 +487,13 @@ void select_row_breakpoints(float* a, uint64_t n_s, int n_regions, Rng& rng, flo
     stack.reserve(256);
     stack.push_back({0, n_s, 0, nt});
     auto target = [span](size_t t) { return span * (t + 1) - 1; };
+    // exact floor(x / span) for x, span < 2^32: x * ceil(2^64 / span) >> 64
+    const unsigned __int128 recip = span > 1 ? (~static_cast<unsigned __int128>(0) >> 64) / span + 1 : 0;
+    auto div_span = [span, recip](size_t x) -> size_t {
+        if (span == 1) return x;
+        if ((x | span) >> 32) return x / span;
+        return static_cast<size_t>((static_cast<unsigned __int128>(x) * recip) >> 64);
+    };
     uint64_t nd = 0;
     while (!stack.empty()) {
         const Item it = stack.back();
@@ -498,22 +505,11 @@ void select_row_breakpoints(float* a, uint64_t n_s, int n_regions, Rng& rng, flo
         }
         const size_t p = hoare_partition(a, it.lo, it.hi, rng);
         ++nd;
-        // targets are an arithmetic progression: count those below / at p
-        size_t below = it.tlo, above;
-        {
-            size_t lo = it.tlo, hi = it.thi;
-            while (lo < hi) {
-                const size_t m = lo + (hi - lo) / 2;
-                if (target(m) < p) lo = m + 1; else hi = m;
-            }
-            below = lo;
-            hi = it.thi;
-            while (lo < hi) {
-                const size_t m = lo + (hi - lo) / 2;
-                if (target(m) <= p) lo = m + 1; else hi = m;
-            }
-            above = lo;
-        }
+        // targets are an arithmetic progression: #{t : span(t+1)-1 < p} =
+        // floor(p / span), #{t : span(t+1)-1 <= p} = floor((p+1) / span),
+        // clamped to the item's target range (lower_bound / upper_bound)
+        const size_t below = std::min(std::max(div_span(p), it.tlo), it.thi);
+        const size_t above = std::min(std::max(div_span(p + 1), it.tlo), it.thi);
         stack.push_back({it.lo, p, it.tlo, below});
         stack.push_back({p + 1, it.hi, above, it.thi});
     }

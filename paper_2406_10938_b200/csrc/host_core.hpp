@@ -21,10 +21,10 @@ public:
     uint64_t next_u64() { return gen_(); }
     // rng.hpp:20-26
     uint64_t bounded(uint64_t bound) {
-        const uint64_t threshold = (0 - bound) % bound;
+        // threshold = 2^64 mod bound < bound, so r >= bound accepts without it
         for (;;) {
             const uint64_t r = gen_();
-            if (r >= threshold) return r % bound;
+            if (r >= bound || r >= (0 - bound) % bound) return r % bound;
         }
     }
     double real01() { return static_cast<double>(gen_() >> 11) * 0x1.0p-53; }

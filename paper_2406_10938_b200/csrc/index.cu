@@ -239,6 +239,12 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     }
     X->timings.emplace_back("host_params_family", ms_since(t0));
     t0 = Clock::now();
+    {  // peak device footprint of the build (projections, codes, trees and their
+       // sort temporaries, verification rows, r_min distances)
+        const size_t per_pt = static_cast<size_t>(LK) * 5 + 2 * (static_cast<size_t>(d) + 32) +
+                              4 * static_cast<size_t>(d) + static_cast<size_t>(L) * 64 + 96;
+        reserve_mempool(device, n * per_pt, s);
+    }
     if ((flags & DETLSH_F_DEVICE_PTRS) && (flags & DETLSH_F_BORROW_DATA)) {
         X->data = points;
     } else {
@@ -367,8 +373,12 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             for (int j = 0; j < rows_needed; ++j)
                 sampler.select_row(h_sample + static_cast<size_t>(j) * n_s, rows + j * W);
         };
+        double t_idx = 0.0, t_wait = 0.0, t_replay = 0.0;
+        const auto t_loop = Clock::now();
         for (int i = 0; i < L; ++i) {
+            auto tq = Clock::now();
             const auto& idx = sampler.next_space_indices();
+            t_idx += ms_since(tq);
             DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), idx.data(), n_s * 4, cudaMemcpyHostToDevice, s));
             launch_gather_sample(d_proj + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
                                  d_sample.get(), s);
@@ -382,10 +392,18 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                                  s, /*sync=*/false);
             launch_space(i);
             if (replay) {
+                tq = Clock::now();
                 DETLSH_CUDA(cudaEventSynchronize(copied));
+                t_wait += ms_since(tq);
+                tq = Clock::now();
                 replay_space(i, K);
+                t_replay += ms_since(tq);
             }
         }
+        X->timings.emplace_back("bp_sample_indices", t_idx);
+        X->timings.emplace_back("bp_sample_wait", t_wait);
+        X->timings.emplace_back("bp_replay", t_replay);
+        X->timings.emplace_back("bp_loop", ms_since(t_loop));
         X->h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
         DETLSH_CUDA(cudaMemcpyAsync(X->h_table.data(), X->table.get(), X->h_table.size() * 4,
                                     cudaMemcpyDeviceToHost, s));

@@ -102,4 +102,19 @@ void ensure_mempool(int device) {
     done[device] = true;
 }
 
+void reserve_mempool(int device, size_t bytes, cudaStream_t s) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+    uint64_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    if (reserved >= used + bytes) return;
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+        cudaGetLastError();  // best effort: the build allocates what it needs anyway
+        return;
+    }
+    cudaFreeAsync(p, s);
+}
+
 }  // namespace detlsh_b200
