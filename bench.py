@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--sample", choices=["reference", "gpu"], default="reference",
                     help="breakpoint sample mode of the headline build")
+    ap.add_argument("--shard", choices=["weak", "strong"], default="weak",
+                    help="N>1: weak = every rank indexes its own n-point shard of a world x n "
+                         "dataset (fixed per-GPU work); strong = the config's n split across ranks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=200)
     ap.add_argument("--cpu-build-rows", type=int, default=250_000)
@@ -368,8 +371,15 @@ def main():
     base, Q = gen.make(cfg, nq=args.nq)
     n, d = base.shape
     nq = Q.shape[0]
-    s0, s1 = shard_bounds(n, world, rank)
-    shard = np.ascontiguousarray(base[s0:s1])
+    if world > 1 and args.shard == "weak":
+        # weak scaling: rank r holds points [r n, (r+1) n) of a world x n dataset
+        shard = base if rank == 0 else np.ascontiguousarray(gen.make_shard(cfg, rank, n))
+        s0 = rank * n
+        n_total = world * n
+    else:
+        s0, s1 = shard_bounds(n, world, rank)
+        shard = np.ascontiguousarray(base[s0:s1])
+        n_total = n
     n_loc = shard.shape[0]
     params = D.LshParams(beta=args.beta, k=args.k)
     k = args.k
@@ -469,7 +479,8 @@ def main():
     shard_pinned = torch.from_numpy(shard).pin_memory().numpy()  # host input, pinned
 
     def e2e_build():
-        ix = D.build_index(shard_pinned, params, seed=args.seed, sample=args.sample, keep_codes=False)
+        ix = D.build_index(shard_pinned, params, seed=args.seed, device=local, sample=args.sample,
+                           keep_codes=False)
         _ = ix.params.r_min  # result read back (params travel D2H inside build)
         return ix
 
@@ -494,21 +505,31 @@ def main():
     e2e_query_ms, _ = timed(e2e_query, max(1, args.steps))
     e2e_query_ms = max_over_ranks(e2e_query_ms)
 
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
     # ---------------- quality (merged results vs exact kNN) ----------------
-    integer = bool(np.all(base == np.round(base)) and base.min() >= 0 and base.max() <= 255)
     out_ids = r_ids.cpu().numpy().astype(np.int64)
     out_d = r_d.cpu().numpy()
     out_h = r_h.cpu().numpy()
     # exact ground truth with the library's brute_force_knn (metrics.cpp:8-33
-    # semantics); the squared k-th returned distance bounds each query's search
+    # semantics); the squared k-th returned distance bounds each query's search.
+    # N > 1: every rank's exact list over its own shard, merged like the ANN lists
+    # (the global exact top-k is contained in the union of the shard top-k's).
     bound = np.where(out_h == k, out_d[:, k - 1] ** 2 * (1 + 1e-12), np.inf)
-    gt_ids, gt_d = D.brute_force_knn(base, Q, k, dist2_bound=bound)
-    gt_ids = gt_ids.astype(np.int64)
+    if world > 1:
+        bound = None  # a shard may hold fewer than k points inside the global bound
+    gt_ids, gt_d = D.brute_force_knn(shard, Q, k, dist2_bound=bound, device=local)
+    gt_ids = gt_ids.astype(np.int64) + s0
+    if world > 1:
+        t_i = torch.from_numpy(gt_ids).cuda()
+        t_d = torch.from_numpy(np.ascontiguousarray(gt_d, np.float64)).cuda()
+        t_h = torch.full((nq,), min(k, n_loc), dtype=torch.int32, device="cuda")
+        gather_topk(t_d, t_i, t_h, g_d, g_i, g_h)
+        D.merge_topk_device(g_d, g_i, g_h, k, m_d, m_i, m_h, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        gt_ids, gt_d = m_i.cpu().numpy().astype(np.int64), m_d.cpu().numpy()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
     rec, rat = recall_ratio(out_ids, out_d, out_h, gt_ids, gt_d, k)
 
     budget = D.candidate_budget(idx.params.beta, n_loc, k)
@@ -541,15 +562,16 @@ def main():
     m_ref = min(args.cpu_queries, nq)
     rec_ref, rat_ref = recall_ratio(out_ids[:m_ref], out_d[:m_ref], out_h[:m_ref], gt_ids[:m_ref],
                                     gt_d[:m_ref], k)
-    value = n / (build_ms / 1e3) / 1e6
+    value = n_total / (build_ms / 1e3) / 1e6
     qps = nq / (query_ms / 1e3)
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(build_ms, 3),
-        "higher_is_better": True, "scaling": "weak" if world > 1 else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.shard if world > 1 else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg}: n={n}, d={d}, nq={nq}, K=16, L=4, N_r=256, leaf=128, "
+        "config": {"workload": f"{cfg}: n={n_total}, d={d}, nq={nq}, K=16, L=4, N_r=256, leaf=128, "
                                f"k={k}, c=1.5, beta={args.beta}",
+                   "points_per_gpu": n_loc,
                    "sample_mode": args.sample, "parallelism": f"point-shard x{world}",
                    "l2": "inputs larger than L2 (dataset 512 MB, candidate rows 51 MB/query)"},
         "query": {"value": round(qps, 2), "unit": "queries/s", "ms_per_step": round(query_ms, 3),
@@ -560,10 +582,10 @@ def main():
                   "e2e": {"value": round(nq / (e2e_query_ms / 1e3), 2), "unit": "queries/s",
                           "h2d_bytes_per_step": int(nq * d * 4),
                           "d2h_bytes_per_step": int(nq * k * 12 + nq * 20)}},
-        "e2e": {"value": round(n / (e2e_build_ms / 1e3) / 1e6, 3), "unit": "Mpoints/s",
+        "e2e": {"value": round(n_total / (e2e_build_ms / 1e3) / 1e6, 3), "unit": "Mpoints/s",
                 "h2d_bytes_per_step": int(n_loc * d * 4), "d2h_bytes_per_step": 96},
         "gpu_launches": build_launches,
-        "build_other_sample": {"sample_mode": other, "value": round(n / (other_ms / 1e3) / 1e6, 3),
+        "build_other_sample": {"sample_mode": other, "value": round(n_total / (other_ms / 1e3) / 1e6, 3),
                                "unit": "Mpoints/s", "ms_per_step": round(other_ms, 3),
                                "parity": "hybrid oracle (reference stage functions, same table)"
                                if other == "gpu" else "bit-exact vs reference"},

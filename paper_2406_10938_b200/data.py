@@ -23,9 +23,11 @@ CONFIGS = {
 
 
 def mixture(total: int, d: int, seed: int, clusters: int = 100, lo: float = 0.0,
-            hi: float = 100.0, sigma: float = 5.0) -> np.ndarray:
+            hi: float = 100.0, sigma: float = 5.0, sample_seed: int | None = None) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed))
     centres = rng.uniform(lo, hi, size=(clusters, d)).astype(np.float32)
+    if sample_seed is not None:  # same centres, another draw of members
+        rng = np.random.Generator(np.random.PCG64(sample_seed))
     pick = rng.integers(0, clusters, size=total)
     out = np.empty((total, d), np.float32)
     step = 1 << 16
@@ -98,3 +100,24 @@ def make(config: str, n: int | None = None, nq: int | None = None):
     else:
         raise ValueError(config)
     return allp[:n], allp[n:]
+
+
+def make_shard(config: str, rank: int, n: int | None = None) -> np.ndarray:
+    """Rank `rank`'s n points of the weak-scaling dataset (world x n points): shard 0
+    is make(config)'s base, shard r > 0 is an independent draw of the same
+    distribution (seed + 1000 r).  The held-out queries stay make(config)'s."""
+    c = CONFIGS[config]
+    n = c["n"] if n is None else n
+    if rank == 0:
+        return make(config, n=n)[0]
+    seed = c["seed"] + 1000 * rank
+    if config == "c1":
+        return mixture(n, c["d"], c["seed"], sample_seed=seed)
+    if config in ("c2", "c5"):
+        return sparse_geometric(n, c["d"], seed)
+    if config == "c3":
+        return blobs784(n, seed)
+    if config == "c4":
+        return unit_gaussian(n, c["d"], seed)
+    raise ValueError(config)
+
