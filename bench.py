@@ -211,7 +211,7 @@ def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0, plan=None):
         return 4.0 * d * budget * nq  # every verified candidate row (4d B/candidate)
     if kernel == "encode":
         return 5.0 * K * n  # one space per launch: fp32 projections in, u8 codes out
-    if kernel == "tree_build":
+    if kernel == "tree_sort":
         return (K + 4.0) * n  # one tree: read its codes, write the leaf-order permutation
     if kernel == "rmin_dist":
         return (4.0 * L * K + 8.0 * 10) * n  # read projections, write 10 probe distances
@@ -635,9 +635,7 @@ def roofline_tc(prof, steps, n, nq, row_u8, peak_bf16):
 
 def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exclude=(),
              row_u8=0, plan=None):
-    # nested scopes (tree_level_split inside tree_build) are not separate work
-    items = [(kk, v) for kk, v in prof.items()
-             if (only is None or kk in only) and kk not in exclude and kk != "tree_level_split"]
+    items = [(kk, v) for kk, v in prof.items() if (only is None or kk in only) and kk not in exclude]
     if not items:
         return None
     kern, (ms, launches) = max(items, key=lambda kv: kv[1][0])
@@ -645,13 +643,27 @@ def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exc
     if kern == "query_fast" and "tc_score" not in prof:
         plan = None  # no tensor-core hand-off in this run: the kernel verified everything
     b = algo_bytes(kern, n, d, nq, budget, K, L, row_u8, plan)
-    total = sum(v[0] for kk, v in prof.items() if kk != "tree_level_split")
+    total = sum(v[0] for kk, v in prof.items())
     units = nq if kern == "query_fast" else n
     traffic, tsrc = ncu_traffic(kern, units)
     out = {"kernel": kern, "bound": "hbm", "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
            "launch_ms": round(per_launch_ms, 4), "launches_per_step": launches / steps,
            "share_of_kernel_time": round(ms / total, 4) if total else None,
            "traffic": traffic, "traffic_source": tsrc}
+    if kern == "project_exact":
+        # d x (L K) fp64 FMA chain per point on the FP64 tensor pipe (DMMA): the
+        # bound is FP64 tensor throughput; no FP64 figure is measured in
+        # MEASURED_PEAKS.json, so the peak is B200's nominal 45 TF/s
+        fl = 2.0 * n * K * L * d
+        ach = fl / (per_launch_ms / 1e3) / 1e12
+        b = algo_bytes(kern, n, d, nq, budget, K, L)
+        out.update({"bound": "tensor", "unit": "TFLOP/s", "peak": 45.0,
+                    "peak_kind": "nominal B200 FP64 tensor (no measured FP64 peak)",
+                    "achieved": round(ach, 3), "frac": round(ach / 45.0, 5), "algorithmic_flops": fl,
+                    "hbm_view": {"algorithmic_bytes": b,
+                                 "achieved_gbs": round(b / (per_launch_ms / 1e3) / 1e9, 2),
+                                 "frac": round(b / (per_launch_ms / 1e3) / 1e9 / hbm, 5)}})
+        return out
     if b is None:
         out.update({"achieved": None, "frac": None})
     else:

@@ -1,6 +1,8 @@
 // Scan + stable radix sort (see primitives.cuh).
 #include "primitives.cuh"
 
+#include <algorithm>
+
 namespace detlsh_b200 {
 
 namespace {
@@ -146,18 +148,26 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* t
 namespace {
 
 constexpr int kRadixThreads = 256;
-constexpr int kRadixRounds = 16;
-constexpr int kRadixTile = kRadixThreads * kRadixRounds;  // 4096
+constexpr int kRadixMaxRounds = 16;
+
+// Rounds of 256 keys per tile: enough tiles to give every SM several CTAs
+// (small sorts such as the node-id sort would otherwise run a handful of
+// CTAs through 16 serial rounds each), at most 16 (tiles of 4096).
+int radix_rounds(size_t n) {
+    const size_t want_tiles = 148 * 4;
+    size_t r = (n + 256 * want_tiles - 1) / (256 * want_tiles);
+    return static_cast<int>(std::max<size_t>(1, std::min<size_t>(kRadixMaxRounds, r)));
+}
 
 template <typename KeyT>
 __global__ void radix_upsweep(const KeyT* __restrict__ keys, size_t n, int shift,
-                              uint32_t* __restrict__ hist, uint32_t num_tiles) {
+                              uint32_t* __restrict__ hist, uint32_t num_tiles, int rounds) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
     __syncthreads();
-    const size_t base = static_cast<size_t>(blockIdx.x) * kRadixTile;
+    const size_t base = static_cast<size_t>(blockIdx.x) * kRadixThreads * rounds;
 #pragma unroll 4
-    for (int r = 0; r < kRadixRounds; ++r) {
+    for (int r = 0; r < rounds; ++r) {
         const size_t idx = base + static_cast<size_t>(r) * kRadixThreads + threadIdx.x;
         if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & 0xff], 1u);
     }
@@ -169,16 +179,16 @@ template <typename KeyT>
 __global__ void radix_downsweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                 KeyT* __restrict__ kout, uint32_t* __restrict__ vout, size_t n,
                                 int shift, const uint32_t* __restrict__ offsets,
-                                uint32_t num_tiles) {
+                                uint32_t num_tiles, int rounds) {
     __shared__ uint32_t wh[kRadixThreads / 32][256];
     __shared__ uint32_t running[256];
     __shared__ uint32_t gbase[256];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     running[tid] = 0;
     gbase[tid] = offsets[static_cast<size_t>(tid) * num_tiles + blockIdx.x];
-    const size_t base = static_cast<size_t>(blockIdx.x) * kRadixTile;
+    const size_t base = static_cast<size_t>(blockIdx.x) * kRadixThreads * rounds;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    for (int r = 0; r < kRadixRounds; ++r) {
+    for (int r = 0; r < rounds; ++r) {
         const size_t idx = base + static_cast<size_t>(r) * kRadixThreads + tid;
         if (base + static_cast<size_t>(r) * kRadixThreads >= n) break;  // uniform
 #pragma unroll
@@ -220,7 +230,8 @@ __global__ void radix_downsweep(const KeyT* __restrict__ kin, const uint32_t* __
 }  // namespace
 
 size_t radix_temp_elems(size_t n) {
-    const size_t tiles = (n + kRadixTile - 1) / kRadixTile;
+    const size_t tile = static_cast<size_t>(kRadixThreads) * radix_rounds(n);
+    const size_t tiles = (n + tile - 1) / tile;
     return 256 * tiles * 2 + scan_temp_elems(256 * tiles) + 8;
 }
 
@@ -228,7 +239,9 @@ template <typename KeyT>
 bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, int begin_bit,
                       int end_bit, uint32_t* tmp, cudaStream_t s) {
     if (n <= 1) return false;
-    const uint32_t tiles = static_cast<uint32_t>((n + kRadixTile - 1) / kRadixTile);
+    const int rounds = radix_rounds(n);
+    const size_t tile = static_cast<size_t>(kRadixThreads) * rounds;
+    const uint32_t tiles = static_cast<uint32_t>((n + tile - 1) / tile);
     uint32_t* hist = tmp;
     uint32_t* offs = tmp + 256 * static_cast<size_t>(tiles);
     uint32_t* stmp = offs + 256 * static_cast<size_t>(tiles);
@@ -238,10 +251,10 @@ bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, 
         uint32_t* vi = flipped ? v1 : v0;
         KeyT* ko = flipped ? k0 : k1;
         uint32_t* vo = flipped ? v0 : v1;
-        radix_upsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, n, bit, hist, tiles);
+        radix_upsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, n, bit, hist, tiles, rounds);
         DETLSH_LAUNCH_CHECK();
         exclusive_scan_u32(hist, offs, 256 * static_cast<size_t>(tiles), stmp, nullptr, s);
-        radix_downsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, vi, ko, vo, n, bit, offs, tiles);
+        radix_downsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, vi, ko, vo, n, bit, offs, tiles, rounds);
         DETLSH_LAUNCH_CHECK();
         flipped = !flipped;
     }

@@ -20,6 +20,7 @@
 // splitting (one CTA per splitting node) -> node-id radix sort -> flatten.
 #include <algorithm>
 #include <chrono>
+#include <optional>
 
 #include "primitives.cuh"
 #include "tree.cuh"
@@ -363,20 +364,28 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     DevBuf<uint32_t> k0(n), k1(n), v1(n), flags(n), ridx(n);
     T.perm.alloc(n);
     DevBuf<uint32_t> rtmp(std::max(radix_temp_elems(n), scan_temp_elems(n)));
-    ProfScope ps_all("tree_build", s);
-    slot_key_kernel<<<grid_for(n), 256, 0, s>>>(d_codes, n, K, sbits, k0.get(), T.perm.get());
-    DETLSH_LAUNCH_CHECK();
-    const bool flip = radix_sort_pairs<uint32_t>(k0.get(), T.perm.get(), k1.get(), v1.get(), n, 0,
-                                                 ((K + 7) / 8) * 8, rtmp.get(), s);
+    // profile scopes cover device work only (the host reads between phases
+    // are outside them), so each is a kernel-time figure
+    bool flip = false;
+    {
+        ProfScope ps("tree_sort", s);
+        slot_key_kernel<<<grid_for(n), 256, 0, s>>>(d_codes, n, K, sbits, k0.get(), T.perm.get());
+        DETLSH_LAUNCH_CHECK();
+        flip = radix_sort_pairs<uint32_t>(k0.get(), T.perm.get(), k1.get(), v1.get(), n, 0, ((K + 7) / 8) * 8,
+                                          rtmp.get(), s);
+        if (flip) DETLSH_CUDA(cudaMemcpyAsync(T.perm.get(), v1.get(), n * 4, cudaMemcpyDeviceToDevice, s));
+    }
     uint32_t* skeys = flip ? k1.get() : k0.get();
-    if (flip) DETLSH_CUDA(cudaMemcpyAsync(T.perm.get(), v1.get(), n * 4, cudaMemcpyDeviceToDevice, s));
 
     // 3-4. root nodes
-    head_flag_kernel<<<grid_for(n), 256, 0, s>>>(skeys, n, flags.get());
-    DETLSH_LAUNCH_CHECK();
     DevBuf<uint32_t> counters(4);
-    DETLSH_CUDA(cudaMemsetAsync(counters.get(), 0, 4 * sizeof(uint32_t), s));
-    exclusive_scan_u32(flags.get(), ridx.get(), n, rtmp.get(), counters.get(), s);
+    {
+        ProfScope ps("tree_roots", s);
+        head_flag_kernel<<<grid_for(n), 256, 0, s>>>(skeys, n, flags.get());
+        DETLSH_LAUNCH_CHECK();
+        DETLSH_CUDA(cudaMemsetAsync(counters.get(), 0, 4 * sizeof(uint32_t), s));
+        exclusive_scan_u32(flags.get(), ridx.get(), n, rtmp.get(), counters.get(), s);
+    }
     uint32_t R = 0;
     DETLSH_CUDA(cudaMemcpyAsync(&R, counters.get(), 4, cudaMemcpyDeviceToHost, s));
     DETLSH_CUDA(cudaStreamSynchronize(s));
@@ -384,19 +393,22 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     BuildNodes B;
     B.grow(std::max<size_t>(R + 2 * (n / (cap + 1)) + 64, 1024), 0, K, s);
     DevBuf<uint32_t> rslot(R);
-    root_init_kernel<<<grid_for(n), 256, 0, s>>>(skeys, T.perm.get(), flags.get(), ridx.get(), n, K,
-                                                 B.key.get(), B.begin.get(), B.depth.get(),
-                                                 B.split.get(), B.bits.get(), B.value.get(),
-                                                 rslot.get());
-    DETLSH_LAUNCH_CHECK();
     DevBuf<uint32_t> actA(std::max<size_t>(R, 1)), actB;
     uint32_t* d_act_n = counters.get() + 1;
     uint32_t* d_next_n = counters.get() + 2;
     uint32_t* d_invalid = counters.get() + 3;
-    DETLSH_CUDA(cudaMemsetAsync(counters.get() + 1, 0, 3 * sizeof(uint32_t), s));
-    root_count_kernel<<<grid_for(R), 256, 0, s>>>(B.begin.get(), R, n, B.count.get(), cap,
-                                                  actA.get(), d_act_n);
-    DETLSH_LAUNCH_CHECK();
+    {
+        ProfScope ps("tree_roots", s);
+        root_init_kernel<<<grid_for(n), 256, 0, s>>>(skeys, T.perm.get(), flags.get(), ridx.get(), n, K,
+                                                     B.key.get(), B.begin.get(), B.depth.get(),
+                                                     B.split.get(), B.bits.get(), B.value.get(),
+                                                     rslot.get());
+        DETLSH_LAUNCH_CHECK();
+        DETLSH_CUDA(cudaMemsetAsync(counters.get() + 1, 0, 3 * sizeof(uint32_t), s));
+        root_count_kernel<<<grid_for(R), 256, 0, s>>>(B.begin.get(), R, n, B.count.get(), cap,
+                                                      actA.get(), d_act_n);
+        DETLSH_LAUNCH_CHECK();
+    }
     uint32_t A = 0;
     DETLSH_CUDA(cudaMemcpyAsync(&A, d_act_n, 4, cudaMemcpyDeviceToHost, s));
     DETLSH_CUDA(cudaStreamSynchronize(s));
@@ -409,13 +421,15 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
         B.grow(total + 2 * static_cast<size_t>(A), total, K, s);
         actB.grow(2 * static_cast<size_t>(A), 0, s);
         DETLSH_CUDA(cudaMemsetAsync(d_next_n, 0, 4, s));
-        ProfScope ps("tree_level_split", s);
-        level_split_kernel<<<A, kLevelThreads, 0, s>>>(
-            d_codes, K, sbits, cap, actA.get(), static_cast<uint32_t>(total), T.perm.get(),
-            ptmp.get(), B.key.get(), B.begin.get(), B.count.get(), B.depth.get(), B.split.get(),
-            B.left.get(), B.right.get(), B.bits.get(), B.value.get(), actB.get(), d_next_n,
-            d_invalid);
-        DETLSH_LAUNCH_CHECK();
+        {
+            ProfScope ps("tree_level_split", s);
+            level_split_kernel<<<A, kLevelThreads, 0, s>>>(
+                d_codes, K, sbits, cap, actA.get(), static_cast<uint32_t>(total), T.perm.get(),
+                ptmp.get(), B.key.get(), B.begin.get(), B.count.get(), B.depth.get(), B.split.get(),
+                B.left.get(), B.right.get(), B.bits.get(), B.value.get(), actB.get(), d_next_n,
+                d_invalid);
+            DETLSH_LAUNCH_CHECK();
+        }
         total += 2 * static_cast<uint64_t>(A);
         DETLSH_CUDA(cudaMemcpyAsync(&A, d_next_n, 4, cudaMemcpyDeviceToHost, s));
         DETLSH_CUDA(cudaStreamSynchronize(s));
@@ -435,6 +449,8 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     DevBuf<uint64_t> ka(total), kb(total);
     DevBuf<uint32_t> va(total), vb(total), id_of_bn(total);
     DevBuf<uint32_t> stmp(radix_temp_elems(total) + scan_temp_elems(total));
+    std::optional<ProfScope> ps_ids;
+    ps_ids.emplace("tree_ids", s);
     DETLSH_CUDA(cudaMemcpyAsync(ka.get(), B.key.get(), total * 8, cudaMemcpyDeviceToDevice, s));
     clamp_invalid_keys<<<grid_for(total), 256, 0, s>>>(ka.get(), total, invalid_key);
     DETLSH_LAUNCH_CHECK();
@@ -470,6 +486,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     DETLSH_LAUNCH_CHECK();
     DETLSH_CUDA(cudaMemsetAsync(counters.get(), 0, 8, s));
     exclusive_scan_u32(leaf_flag.get(), leaf_idx.get(), valid, stmp.get(), counters.get(), s);
+    ps_ids.reset();
     uint32_t nl = 0;
     DETLSH_CUDA(cudaMemcpyAsync(&nl, counters.get(), 4, cudaMemcpyDeviceToHost, s));
     DETLSH_CUDA(cudaStreamSynchronize(s));
@@ -479,12 +496,15 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     T.leaf_count.alloc(nl);
     T.leaf_box.alloc(static_cast<size_t>(nl) * kBoxStride * 2);
     T.leaf_cr.alloc(nl);
-    leaves_kernel<<<grid_for(valid), 256, 0, s>>>(valid, K, sbits, leaf_flag.get(), leaf_idx.get(),
-                                                  T.bits.get(), T.value.get(), T.node_begin.get(),
-                                                  T.node_count.get(), T.leaf_node.get(),
-                                                  T.leaf_begin.get(), T.leaf_count.get(),
-                                                  T.leaf_box.get(), T.leaf_cr.get(), counters.get() + 1);
-    DETLSH_LAUNCH_CHECK();
+    {
+        ProfScope ps("tree_leaves", s);
+        leaves_kernel<<<grid_for(valid), 256, 0, s>>>(valid, K, sbits, leaf_flag.get(), leaf_idx.get(),
+                                                      T.bits.get(), T.value.get(), T.node_begin.get(),
+                                                      T.node_count.get(), T.leaf_node.get(),
+                                                      T.leaf_begin.get(), T.leaf_count.get(),
+                                                      T.leaf_box.get(), T.leaf_cr.get(), counters.get() + 1);
+        DETLSH_LAUNCH_CHECK();
+    }
     uint32_t mx = 0;
     DETLSH_CUDA(cudaMemcpyAsync(&mx, counters.get() + 1, 4, cudaMemcpyDeviceToHost, s));
     DETLSH_CUDA(cudaStreamSynchronize(s));
