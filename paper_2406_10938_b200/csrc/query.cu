@@ -1752,14 +1752,29 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             uint64_t chunk = (3ULL << 30) / (W * 4 + 160 * 1024);
             chunk = std::max<uint64_t>(256, chunk / 256 * 256);
             chunk = std::min<uint64_t>(chunk, (P.nq + 255) / 256 * 256);
-            DevBuf<uint32_t> flags(chunk * LW), cut(chunk * 2), bm(chunk * W), tmap(chunk / 256 * TW);
-            DevBuf<int32_t> tau2(chunk), qn(chunk);
-            DevBuf<uint32_t> surv_cnt(chunk);
-            DevBuf<uint8_t> q8(chunk * R);
-            DevBuf<uint64_t> surv(chunk * kTcFinishCap);
             const uint64_t rec_cap = chunk * 8192;  // candidate threshold passes staged per chunk
-            DevBuf<uint4> rec(rec_cap);
-            DevBuf<unsigned long long> rec_cnt(1);
+            grow_scratch(X.tc_flags, chunk * LW);
+            grow_scratch(X.tc_cut, chunk * 2);
+            grow_scratch(X.tc_bm, chunk * W);
+            grow_scratch(X.tc_tmap, (chunk + 255) / 256 * TW);
+            grow_scratch(X.tc_tau2, chunk);
+            grow_scratch(X.tc_qn, chunk);
+            grow_scratch(X.tc_surv_cnt, chunk);
+            grow_scratch(X.tc_q8, chunk * R);
+            grow_scratch(X.tc_surv, chunk * kTcFinishCap);
+            grow_scratch(X.tc_rec, rec_cap);
+            grow_scratch(X.tc_rec_cnt, 1);
+            DevBuf<uint32_t>& flags = X.tc_flags;
+            DevBuf<uint32_t>& cut = X.tc_cut;
+            DevBuf<uint32_t>& bm = X.tc_bm;
+            DevBuf<uint32_t>& tmap = X.tc_tmap;
+            DevBuf<int32_t>& tau2 = X.tc_tau2;
+            DevBuf<int32_t>& qn = X.tc_qn;
+            DevBuf<uint32_t>& surv_cnt = X.tc_surv_cnt;
+            DevBuf<uint8_t>& q8 = X.tc_q8;
+            DevBuf<uint64_t>& surv = X.tc_surv;
+            DevBuf<uint4>& rec = X.tc_rec;
+            DevBuf<unsigned long long>& rec_cnt = X.tc_rec_cnt;
             over_list.alloc(P.nq);
             for (uint64_t c0 = 0; c0 < P.nq; c0 += chunk) {
                 const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);

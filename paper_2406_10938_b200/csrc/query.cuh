@@ -83,6 +83,16 @@ struct QueryScratch {
     DevBuf<uint32_t> counters;
     DevBuf<unsigned long long> phases;  // [6] fast-path phase cycles (profiling only)
     size_t fast_slots = 0, slow_slots = 0;
+    // tensor-core hand-off staging (per chunk of queries), kept across calls:
+    // several of these are GB-sized and re-allocating them from the pool per
+    // batch costs fresh mappings whenever the pool is fragmented.  Nothing reads
+    // them after run_query_batch's last host sync, so the next call may reuse them.
+    DevBuf<uint32_t> tc_flags, tc_cut, tc_bm, tc_tmap, tc_surv_cnt;
+    DevBuf<int32_t> tc_tau2, tc_qn;
+    DevBuf<uint8_t> tc_q8;
+    DevBuf<uint64_t> tc_surv;
+    DevBuf<uint4> tc_rec;
+    DevBuf<unsigned long long> tc_rec_cnt;
 };
 
 // ---- tensor-core exact verification (tc_score.cu) ----

@@ -280,18 +280,37 @@ __global__ void order_pick_kernel(const uint64_t* __restrict__ sorted, int R, ui
 }
 
 // Encode: one thread per (space, point); the space's K boundary rows sit in
-// shared memory; branchless lower_bound = #{b : row[b] < v}.
+// shared memory in Eytzinger (BFS) order, padded with +inf to a complete tree
+// of 2^H - 1 nodes, so lower_bound = #{b : row[b] < v} is H branch-free steps
+// i = 2i + (e[i] < v) ending at i = 2^H + count.  Level l touches 2^l
+// consecutive words, so the first six levels are bank-conflict free (the
+// sorted-array search strides by multiples of 32 words and serialises).
 __global__ void encode_kernel(const float* __restrict__ proj, uint64_t n, int K,
-                              const float* __restrict__ table, int NR, int steps,
+                              const float* __restrict__ table, int NR, int H,
                               uint8_t* __restrict__ codes) {
-    extern __shared__ float srow[];  // [K][NR+1]
+    extern __shared__ float se[];  // [K][2^H], node i of dim j at se[j * 2^H + i]
     const int sp = blockIdx.y;
     const int W = NR + 1;
-    for (int i = threadIdx.x; i < K * W; i += blockDim.x)
-        srow[i] = table[static_cast<uint64_t>(sp) * K * W + i];
+    const int T = 1 << H;
+    for (int x = threadIdx.x; x < K * T; x += blockDim.x) {
+        const int j = x >> H, i = x & (T - 1);
+        float val = __int_as_float(0x7f800000);  // +inf padding (and unused slot 0)
+        if (i > 0) {
+            const int dpt = 31 - __clz(i);
+            const int sidx = ((2 * (i - (1 << dpt)) + 1) << (H - 1 - dpt)) - 1;
+            if (sidx < W) val = table[static_cast<uint64_t>(sp) * K * W + static_cast<uint64_t>(j) * W + sidx];
+        }
+        se[x] = val;
+    }
     __syncthreads();
     const float* P = proj + static_cast<uint64_t>(sp) * n * K;
     uint8_t* C = codes + static_cast<uint64_t>(sp) * n * K;
+    auto region = [&](const float* e, float v) {
+        uint32_t i = 1;
+        for (int s = 0; s < H; ++s) i = 2 * i + (e[i] < v ? 1u : 0u);
+        int reg = static_cast<int>(i - static_cast<uint32_t>(T)) - 1;  // lower_bound - 1
+        return reg < 0 ? 0 : (reg > NR - 1 ? NR - 1 : reg);
+    };
     for (uint64_t z = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; z < n;
          z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         if (K == 16) {
@@ -302,29 +321,25 @@ __global__ void encode_kernel(const float* __restrict__ proj, uint64_t n, int K,
                 const float4 f = src[q];
                 v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
             }
+            // the 16 searches advance level by level together (16 independent loads in flight)
+            uint32_t idx[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) idx[j] = 1;
+            for (int st = 0; st < H; ++st) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) idx[j] = 2 * idx[j] + (se[j * T + idx[j]] < v[j] ? 1u : 0u);
+            }
             uint32_t packed[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const float* row = srow + j * W;
-                int pos = 0;
-                for (int s = steps; s; s >>= 1)
-                    if (pos + s <= W && row[pos + s - 1] < v[j]) pos += s;
-                int reg = pos - 1;
+                int reg = static_cast<int>(idx[j] - static_cast<uint32_t>(T)) - 1;  // lower_bound - 1
                 reg = reg < 0 ? 0 : (reg > NR - 1 ? NR - 1 : reg);
                 packed[j >> 2] |= static_cast<uint32_t>(reg) << (8 * (j & 3));
             }
             reinterpret_cast<uint4*>(C + z * 16)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
         } else {
-            for (int j = 0; j < K; ++j) {
-                const float v = P[z * K + j];
-                const float* row = srow + j * W;
-                int pos = 0;
-                for (int s = steps; s; s >>= 1)
-                    if (pos + s <= W && row[pos + s - 1] < v) pos += s;
-                int reg = pos - 1;
-                reg = reg < 0 ? 0 : (reg > NR - 1 ? NR - 1 : reg);
-                C[z * K + j] = static_cast<uint8_t>(reg);
-            }
+            for (int j = 0; j < K; ++j)
+                C[z * K + j] = static_cast<uint8_t>(region(se + j * T, P[z * K + j]));
         }
     }
 }
@@ -549,15 +564,17 @@ void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_region
 void launch_encode(const float* d_proj, uint64_t n, int K, int L, const float* d_table,
                    int n_regions, uint8_t* d_codes, cudaStream_t s) {
     if (n == 0) return;
-    int steps = 1;
-    while (steps * 2 <= n_regions + 1) steps *= 2;
-    const size_t smem = static_cast<size_t>(K) * (n_regions + 1) * sizeof(float);
+    int H = 1;  // complete tree of 2^H - 1 >= N_r + 1 nodes
+    while ((1 << H) - 1 < n_regions + 1) ++H;
+    const size_t smem = static_cast<size_t>(K) * (static_cast<size_t>(1) << H) * sizeof(float);
+    DETLSH_CUDA(cudaFuncSetAttribute(encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
     int dev = 0;
     cudaGetDevice(&dev);
     const unsigned gx = static_cast<unsigned>(
         std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8));
     ProfScope ps("encode", s);
-    encode_kernel<<<dim3(gx, L), 256, smem, s>>>(d_proj, n, K, d_table, n_regions, steps, d_codes);
+    encode_kernel<<<dim3(gx, L), 256, smem, s>>>(d_proj, n, K, d_table, n_regions, H, d_codes);
     DETLSH_LAUNCH_CHECK();
 }
 

@@ -161,6 +161,7 @@ constexpr int kEpiWords = kEpiCols / 32;           // candidate words per lane (
 constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr uint32_t kTcRecChunk = 1024;  // records reserved per warp at a time
 constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
+constexpr uint32_t kWaitHintNs = 20000;  // mbarrier try_wait suspend hint (woken on completion)
 
 __device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 4u : 2u; }
 
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                 const int32_t t = qq < a.nq ? a.tau2[qq] : -1;
                 const int32_t qn = qq < a.nq ? a.qn[qq] : 0;
                 sqn[r] = qn;
-                snh[r] = t < 0 ? -0x40000000 : t - qn;  // -2^30: no row can pass
+                snh[r] = t < 0 ? -0x20000000 : t - qn;  // -2^29: no row can pass
             }
             umma::fence_async_smem();
             umma::fence_before_sync();
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             if (lane == 0) {
                 for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
                     const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
-                    umma::mbar_wait(&empty[s], ph ^ 1);
+                    umma::mbar_wait_hint(&empty[s], ph ^ 1, kWaitHintNs);
                     umma::mbar_arrive_expect_tx(&full[s], tile_bytes);
                     umma::bulk_g2s(sA + s * tile_bytes, a.rows + static_cast<uint64_t>(t) * tile_bytes, tile_bytes,
                                    &full[s]);
@@ -277,8 +278,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                 for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
                     const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
                     const uint32_t acc = i & 1, aph = (i >> 1) & 1;
-                    umma::mbar_wait(&tempty[acc], aph ^ 1);
-                    umma::mbar_wait(&full[s], ph);
+                    umma::mbar_wait_hint(&tempty[acc], aph ^ 1, kWaitHintNs);
+                    umma::mbar_wait_hint(&full[s], ph, kWaitHintNs);
                     umma::fence_after_sync();
                     const uint32_t a0 = umma::smem_u32(sA + s * tile_bytes), b0 = umma::smem_u32(sB);
                     for (int k = 0; k < R / 32; ++k) {
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                     w[e] = (qq < a.nq && word < a.W) ? __ldg(a.bm + qq * a.W + word) : 0u;
                 }
             };
+            const int32_t one = 1 + static_cast<int32_t>(a.n >> 62), two = one + one;  // 1, 2 at run time
             uint32_t pw[kEpiWords], nw[kEpiWords];
 #pragma unroll
             for (int e = 0; e < kEpiWords; ++e) nw[e] = 0;
@@ -312,26 +314,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
                 const uint32_t i = it + j, acc = i & 1, aph = (i >> 1) & 1;
                 const uint64_t r = static_cast<uint64_t>(t) * kTcRows + row;
-                const int32_t xn = r < a.n ? __ldg(a.xn + r) : 0x7fffffff;  // padded rows never pass
+                const int32_t xn = r < a.n ? __ldg(a.xn + r) : 0x40000000;  // padded rows never pass
+                const int32_t nxn = -xn;
                 const uint32_t tn = next_tile(trow, t + 1, rt1);
                 if (tn < rt1) load_words(tn, nw);  // next tile's words, in flight during this one
-                umma::mbar_wait(&tfull[acc], aph);
+                umma::mbar_wait_hint(&tfull[acc], aph, kWaitHintNs);
                 umma::fence_after_sync();
                 const uint32_t tbase = tmem + (static_cast<uint32_t>(sub * 32) << 16) + acc * kTcQueries;
                 for (int c0 = cbeg; c0 < cbeg + kEpiCols; c0 += 32) {
                     uint32_t v[32];
                     umma::tmem_ld32(tbase + c0, v);
-                    // threshold mask: bit e <=> 2 q.x + tau^2 - |q|^2 >= |x|^2
-                    uint32_t mask = 0;
+                    // threshold mask: bit e <=> 2 q.x + tau^2 - |q|^2 - |x|^2 >= 0.
+                    // t = (2 v + h) - |x|^2 as two IMADs (FMA pipe: `two`/`one`
+                    // are opaque to the compiler, which would otherwise pick
+                    // ALU adds), its sign bit funnel-shifted into a fail mask
+                    // (one ALU op per element; |t| < 2^31 by the bounds above)
+                    // (four independent 8-column chains keep the shifts off
+                    // each other's latency)
+                    uint32_t fail[4] = {0, 0, 0, 0};
                     const int4* nh4 = reinterpret_cast<const int4*>(snh + c0);
+                    auto step = [&](uint32_t& f, uint32_t vv, int32_t h) {
+                        const int32_t t = static_cast<int32_t>(vv) * two + h;
+                        f = __funnelshift_l(static_cast<uint32_t>(t * one + nxn), f, 1);
+                    };
 #pragma unroll
-                    for (int e4 = 0; e4 < 8; ++e4) {
-                        const int4 h = nh4[e4];
-                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 0]) + h.x >= xn) << (4 * e4 + 0);
-                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 1]) + h.y >= xn) << (4 * e4 + 1);
-                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 2]) + h.z >= xn) << (4 * e4 + 2);
-                        mask |= static_cast<uint32_t>(2 * static_cast<int32_t>(v[4 * e4 + 3]) + h.w >= xn) << (4 * e4 + 3);
+                    for (int e4 = 1; e4 >= 0; --e4) {
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {  // chain g: columns 8g .. 8g+7
+                            const int4 h = nh4[2 * g + e4];
+                            step(fail[g], v[8 * g + 4 * e4 + 3], h.w);
+                            step(fail[g], v[8 * g + 4 * e4 + 2], h.z);
+                            step(fail[g], v[8 * g + 4 * e4 + 1], h.y);
+                            step(fail[g], v[8 * g + 4 * e4 + 0], h.x);
+                        }
                     }
+                    const uint32_t mask = ~(fail[0] | fail[1] << 8 | fail[2] << 16 | fail[3] << 24);
                     // rare: columns where some lane passed.  The chunk's values are
                     // stashed in shared memory so this loop stays small and indexes
                     // them dynamically; candidate (row, query, dist^2) records go to

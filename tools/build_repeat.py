@@ -9,7 +9,8 @@ from paper_2406_10938_b200 import data as gen
 base, _ = gen.make("c2", nq=16)
 dev = torch.from_numpy(base).cuda()
 p = D.LshParams(beta=0.1, k=50)
-modes = sys.argv[1:] or ["gpu", "gpu", "reference", "gpu"]
+keep = "--keep" in sys.argv  # bench.py's pattern: the previous index lives until the next is built
+modes = [m for m in sys.argv[1:] if not m.startswith("--")] or ["gpu", "gpu", "reference", "gpu"]
 out = None
 spikes = []
 for mode in modes:
@@ -17,7 +18,8 @@ for mode in modes:
     for _ in range(5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        out = None  # drop the previous index
+        if not keep:
+            out = None  # drop the previous index
         t1 = time.perf_counter()
         out = D.build_index(dev, p, seed=2, sample=mode, borrow=True, keep_codes=False)
         torch.cuda.synchronize()
