@@ -1742,7 +1742,6 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             const int R = P.row_u8;
             const uint32_t LW = (P.trees_num_leaves0 + 31) / 32;
             const uint64_t W = (P.n + 31) / 32;
-            const uint32_t TW = static_cast<uint32_t>(((P.n + 127) / 128 + 31) / 32);
             // test hook: a smaller staging buffer forces the overflow re-run
             uint32_t tc_cap = kTcFinishCap;
             if (const char* e = std::getenv("DETLSH_TEST_TC_CAP"))
@@ -1756,7 +1755,6 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             grow_scratch(X.tc_flags, chunk * LW);
             grow_scratch(X.tc_cut, chunk * 2);
             grow_scratch(X.tc_bm, chunk * W);
-            grow_scratch(X.tc_tmap, (chunk + 255) / 256 * TW);
             grow_scratch(X.tc_tau2, chunk);
             grow_scratch(X.tc_qn, chunk);
             grow_scratch(X.tc_surv_cnt, chunk);
@@ -1767,7 +1765,6 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             DevBuf<uint32_t>& flags = X.tc_flags;
             DevBuf<uint32_t>& cut = X.tc_cut;
             DevBuf<uint32_t>& bm = X.tc_bm;
-            DevBuf<uint32_t>& tmap = X.tc_tmap;
             DevBuf<int32_t>& tau2 = X.tc_tau2;
             DevBuf<int32_t>& qn = X.tc_qn;
             DevBuf<uint32_t>& surv_cnt = X.tc_surv_cnt;
@@ -1780,7 +1777,6 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);
                 DETLSH_CUDA(cudaMemsetAsync(flags.get(), 0, m * LW * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(bm.get(), 0, m * W * 4, s));
-                DETLSH_CUDA(cudaMemsetAsync(tmap.get(), 0xff, (m + 255) / 256 * TW * 4, s));  // no tile skipping
                 DETLSH_CUDA(cudaMemsetAsync(tau2.get(), 0xff, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(surv_cnt.get(), 0, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + 3, 0, 4, s));
@@ -1811,8 +1807,6 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 a.cap = tc_cap;
                 a.order = Pp.order;
                 a.slot0 = c0;
-                a.tmap = tmap.get();
-                a.TW = TW;
                 a.work = X.counters.get() + 3;
                 a.rec = rec.get();
                 a.rec_cnt = rec_cnt.get();

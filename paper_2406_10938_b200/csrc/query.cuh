@@ -87,7 +87,7 @@ struct QueryScratch {
     // several of these are GB-sized and re-allocating them from the pool per
     // batch costs fresh mappings whenever the pool is fragmented.  Nothing reads
     // them after run_query_batch's last host sync, so the next call may reuse them.
-    DevBuf<uint32_t> tc_flags, tc_cut, tc_bm, tc_tmap, tc_surv_cnt;
+    DevBuf<uint32_t> tc_flags, tc_cut, tc_bm, tc_surv_cnt;
     DevBuf<int32_t> tc_tau2, tc_qn;
     DevBuf<uint8_t> tc_q8;
     DevBuf<uint64_t> tc_surv;
@@ -114,8 +114,6 @@ struct TcScoreArgs {
     // slot s of this batch is query order[slot0 + s] (or slot0 + s)
     const uint32_t* order;
     uint64_t slot0;
-    const uint32_t* tmap;  // [query tiles][TW] occupied 128-row tiles
-    uint32_t TW;
     uint32_t* work;        // unit counter (zeroed by the caller)
     uint4* rec;            // threshold passes {row, slot, dist^2, 0}; row ~0u: padding
     unsigned long long* rec_cnt;  // reserved records (zeroed by the caller)

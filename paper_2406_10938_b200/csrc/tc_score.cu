@@ -165,15 +165,6 @@ constexpr uint32_t kWaitHintNs = 20000;  // mbarrier try_wait suspend hint (woke
 
 __device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 4u : 2u; }
 
-__device__ __forceinline__ uint32_t next_tile(const uint32_t* __restrict__ row, uint32_t t, uint32_t t1) {
-    while (t < t1) {
-        const uint32_t w = __ldg(row + (t >> 5)) >> (t & 31);
-        if (w) return min(t + __ffs(w) - 1, t1);
-        t = (t | 31) + 1;
-    }
-    return t1;
-}
-
 // A warp's next run of kTcRecChunk record slots; the unused tail of the old
 // run becomes padding.  (Called warp-uniformly.)
 __device__ __noinline__ void tc_reserve(uint4* rec, unsigned long long* rec_cnt, uint64_t rec_cap, uint64_t& next,
@@ -232,16 +223,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
         const uint32_t qt = u % n_qt, g = u / n_qt;
         const uint32_t rt0 = static_cast<uint32_t>(static_cast<uint64_t>(n_rt) * g / G);
         const uint32_t rt1 = static_cast<uint32_t>(static_cast<uint64_t>(n_rt) * (g + 1) / G);
-        const uint32_t* trow = a.tmap + static_cast<uint64_t>(qt) * a.TW;
         const uint64_t q0 = static_cast<uint64_t>(qt) * kTcQueries;
-        uint32_t ntiles = 0;  // occupied tiles of the unit (every role walks the same list)
-        for (uint32_t w = rt0 >> 5; w <= (rt1 - 1) >> 5; ++w) {
-            uint32_t x = __ldg(trow + w);
-            if (w == rt0 >> 5) x &= ~0u << (rt0 & 31);
-            if (w == (rt1 - 1) >> 5 && (rt1 & 31)) x &= (1u << (rt1 & 31)) - 1u;
-            ntiles += __popc(x);
-        }
-        if (ntiles == 0) continue;  // nothing to score (uniform)
+        // dense: each query tile's candidates reach nearly every row tile, so
+        // every tile of the range is scored (no per-tile occupancy lookups)
+        const uint32_t ntiles = rt1 - rt0;
+        if (ntiles == 0) continue;  // uniform
         if (qt != loaded_qt) {  // every MMA of the previous unit has completed (epilogue drained it)
             for (int i = tid; i < kTcQueries * kch; i += blockDim.x) {
                 const int kc = i / kTcQueries, r = i % kTcQueries;
@@ -265,7 +251,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
         }
         if (warp == kProducerWarp) {
             if (lane == 0) {
-                for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
+                for (uint32_t t = rt0, j = 0; t < rt1; ++t, ++j) {
                     const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
                     umma::mbar_wait_hint(&empty[s], ph ^ 1, kWaitHintNs);
                     umma::mbar_arrive_expect_tx(&full[s], tile_bytes);
@@ -275,7 +261,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             }
         } else if (warp == kMmaWarp) {
             if (lane == 0) {
-                for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
+                for (uint32_t t = rt0, j = 0; t < rt1; ++t, ++j) {
                     const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
                     const uint32_t acc = i & 1, aph = (i >> 1) & 1;
                     umma::mbar_wait_hint(&tempty[acc], aph ^ 1, kWaitHintNs);
@@ -309,14 +295,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             uint32_t pw[kEpiWords], nw[kEpiWords];
 #pragma unroll
             for (int e = 0; e < kEpiWords; ++e) nw[e] = 0;
-            load_words(next_tile(trow, rt0, rt1), pw);
+            load_words(rt0, pw);
             const uint32_t lt_mask = (1u << lane) - 1u;
-            for (uint32_t t = next_tile(trow, rt0, rt1), j = 0; t < rt1; t = next_tile(trow, t + 1, rt1), ++j) {
+            for (uint32_t t = rt0, j = 0; t < rt1; ++t, ++j) {
                 const uint32_t i = it + j, acc = i & 1, aph = (i >> 1) & 1;
                 const uint64_t r = static_cast<uint64_t>(t) * kTcRows + row;
                 const int32_t xn = r < a.n ? __ldg(a.xn + r) : 0x40000000;  // padded rows never pass
                 const int32_t nxn = -xn;
-                const uint32_t tn = next_tile(trow, t + 1, rt1);
+                const uint32_t tn = t + 1;
                 if (tn < rt1) load_words(tn, nw);  // next tile's words, in flight during this one
                 umma::mbar_wait_hint(&tfull[acc], aph, kWaitHintNs);
                 umma::fence_after_sync();
