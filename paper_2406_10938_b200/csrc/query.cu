@@ -977,7 +977,7 @@ __device__ int32_t kth_dist2(const QueryPlan& P, const FastSlot& F, const Smem& 
     return static_cast<int32_t>((cb << sh) | fb);
 }
 
-__global__ void __launch_bounds__(kQueryThreads, 3) query_fast_kernel(
+__global__ void __launch_bounds__(kQueryThreads, 5) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
@@ -1706,7 +1706,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     if (P.k <= kFastMaxK && !P.rc_mode) {
         int per_sm = 0;
         DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, query_fast_kernel, kQueryThreads, smem));
-        per_sm = std::max(1, std::min(per_sm, 4));
+        per_sm = std::max(1, std::min(per_sm, 6));
         const size_t fast_bytes = fast_slot_bytes(P.max_leaves, P.budget);
         const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
         grow_scratch(X.fast, slots * fast_bytes);
