@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <memory>
+#include <numeric>
 #include <stdexcept>
 #include <thread>
 
@@ -70,8 +72,9 @@ struct PinnedBuf {
     }
 };
 
-float* pinned_scratch(size_t bytes) {
-    thread_local PinnedBuf buf;
+float* pinned_scratch(size_t bytes, int slot = 0) {
+    thread_local PinnedBuf bufs[2];
+    PinnedBuf& buf = bufs[slot];
     if (buf.bytes < bytes) {
         if (buf.p) cudaFreeHost(buf.p);
         buf.p = nullptr;
@@ -245,16 +248,6 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                               4 * static_cast<size_t>(d) + static_cast<size_t>(L) * 64 + 96;
         reserve_mempool(device, n * per_pt, s);
     }
-    if ((flags & DETLSH_F_DEVICE_PTRS) && (flags & DETLSH_F_BORROW_DATA)) {
-        X->data = points;
-    } else {
-        X->data_buf.alloc(n * static_cast<size_t>(d));
-        DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
-                                    (flags & DETLSH_F_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice
-                                                                   : cudaMemcpyHostToDevice,
-                                    s));
-        X->data = X->data_buf.get();
-    }
     if (!paa) {
         X->coeffs.alloc(X->h_coeffs.size());
         DETLSH_CUDA(cudaMemcpyAsync(X->coeffs.get(), X->h_coeffs.data(), X->h_coeffs.size() * 4,
@@ -264,18 +257,122 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     }
     DevBuf<float> proj(static_cast<size_t>(L) * n * K);
     X->sample_size = sample_size_for(p.sample_fraction, n, NR);
+    const uint64_t n_s = X->sample_size;
     X->table.alloc(static_cast<size_t>(L) * K * W);
     X->codes.alloc(static_cast<size_t>(L) * n * K);
     X->trees.resize(L);
     for (auto& t : X->trees) t = std::make_unique<DevTree>();
+    auto project_all = [&]() {
+        if (paa) launch_project_paa(X->data, n, d, K, proj.get(), s);
+        else launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s);
+    };
+    // reference-compatible sample (encoder.cpp:105-143): one RNG stream picks
+    // every space's sample and pivots, so the host replay is sequential
+    std::unique_ptr<RefSampler> sampler_ptr;
+    if (!X->sample_gpu)
+        sampler_ptr = std::make_unique<RefSampler>(n, n_s, NR, mix_seed(seed, kStreamBreakpoints));
+    std::vector<float> h_rows;  // replayed boundary rows [L][K][W]
+    if (!X->sample_gpu) h_rows.assign(static_cast<size_t>(L) * K * W, 0.0f);
+    // Host input in reference mode: space 0's sample positions depend on the
+    // seed alone, so its rows are gathered on the host, uploaded and projected
+    // on their own (a row's projection does not depend on the other rows), and
+    // space 0's replay runs while the full dataset is still being uploaded and
+    // projected by a helper thread.
+    const bool early0 = !X->sample_gpu && !(flags & DETLSH_F_DEVICE_PTRS);
+    DevBuf<float> d_sample0;
+    cudaEvent_t table0 = nullptr;
+    struct EvOne0 {
+        cudaEvent_t& e;
+        ~EvOne0() {
+            if (e) cudaEventDestroy(e);
+        }
+    } table0_guard{table0};
+    if ((flags & DETLSH_F_DEVICE_PTRS) && (flags & DETLSH_F_BORROW_DATA)) {
+        X->data = points;
+        project_all();
+    } else if (!early0) {
+        X->data_buf.alloc(n * static_cast<size_t>(d));
+        DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
+                                    (flags & DETLSH_F_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice
+                                                                   : cudaMemcpyHostToDevice,
+                                    s));
+        X->data = X->data_buf.get();
+        project_all();
+    } else {
+        X->data_buf.alloc(n * static_cast<size_t>(d));
+        X->data = X->data_buf.get();
+        cudaEvent_t coeffs_ready;
+        DETLSH_CUDA(cudaEventCreateWithFlags(&coeffs_ready, cudaEventDisableTiming));
+        DETLSH_CUDA(cudaEventRecord(coeffs_ready, s));
+        cudaStream_t s2 = X->side[L]->s;  // free until the r_min worker starts
+        {
+            StreamScope sc(s2);
+            const auto& idx0 = sampler_ptr->next_space_indices();
+            float* G = pinned_scratch(n_s * static_cast<size_t>(d) * sizeof(float), 1);
+            const int nt = 8;
+            std::vector<std::thread> gth;
+            for (int w = 0; w < nt; ++w)
+                gth.emplace_back([&, w]() {
+                    for (uint64_t t = w; t < n_s; t += nt)
+                        std::memcpy(G + t * d, points + static_cast<uint64_t>(idx0[t]) * d, d * sizeof(float));
+                });
+            for (auto& th : gth) th.join();
+            DevBuf<float> dG(n_s * static_cast<size_t>(d)), dGp(static_cast<size_t>(L) * n_s * K);
+            DevBuf<uint32_t> iota(n_s);
+            std::vector<uint32_t> h_iota(n_s);
+            std::iota(h_iota.begin(), h_iota.end(), 0u);
+            DETLSH_CUDA(cudaMemcpyAsync(dG.get(), G, n_s * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s2));
+            DETLSH_CUDA(cudaMemcpyAsync(iota.get(), h_iota.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
+            DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
+            if (paa) launch_project_paa(dG.get(), n_s, d, K, dGp.get(), s2);
+            else launch_project_exact(dG.get(), n_s, d, X->coeffs_t.get(), K, L, dGp.get(), s2);
+            d_sample0.alloc(static_cast<size_t>(K) * n_s);
+            launch_gather_sample(dGp.get(), iota.get(), n_s, K, d_sample0.get(), s2);
+            float* h_sample = pinned_scratch(static_cast<size_t>(K) * n_s * sizeof(float));
+            DETLSH_CUDA(cudaMemcpyAsync(h_sample, d_sample0.get(), static_cast<size_t>(K) * n_s * 4,
+                                        cudaMemcpyDeviceToHost, s2));
+            cudaEvent_t copied0;
+            DETLSH_CUDA(cudaEventCreateWithFlags(&copied0, cudaEventDisableTiming));
+            DETLSH_CUDA(cudaEventRecord(copied0, s2));
+            gpu_order_stat_table(d_sample0.get(), K, n_s, NR, X->table.get(), s2, /*sync=*/false);
+            DETLSH_CUDA(cudaEventCreateWithFlags(&table0, cudaEventDisableTiming));
+            DETLSH_CUDA(cudaEventRecord(table0, s2));
+            // helper: full upload (blocks for pageable sources) + full projection on s,
+            // issued after the sample rows so their copy is not queued behind it
+            std::exception_ptr up_err;
+            std::thread uploader([&]() {
+                try {
+                    DETLSH_CUDA(cudaSetDevice(device));
+                    StreamScope sc(s);
+                    DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
+                                                cudaMemcpyHostToDevice, s));
+                    project_all();
+                } catch (...) {
+                    up_err = std::current_exception();
+                }
+            });
+            struct Joiner {
+                std::thread& t;
+                ~Joiner() {
+                    if (t.joinable()) t.join();
+                }
+            } joiner{uploader};
+            DETLSH_CUDA(cudaEventSynchronize(copied0));
+            cudaEventDestroy(copied0);
+            X->timings.emplace_back("bp_space0_sample", ms_since(t0));
+            const auto tr = Clock::now();
+            if (L > 1)
+                for (int j = 0; j < K; ++j)
+                    sampler_ptr->select_row(h_sample + static_cast<size_t>(j) * n_s, h_rows.data() + j * W);
+            X->timings.emplace_back("bp_space0_replay", ms_since(tr));
+            uploader.join();
+            if (up_err) std::rethrow_exception(up_err);
+        }
+        cudaEventDestroy(coeffs_ready);
+        DETLSH_CUDA(cudaStreamWaitEvent(s, table0, 0));  // space 0's boundaries before its encode
+    }
     DETLSH_CUDA(cudaStreamSynchronize(s));
-    X->timings.emplace_back("upload", ms_since(t0));
-    // exact projection
-    t0 = Clock::now();
-    if (paa) launch_project_paa(X->data, n, d, K, proj.get(), s);
-    else launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s);
-    DETLSH_CUDA(cudaStreamSynchronize(s));
-    X->timings.emplace_back("project", ms_since(t0));
+    X->timings.emplace_back("upload_project", ms_since(t0));
 
     // exact u8 verification rows (integral datasets): decided now, packed in
     // tree-0 leaf order by the space-0 worker right after tree 0 (query.cu)
@@ -356,12 +453,11 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         // while the GPU encodes and builds, space L-1 not at all.  The one
         // value an order statistic leaves open is the sign of a zero
         // boundary (-0 == +0); those rows take the replayed value.
-        const uint64_t n_s = X->sample_size;
-        RefSampler sampler(n, n_s, NR, mix_seed(seed, kStreamBreakpoints));
+        // (host input: space 0 was sampled, sorted and replayed during the upload)
+        RefSampler& sampler = *sampler_ptr;
         DevBuf<uint32_t> d_idx(n_s);
         DevBuf<float> d_sample(static_cast<size_t>(K) * n_s);
         float* h_sample = pinned_scratch(static_cast<size_t>(K) * n_s * sizeof(float));
-        std::vector<float> h_rows(static_cast<size_t>(L) * K * W, 0.0f);  // replayed rows
         cudaEvent_t copied;
         DETLSH_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
         struct EvOne {
@@ -376,6 +472,10 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         double t_idx = 0.0, t_wait = 0.0, t_replay = 0.0;
         const auto t_loop = Clock::now();
         for (int i = 0; i < L; ++i) {
+            if (i == 0 && early0) {
+                launch_space(0);  // s already waits for space 0's table
+                continue;
+            }
             auto tq = Clock::now();
             const auto& idx = sampler.next_space_indices();
             t_idx += ms_since(tq);
@@ -415,7 +515,8 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             for (int b = 0; b < W; ++b)
                 if (X->h_table[base + static_cast<size_t>(j) * W + b] == 0.0f) last_zero = j;
         if (last_zero >= 0) {
-            DETLSH_CUDA(cudaMemcpyAsync(h_sample, d_sample.get(), static_cast<size_t>(K) * n_s * 4,
+            const float* last_sample = (early0 && L == 1) ? d_sample0.get() : d_sample.get();
+            DETLSH_CUDA(cudaMemcpyAsync(h_sample, last_sample, static_cast<size_t>(K) * n_s * 4,
                                         cudaMemcpyDeviceToHost, s));
             DETLSH_CUDA(cudaStreamSynchronize(s));
             replay_space(L - 1, last_zero + 1);
