@@ -456,7 +456,7 @@ size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
     if (a[hi - 1] < a[mid]) std::swap(a[mid], a[hi - 1]);
     std::swap(a[mid], a[lo + 1]);
     const float pv = a[lo + 1];
-    const size_t j = len < 32        ? hoare_scan_simple(a, lo, hi, pv)
+    const size_t j = len < 12        ? hoare_scan_simple(a, lo, hi, pv)  // (measured crossover)
                      : have_avx512() ? hoare_scan_avx512(a, lo, hi, pv)
                      : have_avx2()   ? hoare_scan_avx2(a, lo, hi, pv)
                                      : hoare_scan_blocked(a, lo, hi, pv);
