@@ -73,7 +73,7 @@ struct PinnedBuf {
 };
 
 float* pinned_scratch(size_t bytes, int slot = 0) {
-    thread_local PinnedBuf bufs[2];
+    thread_local PinnedBuf bufs[4];  // 0: build samples, 1: sample rows, 2: query results, 3: query upload
     PinnedBuf& buf = bufs[slot];
     if (buf.bytes < bytes) {
         if (buf.p) cudaFreeHost(buf.p);
@@ -590,8 +590,19 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     DevBuf<float> dq;
     const float* q = queries;
     if (!dev) {
+        const size_t qbytes = nq * static_cast<size_t>(d) * 4;
         dq.alloc(nq * static_cast<size_t>(d));
-        DETLSH_CUDA(cudaMemcpyAsync(dq.get(), queries, nq * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s));
+        cudaPointerAttributes at{};
+        const bool pageable = cudaPointerGetAttributes(&at, queries) != cudaSuccess ||
+                              at.type == cudaMemoryTypeUnregistered;
+        cudaGetLastError();
+        const void* src = queries;
+        if (pageable) {  // staged through pinned memory (see the result copies below)
+            float* stage = pinned_scratch(qbytes, 3);
+            std::memcpy(stage, queries, qbytes);
+            src = stage;
+        }
+        DETLSH_CUDA(cudaMemcpyAsync(dq.get(), src, qbytes, cudaMemcpyHostToDevice, s));
         q = dq.get();
     }
     DevBuf<float> qproj(static_cast<size_t>(L) * nq * K);
@@ -648,11 +659,42 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     }
     run_query_batch(P, X.scratch, X.device, s, X.main.s);
     if (!dev) {
-        if (ids) DETLSH_CUDA(cudaMemcpyAsync(ids, P.ids, nq * k * 4, cudaMemcpyDeviceToHost, s));
-        if (dists) DETLSH_CUDA(cudaMemcpyAsync(dists, P.dists, nq * k * 8, cudaMemcpyDeviceToHost, s));
-        if (n_hits) DETLSH_CUDA(cudaMemcpyAsync(n_hits, P.n_hits, nq * 4, cudaMemcpyDeviceToHost, s));
-        if (radius) DETLSH_CUDA(cudaMemcpyAsync(radius, P.radius, nq * 8, cudaMemcpyDeviceToHost, s));
-        if (cands) DETLSH_CUDA(cudaMemcpyAsync(cands, P.cands, nq * 8, cudaMemcpyDeviceToHost, s));
+        // results to host: pageable destinations go through one pinned staging
+        // buffer (a pageable D2H is staged by the driver at a fraction of the
+        // link rate), then a host copy; pinned destinations are copied directly
+        struct Out {
+            void* dst;
+            const void* src;
+            size_t bytes;
+        };
+        const Out outs[5] = {{ids, P.ids, nq * k * 4}, {dists, P.dists, nq * k * 8}, {n_hits, P.n_hits, nq * 4},
+                             {radius, P.radius, nq * 8}, {cands, P.cands, nq * 8}};
+        auto pageable = [](const void* ptr) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+                cudaGetLastError();
+                return true;
+            }
+            return at.type == cudaMemoryTypeUnregistered;
+        };
+        size_t staged = 0;
+        for (const Out& o : outs)
+            if (o.dst && pageable(o.dst)) staged += (o.bytes + 255) / 256 * 256;
+        uint8_t* stage = staged ? reinterpret_cast<uint8_t*>(pinned_scratch(staged, 2)) : nullptr;
+        size_t off = 0;
+        std::vector<std::pair<const Out*, size_t>> copies;
+        for (const Out& o : outs) {
+            if (!o.dst) continue;
+            if (pageable(o.dst)) {
+                DETLSH_CUDA(cudaMemcpyAsync(stage + off, o.src, o.bytes, cudaMemcpyDeviceToHost, s));
+                copies.emplace_back(&o, off);
+                off += (o.bytes + 255) / 256 * 256;
+            } else {
+                DETLSH_CUDA(cudaMemcpyAsync(o.dst, o.src, o.bytes, cudaMemcpyDeviceToHost, s));
+            }
+        }
+        DETLSH_CUDA(cudaStreamSynchronize(s));
+        for (const auto& c : copies) std::memcpy(c.first->dst, stage + c.second, c.first->bytes);
     }
     DETLSH_CUDA(cudaStreamSynchronize(s));
 }
