@@ -278,7 +278,8 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     // on their own (a row's projection does not depend on the other rows), and
     // space 0's replay runs while the full dataset is still being uploaded and
     // projected by a helper thread.
-    const bool early0 = !X->sample_gpu && !(flags & DETLSH_F_DEVICE_PTRS);
+    const bool dev_in = (flags & DETLSH_F_DEVICE_PTRS) != 0;
+    const bool early0 = !X->sample_gpu;
     DevBuf<float> d_sample0;
     cudaEvent_t table0 = nullptr;
     struct EvOne0 {
@@ -287,7 +288,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             if (e) cudaEventDestroy(e);
         }
     } table0_guard{table0};
-    if ((flags & DETLSH_F_DEVICE_PTRS) && (flags & DETLSH_F_BORROW_DATA)) {
+    if (!early0 && dev_in && (flags & DETLSH_F_BORROW_DATA)) {
         X->data = points;
         project_all();
     } else if (!early0) {
@@ -299,29 +300,46 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         X->data = X->data_buf.get();
         project_all();
     } else {
-        X->data_buf.alloc(n * static_cast<size_t>(d));
-        X->data = X->data_buf.get();
+        // device input: the dataset is (copied) on the device and projected on s
+        // at once; space 0's sample rows are gathered by a kernel on s2
+        if (dev_in && (flags & DETLSH_F_BORROW_DATA)) {
+            X->data = points;
+        } else {
+            X->data_buf.alloc(n * static_cast<size_t>(d));
+            X->data = X->data_buf.get();
+            if (dev_in)
+                DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
+                                            cudaMemcpyDeviceToDevice, s));
+        }
         cudaEvent_t coeffs_ready;
         DETLSH_CUDA(cudaEventCreateWithFlags(&coeffs_ready, cudaEventDisableTiming));
-        DETLSH_CUDA(cudaEventRecord(coeffs_ready, s));
+        DETLSH_CUDA(cudaEventRecord(coeffs_ready, s));  // (device input: the dataset copy too)
+        if (dev_in) project_all();
         cudaStream_t s2 = X->side[L]->s;  // free until the r_min worker starts
         {
             StreamScope sc(s2);
             const auto& idx0 = sampler_ptr->next_space_indices();
-            float* G = pinned_scratch(n_s * static_cast<size_t>(d) * sizeof(float), 1);
-            const int nt = 8;
-            std::vector<std::thread> gth;
-            for (int w = 0; w < nt; ++w)
-                gth.emplace_back([&, w]() {
-                    for (uint64_t t = w; t < n_s; t += nt)
-                        std::memcpy(G + t * d, points + static_cast<uint64_t>(idx0[t]) * d, d * sizeof(float));
-                });
-            for (auto& th : gth) th.join();
             DevBuf<float> dG(n_s * static_cast<size_t>(d)), dGp(static_cast<size_t>(L) * n_s * K);
             DevBuf<uint32_t> iota(n_s);
             std::vector<uint32_t> h_iota(n_s);
             std::iota(h_iota.begin(), h_iota.end(), 0u);
-            DETLSH_CUDA(cudaMemcpyAsync(dG.get(), G, n_s * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s2));
+            if (dev_in) {
+                DevBuf<uint32_t> d_idx0(n_s);
+                DETLSH_CUDA(cudaMemcpyAsync(d_idx0.get(), idx0.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
+                DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
+                launch_pack_f32(X->data, d_idx0.get(), n_s, d, dG.get(), s2);  // rows idx0[t]
+            } else {
+                float* G = pinned_scratch(n_s * static_cast<size_t>(d) * sizeof(float), 1);
+                const int nt = 8;
+                std::vector<std::thread> gth;
+                for (int w = 0; w < nt; ++w)
+                    gth.emplace_back([&, w]() {
+                        for (uint64_t t = w; t < n_s; t += nt)
+                            std::memcpy(G + t * d, points + static_cast<uint64_t>(idx0[t]) * d, d * sizeof(float));
+                    });
+                for (auto& th : gth) th.join();
+                DETLSH_CUDA(cudaMemcpyAsync(dG.get(), G, n_s * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s2));
+            }
             DETLSH_CUDA(cudaMemcpyAsync(iota.get(), h_iota.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
             DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
             if (paa) launch_project_paa(dG.get(), n_s, d, K, dGp.get(), s2);
@@ -341,6 +359,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             // issued after the sample rows so their copy is not queued behind it
             std::exception_ptr up_err;
             std::thread uploader([&]() {
+                if (dev_in) return;  // already projecting on s
                 try {
                     DETLSH_CUDA(cudaSetDevice(device));
                     StreamScope sc(s);

@@ -162,6 +162,22 @@ def test_reference_sample_with_zero_boundaries(gpu, port, L):
         assert_tree_equal(idx.tree(i), oi.tree_export(i), f"tree {i}")
 
 
+@pytest.mark.parametrize("borrow", [True, False])
+def test_device_input_build_equals_host_input_build(gpu, borrow):
+    """Reference-sample builds from a CUDA tensor (space 0's sample rows gathered
+    on the device) and from host memory (gathered on the host, uploaded ahead of
+    the dataset) give the same index."""
+    import torch
+    data = gaussian(6000, 48, 17, 2.0)
+    c = dict(K=16, L=3, n_regions=256, leaf_capacity=64, sample_fraction=0.2, beta=0.1, k=10)
+    a = gpu.build_index(data, _params(**c), seed=21)
+    b = gpu.build_index(torch.from_numpy(data).cuda(), _params(**c), seed=21, borrow=borrow)
+    assert bits_equal(a.table(), b.table())
+    assert a.params.r_min == b.params.r_min
+    for i in range(3):
+        assert_tree_equal(a.tree(i), b.tree(i), f"tree {i}")
+
+
 def test_exhaustive_budget_is_brute_force_with_ties(gpu, port):
     """beta = 1 (test_query.cpp:342-396): the pipeline reduces to exact kNN incl. tie order."""
     g = np.random.Generator(np.random.PCG64(401))
