@@ -163,7 +163,7 @@ constexpr uint32_t kTcRecChunk = 1024;  // records reserved per warp at a time
 constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
 constexpr uint32_t kWaitHintNs = 20000;  // mbarrier try_wait suspend hint (woken on completion)
 
-__device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 4u : 2u; }
+__device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 3u : 2u; }
 
 // A warp's next run of kTcRecChunk record slots; the unused tail of the old
 // run becomes padding.  (Called warp-uniformly.)
@@ -180,7 +180,7 @@ __device__ __noinline__ void tc_reserve(uint4* rec, unsigned long long* rec_cnt,
 __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, uint32_t n_rt, uint32_t n_qt,
                                                                  uint32_t G) {
     extern __shared__ __align__(1024) uint8_t sm[];
-    __shared__ __align__(8) uint64_t full[4], empty[4], tfull[2], tempty[2];
+    __shared__ __align__(8) uint64_t full[6], empty[6], tfull[2], tempty[2];
     __shared__ uint32_t tslot, unit_s;
     const int R = a.R, kch = R / 16;
     const uint32_t stages = tc_stages(R);
@@ -313,6 +313,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                     const int c0 = cbeg + 32 * k;
                     uint32_t v[32];
                     umma::tmem_ld32(tbase + c0, v);
+                    if (k == kEpiWords - 1) {  // this warp's last TMEM read of the tile: release the
+                        umma::fence_before_sync();  // accumulator before testing (the MMA two tiles
+                        __syncwarp();               // ahead can start while the values are in registers)
+                        if (lane == 0) umma::mbar_arrive(&tempty[acc]);
+                    }
                     // threshold mask: bit e <=> 2 q.x + tau^2 - |q|^2 - |x|^2 >= 0.
                     // t = (2 v + h) - |x|^2 as two IMADs (FMA pipe: `two`/`one`
                     // are opaque to the compiler, which would otherwise pick
@@ -370,9 +375,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                         __syncwarp();
                     }
                 }
-                umma::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) umma::mbar_arrive(&tempty[acc]);
 #pragma unroll
                 for (int e = 0; e < kEpiWords; ++e) pw[e] = nw[e];
             }
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(256) tc_finish_kernel(TcScoreArgs a, const uin
 }  // namespace
 
 size_t tc_score_smem(int R) {
-    const size_t need = static_cast<size_t>(kTcQueries + (R <= 128 ? 4 : 2) * kTcRows) * R + 2 * kTcQueries * 4 +
+    const size_t need = static_cast<size_t>(kTcQueries + (R <= 128 ? 3 : 2) * kTcRows) * R + 2 * kTcQueries * 4 +
                         kEpiWarps * 32 * kTcStash * 4 + 1024;
     return std::max<size_t>(need, 120 * 1024);  // one CTA per SM: it owns all 512 TMEM columns
 }
