@@ -162,6 +162,7 @@ constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr uint32_t kTcRecChunk = 1024;  // records reserved per warp at a time
 constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
 constexpr uint32_t kWaitHintNs = 20000;  // mbarrier try_wait suspend hint (woken on completion)
+constexpr int kQSplit = 2;               // MMAs (and accumulator barriers) per tile, one per query part (4: slower)
 
 __device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 3u : 2u; }
 
@@ -180,7 +181,10 @@ __device__ __noinline__ void tc_reserve(uint4* rec, unsigned long long* rec_cnt,
 __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, uint32_t n_rt, uint32_t n_qt,
                                                                  uint32_t G) {
     extern __shared__ __align__(1024) uint8_t sm[];
-    __shared__ __align__(8) uint64_t full[6], empty[6], tfull[2], tempty[2];
+    // tfull/tempty per (accumulator, query part): the kQSplit query parts of a
+    // tile are separate MMAs, so the epilogue warps of one part never wait for
+    // another part's stragglers
+    __shared__ __align__(8) uint64_t full[6], empty[6], tfull[2][kQSplit], tempty[2][kQSplit];
     __shared__ uint32_t tslot, unit_s;
     const int R = a.R, kch = R / 16;
     const uint32_t stages = tc_stages(R);
@@ -197,8 +201,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             umma::mbar_init(&empty[s], 1);
         }
         for (int s = 0; s < 2; ++s) {
-            umma::mbar_init(&tfull[s], 1);
-            umma::mbar_init(&tempty[s], kEpiWarps);
+            for (int h = 0; h < kQSplit; ++h) {
+                umma::mbar_init(&tfull[s][h], 1);
+                umma::mbar_init(&tempty[s][h], kEpiWarps / kQSplit);
+            }
         }
         umma::fence_mbar_init();
     }
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tmem = tslot;
-    const uint32_t idesc = umma::idesc_u8_s32(kTcRows, kTcQueries);
+    const uint32_t idesc = umma::idesc_u8_s32(kTcRows, kTcQueries / kQSplit);  // one query part per MMA
     const uint32_t units = n_qt * G;
     uint32_t it = 0;  // tiles processed by this CTA so far (pipeline phases)
     uint32_t loaded_qt = 0xffffffffu;
@@ -264,21 +270,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                 for (uint32_t t = rt0, j = 0; t < rt1; ++t, ++j) {
                     const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
                     const uint32_t acc = i & 1, aph = (i >> 1) & 1;
-                    umma::mbar_wait_hint(&tempty[acc], aph ^ 1, kWaitHintNs);
                     umma::mbar_wait_hint(&full[s], ph, kWaitHintNs);
-                    umma::fence_after_sync();
                     const uint32_t a0 = umma::smem_u32(sA + s * tile_bytes), b0 = umma::smem_u32(sB);
-                    for (int k = 0; k < R / 32; ++k) {
-                        const uint64_t da = umma::smem_desc(a0 + 2 * k * kTcRows * 16, kTcRows * 16, 128);
-                        const uint64_t db = umma::smem_desc(b0 + 2 * k * kTcQueries * 16, kTcQueries * 16, 128);
-                        umma::mma_u8(tmem + acc * kTcQueries, da, db, idesc, k > 0 ? 1u : 0u);
+                    for (int h = 0; h < kQSplit; ++h) {
+                        umma::mbar_wait_hint(&tempty[acc][h], aph ^ 1, kWaitHintNs);
+                        umma::fence_after_sync();
+                        // part h's queries start (256 / kQSplit) / 8 eight-row groups in (K-major core layout)
+                        constexpr int kQP = kTcQueries / kQSplit;
+                        for (int k = 0; k < R / 32; ++k) {
+                            const uint64_t da = umma::smem_desc(a0 + 2 * k * kTcRows * 16, kTcRows * 16, 128);
+                            const uint64_t db = umma::smem_desc(b0 + 2 * k * kTcQueries * 16 + h * kQP * 16,
+                                                                kTcQueries * 16, 128);
+                            umma::mma_u8(tmem + acc * kTcQueries + h * kQP, da, db, idesc, k > 0 ? 1u : 0u);
+                        }
+                        umma::commit(&tfull[acc][h]);
                     }
                     umma::commit(&empty[s]);
-                    umma::commit(&tfull[acc]);
                 }
             }
         } else {
             const int sub = warp & 3, part = warp >> 2;
+            const int half = part * kQSplit / (kEpiWarps / 4);  // this warp's MMA query part
             const int row = sub * 32 + lane;
             const int cbeg = part * kEpiCols;  // this warp's query columns [cbeg, cbeg + kEpiCols)
             // candidate words of this warp's 32 rows for its query columns (lane l
@@ -305,7 +317,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                 const int32_t nxn = -xn;
                 const uint32_t tn = t + 1;
                 if (tn < rt1) load_words(tn, nw);  // next tile's words, in flight during this one
-                umma::mbar_wait_hint(&tfull[acc], aph, kWaitHintNs);
+                umma::mbar_wait_hint(&tfull[acc][half], aph, kWaitHintNs);
                 umma::fence_after_sync();
                 const uint32_t tbase = tmem + (static_cast<uint32_t>(sub * 32) << 16) + acc * kTcQueries;
 #pragma unroll
@@ -316,7 +328,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
                     if (k == kEpiWords - 1) {  // this warp's last TMEM read of the tile: release the
                         umma::fence_before_sync();  // accumulator before testing (the MMA two tiles
                         __syncwarp();               // ahead can start while the values are in registers)
-                        if (lane == 0) umma::mbar_arrive(&tempty[acc]);
+                        if (lane == 0) umma::mbar_arrive(&tempty[acc][half]);
                     }
                     // threshold mask: bit e <=> 2 q.x + tau^2 - |q|^2 - |x|^2 >= 0.
                     // t = (2 v + h) - |x|^2 as two IMADs (FMA pipe: `two`/`one`
