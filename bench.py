@@ -548,8 +548,10 @@ def main():
 
     budget = D.candidate_budget(idx.params.beta, n_loc, k)
     hbm, peak_kind = peaks()
+    # candidates are single kernels: `rmin_select` and the `tree_*` scopes time
+    # loops of small kernels with host reads between them, not one kernel
     build_roof = roofline(prof_build, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
-                          exclude=("query_fast", "query_slow"))
+                          only=("project_exact", "encode", "rmin_dist", "pack_u8", "gather_sample"))
     proj = prof_build.get("project_exact")
     build_roof_proj = None
     if proj:
