@@ -1773,10 +1773,25 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             DevBuf<uint4>& rec = X.tc_rec;
             DevBuf<unsigned long long>& rec_cnt = X.tc_rec_cnt;
             over_list.alloc(P.nq);
+            // the row bitmaps (n/8 bytes per query) are zeroed on the index's own
+            // stream while the plan kernel runs; tc_expand waits for it
+            cudaEvent_t ev_prev, ev_bm;
+            DETLSH_CUDA(cudaEventCreateWithFlags(&ev_prev, cudaEventDisableTiming));
+            DETLSH_CUDA(cudaEventCreateWithFlags(&ev_bm, cudaEventDisableTiming));
+            struct EvPair {
+                cudaEvent_t a, b;
+                ~EvPair() {
+                    cudaEventDestroy(a);
+                    cudaEventDestroy(b);
+                }
+            } ev_guard{ev_prev, ev_bm};
             for (uint64_t c0 = 0; c0 < P.nq; c0 += chunk) {
                 const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);
+                DETLSH_CUDA(cudaEventRecord(ev_prev, s));  // after the previous chunk's reads of bm
+                DETLSH_CUDA(cudaStreamWaitEvent(alloc_s, ev_prev, 0));
+                DETLSH_CUDA(cudaMemsetAsync(bm.get(), 0, m * W * 4, alloc_s));
+                DETLSH_CUDA(cudaEventRecord(ev_bm, alloc_s));
                 DETLSH_CUDA(cudaMemsetAsync(flags.get(), 0, m * LW * 4, s));
-                DETLSH_CUDA(cudaMemsetAsync(bm.get(), 0, m * W * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(tau2.get(), 0xff, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(surv_cnt.get(), 0, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + 3, 0, 4, s));
@@ -1788,6 +1803,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 Pc.tc_cut = cut.get();
                 Pc.tc_tau2 = tau2.get();
                 launch_fast(Pc);
+                DETLSH_CUDA(cudaStreamWaitEvent(s, ev_bm, 0));
                 launch_tc_expand(flags.get(), LW, cut.get(), tau2.get(), m, P.trees_leaf_begin0, P.trees_leaf_count0,
                                  P.trees_num_leaves0, bm.get(), W, s);
                 launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, q8.get(), qn.get(), s);
