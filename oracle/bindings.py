@@ -114,6 +114,9 @@ class Oracle:
             fn = self.f(name)
             if s is not None:
                 fn.argtypes, fn.restype = s
+        # handles are pointers: the default int restype would truncate them
+        self.f("build_index").restype = vp
+        self.f("build_index_with_table").restype = vp
         if self.kind == "port":
             self.f("select_breakpoints").argtypes = [vp, u64, i32, i32, i32, dbl, u64, vp, vp, vp, vp]
             self.f("range_query_optimized").argtypes = [vp, vp, vp, dbl, u64, vp]

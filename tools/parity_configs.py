@@ -17,6 +17,7 @@ from oracle.bindings import Oracle, make_params, ref_available  # noqa: E402
 CASES = [
     ("c1", 100_000, 1000, 1000),   # full config 1, all queries checked
     ("c2", 200_000, 200, 200),
+    ("c2", 1_000_000, 2000, 300),  # full C2 index: tensor-core verification path
     ("c3", 100_000, 100, 100),
     ("c4", 1_000_000, 100, 50),
 ]
