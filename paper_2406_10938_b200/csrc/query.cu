@@ -225,45 +225,6 @@ __device__ void build_half_tables(const QueryPlan& P, const Smem& S) {
     __syncthreads();
 }
 
-// Exact mindist of tree-0 leaf li straight from the breakpoint table (no fp64
-// table in smem): the same operations in the same order as leaf_mindist.
-__device__ __forceinline__ double leaf_mindist_direct(const QueryPlan& P, const QTree& T, uint32_t li,
-                                                      const Smem& S) {
-    const uint4* box = reinterpret_cast<const uint4*>(T.leaf_box + static_cast<size_t>(li) * 64);
-    uint32_t w[12];
-    {
-        const uint4 a = __ldg(box), b = __ldg(box + 1);
-        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-        if (P.K > 16) {
-            const uint4 c = __ldg(box + 2);
-            w[8] = c.x; w[9] = c.y; w[10] = c.z; w[11] = c.w;
-        } else {
-            w[8] = w[9] = w[10] = w[11] = 0;
-        }
-    }
-    const int W = P.NR + 1;
-    double acc = 0.0;
-#pragma unroll
-    for (int j = 0; j < kMaxK; ++j) {
-        if (j < P.K) {
-            const uint32_t half = w[j >> 1] >> ((j & 1) * 16);
-            const int lo = half & 0xff, hi = (half >> 8) & 0xff;
-            int e = -1;
-            if (lo > 0 && lo >= S.ubv[j]) e = lo;
-            else if (hi < P.NR - 1 && hi + 1 < S.lbv[j]) e = hi + 1;
-            double pen_sq = 0.0;
-            if (e >= 0) {
-                const double D = __dsub_rn(static_cast<double>(__ldg(P.table + j * W + e)),
-                                           static_cast<double>(S.qp[j]));
-                pen_sq = __dmul_rn(D, D);
-            }
-            acc = __dadd_rn(acc, pen_sq);
-        }
-    }
-    return __dsqrt_rn(acc);
-}
-
 __device__ __forceinline__ double leaf_mindist(const QueryPlan& P, const QTree& T, uint32_t li,
                                                const Smem& S) {
     // box: per dim j, bytes (lo region, hi region) at 2j, 2j+1; kept in
@@ -297,48 +258,12 @@ __device__ __forceinline__ double leaf_mindist(const QueryPlan& P, const QTree& 
     return __dsqrt_rn(acc);
 }
 
-// Branchless, two-leaf-interleaved mindist for K <= 16 (the fast path's hot
-// loop): per dim the penalty index is selected without branches (both edge
-// candidates are valid table indices), the per-query thresholds live in
-// registers (lub[j] = lbv | ubv << 16), and two independent fp64 chains give
-// ILP.  Same operations in the same order as leaf_mindist.
+// A leaf's 64-byte (lo, hi) region box as eight words.
 __device__ __forceinline__ void box_words(const QTree& T, uint32_t li, uint32_t (&w)[8]) {
     const uint4* box = reinterpret_cast<const uint4*>(T.leaf_box + static_cast<size_t>(li) * 64);
     const uint4 a = __ldg(box), b = __ldg(box + 1);
     w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
     w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-}
-
-__device__ __forceinline__ double pen_sq16(const double* __restrict__ sqj, uint32_t half, uint32_t lub,
-                                           int NR) {
-    const int lo = half & 0xff, hi = (half >> 8) & 0xff;
-    const int lbv = lub & 0xffff, ubv = lub >> 16;
-    const bool use_lo = lo > 0 && lo >= ubv;
-    const bool use_hi = hi < NR - 1 && hi + 1 < lbv;
-    const double v = sqj[use_lo ? lo : hi + 1];
-    return (use_lo || use_hi) ? v : 0.0;
-}
-
-__device__ __forceinline__ void leaf_mindist2_k16(const QueryPlan& P, const QTree& T, uint32_t li0,
-                                                  uint32_t li1, const Smem& S, const uint32_t (&lub)[16],
-                                                  double& md0, double& md1) {
-    uint32_t w0[8], w1[8];
-    box_words(T, li0, w0);
-    box_words(T, li1, w1);
-    const int W = P.NR + 1;
-    double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        if (j < P.K) {
-            const double* sqj = S.sq + j * W;
-            const uint32_t h0 = w0[j >> 1] >> ((j & 1) * 16);
-            const uint32_t h1 = w1[j >> 1] >> ((j & 1) * 16);
-            a0 = __dadd_rn(a0, pen_sq16(sqj, h0, lub[j], P.NR));
-            a1 = __dadd_rn(a1, pen_sq16(sqj, h1, lub[j], P.NR));
-        }
-    }
-    md0 = __dsqrt_rn(a0);
-    md1 = __dsqrt_rn(a1);
 }
 
 // Exact round: histogram bin of an exact mindist (0xffff: outside the radius).

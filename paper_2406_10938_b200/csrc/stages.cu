@@ -22,92 +22,10 @@ __global__ void coeffs_t_kernel(const float* __restrict__ c, int LK, int d, int 
     }
 }
 
-// ---------------------------------------------------------------------------
-// Exact projection.  CTA = 256 threads = 64 point-lanes x 4 output groups;
-// each thread owns 2 points (p, p+64) x 16 outputs -> 32 fp64 accumulators.
-// Dims are streamed in chunks of 32 through shared memory: the point chunk as
-// fp32 (padded rows, conflict-free), the coefficient chunk pre-widened to
-// fp64 and read as warp-wide broadcasts.  The accumulation order is t = 0..d-1
-// for every output, exactly as project_point_into (projection.cpp:31-37).
-// ---------------------------------------------------------------------------
 constexpr int kPT = 128;  // points per tile
 constexpr int kDC = 32;   // dims per chunk
-constexpr int kJB = 16;   // outputs per thread
 
-__global__ void __launch_bounds__(256) project_exact_kernel(
-    const float* __restrict__ pts, uint64_t n, int d, const double* __restrict__ ct, int LK,
-    int LKp, int K, float* __restrict__ out) {
-    __shared__ float sx[kPT][kDC + 1];
-    __shared__ __align__(16) double sa[kDC][64];
-    const int tid = threadIdx.x;
-    const int p = tid & 63, g = tid >> 6;
-    const uint64_t tiles = (n + kPT - 1) / kPT;
-    for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const uint64_t z0 = tile * kPT;
-        for (int jp = 0; jp < LKp; jp += 64) {
-            double acc0[kJB], acc1[kJB];
-#pragma unroll
-            for (int j = 0; j < kJB; ++j) acc0[j] = acc1[j] = 0.0;
-            for (int t0 = 0; t0 < d; t0 += kDC) {
-                __syncthreads();
-                // points: kPT x kDC floats, coalesced along t
-                for (int i = tid; i < kPT * kDC; i += 256) {
-                    const int pp = i / kDC, c = i % kDC;
-                    const uint64_t z = z0 + pp;
-                    const int t = t0 + c;
-                    sx[pp][c] = (z < n && t < d) ? pts[z * d + t] : 0.0f;
-                }
-                for (int i = tid; i < kDC * 64; i += 256) {
-                    const int c = i / 64, j = i % 64;
-                    const int t = t0 + c;
-                    sa[c][j] = t < d ? ct[static_cast<int64_t>(t) * LKp + jp + j] : 0.0;
-                }
-                __syncthreads();
-#pragma unroll 4
-                for (int c = 0; c < kDC; ++c) {
-                    const double x0 = static_cast<double>(sx[p][c]);
-                    const double x1 = static_cast<double>(sx[p + 64][c]);
-                    const double2* arow = reinterpret_cast<const double2*>(&sa[c][g * kJB]);
-#pragma unroll
-                    for (int j2 = 0; j2 < kJB / 2; ++j2) {
-                        const double2 a = arow[j2];
-                        acc0[2 * j2] = fma(a.x, x0, acc0[2 * j2]);
-                        acc0[2 * j2 + 1] = fma(a.y, x0, acc0[2 * j2 + 1]);
-                        acc1[2 * j2] = fma(a.x, x1, acc1[2 * j2]);
-                        acc1[2 * j2 + 1] = fma(a.y, x1, acc1[2 * j2 + 1]);
-                    }
-                }
-            }
-            // store: output j' = jp + g*16 + j  -> (space, dim) = divmod(j', K)
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                const uint64_t z = z0 + p + half * 64;
-                if (z >= n) continue;
-                const double* acc = half ? acc1 : acc0;
-                const int jb = jp + g * kJB;
-                if (K == 16 && jb + kJB <= LK) {
-                    const int sp = jb / 16;
-                    float4* o = reinterpret_cast<float4*>(out + (static_cast<uint64_t>(sp) * n + z) * 16);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        o[q] = make_float4(static_cast<float>(acc[4 * q]), static_cast<float>(acc[4 * q + 1]),
-                                           static_cast<float>(acc[4 * q + 2]), static_cast<float>(acc[4 * q + 3]));
-                } else {
-#pragma unroll
-                    for (int j = 0; j < kJB; ++j) {
-                        const int jj = jb + j;
-                        if (jj < LK) {
-                            const int sp = jj / K, dim = jj % K;
-                            out[(static_cast<uint64_t>(sp) * n + z) * K + dim] = static_cast<float>(acc[j]);
-                        }
-                    }
-                }
-            }
-        }
-    }
-}
-
-// The same contraction on the FP64 tensor cores: mma.sync m8n8k4 f64 chains
+// Exact projection (projection.cpp:31-37) on the FP64 tensor cores: mma.sync m8n8k4 f64 chains
 // accumulate exactly as the sequential fma chain in k order (pinned on B200 by
 // tools/probes/dmma_order.cu, 0 mismatches in 128 000 dot products, and by the
 // projection parity tests), so k-steps issued in t order reproduce the

@@ -14,7 +14,7 @@ namespace {
 __global__ void __launch_bounds__(128) tc_gemm_u8_test_kernel(const uint8_t* __restrict__ A,
                                                               const uint8_t* __restrict__ B, int N,
                                                               int K, int32_t* __restrict__ C) {
-    extern __shared__ __align__(128) uint8_t sm[];
+    extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ uint32_t tslot;
     uint8_t* sA = sm;
