@@ -296,13 +296,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             // candidate words of this warp's 32 rows for its query columns (lane l
             // holds column cbeg + 32 e + l in slot e: chunk e's words sit in one
             // register across the warp), prefetched one tile ahead
-            auto load_words = [&](uint32_t t, uint32_t (&w)[kEpiWords]) {
+            // (per-lane row pointers hoisted out of the tile loop; a query
+            // past the batch reads nothing)
+            const uint32_t* wrow[kEpiWords];
 #pragma unroll
-                for (int e = 0; e < kEpiWords; ++e) {
-                    const uint64_t qq = q0 + cbeg + 32 * e + lane;
-                    const uint64_t word = static_cast<uint64_t>(t) * 4 + sub;
-                    w[e] = (qq < a.nq && word < a.W) ? __ldg(a.bm + qq * a.W + word) : 0u;
-                }
+            for (int e = 0; e < kEpiWords; ++e) {
+                const uint64_t qq = q0 + cbeg + 32 * e + lane;
+                wrow[e] = qq < a.nq ? a.bm + qq * a.W + sub : nullptr;
+            }
+            auto load_words = [&](uint32_t t, uint32_t (&w)[kEpiWords]) {
+                const bool in = static_cast<uint64_t>(t) * 4 + sub < a.W;
+#pragma unroll
+                for (int e = 0; e < kEpiWords; ++e) w[e] = (in && wrow[e]) ? __ldg(wrow[e] + 4ull * t) : 0u;
             };
             const int32_t one = 1 + static_cast<int32_t>(a.n >> 62), two = one + one;  // 1, 2 at run time
             uint32_t pw[kEpiWords], nw[kEpiWords];
