@@ -422,8 +422,13 @@ def main():
         return D.build_index(dev_shard, params, seed=args.seed, sample=args.sample, borrow=True,
                              keep_codes=False)
 
+    # warm-ups run with the event profile on (then discarded) so the timed steps
+    # reuse pooled CUDA events instead of creating them
+    lib.detlsh_profile_enable(1)
     for _ in range(args.warmup):
         idx = build()
+    lib.detlsh_profile_enable(0)
+    collect_profile(lib)
     del idx
     clocks = ClockSampler(local)
     clocks.start()
@@ -474,8 +479,11 @@ def main():
         D.merge_topk_device(g_d, g_i, g_h, k, m_d, m_i, m_h, stream=stream.cuda_stream)
         return m_i, m_d, m_h
 
+    lib.detlsh_profile_enable(1)
     for _ in range(args.warmup):
         query()
+    lib.detlsh_profile_enable(0)
+    collect_profile(lib)
     lc0 = lib.detlsh_launch_count()
     lib.detlsh_profile_enable(1)
     query_ms, (r_ids, r_d, r_h) = timed(query, args.steps)

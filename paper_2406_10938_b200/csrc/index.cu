@@ -342,8 +342,8 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             }
             DETLSH_CUDA(cudaMemcpyAsync(iota.get(), h_iota.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
             DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
-            if (paa) launch_project_paa(dG.get(), n_s, d, K, dGp.get(), s2);
-            else launch_project_exact(dG.get(), n_s, d, X->coeffs_t.get(), K, L, dGp.get(), s2);
+            if (paa) launch_project_paa(dG.get(), n_s, d, K, dGp.get(), s2, "project_sample");
+            else launch_project_exact(dG.get(), n_s, d, X->coeffs_t.get(), K, L, dGp.get(), s2, "project_sample");
             d_sample0.alloc(static_cast<size_t>(K) * n_s);
             launch_gather_sample(dGp.get(), iota.get(), n_s, K, d_sample0.get(), s2);
             float* h_sample = pinned_scratch(static_cast<size_t>(K) * n_s * sizeof(float));

@@ -423,22 +423,23 @@ void prepare_coeffs_t(const float* d_coeffs, int LK, int d, double* d_ct, cudaSt
 }
 
 void launch_project_exact(const float* d_points, uint64_t n, int d, const double* d_ct, int K,
-                          int L, float* d_out, cudaStream_t s) {
+                          int L, float* d_out, cudaStream_t s, const char* prof) {
     if (n == 0) return;
     const int LK = K * L;
     const uint64_t tiles = (n + kPT - 1) / kPT;
     int dev = 0;
     cudaGetDevice(&dev);
     const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count(dev)) * 8);
-    ProfScope ps("project_exact", s);
+    ProfScope ps(prof, s);
     project_dmma_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_points, n, d, d_ct, LK,
                                                                      lk_padded(LK), K, d_out);
     DETLSH_LAUNCH_CHECK();
 }
 
-void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* d_out, cudaStream_t s) {
+void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* d_out, cudaStream_t s,
+                        const char* prof) {
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n * K + 255) / 256, 65535)));
-    ProfScope ps("project_paa", s);
+    ProfScope ps(prof, s);
     project_paa_kernel<<<grid, 256, 0, s>>>(d_points, n, d, K, d_out);
     DETLSH_LAUNCH_CHECK();
 }

@@ -16,13 +16,15 @@ void prepare_coeffs_t(const float* d_coeffs, int LK, int d, double* d_coeffs_t, 
 // project_dataset (projection.cpp:47-60), exact: fp64 FMA chain in t order
 // (float x float is exact in double, so fma == mul+add), rounded once.
 // out [L][n][K] fp32.
+// `prof` names the profile scope (the early sample-row projection is reported apart)
 void launch_project_exact(const float* d_points, uint64_t n, int d, const double* d_coeffs_t,
-                          int K, int L, float* d_out, cudaStream_t s);
+                          int K, int L, float* d_out, cudaStream_t s, const char* prof = "project_exact");
 
 // paa_project_dataset (projection.cpp:62-90): out [1][n][K] fp32, segment j =
 // [j*(d/K), (j+1)*(d/K)) (the last takes the remainder), mean = sequential
 // double sum / length, rounded once to float.
-void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* d_out, cudaStream_t s);
+void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* d_out, cudaStream_t s,
+                        const char* prof = "project_paa");
 
 // sample values: out[j][t] = proj[space][idx[t]][j]  (j < K, t < n_s)
 void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
