@@ -902,7 +902,11 @@ __device__ int32_t kth_dist2(const QueryPlan& P, const FastSlot& F, const Smem& 
     return static_cast<int32_t>((cb << sh) | fb);
 }
 
-__global__ void __launch_bounds__(kQueryThreads, 5) query_fast_kernel(
+// MINB CTAs per SM: 5 for u8 rows (the plan / u8 scoring is load-latency bound
+// and gains from more CTAs), 3 for fp32 rows (the 32-float row chunks in
+// flight need the registers; at 48 registers they spill)
+template <int MINB>
+__global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
@@ -1585,7 +1589,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     const int sms = sm_count(device);
     const size_t smem = smem_bytes(P.K, P.NR, P.d, P.row_u8);
     if (smem > 220 * 1024) throw InvalidArgument("ck_ann: query dimension too large for the staging buffer");
-    DETLSH_CUDA(cudaFuncSetAttribute(query_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    auto* const fast_kernel = P.data_u8 ? &query_fast_kernel<5> : &query_fast_kernel<3>;
+    DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // persistent scratch lives on the index's own stream (it outlives any
     // caller stream); make it visible to `s` before use
@@ -1630,7 +1635,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     const uint32_t* slow_list = X.slow_list.get();
     if (P.k <= kFastMaxK && !P.rc_mode) {
         int per_sm = 0;
-        DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, query_fast_kernel, kQueryThreads, smem));
+        DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast_kernel, kQueryThreads, smem));
         per_sm = std::max(1, std::min(per_sm, 6));
         const size_t fast_bytes = fast_slot_bytes(P.max_leaves, P.budget);
         const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
@@ -1639,7 +1644,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             const uint64_t m = Pc.q_end - Pc.q_begin;
             if (m == 0) return;
             ProfScope ps("query_fast", s);
-            query_fast_kernel<<<static_cast<unsigned>(std::min<uint64_t>(slots, m)), kQueryThreads, smem, s>>>(
+            fast_kernel<<<static_cast<unsigned>(std::min<uint64_t>(slots, m)), kQueryThreads, smem, s>>>(
                 Pc, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
             DETLSH_LAUNCH_CHECK();
         };
