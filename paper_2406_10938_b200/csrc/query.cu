@@ -1589,7 +1589,25 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     const int sms = sm_count(device);
     const size_t smem = smem_bytes(P.K, P.NR, P.d, P.row_u8);
     if (smem > 220 * 1024) throw InvalidArgument("ck_ann: query dimension too large for the staging buffer");
-    auto* const fast_kernel = P.data_u8 ? &query_fast_kernel<5> : &query_fast_kernel<3>;
+    // tau^2 = k-th smallest dist^2 over the rows of the nearest leaves.  If
+    // those rows were a uniform sample of the candidates, about
+    // k * budget / tau_rows candidates would pass it; size the sample so
+    // that is a quarter of the survivor staging buffer (nearest-leaf rows
+    // do better than uniform; measured on C2, 2x this sample trades 1 ms
+    // of plan for 2.5 ms of scoring), and keep the tensor-core path only
+    // where the sample is a small part of the budget.
+    const uint64_t tau_rows = std::max<uint64_t>(
+        std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + kTcFinishCap - 1) / kTcFinishCap);
+    const bool tc_ok = P.tc_allowed && P.data_u8 && P.xn_u8 && P.data_tc && P.row_u8 % 32 == 0 &&
+                       P.row_u8 <= 256 && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
+                       2ULL * P.k <= kTcFinishCap && 8 * tau_rows <= P.budget && P.k <= kFastMaxK && !P.rc_mode;
+    // plan-kernel occupancy: 5 CTAs/SM when it hands verification to the
+    // tensor cores (load-latency bound plan), 3 when it verifies candidates
+    // itself (the row chunks in flight need the registers); measured on C1-C4.
+    // DETLSH_FAST_MINB=3|5 overrides (measurement hook).
+    const char* minb_env = std::getenv("DETLSH_FAST_MINB");
+    const bool five = minb_env ? std::atoi(minb_env) == 5 : tc_ok;
+    auto* const fast_kernel = five ? &query_fast_kernel<5> : &query_fast_kernel<3>;
     DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // persistent scratch lives on the index's own stream (it outlives any
@@ -1652,19 +1670,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         // candidate set to the tcgen05 dataset-major scorer (tc_score.cu)
         // test hook: exact fp64 mindists for every leaf (no approximate round)
         if (std::getenv("DETLSH_TEST_EXACT_SCAN")) Pp.force_exact = 1;
-        // tau^2 = k-th smallest dist^2 over the rows of the nearest leaves.  If
-        // those rows were a uniform sample of the candidates, about
-        // k * budget / tau_rows candidates would pass it; size the sample so
-        // that is a quarter of the survivor staging buffer (nearest-leaf rows
-        // do better than uniform; measured on C2, 2x this sample trades 1 ms
-        // of plan for 2.5 ms of scoring), and keep the tensor-core path only
-        // where the sample is a small part of the budget.
-        const uint64_t tau_rows = std::max<uint64_t>(
-            std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + kTcFinishCap - 1) / kTcFinishCap);
         Pp.tc_tau_rows = static_cast<uint32_t>(std::min<uint64_t>(tau_rows, 0xffffffffULL));
-        const bool tc_ok = P.tc_allowed && P.data_u8 && P.xn_u8 && P.data_tc && P.row_u8 % 32 == 0 &&
-                           P.row_u8 <= 256 && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
-                           2ULL * P.k <= kTcFinishCap && 8 * tau_rows <= P.budget;
         DevBuf<uint32_t> over_list;
         if (!tc_ok) {
             launch_fast(Pp);
