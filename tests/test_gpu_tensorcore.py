@@ -70,3 +70,28 @@ def test_tc_verification_equals_gather_path_and_oracle(gpu, port, monkeypatch, d
         assert np.array_equal(ra.ids[qi], ids), f"query {qi}"
         assert np.array_equal(ra.dists[qi].view(np.uint64), np.asarray(ds).view(np.uint64)), f"query {qi}"
         assert ra.radius_used[qi] == rad and int(ra.candidates_seen[qi]) == cs
+
+
+def test_host_buffers_pinned_and_pageable_agree(gpu):
+    """The C-ABI query with pinned host buffers (direct copies) and with pageable
+    ones (staged through the library's pinned buffers) returns the same bytes."""
+    import ctypes as C
+    import torch
+    from paper_2406_10938_b200 import _lib
+    rng = np.random.default_rng(5)
+    data = rng.integers(0, 256, size=(20000, 64)).astype(np.float32)
+    Q = rng.integers(0, 256, size=(300, 64)).astype(np.float32)
+    idx = gpu.build_index(data, gpu.LshParams(beta=0.5, k=20), seed=3)
+    ref = gpu.ck_ann_batch(idx, Q, 20)
+    nq, k = Q.shape[0], 20
+    qp = torch.from_numpy(Q).pin_memory()
+    outs = [torch.zeros((nq, k), dtype=torch.int32).pin_memory(), torch.zeros((nq, k), dtype=torch.float64).pin_memory(),
+            torch.zeros(nq, dtype=torch.int32).pin_memory(), torch.zeros(nq, dtype=torch.float64).pin_memory(),
+            torch.zeros(nq, dtype=torch.int64).pin_memory()]
+    p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    _lib.check(_lib.load().detlsh_gpu_query(idx.handle, p(qp), nq, k, 0, *[p(t) for t in outs], None))
+    assert np.array_equal(outs[0].numpy().view(np.uint32), ref.ids)
+    assert np.array_equal(outs[1].numpy().view(np.uint64), ref.dists.view(np.uint64))
+    assert np.array_equal(outs[2].numpy(), ref.n_hits)
+    assert np.array_equal(outs[3].numpy().view(np.uint64), ref.radius_used.view(np.uint64))
+    assert np.array_equal(outs[4].numpy().view(np.uint64), ref.candidates_seen.view(np.uint64))
