@@ -603,6 +603,15 @@ __device__ uint32_t topk_finish(const Smem& S, int k) {
     return c;
 }
 
+// OR rows [a0, a1) into a row bitmap (global atomics: neighbouring leaves share words)
+__device__ __forceinline__ void or_row_range(uint32_t* bm, uint32_t a0, uint32_t a1) {
+    for (uint32_t w = a0 >> 5; a0 < a1 && w <= (a1 - 1) >> 5; ++w) {
+        const uint32_t lo = max(a0, w << 5), hi = min(a1, (w << 5) + 32);
+        const uint32_t nbits = hi - lo;
+        atomicOr(bm + w, (nbits == 32 ? 0xffffffffu : ((1u << nbits) - 1u)) << (lo & 31));
+    }
+}
+
 __device__ __forceinline__ uint32_t sqdiff4(uint32_t a, uint32_t b, uint32_t acc) {
     const uint32_t d = __vabsdiffu4(a, b);
     return __dp4a(d, d, acc);
@@ -941,7 +950,7 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
         const double r2_in = r2 * (1.0 - 1e-12), r2_out = r2 * (1.0 + 1e-12);
         bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30 && !P.force_exact;
         // tensor-core hand-off for this query (u8 rows, large budget)
-        const bool tc_eligible = P.tc_flags != nullptr && u8 && B32 >= kTcMinBudget;
+        const bool tc_eligible = P.tc_bm != nullptr && u8 && B32 >= kTcMinBudget;
         if (approx) build_pen_tables(P, S);
         else build_sq(P, 0, S);
         if (approx) build_half_tables(P, S);
@@ -1274,30 +1283,22 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             __syncthreads();
             const uint32_t nt = min(emit_rows(F.tau, n_tau, T0, F.cand, B32, S), B32);
             const int32_t tau2 = kth_dist2(P, F, S, nt, P.k);  // exact k-th smallest among those rows
-            // candidate set: one flag bit per tree-0 leaf taken whole (built in
-            // smem when it fits, else with global atomics on the zeroed slot) +
-            // the cut leaf and the end row of its taken prefix; tc_expand turns
-            // them into the row bitmap tc_score reads
+            // candidate set: this query's row bitmap over tree-0 rows, written
+            // here (zeroed, then each whole leaf's row range and the cut leaf's
+            // taken prefix OR-ed in); tc_score_kernel reads it
             const uint64_t slot = qs - P.q_begin;
-            uint32_t* fl = P.tc_flags + slot * P.tc_LW;
-            const bool fl_smem = P.tc_LW * 4 <= union_bytes(P.K, P.NR) - 64;
-            uint32_t* sfl = reinterpret_cast<uint32_t*>(S.th);  // union: idle after kth_dist2
-            if (fl_smem) {
-                for (uint32_t w = threadIdx.x; w < P.tc_LW; w += blockDim.x) sfl[w] = 0;
-                __syncthreads();
-            }
+            uint32_t* row = P.tc_bm + slot * P.tc_W;
+            for (uint64_t w = threadIdx.x; w < P.tc_W / 4; w += blockDim.x)
+                reinterpret_cast<uint4*>(row)[w] = make_uint4(0u, 0u, 0u, 0u);
+            __syncthreads();  // (the zeros are visible to the whole block)
             for (uint32_t i = threadIdx.x; i < n_full; i += blockDim.x) {
                 const uint32_t li = F.full[i];
-                if (fl_smem) atomicOr(&sfl[li >> 5], 1u << (li & 31));
-                else atomicOr(&fl[li >> 5], 1u << (li & 31));
-            }
-            if (fl_smem) {
-                __syncthreads();
-                for (uint32_t w = threadIdx.x; w < P.tc_LW; w += blockDim.x) fl[w] = sfl[w];
+                const uint32_t a0 = __ldg(T0.leaf_begin + li);
+                or_row_range(row, a0, a0 + __ldg(T0.leaf_count + li));
             }
             if (threadIdx.x == 0) {
-                P.tc_cut[2 * slot] = cut_li;
-                P.tc_cut[2 * slot + 1] = __ldg(T0.leaf_begin + cut_li) + static_cast<uint32_t>(take_cut);
+                const uint32_t a0 = __ldg(T0.leaf_begin + cut_li);
+                or_row_range(row, a0, a0 + static_cast<uint32_t>(take_cut));
             }
             if (threadIdx.x == 0) P.tc_tau2[qs - P.q_begin] = tau2;
             __syncthreads();
@@ -1676,20 +1677,17 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             launch_fast(Pp);
         } else {
             const int R = P.row_u8;
-            const uint32_t LW = (P.trees_num_leaves0 + 31) / 32;
-            const uint64_t W = (P.n + 31) / 32;
+            const uint64_t W = ((P.n + 31) / 32 + 3) / 4 * 4;  // bitmap words per query, rows 16-B aligned
             // test hook: a smaller staging buffer forces the overflow re-run
             uint32_t tc_cap = kTcFinishCap;
             if (const char* e = std::getenv("DETLSH_TEST_TC_CAP"))
                 tc_cap = static_cast<uint32_t>(std::max(1L, std::min<long>(std::atol(e), kTcFinishCap)));
-            // per processing slot: leaf flags, row bitmap (n/8 bytes), survivors
-            // (32 KB), pass records (128 KB); a chunk stays under ~3 GB
+            // per processing slot: row bitmap (n/8 bytes), survivors (32 KB),
+            // pass records (128 KB); a chunk stays under ~3 GB
             uint64_t chunk = (3ULL << 30) / (W * 4 + 160 * 1024);
             chunk = std::max<uint64_t>(256, chunk / 256 * 256);
             chunk = std::min<uint64_t>(chunk, (P.nq + 255) / 256 * 256);
             const uint64_t rec_cap = chunk * 8192;  // candidate threshold passes staged per chunk
-            grow_scratch(X.tc_flags, chunk * LW);
-            grow_scratch(X.tc_cut, chunk * 2);
             grow_scratch(X.tc_bm, chunk * W);
             grow_scratch(X.tc_tau2, chunk);
             grow_scratch(X.tc_qn, chunk);
@@ -1698,8 +1696,6 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             grow_scratch(X.tc_surv, chunk * kTcFinishCap);
             grow_scratch(X.tc_rec, rec_cap);
             grow_scratch(X.tc_rec_cnt, 1);
-            DevBuf<uint32_t>& flags = X.tc_flags;
-            DevBuf<uint32_t>& cut = X.tc_cut;
             DevBuf<uint32_t>& bm = X.tc_bm;
             DevBuf<int32_t>& tau2 = X.tc_tau2;
             DevBuf<int32_t>& qn = X.tc_qn;
@@ -1709,39 +1705,18 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             DevBuf<uint4>& rec = X.tc_rec;
             DevBuf<unsigned long long>& rec_cnt = X.tc_rec_cnt;
             over_list.alloc(P.nq);
-            // the row bitmaps (n/8 bytes per query) are zeroed on the index's own
-            // stream while the plan kernel runs; tc_expand waits for it
-            cudaEvent_t ev_prev, ev_bm;
-            DETLSH_CUDA(cudaEventCreateWithFlags(&ev_prev, cudaEventDisableTiming));
-            DETLSH_CUDA(cudaEventCreateWithFlags(&ev_bm, cudaEventDisableTiming));
-            struct EvPair {
-                cudaEvent_t a, b;
-                ~EvPair() {
-                    cudaEventDestroy(a);
-                    cudaEventDestroy(b);
-                }
-            } ev_guard{ev_prev, ev_bm};
             for (uint64_t c0 = 0; c0 < P.nq; c0 += chunk) {
                 const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);
-                DETLSH_CUDA(cudaEventRecord(ev_prev, s));  // after the previous chunk's reads of bm
-                DETLSH_CUDA(cudaStreamWaitEvent(alloc_s, ev_prev, 0));
-                DETLSH_CUDA(cudaMemsetAsync(bm.get(), 0, m * W * 4, alloc_s));
-                DETLSH_CUDA(cudaEventRecord(ev_bm, alloc_s));
-                DETLSH_CUDA(cudaMemsetAsync(flags.get(), 0, m * LW * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(tau2.get(), 0xff, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(surv_cnt.get(), 0, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + 3, 0, 4, s));
                 QueryPlan Pc = Pp;
                 Pc.q_begin = c0;
                 Pc.q_end = c0 + m;
-                Pc.tc_flags = flags.get();
-                Pc.tc_LW = LW;
-                Pc.tc_cut = cut.get();
+                Pc.tc_bm = bm.get();
+                Pc.tc_W = W;
                 Pc.tc_tau2 = tau2.get();
                 launch_fast(Pc);
-                DETLSH_CUDA(cudaStreamWaitEvent(s, ev_bm, 0));
-                launch_tc_expand(flags.get(), LW, cut.get(), tau2.get(), m, P.trees_leaf_begin0, P.trees_leaf_count0,
-                                 P.trees_num_leaves0, bm.get(), W, s);
                 launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, q8.get(), qn.get(), s);
                 TcScoreArgs a{};
                 a.rows = P.data_tc;

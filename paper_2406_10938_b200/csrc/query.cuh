@@ -58,11 +58,11 @@ struct QueryPlan {
     // processed range of processing slots [q_begin, q_end)
     uint64_t q_begin, q_end;
     // tensor-core verification hand-off (null: score every candidate here).
-    // Indexed by slot - q_begin: flag bits over tree-0 leaves taken whole
-    // ([tc_LW] words per slot), the cut leaf and its end row, tau^2.
-    uint32_t* tc_flags;
-    uint32_t tc_LW;
-    uint32_t* tc_cut;  // [slot][2]: cut leaf, end row of its taken prefix
+    // Indexed by slot - q_begin: the candidate set as a bitmap over tree-0
+    // rows ([tc_W] words per slot: whole leaves + the cut leaf's taken
+    // prefix), written by the plan kernel itself, and tau^2.
+    uint32_t* tc_bm;
+    uint64_t tc_W;
     int32_t* tc_tau2;
     int tc_allowed;  // host-side switch (DETLSH_F_NO_TC clears it)
     int force_exact;  // test hook: skip the approximate leaf scan
@@ -87,7 +87,7 @@ struct QueryScratch {
     // several of these are GB-sized and re-allocating them from the pool per
     // batch costs fresh mappings whenever the pool is fragmented.  Nothing reads
     // them after run_query_batch's last host sync, so the next call may reuse them.
-    DevBuf<uint32_t> tc_flags, tc_cut, tc_bm, tc_surv_cnt;
+    DevBuf<uint32_t> tc_bm, tc_surv_cnt;
     DevBuf<int32_t> tc_tau2, tc_qn;
     DevBuf<uint8_t> tc_q8;
     DevBuf<uint64_t> tc_surv;
@@ -126,11 +126,6 @@ void launch_tc_pack_queries(const float* q, const uint32_t* order, uint64_t slot
 void launch_row_norms_u8(const uint8_t* rows, uint64_t n, int R, int32_t* xn, cudaStream_t s);
 // u8 rows -> 128-row tiles in the MMA operand layout ([ceil(n/128)][R/16][128][16] bytes)
 void launch_pack_tc_tiles(const uint8_t* rows, uint64_t n, int R, uint8_t* tiles, cudaStream_t s);
-// Leaf flags + cut (plan kernel) -> candidate row bitmaps [m][W] (zeroed) for
-// the TC queries (tau2 >= 0) of a chunk.
-void launch_tc_expand(const uint32_t* flags, uint32_t LW, const uint32_t* cut, const int32_t* tau2, uint64_t m,
-                      const uint32_t* leaf_begin, const uint32_t* leaf_count, uint32_t nl, uint32_t* bm, uint64_t W,
-                      cudaStream_t s);
 void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s);
 void launch_tc_finish(const TcScoreArgs& a, const uint32_t* perm0, int k, double r_min,
                       uint64_t budget, uint32_t* ids, double* dists, int32_t* n_hits, double* radius,

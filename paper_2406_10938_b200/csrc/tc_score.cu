@@ -515,54 +515,6 @@ void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s) {
     DETLSH_LAUNCH_CHECK();
 }
 
-namespace {
-__device__ __forceinline__ void or_row_range(uint32_t* bm, uint32_t a0, uint32_t a1) {
-    for (uint32_t w = a0 >> 5; a0 < a1 && w <= (a1 - 1) >> 5; ++w) {
-        const uint32_t lo = max(a0, w << 5), hi = min(a1, (w << 5) + 32);
-        const uint32_t nbits = hi - lo;
-        atomicOr(bm + w, (nbits == 32 ? 0xffffffffu : ((1u << nbits) - 1u)) << (lo & 31));
-    }
-}
-
-// One thread per (slot, flag word) and one per slot for the cut leaf's prefix:
-// every whole leaf's row range is OR-ed into the slot's row bitmap.
-__global__ void tc_expand_kernel(const uint32_t* __restrict__ flags, uint32_t LW, const uint32_t* __restrict__ cut,
-                                 const int32_t* __restrict__ tau2, uint64_t m, const uint32_t* __restrict__ leaf_begin,
-                                 const uint32_t* __restrict__ leaf_count, uint32_t* __restrict__ bm, uint64_t W) {
-    const uint64_t total = m * LW + m;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        if (i < m * LW) {
-            const uint64_t slot = i / LW;
-            uint32_t f = flags[i];
-            if (!f || tau2[slot] < 0) continue;
-            const uint32_t base = static_cast<uint32_t>(i % LW) * 32;
-            uint32_t* row = bm + slot * W;
-            for (; f; f &= f - 1) {
-                const uint32_t li = base + __ffs(f) - 1;
-                const uint32_t a0 = __ldg(leaf_begin + li);
-                or_row_range(row, a0, a0 + __ldg(leaf_count + li));
-            }
-        } else {
-            const uint64_t slot = i - m * LW;
-            if (tau2[slot] < 0) continue;
-            or_row_range(bm + slot * W, __ldg(leaf_begin + cut[2 * slot]), cut[2 * slot + 1]);
-        }
-    }
-}
-}  // namespace
-
-void launch_tc_expand(const uint32_t* flags, uint32_t LW, const uint32_t* cut, const int32_t* tau2, uint64_t m,
-                      const uint32_t* leaf_begin, const uint32_t* leaf_count, uint32_t nl, uint32_t* bm, uint64_t W,
-                      cudaStream_t s) {
-    (void)nl;
-    const uint64_t total = m * LW + m;
-    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 65535)));
-    ProfScope ps("tc_expand", s);
-    tc_expand_kernel<<<grid, 256, 0, s>>>(flags, LW, cut, tau2, m, leaf_begin, leaf_count, bm, W);
-    DETLSH_LAUNCH_CHECK();
-}
-
 void launch_pack_tc_tiles(const uint8_t* rows, uint64_t n, int R, uint8_t* tiles, cudaStream_t s) {
     const uint64_t chunks = (n + kTcRows - 1) / kTcRows * kTcRows * (R / 16);
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, 16384)));
