@@ -205,8 +205,8 @@ def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0, plan=None):
     if kernel == "query_fast" and plan is not None:
         # tensor-core hand-off: per query the plan kernel reads tree 0's 8-byte
         # leaf records, writes and re-reads a 2-byte bin per leaf, scores
-        # tau_rows u8 rows and writes one flag bit per leaf
-        return (12.0 * plan["leaves"] + row_u8 * plan["tau_rows"] + plan["leaves"] / 8.0) * nq
+        # tau_rows u8 rows and writes the n-bit candidate row bitmap
+        return (12.0 * plan["leaves"] + row_u8 * plan["tau_rows"] + n / 8.0) * nq
     if kernel == "query_fast":
         return 4.0 * d * budget * nq  # every verified candidate row (4d B/candidate)
     if kernel == "encode":
@@ -696,7 +696,7 @@ def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exc
         out.update({"achieved": round(ach, 2), "frac": round(ach / hbm, 5),
                     "algorithmic_bytes": b})
         if plan is not None:
-            out["model"] = "plan kernel (tc hand-off): 12 B/leaf x tree-0 leaves + R x tau_rows + leaves/8 per query"
+            out["model"] = "plan kernel (tc hand-off): 12 B/leaf x tree-0 leaves + R x tau_rows + n/8 (row bitmap) per query"
         if kern == "query_fast" and row_u8 and plan is None:
             b8 = float(row_u8) * budget * nq  # bytes the u8 rows actually hold
             out["u8_rows"] = {"bytes": b8, "achieved": round(b8 / (per_launch_ms / 1e3) / 1e9, 2),
