@@ -96,3 +96,20 @@ def test_two_rank_gloo_gather_and_merge(tmp_path, world):
     same = np.mean([len(set(full.ck_ann(Q[q], K)[0].tolist()) & set(got["i"][q].tolist())) / K
                     for q in range(NQ)])
     assert same >= 0.7
+
+
+def test_weak_scaling_shards():
+    """bench.py --shard weak: shard 0 is the N = 1 dataset, shard r > 0 an
+    independent draw of the same distribution (the mixture keeps its centres)."""
+    from paper_2406_10938_b200 import data as gen
+    base = gen.make("c1", n=2000)[0]  # (default nq, as bench.py generates it)
+    s0 = gen.make_shard("c1", 0, 2000)
+    s1 = gen.make_shard("c1", 1, 2000)
+    assert np.array_equal(base, s0)
+    assert s1.shape == s0.shape and not np.array_equal(s0, s1)
+    # same centres: every shard-1 point lies near one of the 100 centres shard 0 uses
+    c = np.random.Generator(np.random.PCG64(gen.CONFIGS["c1"]["seed"])).uniform(0, 100, size=(100, 128))
+    d0 = ((s1[:50, None, :] - c[None, :, :].astype(np.float32)) ** 2).sum(-1).min(1)
+    assert np.all(d0 < (5.0 * 4) ** 2 * 128)
+    g1 = gen.make_shard("c2", 1, 1000)
+    assert g1.shape == (1000, 128) and g1.min() >= 0 and g1.max() <= 255
