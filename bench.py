@@ -44,13 +44,28 @@ def parse():
     ap.add_argument("--seed", type=int, default=2)
     ap.add_argument("--sample", choices=["reference", "gpu"], default="reference",
                     help="breakpoint sample mode of the headline build")
-    ap.add_argument("--shard", choices=["weak", "strong"], default="weak",
-                    help="N>1: weak = every rank indexes its own n-point shard of a world x n "
-                         "dataset (fixed per-GPU work); strong = the config's n split across ranks")
+    ap.add_argument("--shard", choices=["weak", "strong"], default="strong",
+                    help="N>1: strong (default, BASELINE configs 4-5) = the config's one n-point "
+                         "dataset split into N contiguous point shards; weak = every rank indexes "
+                         "its own n-point shard of a world x n dataset (fixed per-GPU work)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=200)
-    ap.add_argument("--cpu-build-rows", type=int, default=250_000)
+    ap.add_argument("--cpu-build-rows", type=int, default=None,
+                    help="rows the reference build is timed on (default: the full n, same config)")
     return ap.parse_args()
+
+
+def relaunch_distributed(args):
+    """`bench.py --gpus N` without a torchrun environment: re-exec under
+    torch.distributed.run with N ranks on this node (one process per GPU)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 # ---------------------------------------------------------------------------
@@ -265,21 +280,24 @@ def run_reference(args, rank):
     n, d = base.shape
     cores = os.cpu_count() or 1
     p = make_params(beta=args.beta, k=args.k)
-    rows = min(n, args.cpu_build_rows)
+    rows = n if args.cpu_build_rows is None else min(n, args.cpu_build_rows)
     sub = np.ascontiguousarray(base[:rows])
     # build: single thread (the reference is single-threaded by design)
     times = []
+    full = None
     for step in range(args.warmup + args.steps):
+        full = None  # one index alive at a time
         t0 = time.perf_counter()
-        oi = orc.build_index(sub, p, args.seed)
+        full = orc.build_index(sub, p, args.seed)
         dt = time.perf_counter() - t0
         if step >= args.warmup:
             times.append(dt)
-        del oi
     build_s = float(np.mean(times))
     build_rate = rows / build_s / 1e6
-    # queries: full-size index (built once, untimed), all host threads
-    full = orc.build_index(base, p, args.seed)
+    # queries: full-size index (the last timed build when it covered all n), all host threads
+    if rows != n:
+        full = None
+        full = orc.build_index(base, p, args.seed)
     nqs = min(args.cpu_queries, Q.shape[0])
     qtimes = []
     for step in range(args.warmup + args.steps):
@@ -292,7 +310,7 @@ def run_reference(args, rank):
     gt_ids, gt_d = exact_knn_gpu_or_cpu(base, Q[:nqs], args.k, integer, orc)
     ids, ds, nh, rad, cs, _ = full.ck_ann_batch(Q[:nqs], args.k, threads=cores)
     rec, rat = recall_ratio(ids, ds, nh, gt_ids, gt_d, args.k)
-    sample = (f"build: first {rows} of {n} rows x {args.steps} steps, 1 thread; "
+    sample = (f"build: {'all' if rows == n else 'first'} {rows} of {n} rows x {args.steps} steps, 1 thread; "
               f"queries: {nqs} per step on the full n={n} index, {cores} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(build_rate, 6), "unit": "Mpoints/s",
@@ -333,23 +351,26 @@ def cpu_baseline(args, base, Q):
     kind = "reference" if ref_available() else "port"
     orc = Oracle(kind)
     n = base.shape[0]
-    rows = min(n, args.cpu_build_rows)
+    rows = n if args.cpu_build_rows is None else min(n, args.cpu_build_rows)
     p = make_params(beta=args.beta, k=args.k)
     t0 = time.perf_counter()
-    orc.build_index(np.ascontiguousarray(base[:rows]), p, args.seed)
+    full = orc.build_index(np.ascontiguousarray(base[:rows]), p, args.seed)
     b = time.perf_counter() - t0
-    full = orc.build_index(base, p, args.seed)
+    if rows != n:
+        full = orc.build_index(base, p, args.seed)
     cores = os.cpu_count() or 1
     nqs = min(args.cpu_queries, Q.shape[0])
     _, _, _, _, _, secs = full.ck_ann_batch(Q[:nqs], args.k, threads=cores)
     return {"value": round(rows / b / 1e6, 6), "unit": "Mpoints/s", "cores": 1, "kind": kind,
-            "sample": f"build_index on the first {rows} rows (1 thread); ck_ann on {nqs} "
+            "sample": f"build_index on {'all' if rows == n else 'the first'} {rows} rows (1 thread); ck_ann on {nqs} "
                       f"queries against the full n={n} index ({cores} threads)",
             "query": {"value": round(nqs / secs, 3), "unit": "queries/s", "cores": cores}}
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args)  # does not return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

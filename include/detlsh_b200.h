@@ -126,10 +126,22 @@ void detlsh_gpu_free(detlsh_gpu_index* index);
  * min(k, |S|) hits); radius_used[q] = r_min * c^t; cands_seen[q] = |S|.
  * Any output pointer may be NULL.  stream: cudaStream_t or NULL (the index's
  * own stream).  With DETLSH_F_DEVICE_PTRS all pointers are device pointers and
- * the call is stream-ordered (returns once enqueued). */
+ * the call is stream-ordered: it returns once enqueued, every decision (the
+ * tensor-core overflow re-runs, the general-path queries) is taken on the
+ * device, and batches on different streams are ordered through the index's
+ * scratch.  The host waits only when a batch needs more scratch than every
+ * earlier batch of the index (the first call of a shape), and when the
+ * per-kernel profile is enabled; after that first call the enqueue can be
+ * captured into a CUDA graph.  Host pointers: the call returns with the
+ * results and reports an internal failure as DETLSH_E_CUDA. */
 int detlsh_gpu_query(const detlsh_gpu_index* index, const float* queries, uint64_t nq,
                      int32_t k, uint32_t flags, uint32_t* ids, double* dists, int32_t* n_hits,
                      double* radius_used, uint64_t* cands_seen, void* stream);
+
+/* Synchronises `stream` (NULL: the index's own) and reports, as DETLSH_E_CUDA,
+ * a failed internal check of any earlier device-pointer batch (the check is
+ * sticky: host-pointer calls report it on return). */
+int detlsh_gpu_query_check(const detlsh_gpu_index* index, void* stream);
 
 /* rc_ann (index.hpp, index.cpp:267-290), batched: for each query the closest
  * candidate of one pass over the trees at radius epsilon * r (budget
@@ -172,6 +184,32 @@ int detlsh_gpu_merge_topk(const double* shard_dists, const uint64_t* shard_ids,
                           const int32_t* shard_hits, int32_t shards, uint64_t nq, int32_t k,
                           double* out_dists, uint64_t* out_ids, int32_t* out_hits,
                           void* stream);
+
+/* ---- point-sharded index, one process --------------------------
+ * The dataset splits into `shards` contiguous row ranges [s*n/S, (s+1)*n/S);
+ * shard s is an independent DET-LSH index (own sample, breakpoints, trees and
+ * r_min; budget ceil(beta * n_s + k)) built on devices[s] with the same seed,
+ * all shards concurrently (a device may hold several).  A query batch runs on
+ * every shard at once; each shard's top-k goes to devices[0] (peer copies over
+ * NVLink) and is merged by (distance, global position) -- the same answer as
+ * the reference's build_index + ck_ann on each shard followed by that merge.
+ * params: the template in, the derived fields (shared by all shards) out;
+ * per-shard r_min through detlsh_gpu_sharded_shard + detlsh_gpu_get_params. */
+typedef struct detlsh_gpu_sharded_index detlsh_gpu_sharded_index;
+int detlsh_gpu_sharded_build(const float* points, uint64_t n, int32_t d, detlsh_params* params, uint64_t seed,
+                             const int32_t* devices, int32_t shards, uint32_t flags,
+                             detlsh_gpu_sharded_index** out);
+/* ids are global u64 positions, [nq][k] ascending by (distance, position).
+ * Device pointers (DETLSH_F_DEVICE_PTRS) live on devices[0] and the call is
+ * stream-ordered on `stream` (a stream of devices[0], or NULL). */
+int detlsh_gpu_sharded_query(detlsh_gpu_sharded_index* index, const float* queries, uint64_t nq, int32_t k,
+                             uint32_t flags, uint64_t* ids, double* dists, int32_t* n_hits, void* stream);
+int32_t detlsh_gpu_sharded_count(const detlsh_gpu_sharded_index* index);
+/* Borrowed handle of shard s (valid while the sharded index lives; never freed
+ * by the caller): every export / query entry point above accepts it. */
+const detlsh_gpu_index* detlsh_gpu_sharded_shard(const detlsh_gpu_sharded_index* index, int32_t s,
+                                                 uint64_t* row_begin, uint64_t* row_end);
+void detlsh_gpu_sharded_free(detlsh_gpu_sharded_index* index);
 
 /* ---- export (DetIndex fields, index.hpp:24-37) ------------------------------ */
 int detlsh_gpu_get_params(const detlsh_gpu_index* index, detlsh_params* out);

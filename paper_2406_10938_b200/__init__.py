@@ -18,6 +18,10 @@ from .api import (  # noqa: F401
     build_det_only_index,
     build_index,
     build_index_with_family,
+    build_sharded_index,
+    ck_ann_sharded,
+    ck_ann_sharded_device,
+    ShardedIndex,
     rc_ann,
     rc_ann_batch,
     read_vectors_device,
@@ -35,6 +39,7 @@ from .api import (  # noqa: F401
     merge_topk_device,
     mix_seed,
     project_dataset,
+    query_check,
     sample_hash_family,
     select_breakpoints,
 )

@@ -83,11 +83,17 @@ def load() -> C.CDLL:
                                           C.POINTER(vp)], C.c_int),
         "detlsh_gpu_free": ([vp], None),
         "detlsh_gpu_query": ([vp, vp, u64, i32, u32, vp, vp, vp, vp, vp, vp], C.c_int),
+        "detlsh_gpu_query_check": ([vp, vp], C.c_int),
         "detlsh_gpu_rc_ann": ([vp, vp, u64, dbl, dbl, u32, vp, vp, vp, vp, vp], C.c_int),
         "detlsh_gpu_brute_force_knn": ([vp, u64, i32, vp, u64, i32, vp, u32, vp, vp, i32, vp], C.c_int),
         "detlsh_vectors_shape": ([C.c_char_p, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)], C.c_int),
         "detlsh_gpu_read_vectors": ([C.c_char_p, vp, u64, i32, i32, vp], C.c_int),
         "detlsh_gpu_merge_topk": ([vp, vp, vp, i32, u64, i32, vp, vp, vp, vp], C.c_int),
+        "detlsh_gpu_sharded_build": ([vp, u64, i32, P, u64, vp, i32, u32, C.POINTER(vp)], C.c_int),
+        "detlsh_gpu_sharded_query": ([vp, vp, u64, i32, u32, vp, vp, vp, vp], C.c_int),
+        "detlsh_gpu_sharded_count": ([vp], i32),
+        "detlsh_gpu_sharded_shard": ([vp, i32, C.POINTER(u64), C.POINTER(u64)], vp),
+        "detlsh_gpu_sharded_free": ([vp], None),
         "detlsh_gpu_get_params": ([vp, P], C.c_int),
         "detlsh_gpu_n": ([vp], u64),
         "detlsh_gpu_d": ([vp], i32),

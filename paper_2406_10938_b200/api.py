@@ -106,6 +106,23 @@ def _as_host_f32(x, ndim=2) -> np.ndarray:
     return a
 
 
+def _check_tensor(t, name: str, dtype, shape, device: int | None = None):
+    """A CUDA tensor the C ABI reads or writes through a raw pointer: its dtype,
+    shape and layout must be exactly what the library assumes."""
+    import torch
+    if not _is_cuda_tensor(t):
+        raise ValueError(f"{name}: expected a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: expected dtype {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: expected a contiguous tensor")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"{name}: tensor is on cuda:{t.device.index}, the index on cuda:{device}")
+    del torch
+
+
 def candidate_budget(beta: float, n: int, k: int) -> int:
     return int(_lib.load().detlsh_candidate_budget(beta, n, k))
 
@@ -146,14 +163,15 @@ def device_count() -> int:
 class DetIndex:
     """Assembled GPU index (detlsh::DetIndex, index.hpp:24-37).  Immutable after build."""
 
-    def __init__(self, handle, params: LshParams, n: int, d: int, device: int):
+    def __init__(self, handle, params: LshParams, n: int, d: int, device: int, owner=None):
         self._h = handle
         self.params = params
         self._n, self._d, self.device = n, d, device
+        self._owner = owner  # borrowed handle (a shard of a ShardedIndex): never freed here
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and getattr(self, "_owner", None) is None:
             try:
                 _lib.load().detlsh_gpu_free(h)
             except Exception:
@@ -255,6 +273,11 @@ def build_index(data, params: LshParams | None = None, seed: int = 0, *, device:
     h = C.c_void_p()
     flags = _flags(sample) | (0 if keep_codes else F_NO_CODES) | (0 if u8_rows else F_NO_U8)
     if _is_cuda_tensor(data):
+        import torch
+        if data.dim() != 2:
+            raise ValueError(f"build_index: expected a 2-d tensor, got shape {tuple(data.shape)}")
+        if data.dtype != torch.float32:
+            raise ValueError(f"build_index: expected float32 points, got {data.dtype}")
         t = data.contiguous()
         n, d = int(t.shape[0]), int(t.shape[1])
         flags |= F_DEVICE_PTRS | (F_BORROW_DATA if borrow else 0)
@@ -325,14 +348,29 @@ def ck_ann_batch(index: DetIndex, queries, k: int, *, stream=None,
 def ck_ann_device(index: DetIndex, queries, k: int, ids, dists, n_hits=None, radius=None,
                   cands=None, stream=None, tensor_cores: bool = True) -> None:
     """Batched ck_ann on device tensors (stream-ordered, no host copies)."""
+    import torch
+
     def p(t):
         return C.c_void_p(t.data_ptr()) if t is not None else None
-    if queries.shape[1] != index.d():
+    if queries.dim() != 2 or queries.shape[1] != index.d():
         raise ValueError("ck_ann: query dimension mismatch")
+    nq = int(queries.shape[0])
+    dev = index.device
+    _check_tensor(queries, "ck_ann: queries", torch.float32, (nq, index.d()), dev)
+    _check_tensor(ids, "ck_ann: ids", torch.int32, (nq, k), dev)
+    _check_tensor(dists, "ck_ann: dists", torch.float64, (nq, k), dev)
+    for t, name, dt in ((n_hits, "n_hits", torch.int32), (radius, "radius", torch.float64),
+                        (cands, "cands", torch.int64)):
+        if t is not None:
+            _check_tensor(t, f"ck_ann: {name}", dt, (nq,), dev)
     flags = F_DEVICE_PTRS | (0 if tensor_cores else F_NO_TC)
-    check(_lib.load().detlsh_gpu_query(index.handle, p(queries), int(queries.shape[0]), k,
-                                       flags, p(ids), p(dists), p(n_hits), p(radius),
-                                       p(cands), stream))
+    check(_lib.load().detlsh_gpu_query(index.handle, p(queries), nq, k, flags, p(ids), p(dists),
+                                       p(n_hits), p(radius), p(cands), stream))
+
+
+def query_check(index: DetIndex, stream=None) -> None:
+    """Synchronise and raise if an earlier device-pointer batch failed an internal check."""
+    check(_lib.load().detlsh_gpu_query_check(index.handle, stream))
 
 
 def brute_force_knn(data, queries, k: int, *, dist2_bound=None, device: int = 0):
@@ -422,11 +460,97 @@ def ck_ann(index: DetIndex, q, k: int) -> QueryResult:
 def merge_topk_device(shard_dists, shard_ids, shard_hits, k: int, out_dists, out_ids, out_hits,
                       stream=None) -> None:
     """Merge per-shard top-k lists ([shards][nq][k], device tensors) into the global top-k."""
+    import torch
     shards, nq = int(shard_dists.shape[0]), int(shard_dists.shape[1])
+    _check_tensor(shard_dists, "merge_topk: shard_dists", torch.float64, (shards, nq, k))
+    _check_tensor(shard_ids, "merge_topk: shard_ids", torch.int64, (shards, nq, k))
+    _check_tensor(shard_hits, "merge_topk: shard_hits", torch.int32, (shards, nq))
+    _check_tensor(out_dists, "merge_topk: out_dists", torch.float64, (nq, k))
+    _check_tensor(out_ids, "merge_topk: out_ids", torch.int64, (nq, k))
+    _check_tensor(out_hits, "merge_topk: out_hits", torch.int32, (nq,))
     check(_lib.load().detlsh_gpu_merge_topk(
         C.c_void_p(shard_dists.data_ptr()), C.c_void_p(shard_ids.data_ptr()),
         C.c_void_p(shard_hits.data_ptr()), shards, nq, k, C.c_void_p(out_dists.data_ptr()),
         C.c_void_p(out_ids.data_ptr()), C.c_void_p(out_hits.data_ptr()), stream))
+
+
+class ShardedIndex:
+    """Point-sharded index in one process (detlsh_gpu_sharded_*):
+    shard s = rows [s*n/S, (s+1)*n/S) on devices[s], an independent DET-LSH
+    index; queries merge per (distance, global position) on devices[0]."""
+
+    def __init__(self, handle, params: LshParams, n: int, d: int, devices):
+        self._h = handle
+        self.params = params
+        self.n, self.d, self.devices = n, d, list(devices)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.load().detlsh_gpu_sharded_free(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def shard(self, s: int) -> DetIndex:
+        """Borrowed view of shard s (a DetIndex: export, per-shard queries)."""
+        lib = _lib.load()
+        b, e = C.c_uint64(0), C.c_uint64(0)
+        h = lib.detlsh_gpu_sharded_shard(self._h, s, C.byref(b), C.byref(e))
+        if not h:
+            raise ValueError("no such shard")
+        cp = Params()
+        check(lib.detlsh_gpu_get_params(h, C.byref(cp)))
+        v = DetIndex(C.c_void_p(h), LshParams.from_c(cp), e.value - b.value, self.d, self.devices[s], owner=self)
+        v.rows = (b.value, e.value)
+        return v
+
+    def shard_count(self) -> int:
+        return int(_lib.load().detlsh_gpu_sharded_count(self._h))
+
+
+def build_sharded_index(data, params: LshParams | None = None, seed: int = 0, *, devices=(0,),
+                        sample: str = SAMPLE_REFERENCE) -> ShardedIndex:
+    """build_index per contiguous point shard, concurrently on `devices`
+    (one shard per entry; a device may appear several times)."""
+    params = params or LshParams()
+    cp = params.to_c()
+    a = _as_host_f32(data)
+    devs = np.ascontiguousarray(devices, np.int32)
+    h = C.c_void_p()
+    check(_lib.load().detlsh_gpu_sharded_build(_ptr(a), a.shape[0], a.shape[1], C.byref(cp), seed,
+                                               _ptr(devs), len(devs), _flags(sample), C.byref(h)))
+    return ShardedIndex(h, LshParams.from_c(cp), a.shape[0], a.shape[1], devs.tolist())
+
+
+def ck_ann_sharded(index: ShardedIndex, queries, k: int, *, tensor_cores: bool = True):
+    """Batched ck_ann over every shard + merge: (ids [nq][k] u64 global positions,
+    dists [nq][k] f64, n_hits [nq] i32), ascending by (distance, position)."""
+    Q = _as_host_f32(queries)
+    if Q.shape[1] != index.d:
+        raise ValueError("ck_ann: query dimension mismatch")
+    nq = Q.shape[0]
+    ids = np.zeros((nq, k), np.uint64)
+    ds = np.zeros((nq, k), np.float64)
+    nh = np.zeros(nq, np.int32)
+    check(_lib.load().detlsh_gpu_sharded_query(index._h, _ptr(Q), nq, k, 0 if tensor_cores else F_NO_TC,
+                                               _ptr(ids), _ptr(ds), _ptr(nh), None))
+    return ids, ds, nh
+
+
+def ck_ann_sharded_device(index: ShardedIndex, queries, k: int, ids, dists, n_hits, stream=None) -> None:
+    """Stream-ordered sharded ck_ann on CUDA tensors of devices[0]."""
+    import torch
+    nq = int(queries.shape[0])
+    dev = index.devices[0]
+    _check_tensor(queries, "ck_ann: queries", torch.float32, (nq, index.d), dev)
+    _check_tensor(ids, "ck_ann: ids", torch.int64, (nq, k), dev)
+    _check_tensor(dists, "ck_ann: dists", torch.float64, (nq, k), dev)
+    _check_tensor(n_hits, "ck_ann: n_hits", torch.int32, (nq,), dev)
+    check(_lib.load().detlsh_gpu_sharded_query(index._h, C.c_void_p(queries.data_ptr()), nq, k, F_DEVICE_PTRS,
+                                               C.c_void_p(ids.data_ptr()), C.c_void_p(dists.data_ptr()),
+                                               C.c_void_p(n_hits.data_ptr()), stream))
 
 
 # ---- stage functions ----------------------------------------------------------------

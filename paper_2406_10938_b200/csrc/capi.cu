@@ -16,6 +16,7 @@
 #include "vecio.cuh"
 #include "gt.cuh"
 #include "query.cuh"
+#include "sharded.cuh"
 #include "stages.cuh"
 #include "tree.cuh"
 
@@ -75,6 +76,14 @@ using namespace detlsh_b200;
 
 struct detlsh_gpu_index {
     std::unique_ptr<GpuIndex> impl;
+};
+struct detlsh_gpu_sharded_index {
+    std::unique_ptr<ShardedIndex> impl;
+    // borrowed per-shard handles (own nothing: release() before destruction)
+    std::vector<std::unique_ptr<detlsh_gpu_index>> views;
+    ~detlsh_gpu_sharded_index() {
+        for (auto& v : views) (void)v->impl.release();
+    }
 };
 struct detlsh_gpu_tree {
     std::unique_ptr<DevTree> impl;
@@ -196,6 +205,56 @@ int detlsh_gpu_query(const detlsh_gpu_index* index, const float* queries, uint64
                    cands_seen, static_cast<cudaStream_t>(stream));
     });
 }
+
+int detlsh_gpu_query_check(const detlsh_gpu_index* index, void* stream) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("ck_ann: index is null");
+        GpuIndex& X = *index->impl;
+        DeviceGuard dg(X.device);
+        std::lock_guard<std::mutex> lock(X.qmu);
+        cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : X.main.s;
+        if (query_invariant_failed(X.scratch, s))
+            throw CudaError("ck_ann: internal invariant violated (budget cut emitted != budget rows)");
+    });
+}
+
+int detlsh_gpu_sharded_build(const float* points, uint64_t n, int32_t d, detlsh_params* params, uint64_t seed,
+                             const int32_t* devices, int32_t shards, uint32_t flags,
+                             detlsh_gpu_sharded_index** out) {
+    return guarded([&] {
+        if (!out) throw InvalidArgument("build_index: out is null");
+        *out = nullptr;
+        auto h = std::make_unique<detlsh_gpu_sharded_index>();
+        h->impl = sharded_build(points, n, d, params, seed, devices, shards, flags);
+        for (auto& sh : h->impl->shards) {
+            h->views.push_back(std::make_unique<detlsh_gpu_index>());
+            h->views.back()->impl.reset(sh.get());
+        }
+        *out = h.release();
+    });
+}
+
+int detlsh_gpu_sharded_query(detlsh_gpu_sharded_index* index, const float* queries, uint64_t nq, int32_t k,
+                             uint32_t flags, uint64_t* ids, double* dists, int32_t* n_hits, void* stream) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("ck_ann: index is null");
+        sharded_query(*index->impl, queries, nq, k, flags, ids, dists, n_hits, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int32_t detlsh_gpu_sharded_count(const detlsh_gpu_sharded_index* index) {
+    return index ? static_cast<int32_t>(index->views.size()) : 0;
+}
+
+const detlsh_gpu_index* detlsh_gpu_sharded_shard(const detlsh_gpu_sharded_index* index, int32_t s,
+                                                 uint64_t* row_begin, uint64_t* row_end) {
+    if (!index || s < 0 || s >= static_cast<int32_t>(index->views.size())) return nullptr;
+    if (row_begin) *row_begin = index->impl->offsets[s];
+    if (row_end) *row_end = index->impl->offsets[s + 1];
+    return index->views[s].get();
+}
+
+void detlsh_gpu_sharded_free(detlsh_gpu_sharded_index* index) { delete index; }
 
 int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint64_t nq, double r,
                       double c, uint32_t flags, uint32_t* ids, double* dists, int32_t* found,

@@ -714,8 +714,12 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
         }
         DETLSH_CUDA(cudaStreamSynchronize(s));
         for (const auto& c : copies) std::memcpy(c.first->dst, stage + c.second, c.first->bytes);
+        // host mode returns results, so it also reports a failed internal
+        // check (device mode: detlsh_gpu_query_check)
+        if (query_invariant_failed(X.scratch, s))
+            throw CudaError("ck_ann: internal invariant violated (budget cut emitted != budget rows)");
     }
-    DETLSH_CUDA(cudaStreamSynchronize(s));
+    // device mode: stream-ordered, returns once enqueued
 }
 
 }  // namespace detlsh_b200

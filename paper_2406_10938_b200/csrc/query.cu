@@ -40,6 +40,7 @@ constexpr int kTopCap = 2048;                   // staged (key, pos) entries
 constexpr int kBins = 1024;                     // mindist histogram bins (fast-path cut)
 constexpr int kFine = kBins * 32;               // approximate round: fine bins kept per leaf
 constexpr uint32_t kTcMinBudget = 8192;         // tensor-core hand-off from this budget on
+constexpr int kMergeMaxShards = 1024;           // merge_topk: shards per call
 constexpr uint32_t kTauRows = 512;              // min rows scored exactly to set tau^2
 static_assert(kFastMaxK == kTopCap - kBatch, "fast-path k bound");
 
@@ -642,6 +643,17 @@ __device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, 
     return f;
 }
 
+// Device-memory ceilings of the per-CTA query scratch (the fast path's slots
+// hold 4 B per budget candidate; the general path's an n-bit bitmap plus 12 B
+// per candidate); DETLSH_FAST_SCRATCH_MB / DETLSH_SLOW_SCRATCH_MB override.
+size_t scratch_limit_env(const char* name, size_t dflt_mb) {
+    const char* e = std::getenv(name);
+    const size_t mb = e ? static_cast<size_t>(std::max(1L, std::atol(e))) : dflt_mb;
+    return mb << 20;
+}
+size_t fast_scratch_limit() { return scratch_limit_env("DETLSH_FAST_SCRATCH_MB", 8192); }
+size_t slow_scratch_limit() { return scratch_limit_env("DETLSH_SLOW_SCRATCH_MB", 512); }
+
 size_t fast_slot_bytes(uint32_t maxl, uint64_t budget) {
     const size_t b = 3 * static_cast<size_t>(maxl) * sizeof(LeafItem) + 8 * static_cast<size_t>(maxl) +
                      4 * budget + 2 * (static_cast<size_t>(maxl) + 8) + 16;
@@ -931,7 +943,8 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             t_prev = t;
         }
     };
-    for (uint64_t qs = P.q_begin + blockIdx.x; qs < P.q_end; qs += gridDim.x) {
+    const uint64_t q_end = P.q_count ? min(P.q_end, P.q_begin + static_cast<uint64_t>(*P.q_count)) : P.q_end;
+    for (uint64_t qs = P.q_begin + blockIdx.x; qs < q_end; qs += gridDim.x) {
         const uint64_t q = P.order ? P.order[qs] : qs;
         const bool u8 = load_query_vec(P, q, S);
         load_query_proj(P, q, 0, S);
@@ -1418,10 +1431,12 @@ __device__ void emit_members(const QueryPlan& P, int tree, const LeafItem* A, ui
 }
 
 __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
-    QueryPlan P, const uint32_t* list, uint32_t count, uint8_t* scratch, size_t slot_bytes) {
+    QueryPlan P, const uint32_t* list, uint32_t count, const uint32_t* count_dev, uint8_t* scratch,
+    size_t slot_bytes) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
     const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.budget);
+    if (count_dev) count = min(count, *count_dev);
     for (uint32_t qi = blockIdx.x; qi < count; qi += gridDim.x) {
         const uint64_t q = list ? list[qi] : qi;
         if (threadIdx.x == 0) S.u32s[7] = 0;  // |S|
@@ -1515,35 +1530,65 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
     }
 }
 
+// One warp per query: lane l owns shards l, l+32, ...; every step the warp
+// takes the smallest (distance, id) head over all shards (two-key shuffle
+// argmin) and the owning lane advances that shard's head.  Any shard count.
 __global__ void merge_topk_kernel(const double* __restrict__ sd, const uint64_t* __restrict__ sid,
                                   const int32_t* __restrict__ sh, int shards, uint64_t nq, int k,
                                   double* od, uint64_t* oid, int32_t* oh) {
-    for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; q < nq;
-         q += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        int head[16];
-        for (int s = 0; s < shards; ++s) head[s] = 0;
-        int out = 0;
-        for (; out < k; ++out) {
-            int best = -1;
-            double bd = 0;
-            uint64_t bi = 0;
-            for (int s = 0; s < shards; ++s) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+    for (uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x / 32) + (threadIdx.x >> 5); q < nq;
+         q += warps) {
+        // this lane's best head over its shards (sentinel: +inf, max id)
+        auto lane_best = [&](double& bd, uint64_t& bi, int& bs, const int* head) {
+            bd = __longlong_as_double(0x7ff0000000000000LL);
+            bi = ~0ULL;
+            bs = -1;
+            for (int j = 0, s = lane; s < shards; ++j, s += 32) {
                 const uint64_t row = static_cast<uint64_t>(s) * nq + q;
-                if (head[s] >= sh[row]) continue;
-                const double d = sd[row * k + head[s]];
-                const uint64_t id = sid[row * k + head[s]];
-                if (best < 0 || d < bd || (d == bd && id < bi)) {
-                    best = s;
+                if (head[j] >= sh[row]) continue;
+                const double d = sd[row * k + head[j]];
+                const uint64_t id = sid[row * k + head[j]];
+                if (bs < 0 || d < bd || (d == bd && id < bi)) {
                     bd = d;
                     bi = id;
+                    bs = s;
                 }
             }
-            if (best < 0) break;
-            od[q * k + out] = bd;
-            oid[q * k + out] = bi;
-            head[best]++;
+        };
+        int head[kMergeMaxShards / 32];
+        for (int j = 0; j < kMergeMaxShards / 32; ++j) head[j] = 0;
+        double bd;
+        uint64_t bi;
+        int bs;
+        lane_best(bd, bi, bs, head);
+        int out = 0;
+        for (; out < k; ++out) {
+            double wd = bd;
+            uint64_t wi = bi;
+            int ws = bs;
+            for (int off = 16; off > 0; off >>= 1) {
+                const double od2 = __shfl_xor_sync(0xffffffffu, wd, off);
+                const uint64_t oi2 = __shfl_xor_sync(0xffffffffu, wi, off);
+                const int os2 = __shfl_xor_sync(0xffffffffu, ws, off);
+                if (os2 >= 0 && (ws < 0 || od2 < wd || (od2 == wd && (oi2 < wi || (oi2 == wi && os2 < ws))))) {
+                    wd = od2;
+                    wi = oi2;
+                    ws = os2;
+                }
+            }
+            if (ws < 0) break;
+            if (lane == 0) {
+                od[q * k + out] = wd;
+                oid[q * k + out] = wi;
+            }
+            if (lane == (ws & 31)) {
+                head[ws >> 5]++;
+                lane_best(bd, bi, bs, head);
+            }
         }
-        oh[q] = out;
+        if (lane == 0) oh[q] = out;
     }
 }
 
@@ -1611,20 +1656,36 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     auto* const fast_kernel = five ? &query_fast_kernel<5> : &query_fast_kernel<3>;
     DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    // persistent scratch lives on the index's own stream (it outlives any
-    // caller stream); make it visible to `s` before use
+    // Persistent scratch lives on the index's own stream (it outlives any
+    // caller stream).  Growing it is the one host wait of a batch, and only
+    // happens when a batch needs more scratch than every earlier one.
+    // under stream capture the graph's own dependencies order its replays;
+    // otherwise the batch waits for the previous one (any stream) to release
+    // the scratch
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    DETLSH_CUDA(cudaStreamIsCapturing(s, &cap_st));
+    const bool capturing = cap_st != cudaStreamCaptureStatusNone;
+    bool grew = false;
     auto grow_scratch = [&](auto& buf, size_t count) {
         if (buf.size() >= count) return;
+        if (capturing) throw InvalidArgument("ck_ann: the first batch of a shape cannot be captured (scratch grows)");
+        if (!grew && X.done) DETLSH_CUDA(cudaEventSynchronize(X.done));  // earlier batches still read it
+        grew = true;
         {
             StreamScope sc(alloc_s);
             buf.alloc(count);
         }
         DETLSH_CUDA(cudaStreamSynchronize(alloc_s));
     };
+    if (!X.done) DETLSH_CUDA(cudaEventCreateWithFlags(&X.done, cudaEventDisableTiming));
+    else if (!capturing) DETLSH_CUDA(cudaStreamWaitEvent(s, X.done, 0));
     grow_scratch(X.counters, 4);
     grow_scratch(X.slow_list, P.nq);
-    DETLSH_CUDA(cudaMemsetAsync(X.counters.get(), 0, 16, s));
+    // counters: slow-path and overflow counts reset per batch; the invariant flag is sticky
+    DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntSlow, 0, 4, s));
+    DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntOver, 0, 4, s));
     QueryPlan Pp = P;
+    Pp.q_count = nullptr;
     if (profiling_enabled()) {
         grow_scratch(X.phases, 8);
         DETLSH_CUDA(cudaMemsetAsync(X.phases.get(), 0, 8 * sizeof(unsigned long long), s));
@@ -1650,14 +1711,16 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         Pp.order = flip ? ov1.get() : ov0.get();
     }
     const size_t items = 3 * static_cast<size_t>(P.max_leaves) * sizeof(LeafItem);
-    uint32_t slow_count = 0;
-    const uint32_t* slow_list = X.slow_list.get();
-    if (P.k <= kFastMaxK && !P.rc_mode) {
+    const bool fast_path = P.k <= kFastMaxK && !P.rc_mode;
+    if (fast_path) {
         int per_sm = 0;
         DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast_kernel, kQueryThreads, smem));
         per_sm = std::max(1, std::min(per_sm, 6));
         const size_t fast_bytes = fast_slot_bytes(P.max_leaves, P.budget);
-        const size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
+        // processing slots: a CTA each, bounded by the scratch they need
+        // (fast_bytes grows with the budget: 4 B per candidate)
+        size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
+        slots = std::max<size_t>(1, std::min<size_t>(slots, fast_scratch_limit() / fast_bytes));
         grow_scratch(X.fast, slots * fast_bytes);
         auto launch_fast = [&](const QueryPlan& Pc) {
             const uint64_t m = Pc.q_end - Pc.q_begin;
@@ -1667,15 +1730,14 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 Pc, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
             DETLSH_LAUNCH_CHECK();
         };
-        // u8 rows with a large budget: the plan kernel hands each query's
-        // candidate set to the tcgen05 dataset-major scorer (tc_score.cu)
         // test hook: exact fp64 mindists for every leaf (no approximate round)
         if (std::getenv("DETLSH_TEST_EXACT_SCAN")) Pp.force_exact = 1;
         Pp.tc_tau_rows = static_cast<uint32_t>(std::min<uint64_t>(tau_rows, 0xffffffffULL));
-        DevBuf<uint32_t> over_list;
         if (!tc_ok) {
             launch_fast(Pp);
         } else {
+            // u8 rows with a large budget: the plan kernel hands each query's
+            // candidate set to the tcgen05 dataset-major scorer (tc_score.cu)
             const int R = P.row_u8;
             const uint64_t W = ((P.n + 31) / 32 + 3) / 4 * 4;  // bitmap words per query, rows 16-B aligned
             // test hook: a smaller staging buffer forces the overflow re-run
@@ -1687,7 +1749,11 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             uint64_t chunk = (3ULL << 30) / (W * 4 + 160 * 1024);
             chunk = std::max<uint64_t>(256, chunk / 256 * 256);
             chunk = std::min<uint64_t>(chunk, (P.nq + 255) / 256 * 256);
-            const uint64_t rec_cap = chunk * 8192;  // candidate threshold passes staged per chunk
+            // pass records staged per chunk: ~8192 per query, plus the runs of
+            // kTcRecChunk slots the scorer's warps reserve ahead of use
+            uint64_t rec_cap = chunk * 8192 + static_cast<uint64_t>(sms) * kTcRecReserve;
+            if (const char* e = std::getenv("DETLSH_TEST_REC_CAP"))  // test hook: force the overflow path
+                rec_cap = std::max<uint64_t>(1, std::min<uint64_t>(std::strtoull(e, nullptr, 10), rec_cap));
             grow_scratch(X.tc_bm, chunk * W);
             grow_scratch(X.tc_tau2, chunk);
             grow_scratch(X.tc_qn, chunk);
@@ -1696,112 +1762,100 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             grow_scratch(X.tc_surv, chunk * kTcFinishCap);
             grow_scratch(X.tc_rec, rec_cap);
             grow_scratch(X.tc_rec_cnt, 1);
-            DevBuf<uint32_t>& bm = X.tc_bm;
-            DevBuf<int32_t>& tau2 = X.tc_tau2;
-            DevBuf<int32_t>& qn = X.tc_qn;
-            DevBuf<uint32_t>& surv_cnt = X.tc_surv_cnt;
-            DevBuf<uint8_t>& q8 = X.tc_q8;
-            DevBuf<uint64_t>& surv = X.tc_surv;
-            DevBuf<uint4>& rec = X.tc_rec;
-            DevBuf<unsigned long long>& rec_cnt = X.tc_rec_cnt;
-            over_list.alloc(P.nq);
+            grow_scratch(X.over_list, P.nq);
             for (uint64_t c0 = 0; c0 < P.nq; c0 += chunk) {
                 const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);
-                DETLSH_CUDA(cudaMemsetAsync(tau2.get(), 0xff, m * 4, s));
-                DETLSH_CUDA(cudaMemsetAsync(surv_cnt.get(), 0, m * 4, s));
-                DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + 3, 0, 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(X.tc_tau2.get(), 0xff, m * 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(X.tc_surv_cnt.get(), 0, m * 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntWork, 0, 4, s));
                 QueryPlan Pc = Pp;
                 Pc.q_begin = c0;
                 Pc.q_end = c0 + m;
-                Pc.tc_bm = bm.get();
+                Pc.tc_bm = X.tc_bm.get();
                 Pc.tc_W = W;
-                Pc.tc_tau2 = tau2.get();
+                Pc.tc_tau2 = X.tc_tau2.get();
                 launch_fast(Pc);
-                launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, q8.get(), qn.get(), s);
+                launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, X.tc_q8.get(), X.tc_qn.get(), s);
                 TcScoreArgs a{};
                 a.rows = P.data_tc;
                 a.xn = P.xn_u8;
-                a.q8 = q8.get();
-                a.qn = qn.get();
-                a.tau2 = tau2.get();
-                a.bm = bm.get();
+                a.q8 = X.tc_q8.get();
+                a.qn = X.tc_qn.get();
+                a.tau2 = X.tc_tau2.get();
+                a.bm = X.tc_bm.get();
                 a.W = W;
                 a.n = P.n;
                 a.nq = m;
                 a.R = R;
-                a.surv_cnt = surv_cnt.get();
-                a.surv = surv.get();
+                a.surv_cnt = X.tc_surv_cnt.get();
+                a.surv = X.tc_surv.get();
                 a.cap = tc_cap;
                 a.order = Pp.order;
                 a.slot0 = c0;
-                a.work = X.counters.get() + 3;
-                a.rec = rec.get();
-                a.rec_cnt = rec_cnt.get();
+                a.work = X.counters.get() + kCntWork;
+                a.rec = X.tc_rec.get();
+                a.rec_cnt = X.tc_rec_cnt.get();
                 a.rec_cap = rec_cap;
-                DETLSH_CUDA(cudaMemsetAsync(rec_cnt.get(), 0, 8, s));
+                DETLSH_CUDA(cudaMemsetAsync(X.tc_rec_cnt.get(), 0, 8, s));
                 launch_tc_score(a, device, s);
-                unsigned long long used = 0;
-                DETLSH_CUDA(cudaMemcpyAsync(&used, rec_cnt.get(), 8, cudaMemcpyDeviceToHost, s));
-                DETLSH_CUDA(cudaStreamSynchronize(s));
-                if (std::getenv("DETLSH_TC_DEBUG"))
-                    std::fprintf(stderr, "tc_score: %llu pass records reserved (cap %llu) for %llu queries\n", used,
-                                 static_cast<unsigned long long>(rec_cap), static_cast<unsigned long long>(m));
-                if (used > rec_cap) {  // pass list overflowed: this chunk takes the gather path
-                    QueryPlan Pg = Pp;
-                    Pg.q_begin = c0;
-                    Pg.q_end = c0 + m;
-                    launch_fast(Pg);
-                    continue;
-                }
+                // queries whose survivors overflowed (or whose chunk's pass
+                // records did) are listed for the gather path below
                 launch_tc_finish(a, P.perm0, P.k, P.r_min, P.budget, P.ids, P.dists, P.n_hits, P.radius,
-                                 P.cands, over_list.get(), X.counters.get() + 2, s);
+                                 P.cands, X.over_list.get(), X.counters.get() + kCntOver, s);
             }
-            uint32_t n_over = 0;
-            DETLSH_CUDA(cudaMemcpyAsync(&n_over, X.counters.get() + 2, 4, cudaMemcpyDeviceToHost, s));
-            DETLSH_CUDA(cudaStreamSynchronize(s));
-            if (n_over) {  // survivors overflowed the staging buffer: gather path for those
-                QueryPlan Pc = Pp;
-                Pc.order = over_list.get();
-                Pc.q_begin = 0;
-                Pc.q_end = n_over;
-                launch_fast(Pc);
-            }
+            // gather path for the listed queries: the count stays on the device
+            QueryPlan Pc = Pp;
+            Pc.order = X.over_list.get();
+            Pc.q_begin = 0;
+            Pc.q_end = P.nq;
+            Pc.q_count = X.counters.get() + kCntOver;
+            launch_fast(Pc);
         }
-        uint32_t flags[2] = {0, 0};
-        DETLSH_CUDA(cudaMemcpyAsync(flags, X.counters.get(), 8, cudaMemcpyDeviceToHost, s));
-        unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (Pp.phase_cycles)
+        if (Pp.phase_cycles && !capturing) {  // profiling only: the phase split is read back here
+            unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             DETLSH_CUDA(cudaMemcpyAsync(ph, Pp.phase_cycles, sizeof(ph), cudaMemcpyDeviceToHost, s));
-        DETLSH_CUDA(cudaStreamSynchronize(s));
-        if (Pp.phase_cycles) {
+            DETLSH_CUDA(cudaStreamSynchronize(s));
             std::lock_guard<std::mutex> lk(g_phase_mu);
             for (int i = 0; i < 8; ++i) g_phase[i] = static_cast<double>(ph[i]);
         }
-        slow_count = flags[0];
-        if (flags[1]) throw CudaError("ck_ann: internal invariant violated (budget cut emitted != budget rows)");
-    } else {
-        slow_count = static_cast<uint32_t>(P.nq);
-        slow_list = nullptr;  // every query takes the general path
     }
-    if (slow_count == 0) return;
+    // general path: the queries the fast path listed (count on the device), or
+    // every query (k beyond the fast path, rc_ann).  A fixed number of slots,
+    // each looping over the list; a slot's bitmap is cleared by the kernel.
+    const uint64_t n_list = fast_path ? P.nq : P.nq;
     const size_t slow_bytes = (items + 12 * P.budget + ((P.n + 31) / 32) * 4 + 255) / 256 * 256;
-    const size_t slots = std::min<size_t>(slow_count, static_cast<size_t>(sms));
+    size_t slots = std::min<size_t>(n_list, static_cast<size_t>(sms));
+    slots = std::max<size_t>(1, std::min<size_t>(slots, slow_scratch_limit() / slow_bytes));
     if (X.slow_slots < slots || X.slow.size() < slots * slow_bytes) {
+        if (capturing) throw InvalidArgument("ck_ann: the first batch of a shape cannot be captured (scratch grows)");
+        if (X.done) DETLSH_CUDA(cudaEventSynchronize(X.done));
         X.slow.release();
         grow_scratch(X.slow, slots * slow_bytes);
         DETLSH_CUDA(cudaMemsetAsync(X.slow.get(), 0, slots * slow_bytes, s));
         X.slow_slots = slots;
     }
-    ProfScope ps("query_slow", s);
-    query_slow_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
-        P, slow_list, slow_count, X.slow.get(), slow_bytes);
-    DETLSH_LAUNCH_CHECK();
+    {
+        ProfScope ps("query_slow", s);
+        query_slow_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
+            P, fast_path ? X.slow_list.get() : nullptr, static_cast<uint32_t>(n_list),
+            fast_path ? X.counters.get() + kCntSlow : nullptr, X.slow.get(), slow_bytes);
+        DETLSH_LAUNCH_CHECK();
+    }
+    if (!capturing) DETLSH_CUDA(cudaEventRecord(X.done, s));
+}
+
+bool query_invariant_failed(QueryScratch& X, cudaStream_t s) {
+    if (!X.counters.get()) return false;
+    uint32_t flag = 0;
+    DETLSH_CUDA(cudaMemcpyAsync(&flag, X.counters.get() + kCntInvariant, 4, cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    return flag != 0;
 }
 
 void launch_merge_topk(const double* sd, const uint64_t* sid, const int32_t* sh, int shards,
                        uint64_t nq, int k, double* od, uint64_t* oid, int32_t* oh, cudaStream_t s) {
-    if (shards > 16) throw InvalidArgument("merge_topk: at most 16 shards");
-    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((nq + 127) / 128, 65535)));
+    if (shards < 1 || shards > kMergeMaxShards) throw InvalidArgument("merge_topk: 1 to 1024 shards");
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((nq + 3) / 4, 65535)));
     merge_topk_kernel<<<grid, 128, 0, s>>>(sd, sid, sh, shards, nq, k, od, oid, oh);
     DETLSH_LAUNCH_CHECK();
 }

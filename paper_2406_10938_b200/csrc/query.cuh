@@ -55,8 +55,10 @@ struct QueryPlan {
     unsigned long long* phase_cycles;
     // optional processing order (locality): processing slot i handles query order[i]
     const uint32_t* order;
-    // processed range of processing slots [q_begin, q_end)
+    // processed range of processing slots [q_begin, q_end); with q_count set
+    // the range ends at min(q_end, *q_count) (a count produced on the device)
     uint64_t q_begin, q_end;
+    const uint32_t* q_count;
     // tensor-core verification hand-off (null: score every candidate here).
     // Indexed by slot - q_begin: the candidate set as a bitmap over tree-0
     // rows ([tc_W] words per slot: whole leaves + the cut leaf's taken
@@ -93,10 +95,20 @@ struct QueryScratch {
     DevBuf<uint64_t> tc_surv;
     DevBuf<uint4> tc_rec;
     DevBuf<unsigned long long> tc_rec_cnt;
+    DevBuf<uint32_t> over_list;
+    // completion of the last batch that used this scratch: a batch on another
+    // stream waits for it (the enqueue is serialised by the index mutex)
+    cudaEvent_t done = nullptr;
+    ~QueryScratch() {
+        if (done) cudaEventDestroy(done);
+    }
 };
 
 // ---- tensor-core exact verification (tc_score.cu) ----
 constexpr uint32_t kTcFinishCap = 4096;  // survivors staged per query
+// pass-record slots one tc_score CTA may hold reserved ahead of use
+// (epilogue warps x the run each reserves; checked in tc_score.cu)
+constexpr uint64_t kTcRecReserve = 16 * 1024;
 
 struct TcScoreArgs {
     const uint8_t* rows;   // u8 rows, tree-0 order, packed by launch_pack_tc_tiles
@@ -130,6 +142,9 @@ void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s);
 void launch_tc_finish(const TcScoreArgs& a, const uint32_t* perm0, int k, double r_min,
                       uint64_t budget, uint32_t* ids, double* dists, int32_t* n_hits, double* radius,
                       uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, cudaStream_t s);
+// counters[] of QueryScratch: [0] slow-path queries, [1] sticky internal-invariant
+// flag, [2] tensor-core overflow queries, [3] tc_score work counter
+constexpr int kCntSlow = 0, kCntInvariant = 1, kCntOver = 2, kCntWork = 3;
 
 // tcgen05 kind::i8 self-test (tc_score.cu): C[128][N] = A[128][K] . B[N][K]^T.
 void tc_gemm_u8_test(const uint8_t* hA, const uint8_t* hB, int N, int K, int32_t* hC);
@@ -138,8 +153,13 @@ void tc_gemm_u8_test(const uint8_t* hA, const uint8_t* hB, int N, int K, int32_t
 // emission, verification+top-k, output), summed over CTAs.
 void last_query_phases(double* out6);
 
+// Stream-ordered: every decision (tensor-core overflow, slow-path queries) is
+// taken on the device; the host never waits, except to grow the scratch on the
+// first call with a larger shape, and when profiling is enabled.
 void run_query_batch(const QueryPlan& plan, QueryScratch& scratch, int device, cudaStream_t s,
                      cudaStream_t alloc_s);
+// Reads the sticky internal-invariant flag (synchronises s).
+bool query_invariant_failed(QueryScratch& scratch, cudaStream_t s);
 
 // k-way merge of per-shard top-k lists: [shards][nq][k] -> [nq][k].
 void launch_merge_topk(const double* sd, const uint64_t* sid, const int32_t* sh, int shards,

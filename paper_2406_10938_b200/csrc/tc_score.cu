@@ -160,6 +160,7 @@ constexpr int kEpiCols = kTcQueries / (kEpiWarps / 4);  // query columns per epi
 constexpr int kEpiWords = kEpiCols / 32;           // candidate words per lane (columns per lane)
 constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
 constexpr uint32_t kTcRecChunk = 1024;  // records reserved per warp at a time
+static_assert(kTcRecReserve >= static_cast<uint64_t>(kEpiWarps) * kTcRecChunk, "rec_cap slack");
 constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
 constexpr uint32_t kWaitHintNs = 20000;  // mbarrier try_wait suspend hint (woken on completion)
 constexpr int kQSplit = 2;               // MMAs (and accumulator barriers) per tile, one per query part (4: slower)
@@ -424,11 +425,14 @@ __global__ void __launch_bounds__(256) tc_finish_kernel(TcScoreArgs a, const uin
                                                         double* radius, uint64_t* cands,
                                                         uint32_t* overflow_list, uint32_t* overflow_n) {
     __shared__ uint64_t key[kTcFinishCap];  // (d2 << 32) | position, sorted ascending
+    // the pass-record list overflowed: no survivor list of this chunk is
+    // complete, so every tensor-core query of the chunk takes the gather path
+    const bool rec_over = *a.rec_cnt > a.rec_cap;
     for (uint64_t slot = blockIdx.x; slot < a.nq; slot += gridDim.x) {
         if (a.tau2[slot] < 0) continue;
         const uint64_t q = a.order ? a.order[a.slot0 + slot] : a.slot0 + slot;
         const uint32_t cnt = a.surv_cnt[slot];
-        if (cnt > a.cap) {  // threshold too loose for the staging buffer: rerun on the gather path
+        if (rec_over || cnt > a.cap) {  // threshold too loose for the staging: rerun on the gather path
             if (threadIdx.x == 0) overflow_list[atomicAdd(overflow_n, 1u)] = static_cast<uint32_t>(q);
             continue;
         }

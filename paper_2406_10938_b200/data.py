@@ -51,23 +51,25 @@ def sparse_geometric(total: int, d: int, seed: int, p: float = 0.05) -> np.ndarr
 
 def blobs784(total: int, seed: int) -> np.ndarray:
     rng = np.random.Generator(np.random.PCG64(seed))
-    yy, xx = np.mgrid[0:28, 0:28]
-    grid = np.stack([yy.ravel(), xx.ravel()], 1).astype(np.float32)  # [784, 2]
+    g28 = np.arange(28, dtype=np.float32)
     out = np.zeros((total, 784), np.float32)
     step = 1 << 13
     for s in range(0, total, step):
         e = min(total, s + step)
         m = e - s
         nb = rng.integers(3, 7, size=m)
-        mask = np.zeros((m, 784), bool)
+        mask = np.zeros((m, 28, 28), bool)
         for b in range(6):
             active = nb > b
             ctr = rng.uniform(0, 27, size=(m, 2)).astype(np.float32)
             rad = rng.uniform(3, 6, size=m).astype(np.float32)
-            d2 = ((grid[None, :, :] - ctr[:, None, :]) ** 2).sum(-1)
-            mask |= active[:, None] & (d2 < 0.5 * (rad ** 2)[:, None])
+            # squared distance of grid cell (y, x) to the blob centre, in float32
+            dy2 = (g28[None, :] - ctr[:, 0:1]) ** 2
+            dx2 = (g28[None, :] - ctr[:, 1:2]) ** 2
+            d2 = dy2[:, :, None] + dx2[:, None, :]
+            mask |= active[:, None, None] & (d2 < 0.5 * (rad ** 2)[:, None, None])
         vals = rng.integers(1, 256, size=(m, 784)).astype(np.float32)
-        out[s:e] = np.where(mask, vals, 0.0)
+        out[s:e] = np.where(mask.reshape(m, 784), vals, 0.0)
     return out
 
 

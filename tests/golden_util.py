@@ -16,7 +16,10 @@ FIELDS = ["K", "L", "c", "beta", "epsilon", "alpha1", "alpha2", "n_regions", "sa
 
 
 def cases():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(HERE, "golden", "*.npz")))
+    """The small fixtures of make_golden.py (the cfg_*.npz config fixtures of
+    make_golden_configs.py are loaded by test_gpu_configs.py)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(HERE, "golden", "*.npz"))
+                  if not os.path.basename(p).startswith("cfg_"))
 
 
 def load(name):

@@ -1,0 +1,108 @@
+"""Stream-ordered batched ck_ann (include/detlsh_b200.h detlsh_gpu_query):
+device-side overflow handling, no host waits, CUDA-graph capture."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _sparse_u8(g, n, d):
+    return np.where(g.random((n, d)) < 0.5, 0, np.minimum(g.geometric(0.05, (n, d)), 255)).astype(np.float32)
+
+
+@pytest.fixture(scope="module")
+def u8_index(gpu):
+    g = np.random.Generator(np.random.PCG64(77))
+    n, d = 60000, 128
+    data = _sparse_u8(g, n, d)
+    idx = gpu.build_index(data, gpu.LshParams(beta=0.2, k=20), seed=5)
+    assert idx.row_u8() == 128
+    return data, idx, g
+
+
+def _far_queries(g, m, d):
+    # far from every point: round 0 of tree 0 does not fill the budget, so
+    # these queries take the general (slow) path
+    return np.full((m, d), 255.0, np.float32) - g.integers(0, 3, (m, d)).astype(np.float32)
+
+
+def test_pass_record_overflow_with_slow_queries(gpu, u8_index, monkeypatch):
+    """A pass-record overflow in tc_score sends the whole chunk to the gather
+    path on the device; more than half of the batch on the slow path must not
+    overrun the slow-query list (each query is listed once)."""
+    data, idx, g = u8_index
+    k = 20
+    Q = np.concatenate([_far_queries(g, 400, data.shape[1]), _sparse_u8(g, 200, data.shape[1])])
+    want = gpu.ck_ann_batch(idx, Q, k, tensor_cores=False)
+    assert (want.radius_used > idx.params.r_min).sum() > Q.shape[0] // 2, "slow path not exercised"
+    monkeypatch.setenv("DETLSH_TEST_REC_CAP", "1000")
+    got = gpu.ck_ann_batch(idx, Q, k)
+    assert np.array_equal(got.n_hits, want.n_hits)
+    assert np.array_equal(got.ids, want.ids)
+    assert np.array_equal(got.dists.view(np.uint64), want.dists.view(np.uint64))
+    assert np.array_equal(got.radius_used, want.radius_used)
+    assert np.array_equal(got.candidates_seen, want.candidates_seen)
+
+
+def test_small_batch_does_not_overflow_records(gpu, u8_index, monkeypatch):
+    """rec_cap covers the runs the scorer's warps reserve ahead of use: a
+    one-query batch on a u8 index must finish on the tensor-core path."""
+    data, idx, g = u8_index
+    Q = _sparse_u8(g, 1, data.shape[1])
+    monkeypatch.setenv("DETLSH_TC_DEBUG", "1")
+    want = gpu.ck_ann_batch(idx, Q, 20, tensor_cores=False)
+    got = gpu.ck_ann_batch(idx, Q, 20)
+    assert np.array_equal(got.ids, want.ids)
+    assert np.array_equal(got.dists, want.dists)
+
+
+def test_device_mode_is_stream_ordered_and_capturable(gpu, u8_index):
+    """Device pointers: the call only enqueues (results appear after the stream
+    is synchronised), two streams reuse the scratch in order, and after one
+    warm-up call the enqueue can be captured into a CUDA graph and replayed."""
+    import torch
+    data, idx, g = u8_index
+    k = 20
+    Q = np.concatenate([_sparse_u8(g, 700, data.shape[1]), _far_queries(g, 20, data.shape[1])])
+    want = gpu.ck_ann_batch(idx, Q, k)
+    nq = Q.shape[0]
+    dq = torch.from_numpy(Q).cuda()
+
+    def outs():
+        return (torch.full((nq, k), -1, dtype=torch.int32, device="cuda"),
+                torch.zeros((nq, k), dtype=torch.float64, device="cuda"),
+                torch.zeros(nq, dtype=torch.int32, device="cuda"),
+                torch.zeros(nq, dtype=torch.float64, device="cuda"),
+                torch.zeros(nq, dtype=torch.int64, device="cuda"))
+
+    def same(o):
+        m = want.n_hits
+        assert np.array_equal(o[2].cpu().numpy(), m)
+        assert np.array_equal(o[0].cpu().numpy().view(np.uint32), want.ids)
+        assert np.array_equal(o[1].cpu().numpy().view(np.uint64), want.dists.view(np.uint64))
+        assert np.array_equal(o[3].cpu().numpy(), want.radius_used)
+        assert np.array_equal(o[4].cpu().numpy().view(np.uint64), want.candidates_seen)
+
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1, o2 = outs(), outs()
+    torch.cuda.synchronize()
+    gpu.ck_ann_device(idx, dq, k, *o1, stream=s1.cuda_stream)
+    gpu.ck_ann_device(idx, dq, k, *o2, stream=s2.cuda_stream)  # waits for s1's batch on the device
+    torch.cuda.synchronize()
+    same(o1)
+    same(o2)
+    gpu.query_check(idx)
+    # graph capture of the (warm) enqueue, replayed twice into fresh outputs
+    o3 = outs()
+    s3 = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s3):
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s3):
+            gpu.ck_ann_device(idx, dq, k, *o3, stream=s3.cuda_stream)
+    for _ in range(2):
+        for t in o3:
+            t.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        same(o3)

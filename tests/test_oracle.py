@@ -115,3 +115,25 @@ def test_rng_streams_match_reference(port, ref):
         u2, g2 = ref.rng_stream(seed, 2000)
         assert np.array_equal(u1, u2) and np.array_equal(g1.view(np.uint64), g2.view(np.uint64))
         assert port.mix_seed(seed, 3) == ref.mix_seed(seed, 3)
+
+
+def test_port_reproduces_full_c1_fixture(port):
+    """The C restatement against the reference's full-size C1 result
+    (tests/golden/cfg_c1.npz, made by the compiled reference): same table,
+    trees, r_min and answers on a strided third of the 1,000 queries."""
+    import os
+    from golden_util import FIELDS
+    from paper_2406_10938_b200 import data as gen
+    g = dict(np.load(os.path.join(os.path.dirname(__file__), "golden", "cfg_c1.npz")))
+    base, Q = gen.make("c1")
+    idx = port.build_index(base, make_params(beta=0.1, k=50), int(g["seed"]))
+    got = np.array([getattr(idx.params, f) for f in FIELDS], np.float64)
+    assert np.array_equal(got.view(np.uint64), g["params"].view(np.uint64))
+    assert np.array_equal(idx.table().view(np.uint32), g["table"].view(np.uint32))
+    for i in range(4):
+        assert tree_hash(idx.tree_export(i)) == str(g["tree_hash"][i])
+    for i in range(0, int(g["nq"]), 3):
+        ids, ds, rad, cs = idx.ck_ann(Q[i], 50)
+        m = int(g["n_hits"][i])
+        assert np.array_equal(ids, g["ids"][i, :m]) and np.array_equal(ds, g["dists"][i, :m])
+        assert rad == g["radius"][i] and cs == g["cands"][i]
