@@ -153,6 +153,34 @@ int detlsh_gpu_rc_ann(const detlsh_gpu_index* index, const float* queries, uint6
                       double c, uint32_t flags, uint32_t* ids, double* dists, int32_t* found,
                       uint64_t* cands_seen, void* stream);
 
+/* estimate_rmin (index.hpp:91, index.cpp:333-374): the smallest radius on the
+ * geometric grid (anchored at the median pairwise projected distance of 32
+ * strided points / epsilon) whose candidate count reaches
+ * candidate_budget(beta, n, k) while radius / c falls short, median over the
+ * n_probes probe queries [n_probes][d] (host, or device with
+ * DETLSH_F_DEVICE_PTRS).  n_probes == 0 -> DETLSH_E_INVALID ("no probe queries"). */
+int detlsh_gpu_estimate_rmin(const detlsh_gpu_index* index, const float* probes, uint64_t n_probes, int32_t k,
+                             uint32_t flags, double* r_min);
+
+/* DetIndex::project_query (index.cpp:181-188) for a batch: out [L][nq][K], the
+ * same bits as the reference's project_point (host, or device pointers). */
+int detlsh_gpu_project_query(const detlsh_gpu_index* index, const float* queries, uint64_t nq, float* out,
+                             uint32_t flags);
+
+/* Range queries on one DE-Tree (de_tree.hpp:85-100), host pointers: q_proj
+ * [nq][K] projected queries of that tree's space, radius [nq].
+ *   default: range_query_optimized -- the entries of every leaf with
+ *     mindist <= radius in ascending (mindist, node index) order, leaf by leaf,
+ *     stopping after `limit` positions (the CandidateSink returning false);
+ *   DETLSH_RANGE_EXACT: range_query_exact -- exactly the positions whose
+ *     projected distance is <= radius, in the reference's DFS order.
+ * positions [nq][cap] (the first cap of each list), counts[q] = the list's
+ * full length. */
+#define DETLSH_RANGE_EXACT 0x100u
+int detlsh_gpu_range_query(const detlsh_gpu_index* index, int32_t tree, const float* q_proj, uint64_t nq,
+                           const double* radius, uint64_t limit, uint32_t flags, uint32_t* positions, uint64_t cap,
+                           uint64_t* counts);
+
 /* ---- exact ground truth ------------------------------------------------------- */
 /* brute_force_knn (metrics.hpp, metrics.cpp:8-33) on the GPU: for each query
  * the k smallest l2_distance_sq (sequential fp64, dataset.hpp:23-30) over all

@@ -150,6 +150,12 @@ class Oracle:
             self.f("build_det_only_index").restype = vp
             self.f("rc_ann").argtypes = [vp, vp, dbl, dbl, vp, vp]
             self.f("rc_ann").restype = i32
+            self.f("index_estimate_rmin").argtypes = [vp, vp, u64, i32]
+            self.f("index_estimate_rmin").restype = dbl
+            self.f("index_project_query").argtypes = [vp, vp, i32, vp]
+            self.f("index_project_query").restype = None
+            self.f("index_range_query").argtypes = [vp, i32, vp, dbl, u64, i32, vp, u64]
+            self.f("index_range_query").restype = u64
 
     # ---- scalar helpers ------------------------------------------------------
     def mix_seed(self, seed, stream):
@@ -363,6 +369,27 @@ class OracleIndex:
         rc = self.o.f("rc_ann")(self.h, _p(q), r, c, C.byref(pos), C.byref(dist))
         assert rc >= 0
         return (pos.value, dist.value) if rc == 1 else None
+
+    def estimate_rmin(self, probes, k):
+        """Reference only: detlsh::estimate_rmin (index.cpp:333-374)."""
+        P = np.ascontiguousarray(probes, np.float32)
+        return float(self.o.f("index_estimate_rmin")(self.h, _p(P), P.shape[0], k))
+
+    def project_query(self, q, space):
+        """Reference only: DetIndex::project_query (index.cpp:181-188)."""
+        q = np.ascontiguousarray(q, np.float32)
+        out = np.empty(self.params.K, np.float32)
+        self.o.f("index_project_query")(self.h, _p(q), space, _p(out))
+        return out
+
+    def range_query(self, tree, q_proj, radius, limit=2**63, exact=False):
+        """Reference only: range_query_optimized (sink stops after `limit`) or
+        range_query_exact on tree `tree` (de_tree.cpp:199-258)."""
+        q = np.ascontiguousarray(q_proj, np.float32)
+        cap = min(self.n, limit)
+        out = np.empty(max(1, cap), np.uint32)
+        m = int(self.o.f("index_range_query")(self.h, tree, _p(q), radius, limit, int(exact), _p(out), cap))
+        return out[:min(m, cap)].copy()
 
     def save(self) -> bytes:
         """Reference only: detlsh::save_index (persist.cpp:99-149) bytes."""

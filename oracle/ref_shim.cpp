@@ -18,6 +18,8 @@
 #include <thread>
 #include <vector>
 
+#include <cmath>
+
 #include "detlsh/chi2.hpp"
 #include "detlsh/de_tree.hpp"
 #include "detlsh/encoder.hpp"
@@ -394,6 +396,54 @@ void ref_index_tree_export(void* h, int tree, int32_t* root_children, uint8_t* i
                            uint32_t* positions) {
     export_tree(idx_of(h).trees[static_cast<size_t>(tree)], root_children, is_leaf, split_dim,
                 left, right, bits, value, ebegin, ecount, positions);
+}
+
+// estimate_rmin (index.cpp:333-374) for caller probes [np][d]; NaN on error.
+double ref_index_estimate_rmin(void* h, const float* probes, uint64_t np, int k) {
+    try {
+        const DetIndex& idx = idx_of(h);
+        std::vector<std::vector<float>> pr;
+        for (uint64_t p = 0; p < np; ++p)
+            pr.emplace_back(probes + p * idx.d(), probes + (p + 1) * idx.d());
+        return estimate_rmin(idx, pr, k);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return std::nan("");
+    }
+}
+
+// DetIndex::project_query (index.cpp:181-188): out [K]
+void ref_index_project_query(void* h, const float* q, int space, float* out) {
+    const DetIndex& idx = idx_of(h);
+    const auto v = idx.project_query(std::span<const float>(q, static_cast<size_t>(idx.d())), space);
+    std::copy(v.begin(), v.end(), out);
+}
+
+// range_query_optimized / range_query_exact (de_tree.cpp:199-258) on tree
+// `tree` of a built index; exact mode looks projected coordinates up by
+// projecting the dataset row (the reference's ProjectedLookup).  Returns the
+// list length; the first `cap` positions go to out.
+uint64_t ref_index_range_query(void* h, int tree, const float* q_proj, double radius, uint64_t limit, int exact,
+                               uint32_t* out, uint64_t cap) {
+    const DetIndex& idx = idx_of(h);
+    const DeTree& t = idx.trees[static_cast<size_t>(tree)];
+    const std::span<const float> q(q_proj, static_cast<size_t>(t.K));
+    std::vector<uint32_t> got;
+    if (exact) {
+        std::vector<float> buf(static_cast<size_t>(t.K));
+        const ProjectedLookup lookup = [&](uint32_t pos) -> const float* {
+            project_point_into(idx.family, idx.data->row(pos), tree, buf.data());
+            return buf.data();
+        };
+        got = range_query_exact(t, idx.table, q, radius, lookup);
+    } else {
+        range_query_optimized(t, idx.table, q, radius, [&](uint32_t pos) {
+            got.push_back(pos);
+            return got.size() < limit;
+        });
+    }
+    for (uint64_t i = 0; i < got.size() && i < cap; ++i) out[i] = got[i];
+    return got.size();
 }
 
 // ck_ann (index.cpp:292-331) for one query; hits written ascending.

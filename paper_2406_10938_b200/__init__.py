@@ -36,6 +36,9 @@ from .api import (  # noqa: F401
     derive_params,
     device_count,
     encode_dataset,
+    estimate_rmin,
+    range_query_exact,
+    range_query_optimized,
     merge_topk_device,
     mix_seed,
     project_dataset,

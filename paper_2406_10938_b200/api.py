@@ -243,8 +243,16 @@ class DetIndex:
 
     def project_query(self, q, space: int) -> np.ndarray:
         """DetIndex::project_query (index.cpp:181-188) via the projection kernel."""
-        fam = self.family()[space:space + 1]
-        return project_dataset(fam, np.asarray(q, np.float32)[None, :], device=self.device)[0, 0]
+        return self.project_queries(np.asarray(q, np.float32).reshape(1, -1))[space, 0]
+
+    def project_queries(self, queries) -> np.ndarray:
+        """project_query for a batch: [L][nq][K] (detlsh_gpu_project_query)."""
+        Q = _as_host_f32(queries)
+        if Q.shape[1] != self._d:
+            raise ValueError("project_query: query dimension mismatch")
+        out = np.empty((self.params.L, Q.shape[0], self.params.K), np.float32)
+        check(_lib.load().detlsh_gpu_project_query(self._h, _ptr(Q), Q.shape[0], _ptr(out), 0))
+        return out
 
 
 def _export_tree(fn, K, nn, n) -> TreeExport:
@@ -371,6 +379,42 @@ def ck_ann_device(index: DetIndex, queries, k: int, ids, dists, n_hits=None, rad
 def query_check(index: DetIndex, stream=None) -> None:
     """Synchronise and raise if an earlier device-pointer batch failed an internal check."""
     check(_lib.load().detlsh_gpu_query_check(index.handle, stream))
+
+
+def estimate_rmin(index: DetIndex, probes, k: int) -> float:
+    """estimate_rmin (index.hpp:91, index.cpp:333-374) over probe queries [np][d]."""
+    P = _as_host_f32(probes)
+    if P.shape[0] and P.shape[1] != index.d():
+        raise ValueError("estimate_rmin: probe dimension mismatch")
+    out = C.c_double(0.0)
+    check(_lib.load().detlsh_gpu_estimate_rmin(index.handle, _ptr(P), P.shape[0], k, 0, C.byref(out)))
+    return float(out.value)
+
+
+def _range_query(index: DetIndex, tree: int, q_proj, radius, limit: int, exact: bool, cap=None):
+    qp = np.ascontiguousarray(np.atleast_2d(np.asarray(q_proj, np.float32)))
+    nq = qp.shape[0]
+    if qp.shape[1] != index.params.K:
+        raise ValueError("range_query: projected query must have K coordinates")
+    rad = np.ascontiguousarray(np.broadcast_to(np.asarray(radius, np.float64), (nq,)))
+    cap = min(index.n(), limit) if cap is None else cap
+    out = np.zeros((nq, max(1, cap)), np.uint32)
+    counts = np.zeros(nq, np.uint64)
+    check(_lib.load().detlsh_gpu_range_query(index.handle, tree, _ptr(qp), nq, _ptr(rad), limit,
+                                             _lib.RANGE_EXACT if exact else 0, _ptr(out), cap, _ptr(counts)))
+    return [out[i, :min(int(counts[i]), cap)].copy() for i in range(nq)]
+
+
+def range_query_optimized(index: DetIndex, tree: int, q_proj, radius: float, limit: int = 2**63):
+    """range_query_optimized (de_tree.hpp:93-100) with a sink that stops after
+    `limit` positions: the entries of every leaf with mindist <= radius in
+    ascending (mindist, node index) order."""
+    return _range_query(index, tree, q_proj, radius, limit, False)[0]
+
+
+def range_query_exact(index: DetIndex, tree: int, q_proj, radius: float):
+    """range_query_exact (de_tree.hpp:85-91): {pos : ||q', o'_pos|| <= radius} in DFS order."""
+    return _range_query(index, tree, q_proj, radius, 2**63, True)[0]
 
 
 def brute_force_knn(data, queries, k: int, *, dist2_bound=None, device: int = 0):

@@ -218,6 +218,34 @@ int detlsh_gpu_query_check(const detlsh_gpu_index* index, void* stream) {
     });
 }
 
+int detlsh_gpu_estimate_rmin(const detlsh_gpu_index* index, const float* probes, uint64_t n_probes, int32_t k,
+                             uint32_t flags, double* r_min) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("estimate_rmin: index is null");
+        if (!r_min) throw InvalidArgument("estimate_rmin: r_min is null");
+        *r_min = estimate_rmin_impl(*index->impl, probes, n_probes, k, flags);
+    });
+}
+
+int detlsh_gpu_project_query(const detlsh_gpu_index* index, const float* queries, uint64_t nq, float* out,
+                             uint32_t flags) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("project_query: index is null");
+        project_queries_impl(*index->impl, queries, nq, out, flags);
+    });
+}
+
+int detlsh_gpu_range_query(const detlsh_gpu_index* index, int32_t tree, const float* q_proj, uint64_t nq,
+                           const double* radius, uint64_t limit, uint32_t flags, uint32_t* positions, uint64_t cap,
+                           uint64_t* counts) {
+    return guarded([&] {
+        if (!index) throw InvalidArgument("range_query: index is null");
+        if (flags & DETLSH_F_DEVICE_PTRS) throw InvalidArgument("range_query: host pointers only");
+        range_query_impl(*index->impl, tree, q_proj, nq, radius, limit, (flags & DETLSH_RANGE_EXACT) != 0, positions,
+                         cap, counts);
+    });
+}
+
 int detlsh_gpu_sharded_build(const float* points, uint64_t n, int32_t d, detlsh_params* params, uint64_t seed,
                              const int32_t* devices, int32_t shards, uint32_t flags,
                              detlsh_gpu_sharded_index** out) {

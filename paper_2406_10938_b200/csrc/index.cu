@@ -587,6 +587,116 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     return X;
 }
 
+// estimate_rmin (index.hpp:91, index.cpp:333-374) for caller-supplied probe
+// queries: the same order-statistic form as the build's r_min,
+// with the probes projected by the index's own projection kernel
+// (project_query, index.cpp:181-188) and the dataset re-projected chunk by
+// chunk (the index keeps no projections, like the reference's DetIndex).
+double estimate_rmin_impl(GpuIndex& X, const float* probes, uint64_t np, int k, uint32_t flags) {
+    if (np == 0) throw InvalidArgument("estimate_rmin: no probe queries");
+    if (!probes) throw InvalidArgument("estimate_rmin: probes is null");
+    DeviceGuard dg(X.device);
+    std::lock_guard<std::mutex> lock(X.qmu);
+    cudaStream_t s = X.main.s;
+    StreamScope scope(s);
+    const int K = X.params.K, L = X.params.L, d = X.d;
+    const uint64_t n = X.n;
+    const bool dev = (flags & DETLSH_F_DEVICE_PTRS) != 0;
+    auto project = [&](const float* pts, uint64_t m, float* out) {
+        if (X.paa) launch_project_paa(pts, m, d, K, out, s, "project_probe");
+        else launch_project_exact(pts, m, d, X.coeffs_t.get(), K, L, out, s, "project_probe");
+    };
+    // probe projections [L][np][K] -> [np][L][K] (the order-statistic kernel's layout)
+    DevBuf<float> dprobe(np * static_cast<size_t>(d)), pp(static_cast<size_t>(L) * np * K),
+        ppt(static_cast<size_t>(L) * np * K);
+    DETLSH_CUDA(cudaMemcpyAsync(dprobe.get(), probes, np * static_cast<size_t>(d) * 4,
+                                dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    project(dprobe.get(), np, pp.get());
+    std::vector<float> h_pp(static_cast<size_t>(L) * np * K), h_ppt(h_pp.size());
+    DETLSH_CUDA(cudaMemcpyAsync(h_pp.data(), pp.get(), h_pp.size() * 4, cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    for (uint64_t p = 0; p < np; ++p)
+        for (int i = 0; i < L; ++i)
+            std::memcpy(&h_ppt[(p * L + i) * K], &h_pp[(static_cast<size_t>(i) * np + p) * K], K * 4);
+    DETLSH_CUDA(cudaMemcpyAsync(ppt.get(), h_ppt.data(), h_ppt.size() * 4, cudaMemcpyHostToDevice, s));
+    // initial guess: median pairwise projected distance of 32 strided points, space 0 (index.cpp:84-109)
+    const uint64_t m = std::min<uint64_t>(32, n);
+    std::vector<uint32_t> h_pos(m);
+    for (uint64_t t = 0; t < m; ++t) h_pos[t] = static_cast<uint32_t>(t * n / m);
+    DevBuf<uint32_t> d_pos(m);
+    DevBuf<float> rows(m * static_cast<size_t>(d)), rp(static_cast<size_t>(L) * m * K);
+    DETLSH_CUDA(cudaMemcpyAsync(d_pos.get(), h_pos.data(), m * 4, cudaMemcpyHostToDevice, s));
+    launch_pack_f32(X.data, d_pos.get(), m, d, rows.get(), s);
+    project(rows.get(), m, rp.get());
+    std::vector<float> sc(m * K);
+    DETLSH_CUDA(cudaMemcpyAsync(sc.data(), rp.get(), sc.size() * 4, cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> pd;
+    for (uint64_t a = 0; a < m; ++a)
+        for (uint64_t b = a + 1; b < m; ++b) {
+            double acc = 0.0;
+            for (int j = 0; j < K; ++j) {
+                const double diff = static_cast<double>(sc[a * K + j]) - static_cast<double>(sc[b * K + j]);
+                acc += diff * diff;
+            }
+            pd.push_back(std::sqrt(acc));
+        }
+    double guess = 1.0;
+    if (!pd.empty()) {
+        std::nth_element(pd.begin(), pd.begin() + pd.size() / 2, pd.end());
+        const double med = pd[pd.size() / 2];
+        if (med > 0.0) guess = med / X.params.epsilon;
+    }
+    // reaches(r) <=> the budget-th smallest D <= eps r; a budget of 0 stops at
+    // the first point found, like budget 1 (count_range_reaches, index.cpp:48)
+    const uint64_t rank = std::max<uint64_t>(1, candidate_budget(X.params.beta, n, k));
+    constexpr int kGroup = 10;
+    const uint64_t chunk = std::min<uint64_t>(n, 1ULL << 22);
+    DevBuf<double> D(std::min<uint64_t>(np, kGroup) * n);
+    DevBuf<float> pc(static_cast<size_t>(L) * chunk * K);
+    std::vector<uint64_t> Tbits(np);
+    for (uint64_t g0 = 0; g0 < np; g0 += kGroup) {
+        const int gn = static_cast<int>(std::min<uint64_t>(kGroup, np - g0));
+        RminSelect sel(gn);
+        rmin_begin(sel, s);
+        for (uint64_t z0 = 0; z0 < n; z0 += chunk) {
+            const uint64_t mz = std::min(chunk, n - z0);
+            project(X.data + z0 * static_cast<uint64_t>(d), mz, pc.get());
+            launch_rmin_dist(pc.get(), mz, z0, n, K, L, ppt.get() + g0 * L * K, sel, D.get(), s);
+        }
+        rmin_select(sel, D.get(), n, rank, Tbits.data() + g0, s);
+    }
+    std::vector<double> T(np);
+    for (uint64_t p = 0; p < np; ++p) std::memcpy(&T[p], &Tbits[p], 8);
+    return rmin_from_order_stats(T, guess, X.params.epsilon, X.params.c);
+}
+
+void project_queries_impl(GpuIndex& X, const float* q, uint64_t nq, float* out, uint32_t flags) {
+    if (nq == 0) return;
+    if (!q || !out) throw InvalidArgument("project_query: null argument");
+    DeviceGuard dg(X.device);
+    std::lock_guard<std::mutex> lock(X.qmu);
+    cudaStream_t s = X.main.s;
+    StreamScope scope(s);
+    const bool dev = (flags & DETLSH_F_DEVICE_PTRS) != 0;
+    const int K = X.params.K, L = X.params.L, d = X.d;
+    DevBuf<float> dq, dout;
+    const float* src = q;
+    float* dst = out;
+    if (!dev) {
+        dq.alloc(nq * static_cast<size_t>(d));
+        DETLSH_CUDA(cudaMemcpyAsync(dq.get(), q, nq * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s));
+        src = dq.get();
+        dout.alloc(static_cast<size_t>(L) * nq * K);
+        dst = dout.get();
+    }
+    if (X.paa) launch_project_paa(src, nq, d, K, dst, s, "project_query");
+    else launch_project_exact(src, nq, d, X.coeffs_t.get(), K, L, dst, s, "project_query");
+    if (!dev)
+        DETLSH_CUDA(cudaMemcpyAsync(out, dst, static_cast<size_t>(L) * nq * K * 4, cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+}
+
 void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t flags,
                 uint32_t* ids, double* dists, int32_t* n_hits, double* radius, uint64_t* cands,
                 cudaStream_t user_stream, const RcArgs* rc) {

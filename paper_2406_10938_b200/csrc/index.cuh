@@ -43,6 +43,8 @@ struct GpuIndex {
     DevBuf<float> data_leaf;  // non-integral datasets: fp32 rows in tree-0 leaf order
     int row_u8 = 0, u8_lpr = 0;
     std::vector<std::unique_ptr<DevTree>> trees;
+    // per tree: leaf indices in the reference's DFS order (range_query_exact), built on first use
+    std::vector<std::unique_ptr<DevBuf<uint32_t>>> dfs_leaves;
     DevBuf<QTree> qtrees;
     uint32_t max_leaves = 0;
     QueryScratch scratch;
@@ -67,6 +69,14 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
                 cudaStream_t user_stream, const RcArgs* rc = nullptr);
 
 void validate_params(const detlsh_params& p, uint64_t n, int d);
+// estimate_rmin (index.hpp:91) for caller probes [np][d] (host or device per flags)
+double estimate_rmin_impl(GpuIndex& X, const float* probes, uint64_t np, int k, uint32_t flags);
+// range_query_optimized / range_query_exact (de_tree.cpp:199-258) on tree `tree`
+// for projected queries [nq][K] (host); positions [nq][cap], counts [nq]
+void range_query_impl(GpuIndex& X, int tree, const float* q_proj, uint64_t nq, const double* radius, uint64_t limit,
+                      bool exact, uint32_t* out, uint64_t cap, uint64_t* counts);
+// DetIndex::project_query (index.cpp:181-188) for a batch: out [L][nq][K]
+void project_queries_impl(GpuIndex& X, const float* q, uint64_t nq, float* out, uint32_t flags);
 // DETL v1 byte stream of the index (persist.cu), identical to detlsh::save_index
 std::vector<uint8_t> save_detl(GpuIndex& X);
 uint64_t sample_size_for(double frac, uint64_t n, int NR);

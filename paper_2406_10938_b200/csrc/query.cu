@@ -1679,7 +1679,10 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     };
     if (!X.done) DETLSH_CUDA(cudaEventCreateWithFlags(&X.done, cudaEventDisableTiming));
     else if (!capturing) DETLSH_CUDA(cudaStreamWaitEvent(s, X.done, 0));
-    grow_scratch(X.counters, 4);
+    if (X.counters.size() < 4) {
+        grow_scratch(X.counters, 4);
+        DETLSH_CUDA(cudaMemsetAsync(X.counters.get(), 0, 16, s));  // incl. the sticky invariant flag
+    }
     grow_scratch(X.slow_list, P.nq);
     // counters: slow-path and overflow counts reset per batch; the invariant flag is sticky
     DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntSlow, 0, 4, s));

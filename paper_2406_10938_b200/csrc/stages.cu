@@ -273,7 +273,7 @@ template <int KT>
 __global__ void __launch_bounds__(256) rmin_dist_kernel(
     const float* __restrict__ proj, uint64_t n, int K, int L, const float* __restrict__ probe_proj,
     int np, double* __restrict__ D, unsigned long long* __restrict__ lo_bits,
-    unsigned long long* __restrict__ hi_bits) {
+    unsigned long long* __restrict__ hi_bits, uint64_t z0, uint64_t d_stride) {
     extern __shared__ float spp[];  // [np][L][K]
     for (int i = threadIdx.x; i < np * L * K; i += blockDim.x) spp[i] = probe_proj[i];
     __syncthreads();
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(256) rmin_dist_kernel(
         for (int p = 0; p < kMaxProbes; ++p) {
             if (p < np) {
                 const double dist = __dsqrt_rn(best[p]);
-                D[static_cast<uint64_t>(p) * n + z] = dist;
+                D[static_cast<uint64_t>(p) * d_stride + z0 + z] = dist;
                 const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(dist));
                 mn[p] = b < mn[p] ? b : mn[p];
                 mx[p] = b > mx[p] ? b : mx[p];
@@ -497,42 +497,69 @@ void launch_encode(const float* d_proj, uint64_t n, int K, int L, const float* d
     DETLSH_LAUNCH_CHECK();
 }
 
+RminSelect::RminSelect(int np_) : np(np_), lo(np_), hi(np_), need(np_), shift(np_), hist(static_cast<size_t>(np_) * kSelBins) {}
+
 void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float* d_probe_proj,
                       int np, uint64_t rank, double* d_D, uint32_t* d_hist, uint64_t* h_T_bits,
                       cudaStream_t s) {
+    (void)d_hist;
     StreamScope scope(s);
+    RminSelect sel(np);
+    rmin_begin(sel, s);
+    launch_rmin_dist(d_proj, n, 0, n, K, L, d_probe_proj, sel, d_D, s);
+    rmin_select(sel, d_D, n, rank, h_T_bits, s);
+}
+
+void rmin_begin(RminSelect& sel, cudaStream_t s) {
+    if (sel.np > kMaxProbes || sel.np < 1) throw InvalidArgument("estimate_rmin: 1 to 10 probes per group");
+    DETLSH_CUDA(cudaMemsetAsync(sel.lo.get(), 0xff, sel.np * sizeof(unsigned long long), s));
+    DETLSH_CUDA(cudaMemsetAsync(sel.hi.get(), 0, sel.np * sizeof(unsigned long long), s));
+}
+
+void launch_rmin_dist(const float* d_proj_chunk, uint64_t m, uint64_t z0, uint64_t n_total, int K, int L,
+                      const float* d_probe_proj, RminSelect& sel, double* d_D, cudaStream_t s) {
+    if (m == 0) return;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (np > kMaxProbes) throw InvalidArgument("estimate_rmin: at most 10 probes");
+    const unsigned gx = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((m + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8)));
+    ProfScope ps("rmin_dist", s);
+    const int np = sel.np;
+    const size_t smem = static_cast<size_t>(np) * L * K * sizeof(float);
+    if (K == 16)
+        rmin_dist_kernel<16><<<gx, 256, smem, s>>>(d_proj_chunk, m, K, L, d_probe_proj, np, d_D, sel.lo.get(),
+                                                   sel.hi.get(), z0, n_total);
+    else
+        rmin_dist_kernel<kMaxK><<<gx, 256, smem, s>>>(d_proj_chunk, m, K, L, d_probe_proj, np, d_D, sel.lo.get(),
+                                                      sel.hi.get(), z0, n_total);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void rmin_select(RminSelect& sel, const double* d_D, uint64_t n, uint64_t rank, uint64_t* h_T_bits,
+                 cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int np = sel.np;
     const unsigned gx = static_cast<unsigned>(
         std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8)));
-    DevBuf<unsigned long long> lo(np), hi(np);
-    DevBuf<uint64_t> need(np);
-    DevBuf<int> shift(np);
     std::vector<uint64_t> h(np, rank);
-    DETLSH_CUDA(cudaMemsetAsync(lo.get(), 0xff, np * sizeof(unsigned long long), s));
-    DETLSH_CUDA(cudaMemsetAsync(hi.get(), 0, np * sizeof(unsigned long long), s));
-    DETLSH_CUDA(cudaMemcpyAsync(need.get(), h.data(), np * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-    DETLSH_CUDA(cudaMemsetAsync(d_hist, 0, static_cast<size_t>(np) * kSelBins * sizeof(uint32_t), s));
-    {
-        ProfScope ps("rmin_dist", s);
-        const size_t smem = static_cast<size_t>(np) * L * K * sizeof(float);
-        if (K == 16)
-            rmin_dist_kernel<16><<<gx, 256, smem, s>>>(d_proj, n, K, L, d_probe_proj, np, d_D, lo.get(), hi.get());
-        else
-            rmin_dist_kernel<kMaxK><<<gx, 256, smem, s>>>(d_proj, n, K, L, d_probe_proj, np, d_D, lo.get(), hi.get());
-        DETLSH_LAUNCH_CHECK();
-    }
+    DETLSH_CUDA(cudaMemcpyAsync(sel.need.get(), h.data(), np * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    DETLSH_CUDA(cudaMemsetAsync(sel.hist.get(), 0, static_cast<size_t>(np) * kSelBins * sizeof(uint32_t), s));
+    unsigned long long* const lo_p = sel.lo.get();
+    unsigned long long* const hi_p = sel.hi.get();
+    uint64_t* const need_p = sel.need.get();
+    int* const shift_p = sel.shift.get();
+    uint32_t* const d_hist = sel.hist.get();
     ProfScope ps("rmin_select", s);
-    rmin_sel_init<<<1, 32, 0, s>>>(lo.get(), hi.get(), np, shift.get());
+    rmin_sel_init<<<1, 32, 0, s>>>(lo_p, hi_p, np, shift_p);
     DETLSH_LAUNCH_CHECK();
     for (int pass = 0; pass < 6; ++pass) {  // 53-bit spans need at most 5 passes of 11 bits
-        rmin_sel_hist<<<dim3(gx, np), 256, 0, s>>>(d_D, n, lo.get(), shift.get(), d_hist);
+        rmin_sel_hist<<<dim3(gx, np), 256, 0, s>>>(d_D, n, lo_p, shift_p, d_hist);
         DETLSH_LAUNCH_CHECK();
-        rmin_sel_pick<<<np, 256, 0, s>>>(d_hist, lo.get(), hi.get(), shift.get(), need.get());
+        rmin_sel_pick<<<np, 256, 0, s>>>(d_hist, lo_p, hi_p, shift_p, need_p);
         DETLSH_LAUNCH_CHECK();
     }
-    DETLSH_CUDA(cudaMemcpyAsync(h_T_bits, lo.get(), np * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaMemcpyAsync(h_T_bits, lo_p, np * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     DETLSH_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -53,6 +53,23 @@ void rmin_order_stats(const float* d_proj, uint64_t n, int K, int L, const float
                       int n_probes, uint64_t rank, double* d_D, uint32_t* d_hist,
                       uint64_t* h_T_bits, cudaStream_t s);
 
+// The same in pieces, for projections produced chunk by chunk: rmin_begin,
+// then launch_rmin_dist per chunk of m points starting at z0 (projections
+// [L][m][K]; D is [np][n_total]), then rmin_select.  At most 10 probes.
+struct RminSelect {
+    int np;
+    DevBuf<unsigned long long> lo, hi;
+    DevBuf<uint64_t> need;
+    DevBuf<int> shift;
+    DevBuf<uint32_t> hist;
+    explicit RminSelect(int np);
+};
+void rmin_begin(RminSelect& sel, cudaStream_t s);
+void launch_rmin_dist(const float* d_proj_chunk, uint64_t m, uint64_t z0, uint64_t n_total, int K, int L,
+                      const float* d_probe_proj, RminSelect& sel, double* d_D, cudaStream_t s);
+void rmin_select(RminSelect& sel, const double* d_D, uint64_t n, uint64_t rank, uint64_t* h_T_bits,
+                 cudaStream_t s);
+
 }  // namespace detlsh_b200
 
 namespace detlsh_b200 {
