@@ -48,6 +48,9 @@ def parse():
                     help="N>1: strong (default, BASELINE configs 4-5) = the config's one n-point "
                          "dataset split into N contiguous point shards; weak = every rank indexes "
                          "its own n-point shard of a world x n dataset (fixed per-GPU work)")
+    ap.add_argument("--plumbing", action="store_true",
+                    help="check the multi-rank launch only (no GPU needed): ranks, shard bounds, "
+                         "the all-gather of per-shard lists; rank 0 prints one JSON line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=200)
     ap.add_argument("--cpu-build-rows", type=int, default=None,
@@ -374,6 +377,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.plumbing:
+        plumbing(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -648,6 +654,43 @@ def main():
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"error": str(e)}
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def plumbing(args, rank, world):
+    """The multi-rank skeleton of the bench without the GPU work: process group
+    (nccl with GPUs, else gloo), the config's point shards, and the all-gather
+    of per-shard top-k lists that the query step merges."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_10938_b200 import data as gen
+    from paper_2406_10938_b200.shard import gather_topk, shard_bounds
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if world > 1:
+        dist.init_process_group(backend)
+    n = gen.CONFIGS[args.config]["n"]
+    s0, s1 = shard_bounds(n, world, rank) if args.shard == "strong" else (rank * n, (rank + 1) * n)
+    k, nq = 4, 3
+    dev = "cuda" if backend == "nccl" else "cpu"
+    # each rank's fake top-k: distances rank + j, ids at the shard's first rows
+    d = torch.tensor([[rank + j for j in range(k)]] * nq, dtype=torch.float64, device=dev)
+    i = torch.tensor([[s0 + j for j in range(k)]] * nq, dtype=torch.int64, device=dev)
+    h = torch.full((nq,), k, dtype=torch.int32, device=dev)
+    gd = torch.zeros((world, nq, k), dtype=torch.float64, device=dev)
+    gi = torch.zeros((world, nq, k), dtype=torch.int64, device=dev)
+    gh = torch.zeros((world, nq), dtype=torch.int32, device=dev)
+    if world > 1:
+        gather_topk(d, i, h, gd, gi, gh)
+        bounds = [None] * world
+        dist.all_gather_object(bounds, (s0, s1))
+    else:
+        gd[0], gi[0], gh[0] = d, i, h
+        bounds = [(s0, s1)]
+    if rank == 0:
+        print(json.dumps({"plumbing": True, "n_gpus": world, "backend": backend, "shard": args.shard,
+                          "scaling": args.shard if world > 1 else "weak", "config": args.config,
+                          "shards": bounds, "gathered_ids": gi[:, 0, 0].tolist()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

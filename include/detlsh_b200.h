@@ -244,6 +244,10 @@ int detlsh_gpu_get_params(const detlsh_gpu_index* index, detlsh_params* out);
 uint64_t detlsh_gpu_n(const detlsh_gpu_index* index);
 int32_t detlsh_gpu_d(const detlsh_gpu_index* index);
 uint64_t detlsh_gpu_sample_size(const detlsh_gpu_index* index);
+/* HashFamily::seed (projection.hpp:18): mix_seed(seed, 0) for build_index, the
+ * caller's for build_index_with_family; has_family is 0 for DET-ONLY (PAA). */
+uint64_t detlsh_gpu_family_seed(const detlsh_gpu_index* index);
+int32_t detlsh_gpu_has_family(const detlsh_gpu_index* index);
 /* Bytes per exact-u8 verification row (0 when the dataset is not integral in [0,255]). */
 int32_t detlsh_gpu_row_u8(const detlsh_gpu_index* index);
 int detlsh_gpu_export_family(const detlsh_gpu_index* index, float* out /* [L][K][d] */);

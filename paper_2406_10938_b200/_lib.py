@@ -102,6 +102,8 @@ def load() -> C.CDLL:
         "detlsh_gpu_n": ([vp], u64),
         "detlsh_gpu_d": ([vp], i32),
         "detlsh_gpu_sample_size": ([vp], u64),
+        "detlsh_gpu_family_seed": ([vp], u64),
+        "detlsh_gpu_has_family": ([vp], i32),
         "detlsh_gpu_row_u8": ([vp], i32),
         "detlsh_gpu_export_family": ([vp, vp], C.c_int),
         "detlsh_gpu_export_table": ([vp, vp], C.c_int),

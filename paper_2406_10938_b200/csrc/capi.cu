@@ -352,6 +352,8 @@ int detlsh_gpu_get_params(const detlsh_gpu_index* index, detlsh_params* out) {
 }
 uint64_t detlsh_gpu_n(const detlsh_gpu_index* index) { return index ? index->impl->n : 0; }
 int32_t detlsh_gpu_d(const detlsh_gpu_index* index) { return index ? index->impl->d : 0; }
+uint64_t detlsh_gpu_family_seed(const detlsh_gpu_index* index) { return index ? index->impl->family_seed : 0; }
+int32_t detlsh_gpu_has_family(const detlsh_gpu_index* index) { return index && !index->impl->paa ? 1 : 0; }
 int32_t detlsh_gpu_row_u8(const detlsh_gpu_index* index) {
     return index ? index->impl->row_u8 : 0;
 }

@@ -31,6 +31,27 @@ def test_facade_compiles_and_links():
 
 
 @pytest.mark.gpu
+def test_facade_reference_signatures_match_reference(ref):
+    """build_index(shared_ptr<const Dataset>, ...), DetIndex::family/table/trees/
+    project_query, estimate_rmin and the range queries through the facade."""
+    if not os.path.exists(DEMO):
+        subprocess.run(["make", "-s", "-C", CPP], check=True)
+    out = subprocess.run([DEMO], check=True, capture_output=True, text=True).stdout.splitlines()
+    f = {x.split()[0]: x.split()[1:] for x in out if x.split()[0] in ("dataset_build", "estimate_rmin", "range")}
+    same, ncoef, ntab, ntrees = map(int, f["dataset_build"])
+    assert same == 1 and ncoef == 4 * 16 * 24 and ntab == 4 * 16 * 257 and ntrees == 4
+    base, Q = lcg_data(5000, 5, 24)
+    ri = ref.build_index(base, make_params(beta=0.1, k=7, leaf_capacity=32), 77)
+    assert float(f["estimate_rmin"][0]) == ri.estimate_rmin(Q[:3], 7)
+    qp = ri.project_query(Q[0], 1)
+    rad = ri.params.epsilon * ri.params.r_min
+    drained = ri.range_query(1, qp, rad, 40)
+    exact = ri.range_query(1, qp, rad, exact=True)
+    assert int(f["range"][0]) == len(drained) and int(f["range"][1]) == len(exact)
+    assert [int(x) for x in f["range"][2:]] == drained[:5].tolist()
+
+
+@pytest.mark.gpu
 def test_facade_program_matches_oracle(port):
     if not os.path.exists(DEMO):
         subprocess.run(["make", "-s", "-C", CPP], check=True)
@@ -38,7 +59,7 @@ def test_facade_program_matches_oracle(port):
     r_min = float(out[0].split()[1])
     detl = [x.split() for x in out if x.startswith("detl ")]
     assert detl and int(detl[0][1]) > 0 and detl[0][2] == "DETL"
-    rows = [tuple(x.split()) for x in out[1:] if not x.startswith("detl ")]
+    rows = [tuple(x.split()) for x in out[1:] if x.split()[0].isdigit()]
     base, Q = lcg_data(5000, 5, 24)
     oi = port.build_index(base, make_params(beta=0.1, k=7, leaf_capacity=32), 77)
     assert r_min == oi.params.r_min

@@ -113,3 +113,22 @@ def test_weak_scaling_shards():
     assert np.all(d0 < (5.0 * 4) ** 2 * 128)
     g1 = gen.make_shard("c2", 1, 1000)
     assert g1.shape == (1000, 128) and g1.min() >= 0 and g1.max() <= 255
+
+
+def test_bench_gpus_2_launches_two_ranks():
+    """`bench.py --gpus 2` without a torchrun environment re-launches itself
+    under torch.distributed.run with two ranks (gloo here), splits the config's
+    n into two contiguous point shards (strong scaling by default) and
+    all-gathers the per-shard lists; rank 0 reports n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                            "MASTER_PORT")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--plumbing"],
+                         check=True, capture_output=True, text=True, env=env, timeout=240).stdout
+    line = json.loads([x for x in out.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["shards"] == [[0, 500000], [500000, 1000000]]
+    assert line["gathered_ids"] == [0, 500000]
