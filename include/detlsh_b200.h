@@ -239,6 +239,15 @@ const detlsh_gpu_index* detlsh_gpu_sharded_shard(const detlsh_gpu_sharded_index*
                                                  uint64_t* row_begin, uint64_t* row_end);
 void detlsh_gpu_sharded_free(detlsh_gpu_sharded_index* index);
 
+/* ---- synthetic data (bench / test utility) ----------------------------------
+ * Rows [row0, row0 + n) of a seeded synthetic dataset, written as fp32
+ * [n][d] into device memory `out` (generated on the GPU: config 5's 51 GB does
+ * not go through host memory).  kind 0: 0 with probability 1/2, else
+ * min(255, geometric(p = 0.05)) -- BASELINE.json configs 2 / 5.  Element
+ * (r, t) depends on (seed, r * d + t) only.  stream NULL: synchronous. */
+int detlsh_gpu_synth(int32_t kind, uint64_t seed, uint64_t row0, uint64_t n, int32_t d, float* out, int32_t device,
+                     void* stream);
+
 /* ---- export (DetIndex fields, index.hpp:24-37) ------------------------------ */
 int detlsh_gpu_get_params(const detlsh_gpu_index* index, detlsh_params* out);
 uint64_t detlsh_gpu_n(const detlsh_gpu_index* index);

@@ -88,6 +88,7 @@ def load() -> C.CDLL:
         "detlsh_gpu_estimate_rmin": ([vp, vp, u64, i32, u32, C.POINTER(dbl)], C.c_int),
         "detlsh_gpu_project_query": ([vp, vp, u64, vp, u32], C.c_int),
         "detlsh_gpu_range_query": ([vp, i32, vp, u64, vp, u64, u32, vp, u64, vp], C.c_int),
+        "detlsh_gpu_synth": ([i32, u64, u64, u64, i32, vp, i32, vp], C.c_int),
         "detlsh_gpu_rc_ann": ([vp, vp, u64, dbl, dbl, u32, vp, vp, vp, vp, vp], C.c_int),
         "detlsh_gpu_brute_force_knn": ([vp, u64, i32, vp, u64, i32, vp, u32, vp, vp, i32, vp], C.c_int),
         "detlsh_vectors_shape": ([C.c_char_p, C.POINTER(u64), C.POINTER(i32), C.POINTER(i32)], C.c_int),

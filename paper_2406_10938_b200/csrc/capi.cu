@@ -22,6 +22,8 @@
 
 namespace detlsh_b200 {
 
+void synth_generate(int kind, uint64_t seed, uint64_t row0, uint64_t n, int d, float* out, cudaStream_t s);
+
 int sm_count(int device) {
     static int cached[64] = {0};
     if (device >= 0 && device < 64 && cached[device]) return cached[device];
@@ -215,6 +217,16 @@ int detlsh_gpu_query_check(const detlsh_gpu_index* index, void* stream) {
         cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : X.main.s;
         if (query_invariant_failed(X.scratch, s))
             throw CudaError("ck_ann: internal invariant violated (budget cut emitted != budget rows)");
+    });
+}
+
+int detlsh_gpu_synth(int32_t kind, uint64_t seed, uint64_t row0, uint64_t n, int32_t d, float* out, int32_t device,
+                     void* stream) {
+    return guarded([&] {
+        if (!out && n) throw InvalidArgument("synth: out is null");
+        DeviceGuard dg(device);
+        synth_generate(kind, seed, row0, n, d, out, static_cast<cudaStream_t>(stream));
+        if (!stream) DETLSH_CUDA(cudaStreamSynchronize(nullptr));
     });
 }
 

@@ -7,7 +7,9 @@ rows of one draw).  numpy PCG64 streams make every byte reproducible.
   C2  n=1e6, d=128: 0 w.p. 0.5 else min(255, geometric(p=0.05)), seed 2
   C3  n=1e6, d=784: 28x28 grid, 3-6 blobs of radius 3-6, non-zeros U[1,255], seed 3
   C4  n=1e7, d=96 : N(0,1) rows L2-normalised, seed 4
-  C5  n=1e8, d=128: as C2, seed 5 (generated in shards)
+  C5  n=1e8, d=128: the C2 distribution, seed 5, generated on the GPU
+      (make_device: a counter-based hash per element, csrc/synth.cu; the
+      51 GB dataset never passes through host memory)
 """
 from __future__ import annotations
 
@@ -123,3 +125,26 @@ def make_shard(config: str, rank: int, n: int | None = None) -> np.ndarray:
         return unit_gaussian(n, c["d"], seed)
     raise ValueError(config)
 
+
+
+def make_device(config: str, n: int | None = None, nq: int | None = None, device: int = 0):
+    """(base [n][d], queries [nq][d]) as CUDA tensors, generated on the GPU
+    (detlsh_gpu_synth kind 0): config c5 (and c2-shaped variants).  Rows
+    [0, n) are the base set, rows [n, n + nq) the held-out queries."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    c = CONFIGS[config]
+    if config not in ("c2", "c5"):
+        raise ValueError("device generation covers the sparse 8-bit configs (c2, c5)")
+    n = c["n"] if n is None else n
+    nq = c["nq"] if nq is None else nq
+    d = c["d"]
+    base = torch.empty((n, d), dtype=torch.float32, device=f"cuda:{device}")
+    Q = torch.empty((nq, d), dtype=torch.float32, device=f"cuda:{device}")
+    lib = _lib.load()
+    _lib.check(lib.detlsh_gpu_synth(0, c["seed"], 0, n, d, C.c_void_p(base.data_ptr()), device, None))
+    _lib.check(lib.detlsh_gpu_synth(0, c["seed"], n, nq, d, C.c_void_p(Q.data_ptr()), device, None))
+    return base, Q
