@@ -440,14 +440,118 @@ bool have_avx512() {
     return v;
 }
 
+// Closed form of the sentinel loop when the pivot value is unique in the
+// segment (no other element compares equal to pv, a[lo] < pv < a[hi-1]).  Then
+// the segment holds `lt` smaller elements in the scan region [lo+2, hi-2], the
+// pivot ends at p = lo + 1 + lt, and the loop swaps the k-th element > pv of
+// the left region [lo+2, p] (ascending) with the k-th element < pv of the right
+// region [p+1, hi-2] (descending) for every k <= m, m being the count of either
+// (equal by the rank balance) — the crossing test fails exactly after the m-th
+// pair.  So the partition is three streaming passes instead of a data-dependent
+// two-pointer walk: count (gives p), compress the right region's small values
+// top-down, then rewrite the left region (compress its large values, expand the
+// small ones into their slots) and the right region (expand the large ones,
+// bottom-up).  Returns false, touching nothing, when pv is not unique; the
+// caller then runs the loop itself.  `buf` holds >= 2 * (hi - lo) + 32 floats
+// (full-width stores past the live entries).
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512dq,popcnt,bmi,bmi2")))
+bool hoare_rewrite_avx512(float* a, size_t lo, size_t hi, float pv, float* buf, size_t* p_out) {
+    if (!(a[lo] < pv) || !(a[hi - 1] > pv)) return false;
+    const __m512 vp = _mm512_set1_ps(pv);
+    const __m512i rev = _mm512_setr_epi32(15, 14, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0);
+    const int64_t s0 = static_cast<int64_t>(lo) + 2, s1 = static_cast<int64_t>(hi) - 1;  // scan region [s0, s1)
+    // pass 1: ranks
+    uint64_t lt = 0, eq = 0;
+    int64_t x = s0;
+    for (; x + 16 <= s1; x += 16) {
+        const __m512 v = _mm512_loadu_ps(a + x);
+        lt += _mm_popcnt_u32(_mm512_cmp_ps_mask(v, vp, _CMP_LT_OQ));
+        eq += _mm_popcnt_u32(_mm512_cmp_ps_mask(v, vp, _CMP_EQ_OQ));
+    }
+    if (x < s1) {
+        const __mmask16 k = static_cast<__mmask16>((1u << (s1 - x)) - 1u);
+        const __m512 v = _mm512_maskz_loadu_ps(k, a + x);
+        lt += _mm_popcnt_u32(_mm512_mask_cmp_ps_mask(k, v, vp, _CMP_LT_OQ));
+        eq += _mm_popcnt_u32(_mm512_mask_cmp_ps_mask(k, v, vp, _CMP_EQ_OQ));
+    }
+    if (eq) return false;
+    const int64_t p = static_cast<int64_t>(lo) + 1 + static_cast<int64_t>(lt);
+    float* bl = buf;              // left region's large values, ascending
+    float* br = buf + (hi - lo) + 16;  // right region's small values, descending position
+    // pass 2: right region [p+1, s1), top-down
+    int64_t nr = 0;
+    int64_t y = s1;  // exclusive top
+    for (; y - 16 >= p + 1; y -= 16) {
+        const __m512 v = _mm512_permutexvar_ps(rev, _mm512_loadu_ps(a + y - 16));
+        const __mmask16 m = _mm512_cmp_ps_mask(v, vp, _CMP_LT_OQ);
+        _mm512_storeu_ps(br + nr, _mm512_maskz_compress_ps(m, v));  // register compress: no
+        nr += _mm_popcnt_u32(m);                                     // microcoded memory form
+    }
+    const int64_t rtail = y - (p + 1);  // positions [p+1, y)
+    if (rtail > 0) {
+        for (int64_t t = y - 1; t >= p + 1; --t) {
+            br[nr] = a[t];
+            nr += a[t] < pv;
+        }
+    }
+    // pass 3: left region [s0, p] ascending — collect its large values, drop
+    // the right region's small ones into their slots
+    int64_t nl = 0, used = 0;
+    x = s0;
+    const int64_t lend = p + 1;
+    for (; x + 16 <= lend; x += 16) {
+        const __m512 v = _mm512_loadu_ps(a + x);
+        const __mmask16 m = _mm512_cmp_ps_mask(v, vp, _CMP_GT_OQ);
+        if (m) {
+            _mm512_storeu_ps(bl + nl, _mm512_maskz_compress_ps(m, v));
+            _mm512_storeu_ps(a + x, _mm512_mask_expand_ps(v, m, _mm512_loadu_ps(br + used)));
+            const int c = _mm_popcnt_u32(m);
+            nl += c;
+            used += c;
+        }
+    }
+    if (x < lend) {
+        const __mmask16 k = static_cast<__mmask16>((1u << (lend - x)) - 1u);
+        const __m512 v = _mm512_maskz_loadu_ps(k, a + x);
+        const __mmask16 m = _mm512_mask_cmp_ps_mask(k, v, vp, _CMP_GT_OQ);
+        if (m) {
+            _mm512_storeu_ps(bl + nl, _mm512_maskz_compress_ps(m, v));
+            _mm512_mask_storeu_ps(a + x, k, _mm512_mask_expand_ps(v, m, _mm512_loadu_ps(br + used)));
+            const int c = _mm_popcnt_u32(m);
+            nl += c;
+            used += c;
+        }
+    }
+    if (nl != nr) throw std::logic_error("hoare_rewrite: stopper counts differ");  // rank balance
+    // pass 4: right region top-down, the k-th small slot from the top takes bl[k]
+    used = 0;
+    y = s1;
+    for (; y - 16 >= p + 1; y -= 16) {
+        const __m512 v = _mm512_permutexvar_ps(rev, _mm512_loadu_ps(a + y - 16));
+        const __mmask16 m = _mm512_cmp_ps_mask(v, vp, _CMP_LT_OQ);
+        if (m) {
+            _mm512_storeu_ps(a + y - 16,
+                             _mm512_permutexvar_ps(rev, _mm512_mask_expand_ps(v, m, _mm512_loadu_ps(bl + used))));
+            used += _mm_popcnt_u32(m);
+        }
+    }
+    for (int64_t t = y - 1; t >= p + 1; --t)
+        if (a[t] < pv) a[t] = bl[used++];
+    std::swap(a[lo + 1], a[p]);
+    *p_out = static_cast<size_t>(p);
+    return true;
+}
+
 bool have_avx2() {
     static const bool v = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("popcnt");
     return v;
 }
 
+size_t kRewriteMin = 64;  // >= 32 (buffer layout);  // segment length from which the closed-form rewrite pays (measured)
+
 // Median-of-three around a seeded pick, sentinel Hoare scan; one bounded()
 // draw per call.  Returns the pivot's sorted position.
-size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
+size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng, float* buf = nullptr) {
     const size_t len = hi - lo;
     const size_t mid = lo + len / 2;
     std::swap(a[mid], a[lo + rng.bounded(len)]);
@@ -456,6 +560,8 @@ size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng) {
     if (a[hi - 1] < a[mid]) std::swap(a[mid], a[hi - 1]);
     std::swap(a[mid], a[lo + 1]);
     const float pv = a[lo + 1];
+    size_t pr;
+    if (buf && len >= kRewriteMin && have_avx512() && hoare_rewrite_avx512(a, lo, hi, pv, buf, &pr)) return pr;
     const size_t j = len < 12        ? hoare_scan_simple(a, lo, hi, pv)  // (measured crossover)
                      : have_avx512() ? hoare_scan_avx512(a, lo, hi, pv)
                      : have_avx2()   ? hoare_scan_avx2(a, lo, hi, pv)
@@ -494,6 +600,9 @@ void select_row_breakpoints(float* a, uint64_t n_s, int n_regions, Rng& rng, flo
         if ((x | span) >> 32) return x / span;
         return static_cast<size_t>((static_cast<unsigned __int128>(x) * recip) >> 64);
     };
+    thread_local std::vector<float> scratch;
+    if (scratch.size() < 2 * n_s + 64) scratch.resize(2 * n_s + 64);
+    float* buf = scratch.data();
     uint64_t nd = 0;
     while (!stack.empty()) {
         const Item it = stack.back();
@@ -503,7 +612,7 @@ void select_row_breakpoints(float* a, uint64_t n_s, int n_regions, Rng& rng, flo
             small_sort(a, it.lo, it.hi);
             continue;
         }
-        const size_t p = hoare_partition(a, it.lo, it.hi, rng);
+        const size_t p = hoare_partition(a, it.lo, it.hi, rng, buf);
         ++nd;
         // targets are an arithmetic progression: #{t : span(t+1)-1 < p} =
         // floor(p / span), #{t : span(t+1)-1 <= p} = floor((p+1) / span),

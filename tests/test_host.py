@@ -71,14 +71,16 @@ def _select_row(sample, n_regions, seed):
     return row, s, dr.value
 
 
-@pytest.mark.parametrize("trial", range(60))
+@pytest.mark.parametrize("trial", range(72))
 def test_host_replay_matches_oracle_partition_for_partition(port, trial):
-    """The blocked Hoare scan reproduces the reference's sentinel loop exactly:
-    same boundaries AND the same final arrangement (so the same later pivots)."""
+    """The blocked Hoare scan, and the closed-form rewrite taken when the pivot
+    value is unique in its segment, reproduce the reference's sentinel loop
+    exactly: same boundaries AND the same final arrangement (so the same later
+    pivots)."""
     g = np.random.Generator(np.random.PCG64(100 + trial))
     n_regions = [2, 8, 16, 256][trial % 4]
     n_s = int(n_regions + g.integers(0, [500, 5000, 60000][trial % 3]))
-    kind = trial % 5
+    kind = trial % 6
     if kind == 0:
         s = g.normal(0, 1, n_s)
     elif kind == 1:
@@ -87,8 +89,12 @@ def test_host_replay_matches_oracle_partition_for_partition(port, trial):
         s = np.sort(g.normal(0, 1, n_s))  # presorted
     elif kind == 3:
         s = np.full(n_s, 2.5)  # all equal
-    else:
+    elif kind == 4:
         s = np.sort(g.normal(0, 1, n_s))[::-1]  # reversed
+    else:  # distinct values with a block of signed zeros (pivot ties on -0 == +0)
+        s = g.normal(0, 1, n_s)
+        z = g.random(n_s) < 0.3
+        s[z] = np.where(g.random(int(z.sum())) < 0.5, -0.0, 0.0)
     s = s.astype(np.float32)
     row, arr, draws = _select_row(s, n_regions, 77 + trial)
     orow, oarr = port.select_row_breakpoints(s, n_regions, 77 + trial)
