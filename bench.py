@@ -218,7 +218,7 @@ def tc_tau_rows(k, budget):
 
 # algorithmic bytes per launch; kernels without a model get null
 def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0, plan=None):
-    if kernel == "project_exact":
+    if kernel in ("project_exact", "project_tc"):
         return 4.0 * d * n  # one read of the fp32 shard (4d B/point)
     if kernel == "query_fast" and plan is not None:
         # tensor-core hand-off: per query the plan kernel reads tree 0's 8-byte
@@ -238,17 +238,33 @@ def algo_bytes(kernel, n, d, nq, budget, K, L, row_u8=0, plan=None):
     return None
 
 
-def ncu_traffic(kernel, units):
+def ncu_traffic(kernel, units, cfg_key):
     """dram__bytes_read+write for `kernel` from the committed ncu capture
-    (profiles/ncu_latest.json: bytes per unit), scaled to this launch."""
+    (profiles/ncu_latest.json), only when that capture ran this same config
+    (`cfg_key`, e.g. "c2:n=1000000:nq=10000"); otherwise null."""
     path = os.path.join(ROOT, "profiles", "ncu_latest.json")
     try:
         with open(path) as f:
             table = json.load(f)
         rec = table.get(kernel) or table[kernel + "_kernel"]
+        if rec.get("config") != cfg_key:
+            return None, None
         return rec["dram_bytes_per_unit"] * units, rec["source"]
     except Exception:
         return None, None
+
+
+OWN_PEAKS_PATH = os.path.join(ROOT, "profiles", "peaks_measured.json")
+
+
+def own_peaks():
+    """FP64-DMMA and tcgen05 kind::i8 peaks measured on a B200 of this pool by
+    tools/probes/peaks.cu (committed JSON), or None."""
+    try:
+        with open(OWN_PEAKS_PATH) as f:
+            return json.load(f)
+    except Exception:
+        return None
 
 
 def peak_bf16():
@@ -585,20 +601,25 @@ def main():
     hbm, peak_kind = peaks()
     # candidates are single kernels: `rmin_select` and the `tree_*` scopes time
     # loops of small kernels with host reads between them, not one kernel
+    cfg_key = f"{cfg}:n={n_loc}:nq={nq}"
     build_roof = roofline(prof_build, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
-                          only=("project_exact", "encode", "rmin_dist", "pack_u8", "gather_sample"))
-    proj = prof_build.get("project_exact")
+                          only=("project_exact", "project_tc", "encode", "rmin_dist", "pack_u8", "gather_sample"),
+                          cfg_key=cfg_key)
     build_roof_proj = None
-    if proj:
-        pms = proj[0] / max(1, proj[1])
-        fl = 2.0 * n_loc * 16 * 4 * d
-        build_roof_proj = {"kernel": "project_exact", "bound": "fp64 tensor (mma.sync m8n8k4 f64)",
-                           "unit": "TFLOP/s", "achieved": round(fl / (pms / 1e3) / 1e12, 2), "peak": 45.0,
-                           "peak_kind": "nominal B200 FP64 tensor (blackwell guide); no measured FP64 peak",
-                           "frac": round(fl / (pms / 1e3) / 1e12 / 45.0, 4), "launch_ms": round(pms, 4)}
+    if "project_tc" in prof_build:  # 8-bit-integer data: tcgen05 kind::i8 over coefficient digits
+        pms = prof_build["project_tc"][0] / max(1, prof_build["project_tc"][1])
+        ops = 2.0 * n_loc * 5 * 64 * ((d + 31) // 32 * 32)  # 5 digit planes x 64 outputs x R
+        op = own_peaks() or {}
+        pk = float(op.get("int8_tcgen05_tops", 2.0 * peak_bf16()))
+        build_roof_proj = {"kernel": "project_tc", "bound": "tensor (tcgen05 kind::i8)", "unit": "TOPS",
+                           "achieved": round(ops / (pms / 1e3) / 1e12, 2), "peak": pk,
+                           "peak_kind": ("measured (profiles/peaks_measured.json)" if "int8_tcgen05_tops" in op
+                                         else "2x measured bf16 burst"),
+                           "frac": round(ops / (pms / 1e3) / 1e12 / pk, 4), "launch_ms": round(pms, 4),
+                           "note": "the projection of 8-bit data is HBM/epilogue bound; see roofline"}
     plan = {"leaves": int(idx.tree(0).is_leaf.sum()), "tau_rows": tc_tau_rows(k, budget)}
     query_roof = roofline(prof_query, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
-                          only=("query_fast",), row_u8=idx.row_u8(), plan=plan)
+                          only=("query_fast",), row_u8=idx.row_u8(), plan=plan, cfg_key=cfg_key)
     query_roof_tc = roofline_tc(prof_query, args.steps, n_loc, nq, idx.row_u8(), peak_bf16())
     step_ms = sum(v[0] for v in prof_query.values()) / args.steps
     step_bytes = 4.0 * d * budget * nq  # candidates_seen x 4d per query
@@ -618,7 +639,7 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(build_ms, 3),
-        "higher_is_better": True, "scaling": args.shard if world > 1 else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": args.shard if world > 1 else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg}: n={n_total}, d={d}, nq={nq}, K=16, L=4, N_r=256, leaf=128, "
                                f"k={k}, c=1.5, beta={args.beta}",
@@ -716,14 +737,16 @@ def roofline_tc(prof, steps, n, nq, row_u8, peak_bf16):
     per_launch_ms = ms / max(1, launches)
     ops = 2.0 * row_u8 * n * nq / max(1, launches / steps)
     ach = ops / (per_launch_ms / 1e3) / 1e12
-    peak = 2.0 * peak_bf16
+    op = own_peaks() or {}
+    peak = float(op.get("int8_tcgen05_tops", 2.0 * peak_bf16))
     return {"kernel": "tc_score", "bound": "tensor", "unit": "TOPS", "achieved": round(ach, 2),
-            "peak": round(peak, 1), "peak_kind": "2x measured bf16 burst (dense int8)",
+            "peak": round(peak, 1), "peak_kind": ("measured tcgen05 kind::i8 (profiles/peaks_measured.json)"
+                                                  if "int8_tcgen05_tops" in op else "2x measured bf16 burst (dense int8)"),
             "frac": round(ach / peak, 5), "launch_ms": round(per_launch_ms, 4), "int8_ops": ops}
 
 
 def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exclude=(),
-             row_u8=0, plan=None):
+             row_u8=0, plan=None, cfg_key=None):
     items = [(kk, v) for kk, v in prof.items() if (only is None or kk in only) and kk not in exclude]
     if not items:
         return None
@@ -734,21 +757,23 @@ def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exc
     b = algo_bytes(kern, n, d, nq, budget, K, L, row_u8, plan)
     total = sum(v[0] for kk, v in prof.items())
     units = nq if kern == "query_fast" else n
-    traffic, tsrc = ncu_traffic(kern, units)
+    traffic, tsrc = ncu_traffic(kern, units, cfg_key)
     out = {"kernel": kern, "bound": "hbm", "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
            "launch_ms": round(per_launch_ms, 4), "launches_per_step": launches / steps,
            "share_of_kernel_time": round(ms / total, 4) if total else None,
            "traffic": traffic, "traffic_source": tsrc}
     if kern == "project_exact":
-        # d x (L K) fp64 FMA chain per point on the FP64 tensor pipe (DMMA): the
-        # bound is FP64 tensor throughput; no FP64 figure is measured in
-        # MEASURED_PEAKS.json, so the peak is B200's nominal 45 TF/s
+        # non-integral data: d x (L K) fp64 FMA chain per point on the FP64
+        # tensor pipe (DMMA); peak = tools/probes/peaks.cu's measured DMMA rate
         fl = 2.0 * n * K * L * d
         ach = fl / (per_launch_ms / 1e3) / 1e12
         b = algo_bytes(kern, n, d, nq, budget, K, L)
-        out.update({"bound": "tensor", "unit": "TFLOP/s", "peak": 45.0,
-                    "peak_kind": "nominal B200 FP64 tensor (no measured FP64 peak)",
-                    "achieved": round(ach, 3), "frac": round(ach / 45.0, 5), "algorithmic_flops": fl,
+        op = own_peaks() or {}
+        pk = float(op.get("fp64_dmma_tflops", 45.0))
+        out.update({"bound": "tensor", "unit": "TFLOP/s", "peak": pk,
+                    "peak_kind": ("measured (profiles/peaks_measured.json, tools/probes/peaks.cu)"
+                                  if "fp64_dmma_tflops" in op else "nominal B200 FP64 tensor"),
+                    "achieved": round(ach, 3), "frac": round(ach / pk, 5), "algorithmic_flops": fl,
                     "hbm_view": {"algorithmic_bytes": b,
                                  "achieved_gbs": round(b / (per_launch_ms / 1e3) / 1e9, 2),
                                  "frac": round(b / (per_launch_ms / 1e3) / 1e9 / hbm, 5)}})
@@ -759,6 +784,13 @@ def roofline(prof, steps, n, d, nq, budget, K, L, hbm, peak_kind, only=None, exc
         ach = b / (per_launch_ms / 1e3) / 1e9
         out.update({"achieved": round(ach, 2), "frac": round(ach / hbm, 5),
                     "algorithmic_bytes": b})
+        if kern == "project_tc" and "project_fixup" in prof:
+            # the projection stage = the tensor-core pass + its fixup / guarded
+            # FP64 pass (both every launch): the same bytes over both
+            fx_ms = prof["project_fixup"][0] / max(1, prof["project_fixup"][1])
+            sa = b / ((per_launch_ms + fx_ms) / 1e3) / 1e9
+            out["stage_with_fixup"] = {"ms": round(per_launch_ms + fx_ms, 4), "achieved": round(sa, 2),
+                                       "frac": round(sa / hbm, 5)}
         if plan is not None:
             out["model"] = "plan kernel (tc hand-off): 12 B/leaf x tree-0 leaves + R x tau_rows + n/8 (row bitmap) per query"
         if kern == "query_fast" and row_u8 and plan is None:

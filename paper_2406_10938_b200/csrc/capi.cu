@@ -489,7 +489,9 @@ int detlsh_gpu_project(const float* coeffs, int32_t K, int32_t L, const float* p
         }
         DevBuf<double> ct(static_cast<size_t>(lk_padded(static_cast<int>(LK))) * d);
         prepare_coeffs_t(c.get(), static_cast<int>(LK), d, ct.get(), s);
-        launch_project_exact(P, n, d, ct.get(), K, L, O, s);
+        ProjTc tc;
+        prepare_proj_tc(c.get(), static_cast<int>(LK), d, tc, s);
+        launch_project_exact(P, n, d, ct.get(), K, L, O, s, "project_exact", &tc);
         if (!dev) from_device(out, O, LK * n * 4, false, s);
         DETLSH_CUDA(cudaStreamSynchronize(s));
     });

@@ -254,6 +254,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                                     cudaMemcpyHostToDevice, s));
         X->coeffs_t.alloc(static_cast<size_t>(lk_padded(LK)) * d);
         prepare_coeffs_t(X->coeffs.get(), LK, d, X->coeffs_t.get(), s);
+        prepare_proj_tc(X->coeffs.get(), LK, d, X->proj_tc, s);
     }
     DevBuf<float> proj(static_cast<size_t>(L) * n * K);
     X->sample_size = sample_size_for(p.sample_fraction, n, NR);
@@ -264,7 +265,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     for (auto& t : X->trees) t = std::make_unique<DevTree>();
     auto project_all = [&]() {
         if (paa) launch_project_paa(X->data, n, d, K, proj.get(), s);
-        else launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s);
+        else launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s, "project_exact", &X->proj_tc);
     };
     // reference-compatible sample (encoder.cpp:105-143): one RNG stream picks
     // every space's sample and pivots, so the host replay is sequential
@@ -343,7 +344,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             DETLSH_CUDA(cudaMemcpyAsync(iota.get(), h_iota.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
             DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
             if (paa) launch_project_paa(dG.get(), n_s, d, K, dGp.get(), s2, "project_sample");
-            else launch_project_exact(dG.get(), n_s, d, X->coeffs_t.get(), K, L, dGp.get(), s2, "project_sample");
+            else launch_project_exact(dG.get(), n_s, d, X->coeffs_t.get(), K, L, dGp.get(), s2, "project_sample", &X->proj_tc);
             d_sample0.alloc(static_cast<size_t>(K) * n_s);
             launch_gather_sample(dGp.get(), iota.get(), n_s, K, d_sample0.get(), s2);
             float* h_sample = pinned_scratch(static_cast<size_t>(K) * n_s * sizeof(float));
@@ -604,7 +605,7 @@ double estimate_rmin_impl(GpuIndex& X, const float* probes, uint64_t np, int k, 
     const bool dev = (flags & DETLSH_F_DEVICE_PTRS) != 0;
     auto project = [&](const float* pts, uint64_t m, float* out) {
         if (X.paa) launch_project_paa(pts, m, d, K, out, s, "project_probe");
-        else launch_project_exact(pts, m, d, X.coeffs_t.get(), K, L, out, s, "project_probe");
+        else launch_project_exact(pts, m, d, X.coeffs_t.get(), K, L, out, s, "project_probe", &X.proj_tc);
     };
     // probe projections [L][np][K] -> [np][L][K] (the order-statistic kernel's layout)
     DevBuf<float> dprobe(np * static_cast<size_t>(d)), pp(static_cast<size_t>(L) * np * K),
@@ -691,7 +692,7 @@ void project_queries_impl(GpuIndex& X, const float* q, uint64_t nq, float* out, 
         dst = dout.get();
     }
     if (X.paa) launch_project_paa(src, nq, d, K, dst, s, "project_query");
-    else launch_project_exact(src, nq, d, X.coeffs_t.get(), K, L, dst, s, "project_query");
+    else launch_project_exact(src, nq, d, X.coeffs_t.get(), K, L, dst, s, "project_query", &X.proj_tc);
     if (!dev)
         DETLSH_CUDA(cudaMemcpyAsync(out, dst, static_cast<size_t>(L) * nq * K * 4, cudaMemcpyDeviceToHost, s));
     DETLSH_CUDA(cudaStreamSynchronize(s));
@@ -736,7 +737,7 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     }
     DevBuf<float> qproj(static_cast<size_t>(L) * nq * K);
     if (X.paa) launch_project_paa(q, nq, d, K, qproj.get(), s);  // DetIndex::project_query (index.cpp:181-188)
-    else launch_project_exact(q, nq, d, X.coeffs_t.get(), K, L, qproj.get(), s);
+    else launch_project_exact(q, nq, d, X.coeffs_t.get(), K, L, qproj.get(), s, "project_exact", &X.proj_tc);
     DevBuf<uint32_t> o_ids;
     DevBuf<double> o_d, o_r;
     DevBuf<int32_t> o_h;

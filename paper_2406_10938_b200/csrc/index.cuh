@@ -13,6 +13,7 @@
 #include "../../include/detlsh_b200.h"
 #include "common.cuh"
 #include "query.cuh"
+#include "stages.cuh"
 #include "tree.cuh"
 
 namespace detlsh_b200 {
@@ -34,6 +35,7 @@ struct GpuIndex {
     std::vector<float> h_coeffs;  // [L][K][d]
     DevBuf<float> coeffs;
     DevBuf<double> coeffs_t;
+    ProjTc proj_tc;  // tensor-core projection operand (8-bit-integer data)
     DevBuf<float> table;
     std::vector<float> h_table;
     DevBuf<uint8_t> codes;

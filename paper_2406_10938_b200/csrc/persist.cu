@@ -114,7 +114,7 @@ std::vector<uint8_t> save_detl(GpuIndex& X) {
     if (!X.codes.get()) {
         proj.alloc(static_cast<size_t>(L) * n * K);
         if (X.paa) launch_project_paa(X.data, n, d, K, proj.get(), s);
-        else launch_project_exact(X.data, n, d, X.coeffs_t.get(), K, L, proj.get(), s);
+        else launch_project_exact(X.data, n, d, X.coeffs_t.get(), K, L, proj.get(), s, "project_exact", &X.proj_tc);
         dcodes.alloc(static_cast<size_t>(L) * n * K);
         launch_encode(proj.get(), n, K, L, X.table.get(), p.n_regions, dcodes.get(), s);
     }

@@ -1,0 +1,555 @@
+// Exact projection of 8-bit-integer datasets on the 5th-generation tensor
+// cores (tcgen05.mma kind::i8), certified against the reference's rounding.
+//
+// The reference computes v = fl32( sequential double sum of a_t * x_t )
+// (projection.cpp:31-37).  For data whose values are integers in [0, 255]:
+//
+//  * every coefficient row o is put on a fixed-point grid, A_t = rint(a_t / 2^sc_o)
+//    with |A_t| < 2^38, and split into five balanced base-256 digits
+//    (A_t = sum_s D_s 256^(4-s), D_s in [-128, 127]);
+//  * one tcgen05 kind::i8 GEMM (data u8 x digits s8, s32 accumulators in TMEM)
+//    yields S_s = sum_t D_s,t x_t exactly, so V = sum_s S_s 256^(4-s) is an
+//    exact integer;
+//  * when the row is on its grid (no coefficient below 2^(sc+23) lost bits) and
+//    sum_t x_t < 2^15, every partial sum of the reference's double chain is a
+//    multiple of 2^sc below 2^(sc+53): the chain is EXACT, so the reference's
+//    value is fl32(V 2^sc), round-to-nearest-even of an exact number;
+//  * otherwise (a row with ntr_o truncated tiny coefficients, ~1 % of rows, or a
+//    point with sum_t x_t >= 2^15) the double chain is within
+//    gamma_(d-1) sum_t |a_t| x_t < (d-1) 2^-15 sum_t x_t units of the exact sum and
+//    the grid within 127.5 ntr_o units, so whenever no fp32 rounding midpoint lies
+//    within that error of V, fl32(V 2^sc) is again the reference's value (round-
+//    to-nearest is constant between midpoints).  The epilogue tests exactly that
+//    (both ends of [V - err, V + err] round alike) and queues the rare undecided
+//    (point, output) pairs, which the fixup kernel recomputes with the
+//    reference's own fp64 chain.
+//
+// One pass over the fp32 dataset (4 d B per point) and one write of the
+// [L][n][K] projections; a non-integral value anywhere (or a fixup overflow)
+// makes the guarded FP64-DMMA kernel recompute everything, stream-ordered.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "stages.cuh"
+#include "umma.cuh"
+
+namespace detlsh_b200 {
+
+namespace {
+
+constexpr int kTP = 128;         // points per tile (MMA M = TMEM lanes)
+constexpr int kDig = 5;          // base-256 digits per coefficient
+constexpr int kEpiWarps = 16;    // four per TMEM lane quadrant (warps 0..15)
+constexpr int kConvWarps = 8;    // fp32 -> u8 operand producers
+constexpr int kMmaWarp = kEpiWarps + kConvWarps;
+constexpr int kLoadWarp = kMmaWarp + 1;  // TMA bulk copies of the fp32 rows
+constexpr int kThreads = (kLoadWarp + 1) * 32;
+constexpr int kCR = 32;                  // rows per staging chunk
+constexpr int kMaxChunks = 8;
+constexpr int kMaxSlots = 4;            // TMEM ring of half-tile accumulators (<= 512 columns)
+constexpr uint32_t kHintNs = 20000;     // mbarrier try_wait suspend hint
+constexpr int kBarConv = 1, kBarEpi = 5;  // named barriers: converter pairs 1-4, epilogue halves 5-6
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// int32 -> double on the FMA + FP64 pipes (the conversion pipe is the scarce
+// one): 2^52 + 2^51 + 2^31 + x has x + 2^31 as its low mantissa word
+__device__ __forceinline__ double i2d(int x) {
+    const uint32_t b = static_cast<uint32_t>(x) + 0x80000000u;
+    return __hiloint2double(0x43380000, static_cast<int>(b)) - 6755401588539392.0;
+}
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
+// kind::i8 instruction descriptor: A = u8 data, B = s8 digits, D = s32.
+__host__ __device__ constexpr uint32_t idesc_u8s8(int M, int N) {
+    return (2u << 4)                                 // D format S32
+           | (0u << 7) | (1u << 10)                  // A unsigned, B signed
+           | (static_cast<uint32_t>(N >> 3) << 17)   // N / 8
+           | (static_cast<uint32_t>(M >> 4) << 24);  // M / 16
+}
+
+// One block per coefficient row o: grid exponent sc_o, truncated-coefficient
+// count, digits into the UMMA K-major operand image: two pieces (output halves)
+// of P = 5 LKp/2 columns each.
+__global__ void proj_tc_prep_kernel(const float* __restrict__ c, int LK, int d, int R, int LKp,
+                                    int P, uint8_t* __restrict__ bimg, int* __restrict__ scale) {
+    const int o = blockIdx.x;
+    __shared__ float red[32];
+    float m = 0.0f;
+    if (o < LK)
+        for (int t = threadIdx.x; t < d; t += blockDim.x) m = fmaxf(m, fabsf(c[static_cast<size_t>(o) * d + t]));
+    for (int s = 16; s; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = 0.0f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+    int e = 0;
+    frexpf(m, &e);  // m < 2^e (m = 0: e = 0, every digit 0, every value falls back)
+    const int sc = e - 38;
+    if (threadIdx.x == 0) scale[o] = sc;
+    __shared__ int ntr;
+    if (threadIdx.x == 0) ntr = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < R; t += blockDim.x) {
+        long long A = 0;
+        if (o < LK && t < d) {
+            const double v = ldexp(static_cast<double>(c[static_cast<size_t>(o) * d + t]), -sc);
+            A = llrint(v);
+            if (static_cast<double>(A) != v) atomicAdd(&ntr, 1);
+        }
+        int dg[kDig];
+        for (int s = kDig - 1; s >= 0; --s) {
+            const long long r = ((A + 128) & 255) - 128;
+            dg[s] = static_cast<int>(r);
+            A = (A - r) >> 8;
+        }
+        // column of digit s of output o: [output half][digit][output within the half]
+        const int Lh = LKp / 2, piece = o / Lh, ol = o % Lh;
+        for (int s = 0; s < kDig; ++s)
+            bimg[static_cast<size_t>(piece) * P * R + umma::tile_off(s * Lh + ol, t >> 4, P) + (t & 15)] =
+                static_cast<uint8_t>(static_cast<int8_t>(dg[s]));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) scale[LKp + o] = o < LK ? ntr : 0;
+}
+
+struct TcArgs {
+    const float* pts;
+    uint64_t n;
+    int d, R, K, LK, LKp, N, P, stages, nslots, nch;  // P = columns per output half, nch staging chunks
+    const uint8_t* bimg;
+    const int* scale;  // [0, LKp): sc_o, [LKp, 2 LKp): ntr_o
+    float* out;
+    uint32_t* status;  // [0] non-integral value seen, [1] undecided outputs queued
+    uint64_t* pend;    // (z << 8 | o)
+    uint32_t cap;
+    uint32_t errd;     // d - 1 (x the test hook's error scale)
+    int force_band;    // test hook: band-test every output
+};
+
+__global__ void __launch_bounds__(kThreads, 1) project_tc_kernel(const TcArgs a) {
+    extern __shared__ __align__(16) uint8_t sm[];  // no-swizzle operands need 16-B alignment only
+    const int R = a.R, N = a.N, stages = a.stages;
+    const uint32_t abytes = kTP * R;
+    uint8_t* sB = sm;
+    uint8_t* sA = sB + static_cast<size_t>(N) * R;
+    const uint32_t cbytes = kCR * a.d * 4;  // one staging chunk: 32 fp32 rows
+    uint8_t* sC = sA + static_cast<size_t>(stages) * abytes;
+    int* xs = reinterpret_cast<int*>(sC + static_cast<size_t>(a.nch) * cbytes);
+    // per output: 2^sc and the data-independent error
+    // (grid truncation 127.5 ntr_o units, FP64 combination 4 units when d > 128)
+    double2* scon = reinterpret_cast<double2*>(xs + stages * kTP);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(scon + a.LKp);
+    uint64_t* full_a = bars;
+    uint64_t* empty_a = bars + stages;
+    uint64_t* slot_full = bars + 2 * stages;  // TMEM ring of half-tile accumulators
+    uint64_t* slot_empty = slot_full + kMaxSlots;
+    uint64_t* cfull = slot_empty + kMaxSlots;  // staging chunk ring
+    uint64_t* cempty = cfull + kMaxChunks;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(cempty + kMaxChunks);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint64_t tiles = (a.n + kTP - 1) / kTP;
+    const uint32_t ncols = 512;
+    const int P = a.P, ns = a.nslots;
+
+    for (int i = tid; i < N * R / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(sB)[i] = reinterpret_cast<const uint4*>(a.bimg)[i];
+    for (int i = tid; i < a.LKp; i += blockDim.x) {
+        const int sc = a.scale[i];
+        const int ntr = a.scale[a.LKp + i];
+        scon[i] = make_double2(ldexp(1.0, sc), ntr > 0 && !a.force_band ? ldexp(127.5 * ntr, sc) : a.force_band ? 0.0 : -1.0);
+    }
+    if (tid == 0) {
+        for (int s = 0; s < stages; ++s) {
+            umma::mbar_init(&full_a[s], kConvWarps);
+            umma::mbar_init(&empty_a[s], 1 + kEpiWarps);
+        }
+        for (int s = 0; s < kMaxSlots; ++s) {
+            umma::mbar_init(&slot_full[s], 1);
+            umma::mbar_init(&slot_empty[s], kEpiWarps / 2);  // the warps of one output half
+        }
+        for (int s = 0; s < kMaxChunks; ++s) {
+            umma::mbar_init(&cfull[s], 1);
+            umma::mbar_init(&cempty[s], kConvWarps / (kTP / kCR));  // the converters of one chunk
+        }
+        umma::fence_mbar_init();
+    }
+    umma::fence_async_smem();
+    if (warp == kMmaWarp) umma::tmem_alloc(tslot, ncols);
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    const uint32_t tmem = *tslot;
+
+    if (warp >= kEpiWarps && warp < kMmaWarp) {
+        // ---- converters: staged fp32 rows -> u8 K-major operand tiles + sum_t x_t ----
+        // warp cw takes rows 16 cw .. 16 cw + 15 of every tile (half a staging chunk)
+        const int cw = warp - kEpiWarps;
+        const int chunk = cw / (kConvWarps / (kTP / kCR));
+        const int nf4 = a.d / 4, rf4 = R / 4;
+        bool bad = false;
+        uint32_t j = 0;
+        for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+            const int st = j % stages;
+            const uint32_t gc = j * (kTP / kCR) + chunk, cs = gc % a.nch;
+            // one warp of the pair on this chunk polls the barriers (stage free,
+            // chunk staged); the other parks in a named barrier instead of spinning
+            if ((cw & 1) == 0) {
+                if (j >= static_cast<uint32_t>(stages)) umma::mbar_wait_hint(&empty_a[st], ((j / stages) - 1) & 1, kHintNs);
+                umma::mbar_wait_hint(&cfull[cs], (gc / a.nch) & 1, kHintNs);
+            }
+            named_bar(kBarConv + chunk, 64);
+            uint8_t* A = sA + static_cast<size_t>(st) * abytes;
+            const float* C = reinterpret_cast<const float*>(sC + static_cast<size_t>(cs) * cbytes);
+            // lane (r, kq): row 8 g + r, dims 16 kc + 4 kq .. +3 for every 16-dim
+            // chunk kc; the stores of a warp fill whole 128-byte core matrices
+            const int r = lane >> 2, kq = lane & 3;
+            for (int g = 2 * cw; g < 2 * cw + 2; ++g) {
+                const int p = 8 * g + r;
+                const uint64_t z = tile * kTP + p;
+                const float* src = C + static_cast<size_t>(p - kCR * chunk) * a.d;
+                const bool live = z < a.n;
+                uint32_t sum = 0;
+#pragma unroll 4
+                for (int kc = 0; kc < rf4 / 4; ++kc) {
+                    const int f = 4 * kc + kq;
+                    uint32_t word = 0;
+                    if (live && f < nf4) {
+                        // x + 2^23 holds an integer x in [0, 255] exactly in its low
+                        // mantissa byte (bits 0x4B0000xx); a fraction is rounded away,
+                        // so (x + 2^23) - 2^23 != x flags it, and a negative, large or
+                        // NaN x leaves the 0x4B0000 prefix.  No conversion-pipe ops.
+                        const float4 v = reinterpret_cast<const float4*>(src)[f];
+                        const float fv[4] = {v.x, v.y, v.z, v.w};
+                        uint32_t b[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float m = __fadd_rn(fv[q], 8388608.0f);
+                            bad |= __fsub_rn(m, 8388608.0f) != fv[q];
+                            b[q] = __float_as_uint(m);
+                        }
+                        bad |= ((b[0] | b[1] | b[2] | b[3]) & 0xffffff00u) != 0x4b000000u;
+                        word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+                        sum = __dp4a(word, 0x01010101u, sum);
+                    }
+                    *reinterpret_cast<uint32_t*>(A + umma::tile_off(p, kc, kTP) + 4 * kq) = word;
+                }
+                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+                if (kq == 0) xs[st * kTP + p] = static_cast<int>(sum);
+            }
+            umma::fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                umma::mbar_arrive(&cempty[cs]);
+                umma::mbar_arrive(&full_a[st]);
+            }
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&a.status[0], 1u);
+    } else if (warp == kLoadWarp) {
+        // ---- TMA: contiguous 32-row chunks of the fp32 dataset into the ring ----
+        if (lane == 0) {
+            uint32_t j = 0;
+            for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+                for (int c = 0; c < kTP / kCR; ++c) {
+                    const uint32_t gc = j * (kTP / kCR) + c, cs = gc % a.nch;
+                    if (gc >= static_cast<uint32_t>(a.nch)) umma::mbar_wait_hint(&cempty[cs], ((gc / a.nch) - 1) & 1, kHintNs);
+                    const uint64_t z0 = tile * kTP + kCR * c;
+                    const uint32_t rows = z0 < a.n ? static_cast<uint32_t>(a.n - z0 < kCR ? a.n - z0 : kCR) : 0u;
+                    umma::mbar_arrive_expect_tx(&cfull[cs], rows * a.d * 4);
+                    if (rows)
+                        umma::bulk_g2s(sC + static_cast<size_t>(cs) * cbytes, a.pts + z0 * a.d, rows * a.d * 4, &cfull[cs]);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kMmaWarp) {
+        // ---- MMA issuer: per tile, one half-tile (output half) per ring slot ----
+        if (lane == 0) {
+            uint32_t j = 0;
+            for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+                const int st = j % stages;
+                umma::mbar_wait_hint(&full_a[st], (j / stages) & 1, kHintNs);
+                const uint32_t aaddr = umma::smem_u32(sA + static_cast<size_t>(st) * abytes);
+                const uint32_t baddr = umma::smem_u32(sB);
+                const uint32_t idesc = idesc_u8s8(kTP, P);
+                for (int hf = 0; hf < 2; ++hf) {
+                    const uint32_t h = 2 * j + hf, sl = h % ns;
+                    if (h >= static_cast<uint32_t>(ns)) umma::mbar_wait_hint(&slot_empty[sl], ((h / ns) - 1) & 1, kHintNs);
+                    umma::fence_after_sync();
+                    for (int ks = 0; ks < R / 32; ++ks) {
+                        const uint64_t da = umma::smem_desc(aaddr + ks * 2 * kTP * 16, kTP * 16, 128);
+                        const uint64_t db = umma::smem_desc(baddr + hf * P * R + ks * 2 * P * 16, P * 16, 128);
+                        umma::mma_u8(tmem + sl * P, da, db, idesc, ks > 0 ? 1u : 0u);
+                    }
+                    umma::commit(&slot_full[sl]);
+                }
+                umma::commit(&empty_a[st]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- epilogue: digits -> exact V -> certified fp32 ----
+        // warp w drains TMEM lane quadrant w % 4 (one point per thread); warps
+        // 8 hf .. 8 hf + 7 take output half hf (groups of 16 outputs, alternating
+        // between the two warps of a quadrant)
+        const int qd = warp & 3, ws = warp >> 2, hf = ws >> 1, sub = ws & 1;
+        const int row = 32 * qd + lane;
+        const int LK = a.LK, K = a.K, Lh = a.LKp / 2;
+        uint32_t j = 0;
+        for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
+            const int st = j % stages;
+            const uint32_t h = 2 * j + hf, sl = h % ns;
+            if (warp == 8 * hf) {  // one poller per output half; the half's other warps park
+                umma::mbar_wait_hint(&slot_full[sl], (h / ns) & 1, kHintNs);
+                umma::mbar_wait(&full_a[st], (j / stages) & 1);  // (the producers' xs writes)
+            }
+            named_bar(kBarEpi + hf, 32 * kEpiWarps / 2);
+            umma::fence_after_sync();
+            const int xsum = xs[st * kTP + row];
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive(&empty_a[st]);
+            const uint64_t z = tile * kTP + row;
+            // double-chain rounding, all outputs: d - 1 rounded additions, so at
+            // most gamma_(d-1) sum |a_t| x_t < (d - 1) 2^-53 (1 + 2^-40) 2^(sc+38)
+            // sum x: (d - 1) 2^-15 units per unit of sum x, rounded up, + 1
+            // (+4: the FP64 combination rounds once |V| may reach 2^53)
+            const bool pt_exact = xsum < 32768;
+            const double eseq_d = static_cast<double>(((static_cast<uint32_t>(xsum) * a.errd + 32767u) >> 15) + 1u +
+                                                      (pt_exact ? 0u : 4u));
+            const uint32_t tl = tmem + (static_cast<uint32_t>(32 * qd) << 16) + sl * P;
+            for (int ogl = 16 * sub; ogl < Lh; ogl += 32) {
+                const int og = hf * Lh + ogl;  // global output index of the group
+#pragma unroll
+                for (int h8 = 0; h8 < 16; h8 += 8) {
+                    const int ob = og + h8;
+                    uint32_t dv[kDig][8];
+#pragma unroll
+                    for (int s = 0; s < kDig; ++s) tmem_ld8(tl + s * Lh + ogl + h8, dv[s]);
+                    umma::tmem_wait_ld();
+                    uint32_t res[8];  // fp32 bits
+                    uint32_t fm = 0;  // undecided outputs of these eight
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        // V = D0 256^4 + D1 256^3 + D2 256^2 + D3 256 + D4 (|D_s| < 2^23):
+                        // two exact int32 pairs, then the FP64 pipe (exact below 2^53,
+                        // i.e. always for d <= 128; a few units otherwise, in the
+                        // constant error term), scaled by 2^sc (exact)
+                        const int hi = static_cast<int>(dv[0][q]) * 256 + static_cast<int>(dv[1][q]);
+                        const int mid = static_cast<int>(dv[2][q]) * 256 + static_cast<int>(dv[3][q]);
+                        const double2 cs = scon[ob + q];  // (2^sc, truncation error; -1: row on its grid)
+                        const double v = fma(fma(i2d(hi), 65536.0, i2d(mid)), 256.0, i2d(static_cast<int>(dv[4][q]))) * cs.x;
+                        res[q] = __float_as_uint(__double2float_rn(v));
+                        if (cs.y >= 0.0 || !pt_exact) {
+                            // undecided iff a rounding midpoint lies in [v - e, v + e]:
+                            // round-to-nearest is monotone, so both ends agree otherwise
+                            const double e = fma(eseq_d, cs.x, fmax(cs.y, 0.0));
+                            const uint32_t f1 = __float_as_uint(__double2float_rn(v + e));
+                            const uint32_t f2 = __float_as_uint(__double2float_rn(v - e));
+                            fm |= static_cast<uint32_t>(f1 != f2) << q;
+                        }
+                    }
+                    if (z >= a.n) fm = 0;
+                    if (ob + 8 > LK) fm &= ob >= LK ? 0u : (1u << (LK - ob)) - 1u;
+                    if (__any_sync(0xffffffffu, fm != 0)) {  // rare: one reservation per warp
+                        const uint32_t c = __popc(fm);
+                        uint32_t incl = c;
+                        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                            const uint32_t t2 = __shfl_up_sync(0xffffffffu, incl, o2);
+                            if (lane >= o2) incl += t2;
+                        }
+                        uint32_t base = 0;
+                        if (lane == 31) base = atomicAdd(&a.status[1], incl);
+                        base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+                        for (uint32_t m = fm; m; m &= m - 1, ++base)
+                            if (base < a.cap) a.pend[base] = (z << 8) | static_cast<uint64_t>(ob + __ffs(m) - 1);
+                    }
+                    if (z < a.n) {
+                        if (K == 16 && (og & 15) == 0 && og + 16 <= LK) {
+                            float4* dst = reinterpret_cast<float4*>(a.out + ((og / 16) * a.n + z) * 16 + h8);
+                            dst[0] = make_float4(__uint_as_float(res[0]), __uint_as_float(res[1]),
+                                                 __uint_as_float(res[2]), __uint_as_float(res[3]));
+                            dst[1] = make_float4(__uint_as_float(res[4]), __uint_as_float(res[5]),
+                                                 __uint_as_float(res[6]), __uint_as_float(res[7]));
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int o = ob + q;
+                                if (o < LK) a.out[(static_cast<uint64_t>(o / K) * a.n + z) * K + (o % K)] = __uint_as_float(res[q]);
+                            }
+                        }
+                    }
+                }
+            }
+            umma::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) umma::mbar_arrive(&slot_empty[sl]);
+        }
+    }
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+    if (warp == kMmaWarp) umma::tmem_free(tmem, ncols);
+}
+
+// The undecided outputs: the reference's own chain (projection.cpp:31-37).
+// A warp takes 32 entries: their point rows are staged in shared memory with
+// coalesced loads, then each lane runs its entry's sequential fp64 chain.
+constexpr int kFixWarps = 2;
+__global__ void __launch_bounds__(32 * kFixWarps) proj_tc_fixup_kernel(
+    const float* __restrict__ pts, int d, const float* __restrict__ c, int K, uint64_t n,
+    const uint32_t* __restrict__ status, const uint64_t* __restrict__ pend, uint32_t cap,
+    float* __restrict__ out) {
+    if (status[0] != 0 || status[1] > cap) return;  // the guarded DMMA pass redoes everything
+    extern __shared__ float rows[];  // [kFixWarps][32][d + 1]
+    const uint32_t cnt = status[1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    float* my = rows + static_cast<size_t>(w) * 32 * (d + 1);
+    for (uint32_t base = (blockIdx.x * kFixWarps + w) * 32u; base < cnt; base += gridDim.x * kFixWarps * 32u) {
+        const uint32_t m = min(32u, cnt - base);
+        for (uint32_t e = 0; e < m; ++e) {
+            const uint64_t z = pend[base + e] >> 8;
+            for (int t = lane; t < d; t += 32) my[e * (d + 1) + t] = __ldg(pts + z * d + t);
+        }
+        __syncwarp();
+        if (lane < static_cast<int>(m)) {
+            const uint64_t ent = pend[base + lane];
+            const uint64_t z = ent >> 8;
+            const int o = static_cast<int>(ent & 255);
+            const float* x = my + lane * (d + 1);
+            const float* wv = c + static_cast<size_t>(o) * d;
+            double dot = 0.0;
+#pragma unroll 8
+            for (int t = 0; t < d; ++t) dot = __fma_rn(static_cast<double>(__ldg(wv + t)), static_cast<double>(x[t]), dot);
+            out[(static_cast<uint64_t>(o / K) * n + z) * K + (o % K)] = __double2float_rn(dot);
+        }
+        __syncwarp();
+    }
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoi(v) : dflt;
+}
+
+}  // namespace
+
+void prepare_proj_tc(const float* d_coeffs, int LK, int d, ProjTc& tc, cudaStream_t s) {
+    tc.ok = false;
+    const int LKp = (LK + 31) / 32 * 32;  // two output halves of whole 16-output groups
+    const int R = (d + 31) / 32 * 32;
+    const int N = kDig * LKp;
+    if (env_int("DETLSH_PROJ_TC", 1) == 0 || LK > 96 || R > 256 || d % 4 != 0) return;
+    const int P = N / 2;  // one MMA (N <= 240) per output half
+    tc.LK = LK;
+    tc.LKp = LKp;
+    tc.d = d;
+    tc.R = R;
+    tc.N = N;
+    tc.P = P;
+    tc.coeffs = d_coeffs;
+    tc.bimg.alloc(static_cast<size_t>(N) * R);
+    tc.scale.alloc(2 * LKp);
+    proj_tc_prep_kernel<<<LKp, 128, 0, s>>>(d_coeffs, LK, d, R, LKp, P, tc.bimg.get(), tc.scale.get());
+    DETLSH_LAUNCH_CHECK();
+    tc.ok = true;
+}
+
+bool launch_project_tc(const float* d_points, uint64_t n, int d, const ProjTc& tc, const double* d_ct,
+                       int K, int L, float* d_out, cudaStream_t s, const char* prof,
+                       uint32_t* d_nonint) {
+    if (!tc.ok || tc.d != d || tc.LK != K * L || n < 4096 || (reinterpret_cast<uintptr_t>(d_points) & 15))
+        return false;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int stages = env_int("DETLSH_TEST_PROJ_STAGES", tc.R <= 128 ? 3 : 2);
+    const size_t fixed = 16 + static_cast<size_t>(tc.N) * tc.R + static_cast<size_t>(stages) * kTP * tc.R +
+                         static_cast<size_t>(stages) * kTP * 4 + 2 * tc.LKp * 8 + 8 +
+                         (2 * stages + 2 * kMaxSlots + 2 * kMaxChunks) * 8 + 16;
+    const size_t cbytes = static_cast<size_t>(kCR) * d * 4;
+    const size_t budget = 227 * 1024;
+    // a whole number of tiles of staging chunks: chunk c of every tile then always
+    // lands in a slot only converter pair c uses, so each slot's full/empty
+    // phases advance one consumer step at a time (parity waits stay valid)
+    const int fit = fixed < budget ? static_cast<int>(std::min<size_t>(kMaxChunks, (budget - fixed) / cbytes)) : 0;
+    const int nch = fit / (kTP / kCR) * (kTP / kCR);
+    if (nch < kTP / kCR) return false;  // (d above ~200: the FP64 DMMA kernel)
+    const int nch_t = env_int("DETLSH_TEST_PROJ_NCH", 0);
+    const int nch_u = nch_t > 0 && nch_t < nch && nch_t % (kTP / kCR) == 0 ? nch_t : nch;
+    const size_t smem = fixed + nch_u * cbytes;
+    static bool attr_set = false;
+    if (!attr_set) {
+        DETLSH_CUDA(cudaFuncSetAttribute(project_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    const uint32_t cap = static_cast<uint32_t>(std::min<uint64_t>(
+        env_int("DETLSH_TEST_PROJ_CAP", -1) >= 0 ? static_cast<uint64_t>(env_int("DETLSH_TEST_PROJ_CAP", 0))
+                                                 : n / 4 + 65536,
+        0xffffffffu));
+    DevBuf<uint32_t> status(2);
+    DevBuf<uint64_t> pend(std::max<uint32_t>(cap, 1));
+    DETLSH_CUDA(cudaMemsetAsync(status.get(), 0, 8, s));
+    TcArgs a;
+    a.pts = d_points;
+    a.n = n;
+    a.d = d;
+    a.R = tc.R;
+    a.K = K;
+    a.LK = tc.LK;
+    a.LKp = tc.LKp;
+    a.N = tc.N;
+    a.P = tc.P;
+    a.stages = stages;
+    a.nslots = std::min(kMaxSlots, 512 / tc.P);
+    a.nch = nch_u;
+    a.bimg = tc.bimg.get();
+    a.scale = tc.scale.get();
+    a.out = d_out;
+    a.status = status.get();
+    a.pend = pend.get();
+    a.cap = cap;
+    a.errd = static_cast<uint32_t>(d - 1) * static_cast<uint32_t>(std::max(1, env_int("DETLSH_TEST_PROJ_ERR_SCALE", 1)));
+    a.force_band = env_int("DETLSH_TEST_PROJ_ERR_SCALE", 1) > 1;
+    const uint64_t tiles = (n + kTP - 1) / kTP;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count(dev))));
+    {
+        ProfScope ps(prof, s);
+        project_tc_kernel<<<grid, kThreads, smem, s>>>(a);
+        DETLSH_LAUNCH_CHECK();
+    }
+    {
+        ProfScope ps("project_fixup", s);
+        const size_t fsm = static_cast<size_t>(kFixWarps) * 32 * (d + 1) * 4;
+        static bool fattr = false;
+        if (!fattr) {
+            DETLSH_CUDA(cudaFuncSetAttribute(proj_tc_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(kFixWarps * 32 * 257 * 4)));
+            fattr = true;
+        }
+        proj_tc_fixup_kernel<<<static_cast<unsigned>(sm_count(dev) * 2), 32 * kFixWarps, fsm, s>>>(
+            d_points, d, tc.coeffs, K, n, status.get(), pend.get(), cap, d_out);
+        DETLSH_LAUNCH_CHECK();
+        launch_project_dmma_guarded(d_points, n, d, d_ct, K, L, d_out, status.get(), cap, s);
+    }
+    if (d_nonint) DETLSH_CUDA(cudaMemcpyAsync(d_nonint, status.get(), 4, cudaMemcpyDeviceToDevice, s));
+    if (env_int("DETLSH_DEBUG_PROJ", 0)) {
+        uint32_t h[2];
+        DETLSH_CUDA(cudaMemcpyAsync(h, status.get(), 8, cudaMemcpyDeviceToHost, s));
+        DETLSH_CUDA(cudaStreamSynchronize(s));
+        fprintf(stderr, "[project_tc] n=%llu nonintegral=%u undecided=%u cap=%u\n",
+                static_cast<unsigned long long>(n), h[0], h[1], cap);
+    }
+    return true;
+}
+
+}  // namespace detlsh_b200

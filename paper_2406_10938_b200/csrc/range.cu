@@ -230,7 +230,7 @@ void range_query_impl(GpuIndex& X, int tree, const float* q_proj, uint64_t nq, c
     const int L = X.params.L;
     DevBuf<float> proj(static_cast<size_t>(L) * n * K);
     if (X.paa) launch_project_paa(X.data, n, X.d, K, proj.get(), s);
-    else launch_project_exact(X.data, n, X.d, X.coeffs_t.get(), K, L, proj.get(), s);
+    else launch_project_exact(X.data, n, X.d, X.coeffs_t.get(), K, L, proj.get(), s, "project_exact", &X.proj_tc);
     const float* pspace = proj.get() + static_cast<size_t>(tree) * n * K;
     DevBuf<uint8_t> pass(n);
     DevBuf<uint32_t> cnt(nl), off(nl);

@@ -1,6 +1,7 @@
 // Build-stage kernels: exact projection, sample gather, GPU-native sample,
 // order-statistic breakpoints, encoding and the r_min order statistics.
 #include <algorithm>
+#include <cstring>
 #include <vector>
 
 #include "primitives.cuh"
@@ -36,7 +37,11 @@ constexpr int kAS = 72;  // padded coefficient row (doubles): B-fragment loads i
 
 __global__ void __launch_bounds__(256) project_dmma_kernel(
     const float* __restrict__ pts, uint64_t n, int d, const double* __restrict__ ct, int LK,
-    int LKp, int K, float* __restrict__ out) {
+    int LKp, int K, float* __restrict__ out, const uint32_t* __restrict__ guard = nullptr,
+    uint32_t guard_cap = 0) {
+    // guarded mode (project_tc.cu): run only when the tensor-core pass saw a
+    // non-integral value or queued more undecided outputs than it could hold
+    if (guard && guard[0] == 0 && guard[1] <= guard_cap) return;
     __shared__ __align__(16) float sx[kPT][kPS];
     __shared__ __align__(16) double sa[kDC][kAS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -422,9 +427,25 @@ void prepare_coeffs_t(const float* d_coeffs, int LK, int d, double* d_ct, cudaSt
     DETLSH_LAUNCH_CHECK();
 }
 
+void launch_project_dmma_guarded(const float* d_points, uint64_t n, int d, const double* d_ct, int K,
+                                 int L, float* d_out, const uint32_t* d_guard, uint32_t cap, cudaStream_t s) {
+    const int LK = K * L;
+    const uint64_t tiles = (n + kPT - 1) / kPT;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(sm_count(dev)) * 2);
+    project_dmma_kernel<<<static_cast<unsigned>(grid), 256, 0, s>>>(d_points, n, d, d_ct, LK, lk_padded(LK),
+                                                                     K, d_out, d_guard, cap);
+    DETLSH_LAUNCH_CHECK();
+}
+
 void launch_project_exact(const float* d_points, uint64_t n, int d, const double* d_ct, int K,
-                          int L, float* d_out, cudaStream_t s, const char* prof) {
+                          int L, float* d_out, cudaStream_t s, const char* prof, const ProjTc* tc,
+                          uint32_t* d_nonint) {
     if (n == 0) return;
+    if (tc && launch_project_tc(d_points, n, d, *tc, d_ct, K, L, d_out, s,
+                                std::strcmp(prof, "project_exact") == 0 ? "project_tc" : prof, d_nonint))
+        return;
     const int LK = K * L;
     const uint64_t tiles = (n + kPT - 1) / kPT;
     int dev = 0;

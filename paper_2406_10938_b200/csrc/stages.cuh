@@ -17,8 +17,36 @@ void prepare_coeffs_t(const float* d_coeffs, int LK, int d, double* d_coeffs_t, 
 // (float x float is exact in double, so fma == mul+add), rounded once.
 // out [L][n][K] fp32.
 // `prof` names the profile scope (the early sample-row projection is reported apart)
+//
+// With `tc` (prepared by prepare_proj_tc for the same coefficients) the exact
+// projection of 8-bit-integer data runs on the tensor cores (project_tc.cu:
+// tcgen05 kind::i8 over base-256 coefficient digits, each output certified
+// against the reference's fp64 rounding, undecided ones recomputed); non-
+// integral data falls back to the FP64 DMMA kernel on the device.  With
+// `d_nonint`, the word receives 0 iff every value was an integer in [0, 255]
+// (the tensor-core pass only; the DMMA path leaves it untouched).
+struct ProjTc;
 void launch_project_exact(const float* d_points, uint64_t n, int d, const double* d_coeffs_t,
-                          int K, int L, float* d_out, cudaStream_t s, const char* prof = "project_exact");
+                          int K, int L, float* d_out, cudaStream_t s, const char* prof = "project_exact",
+                          const ProjTc* tc = nullptr, uint32_t* d_nonint = nullptr);
+
+// Operand image for the tensor-core projection: coefficient digits
+// [N = 5 LKp columns][R bytes] in the UMMA K-major layout (pieces of P
+// columns), fp32 2^sc per output.  ok = false when the shape is not covered
+// (LK > 96, d > 256, d % 4 != 0) or DETLSH_PROJ_TC=0; a launch also declines
+// (-> DMMA) when four 32-row staging chunks do not fit beside the operands (d > ~200).
+struct ProjTc {
+    bool ok = false;
+    int LK = 0, LKp = 0, d = 0, R = 0, N = 0, P = 0;
+    const float* coeffs = nullptr;  // [LK][d] fp32, caller-owned (the fixup reads it)
+    DevBuf<uint8_t> bimg;
+    DevBuf<int> scale;  // [0, LKp): grid exponent sc_o, [LKp, 2 LKp): truncated coefficients
+};
+void prepare_proj_tc(const float* d_coeffs, int LK, int d, ProjTc& tc, cudaStream_t s);
+bool launch_project_tc(const float* d_points, uint64_t n, int d, const ProjTc& tc, const double* d_ct,
+                       int K, int L, float* d_out, cudaStream_t s, const char* prof, uint32_t* d_nonint);
+void launch_project_dmma_guarded(const float* d_points, uint64_t n, int d, const double* d_ct, int K,
+                                 int L, float* d_out, const uint32_t* d_guard, uint32_t cap, cudaStream_t s);
 
 // paa_project_dataset (projection.cpp:62-90): out [1][n][K] fp32, segment j =
 // [j*(d/K), (j+1)*(d/K)) (the last takes the remainder), mean = sequential

@@ -2,7 +2,10 @@
 throughput %, occupancy, L1/L2 hit rates; and update profiles/ncu_latest.json
 (dram bytes per work unit, used by bench.py for the roofline `traffic`).
 
-    python tools/ncu_summary.py REPORT.ncu-rep KERNEL_REGEX UNITS OUT_TXT
+    python tools/ncu_summary.py REPORT.ncu-rep KERNEL_REGEX UNITS OUT_TXT [CONFIG_KEY]
+
+CONFIG_KEY (e.g. c2:n=1000000:nq=10000) names the workload the capture ran;
+bench.py takes `traffic` only from records of its own workload.
 """
 import csv
 import io
@@ -23,7 +26,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
 
 
-def main(rep, pattern, units, out_txt):
+def main(rep, pattern, units, out_txt, config=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -50,7 +53,7 @@ def main(rep, pattern, units, out_txt):
         dram = rec.get("dram__bytes_read.sum", 0) + rec.get("dram__bytes_write.sum", 0)
         summary[short] = {"dram_bytes": dram, "duration_ms": rec.get("gpu__time_duration.sum"),
                           "dram_bytes_per_unit": dram / float(units),
-                          "source": os.path.basename(out_txt)}
+                          "source": os.path.basename(out_txt), "config": config}
     with open(out_txt, "w") as f:
         f.write(f"# ncu summary of {os.path.basename(rep)} (units per launch = {units})\n")
         f.write("\n".join(lines) + "\n")
@@ -64,4 +67,4 @@ def main(rep, pattern, units, out_txt):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], float(sys.argv[3]), sys.argv[4])
+    main(sys.argv[1], sys.argv[2], float(sys.argv[3]), sys.argv[4], sys.argv[5] if len(sys.argv) > 5 else None)
