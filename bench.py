@@ -53,6 +53,8 @@ def parse():
                          "the all-gather of per-shard lists; rank 0 prints one JSON line")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-queries", type=int, default=200)
+    ap.add_argument("--gt-queries", type=int, default=500,
+                    help="c5: queries scored against the exact kNN (device brute force)")
     ap.add_argument("--cpu-build-rows", type=int, default=None,
                     help="rows the reference build is timed on (default: the full n, same config)")
     return ap.parse_args()
@@ -411,10 +413,23 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = D.load()
     cfg = args.config
-    base, Q = gen.make(cfg, nq=args.nq)
-    n, d = base.shape
+    devgen = cfg == "c5"  # 51 GB: generated on the GPU, never through host memory
+    if devgen:
+        base_d, Q_d = gen.make_device(cfg, nq=args.nq, device=local)
+        base = None
+        Q = Q_d.cpu().numpy()
+        n, d = base_d.shape
+    else:
+        base, Q = gen.make(cfg, nq=args.nq)
+        n, d = base.shape
     nq = Q.shape[0]
-    if world > 1 and args.shard == "weak":
+    if devgen:
+        if world > 1 and args.shard == "weak":
+            raise SystemExit("c5: strong (point-sharded) scaling only")
+        s0, s1 = shard_bounds(n, world, rank)
+        shard = None
+        n_total = n
+    elif world > 1 and args.shard == "weak":
         # weak scaling: rank r holds points [r n, (r+1) n) of a world x n dataset
         shard = base if rank == 0 else np.ascontiguousarray(gen.make_shard(cfg, rank, n))
         s0 = rank * n
@@ -423,11 +438,11 @@ def main():
         s0, s1 = shard_bounds(n, world, rank)
         shard = np.ascontiguousarray(base[s0:s1])
         n_total = n
-    n_loc = shard.shape[0]
+    n_loc = (s1 - s0) if devgen else shard.shape[0]
     params = D.LshParams(beta=args.beta, k=args.k)
     k = args.k
-    dev_shard = torch.from_numpy(shard).cuda()
-    dev_Q = torch.from_numpy(Q).cuda()
+    dev_shard = base_d[s0:s1] if devgen else torch.from_numpy(shard).cuda()
+    dev_Q = Q_d if devgen else torch.from_numpy(Q).cuda()
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -537,7 +552,7 @@ def main():
     clk = clocks.stop()
 
     # ---------------- end to end through the public API, host buffers ----------------
-    shard_pinned = torch.from_numpy(shard).pin_memory().numpy()  # host input, pinned
+    shard_pinned = None if devgen else torch.from_numpy(shard).pin_memory().numpy()  # host input, pinned
 
     def e2e_build():
         ix = D.build_index(shard_pinned, params, seed=args.seed, device=local, sample=args.sample,
@@ -545,13 +560,15 @@ def main():
         _ = ix.params.r_min  # result read back (params travel D2H inside build)
         return ix
 
-    w = None
-    for _ in range(args.warmup):  # same live-index pattern as the timed loop
-        w = e2e_build()
-    del w
-    e2e_build_ms, ix2 = timed(e2e_build, max(1, args.steps))
-    e2e_build_ms = max_over_ranks(e2e_build_ms)
-    del ix2
+    e2e_build_ms = None
+    if not devgen:  # (c5's 51 GB shard lives on the device only)
+        w = None
+        for _ in range(args.warmup):  # same live-index pattern as the timed loop
+            w = e2e_build()
+        del w
+        e2e_build_ms, ix2 = timed(e2e_build, max(1, args.steps))
+        e2e_build_ms = max_over_ranks(e2e_build_ms)
+        del ix2
     Qpin = torch.from_numpy(Q).pin_memory().numpy()
 
     def e2e_query():
@@ -581,7 +598,14 @@ def main():
     bound = np.where(out_h == k, out_d[:, k - 1] ** 2 * (1 + 1e-12), np.inf)
     if world > 1:
         bound = None  # a shard may hold fewer than k points inside the global bound
-    gt_ids, gt_d = D.brute_force_knn(shard, Q, k, dist2_bound=bound, device=local)
+    if devgen:  # exact kNN on the device, for the first gt_queries queries
+        m_gt = min(nq, args.gt_queries)
+        gi, gdd = D.brute_force_knn_device(dev_shard, dev_Q[:m_gt].contiguous(), k,
+                                           dist2_bound=None if bound is None else bound[:m_gt])
+        gt_ids, gt_d = gi.cpu().numpy().view(np.uint32), gdd.cpu().numpy()
+        out_ids, out_d, out_h = out_ids[:m_gt], out_d[:m_gt], out_h[:m_gt]
+    else:
+        gt_ids, gt_d = D.brute_force_knn(shard, Q, k, dist2_bound=bound, device=local)
     gt_ids = gt_ids.astype(np.int64) + s0
     if world > 1:
         t_i = torch.from_numpy(gt_ids).cuda()
@@ -645,7 +669,7 @@ def main():
                                f"k={k}, c=1.5, beta={args.beta}",
                    "points_per_gpu": n_loc,
                    "sample_mode": args.sample, "parallelism": f"point-shard x{world}",
-                   "l2": "inputs larger than L2 (dataset 512 MB, candidate rows 51 MB/query)"},
+                   "l2": f"inputs larger than L2 (dataset {n_loc * d * 4 / 1e9:.2f} GB)"},
         "query": {"value": round(qps, 2), "unit": "queries/s", "ms_per_step": round(query_ms, 3),
                   "recall": round(rec, 6), "ratio": round(rat, 6),
                   "recall_on_reference_sample": round(rec_ref, 6),
@@ -654,8 +678,10 @@ def main():
                   "e2e": {"value": round(nq / (e2e_query_ms / 1e3), 2), "unit": "queries/s",
                           "h2d_bytes_per_step": int(nq * d * 4),
                           "d2h_bytes_per_step": int(nq * k * 12 + nq * 20)}},
-        "e2e": {"value": round(n_total / (e2e_build_ms / 1e3) / 1e6, 3), "unit": "Mpoints/s",
-                "h2d_bytes_per_step": int(n_loc * d * 4), "d2h_bytes_per_step": 96},
+        "e2e": ({"value": round(n_total / (e2e_build_ms / 1e3) / 1e6, 3), "unit": "Mpoints/s",
+                 "h2d_bytes_per_step": int(n_loc * d * 4), "d2h_bytes_per_step": 96} if e2e_build_ms else
+                {"value": None, "unit": "Mpoints/s", "note": "c5: the dataset is generated on the device "
+                 "(51 GB); the host-buffer build is not timed"}),
         "gpu_launches": build_launches,
         "build_other_sample": {"sample_mode": other, "value": round(n_total / (other_ms / 1e3) / 1e6, 3),
                                "unit": "Mpoints/s", "ms_per_step": round(other_ms, 3),
@@ -669,9 +695,17 @@ def main():
                                 "query": {k2: round(v[0] / args.steps, 4) for k2, v in prof_query.items()}},
         "clocks": clk,
     }
+    if devgen:
+        line["query"]["recall_queries"] = int(min(nq, args.gt_queries))
     if not args.no_cpu_baseline and world == 1:
         try:
+            if devgen:  # the reference on a bounded host copy: the first cpu_build_rows rows
+                rows = args.cpu_build_rows or 1_000_000
+                base = base_d[:rows].cpu().numpy()
             line["cpu_baseline"] = cpu_baseline(args, base, Q)
+            if devgen:
+                line["cpu_baseline"]["sample"] = (f"c5 shard: the first {base.shape[0]} of {n} rows (copied to the "
+                                                  "host); " + line["cpu_baseline"]["sample"])
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"error": str(e)}
     print(json.dumps(line), flush=True)

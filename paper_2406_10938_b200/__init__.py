@@ -15,6 +15,7 @@ from .api import (  # noqa: F401
     QueryResult,
     TreeExport,
     brute_force_knn,
+    brute_force_knn_device,
     build_det_only_index,
     build_index,
     build_index_with_family,

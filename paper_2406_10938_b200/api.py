@@ -437,6 +437,27 @@ def brute_force_knn(data, queries, k: int, *, dist2_bound=None, device: int = 0)
     return ids, ds
 
 
+def brute_force_knn_device(data, queries, k: int, *, dist2_bound=None, stream=None):
+    """brute_force_knn on CUDA tensors (data [n][d], queries [nq][d] fp32 on one
+    device): (ids [nq][k] uint32 as int32 tensor, dists [nq][k] float64 tensor)."""
+    import torch
+    dev = data.device.index if data.device.index is not None else 0
+    n, d = data.shape
+    nq = int(queries.shape[0])
+    _check_tensor(data, "brute_force_knn: data", torch.float32, (n, d), dev)
+    _check_tensor(queries, "brute_force_knn: queries", torch.float32, (nq, d), dev)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=data.device)
+    ds = torch.empty((nq, k), dtype=torch.float64, device=data.device)
+    b = None
+    if dist2_bound is not None:
+        bt = torch.as_tensor(dist2_bound, dtype=torch.float64, device=data.device).contiguous()
+        b = C.c_void_p(bt.data_ptr())
+    check(_lib.load().detlsh_gpu_brute_force_knn(C.c_void_p(data.data_ptr()), n, d, C.c_void_p(queries.data_ptr()),
+                                                 nq, k, b, F_DEVICE_PTRS, C.c_void_p(ids.data_ptr()),
+                                                 C.c_void_p(ds.data_ptr()), dev, stream))
+    return ids, ds
+
+
 def vectors_shape(path: str):
     """(n, d, kind) of a .fvecs / .bvecs / .ivecs file (io.cpp:28-85 validation)."""
     n = C.c_uint64(0)

@@ -263,9 +263,22 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     X->codes.alloc(static_cast<size_t>(L) * n * K);
     X->trees.resize(L);
     for (auto& t : X->trees) t = std::make_unique<DevTree>();
+    // the tensor-core projection checks every value for [0, 255] integrality on
+    // its way through: its verdict replaces a separate pass (0xffffffff: not run)
+    DevBuf<uint32_t> nonint(1);
+    bool probe_nonint = false;
+    DETLSH_CUDA(cudaMemsetAsync(nonint.get(), 0xff, 4, s));
     auto project_all = [&]() {
-        if (paa) launch_project_paa(X->data, n, d, K, proj.get(), s);
-        else launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s, "project_exact", &X->proj_tc);
+        if (paa) {
+            launch_project_paa(X->data, n, d, K, proj.get(), s);
+            return;
+        }
+        // a glance at the first rows (a few KB) keeps float datasets off the
+        // tensor-core attempt, whose full pass would only end in the FP64 rerun
+        const bool try_tc = X->proj_tc.ok && data_is_u8(X->data, std::min<uint64_t>(n, 4096) * d, s);
+        if (X->proj_tc.ok && !try_tc) probe_nonint = true;  // a non-integral value seen: no u8 rows
+        launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s, "project_exact",
+                             try_tc ? &X->proj_tc : nullptr, nonint.get());
     };
     // reference-compatible sample (encoder.cpp:105-143): one RNG stream picks
     // every space's sample and pivots, so the host replay is sequential
@@ -397,7 +410,13 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     // exact u8 verification rows (integral datasets): decided now, packed in
     // tree-0 leaf order by the space-0 worker right after tree 0 (query.cu)
     t0 = Clock::now();
-    const bool want_u8 = !(flags & DETLSH_F_NO_U8) && data_is_u8(X->data, n * static_cast<uint64_t>(d), s);
+    uint32_t h_nonint = 0xffffffffu;
+    if (!(flags & DETLSH_F_NO_U8)) {
+        DETLSH_CUDA(cudaMemcpyAsync(&h_nonint, nonint.get(), 4, cudaMemcpyDeviceToHost, s));
+        DETLSH_CUDA(cudaStreamSynchronize(s));
+    }
+    const bool want_u8 = !(flags & DETLSH_F_NO_U8) && !probe_nonint &&
+                         (h_nonint == 0xffffffffu ? data_is_u8(X->data, n * static_cast<uint64_t>(d), s) : h_nonint == 0);
     if (want_u8) {
         X->row_u8 = (d + 31) / 32 * 32;  // whole 32-byte MMA K steps
         const int chunks = X->row_u8 / 16;

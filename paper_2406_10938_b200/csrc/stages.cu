@@ -390,18 +390,40 @@ __global__ void rmin_sel_hist(const double* __restrict__ D, uint64_t n,
         if (h[i]) atomicAdd(&ghist[static_cast<size_t>(p) * kSelBins + i], h[i]);
 }
 
-__global__ void rmin_sel_pick(uint32_t* __restrict__ ghist, unsigned long long* lo,
-                              unsigned long long* hi, int* shift, uint64_t* need) {
-    const int p = blockIdx.x;
+// The bin holding the wanted rank: block-wide exclusive scan over the 2048 bin
+// counts (8 per thread), then the owning thread walks its 8 bins.
+__global__ void __launch_bounds__(256) rmin_sel_pick(uint32_t* __restrict__ ghist, unsigned long long* lo,
+                                                     unsigned long long* hi, int* shift, uint64_t* need) {
+    const int p = blockIdx.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
     uint32_t* h = ghist + static_cast<size_t>(p) * kSelBins;
-    if (threadIdx.x == 0) {
-        uint64_t want = need[p], cum = 0;
-        int bin = 0;
-        for (; bin < kSelBins; ++bin) {
-            if (cum + h[bin] >= want) break;
-            cum += h[bin];
+    __shared__ unsigned long long wsum[8];
+    constexpr int kPer = kSelBins / 256;
+    uint32_t c[kPer];
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+        c[e] = h[t * kPer + e];
+        mine += c[e];
+    }
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    unsigned long long base = 0;
+    for (int i = 0; i < w; ++i) base += wsum[i];
+    const unsigned long long excl = base + incl - mine;
+    const uint64_t want = need[p];
+    __syncthreads();  // every thread has read need[p] and the bins
+    if (excl < want && want <= excl + mine) {
+        unsigned long long cum = excl;
+        int bin = t * kPer;
+        for (int e = 0; e < kPer; ++e, ++bin) {
+            if (cum + c[e] >= want) break;
+            cum += c[e];
         }
-        if (bin == kSelBins) bin = kSelBins - 1;  // unreachable: rank <= count in range
         const int sh = shift[p];
         const unsigned long long nlo = lo[p] + (static_cast<unsigned long long>(bin) << sh);
         unsigned long long nhi = nlo + ((1ULL << sh) - 1);
@@ -413,8 +435,8 @@ __global__ void rmin_sel_pick(uint32_t* __restrict__ ghist, unsigned long long* 
         const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
         shift[p] = bits > 11 ? bits - 11 : 0;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) h[i] = 0;
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) h[t * kPer + e] = 0;
 }
 
 }  // namespace
@@ -561,8 +583,10 @@ void rmin_select(RminSelect& sel, const double* d_D, uint64_t n, uint64_t rank, 
     int dev = 0;
     cudaGetDevice(&dev);
     const int np = sel.np;
-    const unsigned gx = static_cast<unsigned>(
-        std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 8)));
+    // two CTAs per SM over all probes: each CTA clears and flushes a 2048-bin
+    // histogram, so more CTAs than that cost more than they hide
+    const unsigned gx = static_cast<unsigned>(std::max<uint64_t>(
+        1, std::min<uint64_t>((n + 255) / 256, (static_cast<uint64_t>(sm_count(dev)) * 2 + np - 1) / np)));
     std::vector<uint64_t> h(np, rank);
     DETLSH_CUDA(cudaMemcpyAsync(sel.need.get(), h.data(), np * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
     DETLSH_CUDA(cudaMemsetAsync(sel.hist.get(), 0, static_cast<size_t>(np) * kSelBins * sizeof(uint32_t), s));
@@ -600,42 +624,60 @@ __global__ void integral_u8_kernel(const float* __restrict__ x, uint64_t total,
     if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
 
-// out[p'] = u8(rows[perm[p']]), zero-padded to row_bytes (multiple of 16)
+// out[p'] = u8(rows[perm[p']]), zero-padded to row_bytes (multiple of 16).
+// One thread per 16-byte output chunk: four float4 reads of the gathered row
+// (d % 4 == 0; scalar reads otherwise), one 16-byte store.
 __global__ void pack_u8_kernel(const float* __restrict__ x, const uint32_t* __restrict__ perm,
                                uint64_t n, int d, int row_bytes, uint8_t* __restrict__ out) {
-    const uint64_t total = n * static_cast<uint64_t>(row_bytes);
+    const uint32_t cpr = static_cast<uint32_t>(row_bytes) / 16;  // chunks per row
+    const uint64_t total = n * cpr;
+    const bool vec = (d & 3) == 0;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t r = i / row_bytes;
-        const int t = static_cast<int>(i % row_bytes);
-        out[i] = t < d ? static_cast<uint8_t>(x[static_cast<uint64_t>(perm[r]) * d + t]) : 0;
+        const uint64_t r = i / cpr;
+        const int t0 = static_cast<int>(i - r * cpr) * 16;
+        const float* src = x + static_cast<uint64_t>(__ldg(perm + r)) * d;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float f[4];
+            const int t = t0 + 4 * q;
+            if (vec && t + 4 <= d) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(src + t));
+                f[0] = v.x, f[1] = v.y, f[2] = v.z, f[3] = v.w;
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) f[e] = t + e < d ? __ldg(src + t + e) : 0.0f;
+            }
+            w[q] = static_cast<uint32_t>(f[0]) | static_cast<uint32_t>(f[1]) << 8 | static_cast<uint32_t>(f[2]) << 16 |
+                   static_cast<uint32_t>(f[3]) << 24;
+        }
+        reinterpret_cast<uint4*>(out)[i] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
-// fp32 rows gathered into tree-0 leaf order (16-byte moves when d % 4 == 0).
+// fp32 rows gathered into tree-0 leaf order (or a sample's rows): one warp per
+// row, 16-byte moves when d % 4 == 0 (no per-element index division).
 __global__ void pack_f32_kernel(const float* __restrict__ x, const uint32_t* __restrict__ perm, uint64_t n,
                                 int d, float* __restrict__ out) {
-    if ((d & 3) == 0) {
-        const int q4 = d / 4;
-        const uint64_t total = n * static_cast<uint64_t>(q4);
-        for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-             i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-            const uint64_t r = i / q4;
-            reinterpret_cast<float4*>(out)[i] =
-                __ldg(reinterpret_cast<const float4*>(x + static_cast<uint64_t>(perm[r]) * d) + (i % q4));
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t r = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint64_t src = static_cast<uint64_t>(__ldg(perm + r)) * d;
+        if ((d & 3) == 0) {
+            const float4* s4 = reinterpret_cast<const float4*>(x + src);
+            float4* d4 = reinterpret_cast<float4*>(out + r * d);
+            for (int q = lane; q < d / 4; q += 32) d4[q] = __ldg(s4 + q);
+        } else {
+            for (int t = lane; t < d; t += 32) out[r * d + t] = __ldg(x + src + t);
         }
-        return;
     }
-    const uint64_t total = n * static_cast<uint64_t>(d);
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-        out[i] = x[static_cast<uint64_t>(perm[i / d]) * d + i % d];
 }
 
 }  // namespace
 
 void launch_pack_f32(const float* d_x, const uint32_t* d_perm, uint64_t n, int d, float* d_out, cudaStream_t s) {
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n * d / 4 + 255) / 256 + 1, 65535));
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, 65535)));
     ProfScope ps("pack_f32", s);
     pack_f32_kernel<<<grid, 256, 0, s>>>(d_x, d_perm, n, d, d_out);
     DETLSH_LAUNCH_CHECK();
@@ -661,7 +703,7 @@ void launch_pack_u8(const float* d_x, const uint32_t* d_perm, uint64_t n, int d,
                     uint8_t* d_out, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
-    const uint64_t total = n * static_cast<uint64_t>(row_bytes);
+    const uint64_t total = n * static_cast<uint64_t>(row_bytes / 16);
     const unsigned grid = static_cast<unsigned>(
         std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, static_cast<uint64_t>(sm_count(dev)) * 16)));
     ProfScope ps("pack_u8", s);
