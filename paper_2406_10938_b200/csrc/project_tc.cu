@@ -41,8 +41,15 @@ namespace {
 
 constexpr int kTP = 128;         // points per tile (MMA M = TMEM lanes)
 constexpr int kDig = 5;          // base-256 digits per coefficient
-constexpr int kEpiWarps = 16;    // four per TMEM lane quadrant (warps 0..15)
-constexpr int kConvWarps = 8;    // fp32 -> u8 operand producers
+#ifndef DETLSH_PTC_EPI
+#define DETLSH_PTC_EPI 16
+#endif
+constexpr int kEpiWarps = DETLSH_PTC_EPI;          // epilogue warps 0 .. kEpiWarps-1 (8 or 16)
+constexpr int kConvWarps = 24 - kEpiWarps;         // fp32 -> u8 operand producers
+constexpr int kEpiSub = kEpiWarps / 8;             // warps per (lane quadrant, output half)
+constexpr int kConvPerChunk = kConvWarps / 4;      // converter warps per 32-row staging chunk
+constexpr int kGroupsPerConv = 16 / kConvWarps;    // 8-row groups per converter warp per tile
+static_assert(kEpiWarps % 8 == 0 && kConvWarps % 4 == 0 && 16 % kConvWarps == 0, "warp split");
 constexpr int kMmaWarp = kEpiWarps + kConvWarps;
 constexpr int kLoadWarp = kMmaWarp + 1;  // TMA bulk copies of the fp32 rows
 constexpr int kThreads = (kLoadWarp + 1) * 32;
@@ -204,23 +211,23 @@ __global__ void __launch_bounds__(kThreads, 1) project_tc_kernel(const TcArgs a)
             const uint32_t gc = j * (kTP / kCR) + chunk, cs = gc % a.nch;
             // one warp of the pair on this chunk polls the barriers (stage free,
             // chunk staged); the other parks in a named barrier instead of spinning
-            if ((cw & 1) == 0) {
+            if (cw % kConvPerChunk == 0) {
                 if (j >= static_cast<uint32_t>(stages)) umma::mbar_wait_hint(&empty_a[st], ((j / stages) - 1) & 1, kHintNs);
                 umma::mbar_wait_hint(&cfull[cs], (gc / a.nch) & 1, kHintNs);
             }
-            named_bar(kBarConv + chunk, 64);
+            named_bar(kBarConv + chunk, 32 * kConvPerChunk);
             uint8_t* A = sA + static_cast<size_t>(st) * abytes;
             const float* C = reinterpret_cast<const float*>(sC + static_cast<size_t>(cs) * cbytes);
             // lane (r, kq): row 8 g + r, dims 16 kc + 4 kq .. +3 for every 16-dim
             // chunk kc; the stores of a warp fill whole 128-byte core matrices
             const int r = lane >> 2, kq = lane & 3;
-            for (int g = 2 * cw; g < 2 * cw + 2; ++g) {
+            for (int g = kGroupsPerConv * cw; g < kGroupsPerConv * (cw + 1); ++g) {
                 const int p = 8 * g + r;
                 const uint64_t z = tile * kTP + p;
                 const float* src = C + static_cast<size_t>(p - kCR * chunk) * a.d;
                 const bool live = z < a.n;
                 uint32_t sum = 0;
-#pragma unroll 4
+#pragma unroll 8
                 for (int kc = 0; kc < rf4 / 4; ++kc) {
                     const int f = 4 * kc + kq;
                     uint32_t word = 0;
@@ -303,14 +310,14 @@ __global__ void __launch_bounds__(kThreads, 1) project_tc_kernel(const TcArgs a)
         // warp w drains TMEM lane quadrant w % 4 (one point per thread); warps
         // 8 hf .. 8 hf + 7 take output half hf (groups of 16 outputs, alternating
         // between the two warps of a quadrant)
-        const int qd = warp & 3, ws = warp >> 2, hf = ws >> 1, sub = ws & 1;
+        const int qd = warp & 3, ws = warp >> 2, hf = ws / kEpiSub, sub = ws % kEpiSub;
         const int row = 32 * qd + lane;
         const int LK = a.LK, K = a.K, Lh = a.LKp / 2;
         uint32_t j = 0;
         for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++j) {
             const int st = j % stages;
             const uint32_t h = 2 * j + hf, sl = h % ns;
-            if (warp == 8 * hf) {  // one poller per output half; the half's other warps park
+            if (warp == 4 * kEpiSub * hf) {  // one poller per output half; the half's other warps park
                 umma::mbar_wait_hint(&slot_full[sl], (h / ns) & 1, kHintNs);
                 umma::mbar_wait(&full_a[st], (j / stages) & 1);  // (the producers' xs writes)
             }
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) project_tc_kernel(const TcArgs a)
             const double eseq_d = static_cast<double>(((static_cast<uint32_t>(xsum) * a.errd + 32767u) >> 15) + 1u +
                                                       (pt_exact ? 0u : 4u));
             const uint32_t tl = tmem + (static_cast<uint32_t>(32 * qd) << 16) + sl * P;
-            for (int ogl = 16 * sub; ogl < Lh; ogl += 32) {
+            for (int ogl = 16 * sub; ogl < Lh; ogl += 16 * kEpiSub) {
                 const int og = hf * Lh + ogl;  // global output index of the group
 #pragma unroll
                 for (int h8 = 0; h8 < 16; h8 += 8) {

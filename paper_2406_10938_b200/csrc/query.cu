@@ -1296,6 +1296,7 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             __syncthreads();
             const uint32_t nt = min(emit_rows(F.tau, n_tau, T0, F.cand, B32, S), B32);
             const int32_t tau2 = kth_dist2(P, F, S, nt, P.k);  // exact k-th smallest among those rows
+            phase(4);  // (profiling: tau rows + tau^2 apart from the bitmap)
             // candidate set: this query's row bitmap over tree-0 rows, written
             // here (zeroed, then each whole leaf's row range and the cut leaf's
             // taken prefix OR-ed in); tc_score_kernel reads it

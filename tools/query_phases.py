@@ -24,7 +24,7 @@ D.ck_ann_batch(idx, Q, 50)
 lib.detlsh_profile_enable(0)
 ph = np.zeros(8)
 lib.detlsh_query_phase_cycles(C.c_void_p(ph.ctypes.data))
-names = ["setup", "leaf_scan", "cut", "emission/tau+flags", "verify_topk", "output"]
+names = ["setup", "leaf_scan", "cut", "emission/flags (tc: bitmap)", "verify_topk (tc: tau rows + tau^2)", "output"]
 tot = ph[:6].sum()
 print(f"{cfg} nq={nq}: {nq/(t1-t0):.0f} q/s (unprofiled wall {1e3*(t1-t0):.1f} ms); "
       f"leaves={idx.tree(0).is_leaf.sum()} exact-round fallbacks={ph[6]:.0f} "
