@@ -465,7 +465,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                 launch_pack_u8(Xp->data, Xp->trees[0]->perm.get(), n, d, R, Xp->data_u8.get(), ts);
                 Xp->xn_u8.alloc(n);
                 launch_row_norms_u8(Xp->data_u8.get(), n, R, Xp->xn_u8.get(), ts);
-                if (R <= 256) {  // tensor-core verification operand tiles
+                if (tc_score_fits(R)) {  // tensor-core verification operand tiles
                     Xp->data_tc.alloc((n + 127) / 128 * 128 * static_cast<uint64_t>(R));
                     launch_pack_tc_tiles(Xp->data_u8.get(), n, R, Xp->data_tc.get(), ts);
                 }

@@ -907,20 +907,29 @@ __device__ int32_t kth_dist2(const QueryPlan& P, const FastSlot& F, const Smem& 
         }
         __syncthreads();
     }
+    // 12-bit digits from the top: the coarse level above, then as many finer
+    // levels as the dist^2 range needs (d > 256 spans more than 24 bits)
     uint32_t cb, before;
     select_count_bin(hist, 4096, static_cast<uint32_t>(k), S, cb, before);
-    const int nfine = 1 << sh;
-    for (int i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
-        const uint32_t d2 = F.cand[i];
-        if ((d2 >> sh) == cb) atomicAdd(&hist[d2 & (nfine - 1)], 1u);
+    uint32_t prefix = cb, need = static_cast<uint32_t>(k) - before;
+    while (sh > 0) {
+        const int nsh = sh > 12 ? sh - 12 : 0;   // the next digit: bits [nsh, sh)
+        const int nb = 1 << (sh - nsh);
+        for (int i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+            const uint32_t d2 = F.cand[i];
+            if ((d2 >> sh) == prefix) atomicAdd(&hist[(d2 >> nsh) & (nb - 1)], 1u);
+        }
+        __syncthreads();
+        uint32_t fb, before2;
+        select_count_bin(hist, nb >= static_cast<int>(blockDim.x) ? nb : static_cast<int>(blockDim.x), need, S, fb,
+                         before2);
+        prefix = (prefix << (sh - nsh)) | fb;
+        need -= before2;
+        sh = nsh;
     }
-    __syncthreads();
-    uint32_t fb, before2;
-    select_count_bin(hist, nfine >= static_cast<int>(blockDim.x) ? nfine : static_cast<int>(blockDim.x),
-                     static_cast<uint32_t>(k) - before, S, fb, before2);
-    return static_cast<int32_t>((cb << sh) | fb);
+    return static_cast<int32_t>(prefix);
 }
 
 // MINB CTAs per SM: 5 for u8 rows (the plan / u8 scoring is load-latency bound
@@ -1645,8 +1654,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // where the sample is a small part of the budget.
     const uint64_t tau_rows = std::max<uint64_t>(
         std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + kTcFinishCap - 1) / kTcFinishCap);
-    const bool tc_ok = P.tc_allowed && P.data_u8 && P.xn_u8 && P.data_tc && P.row_u8 % 32 == 0 &&
-                       P.row_u8 <= 256 && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
+    const bool tc_ok = P.tc_allowed && P.data_u8 && P.xn_u8 && P.data_tc && tc_score_fits(P.row_u8) && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
                        2ULL * P.k <= kTcFinishCap && 8 * tau_rows <= P.budget && P.k <= kFastMaxK && !P.rc_mode;
     // plan-kernel occupancy: 5 CTAs/SM when it hands verification to the
     // tensor cores (load-latency bound plan), 3 when it verifies candidates

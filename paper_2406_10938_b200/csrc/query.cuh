@@ -133,6 +133,8 @@ struct TcScoreArgs {
 };
 
 size_t tc_score_smem(int R);
+// rows of R bytes fit the scorer (R % 32 == 0; R > 256 takes the 128-query, K-chunked shape)
+bool tc_score_fits(int R);
 void launch_tc_pack_queries(const float* q, const uint32_t* order, uint64_t slot0, uint64_t m, int d,
                             int R, uint8_t* q8, int32_t* qn, cudaStream_t s);
 void launch_row_norms_u8(const uint8_t* rows, uint64_t n, int R, int32_t* xn, cudaStream_t s);

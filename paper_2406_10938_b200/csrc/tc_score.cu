@@ -154,18 +154,21 @@ __global__ void pack_tc_tiles_kernel(const uint8_t* __restrict__ rows, uint64_t 
 // branch-free: 2 q.x - (|q|^2 - tau^2) >= |x|^2 per element (IMAD + compare
 // into a mask); only columns where some lane passes are revisited, with
 // single-column TMEM loads, to consult the candidate bitmap.
-constexpr int kEpiWarps = 16;                      // epilogue warps (4 per TMEM lane quarter)
-constexpr int kTcThreads = 32 * (kEpiWarps + 2);   // + producer + MMA issuer
-constexpr int kEpiCols = kTcQueries / (kEpiWarps / 4);  // query columns per epilogue warp
-constexpr int kEpiWords = kEpiCols / 32;           // candidate words per lane (columns per lane)
-constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+// Two shapes of the same kernel: QT queries per tile, EW epilogue warps (4 per
+// TMEM lane quarter per 4-warp group).  Rows of R <= 256 bytes: 256-query
+// tiles, 16 epilogue warps, whole row tiles per stage.  Wider rows (C3,
+// d = 784): the 256-query operand would not fit beside the row stages, so
+// 128-query tiles, 8 epilogue warps, and row tiles streamed in 256-byte K
+// chunks (32 KB per stage, accumulated in TMEM across the chunks).
+constexpr int kEpiWarps = 16;                      // the wide-tile shape's epilogue warps (scratch sizing)
 constexpr uint32_t kTcRecChunk = 1024;  // records reserved per warp at a time
 static_assert(kTcRecReserve >= static_cast<uint64_t>(kEpiWarps) * kTcRecChunk, "rec_cap slack");
+constexpr uint32_t kTcChunkBytes = kTcRows * 256;  // one 256-byte K chunk of a 128-row tile
 constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
 constexpr uint32_t kWaitHintNs = 20000;  // mbarrier try_wait suspend hint (woken on completion)
 constexpr int kQSplit = 2;               // MMAs (and accumulator barriers) per tile, one per query part (4: slower)
 
-__device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 3u : 2u; }
+__host__ __device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 3u : 2u; }
 
 // A warp's next run of kTcRecChunk record slots; the unused tail of the old
 // run becomes padding.  (Called warp-uniformly.)
@@ -179,8 +182,13 @@ __device__ __noinline__ void tc_reserve(uint4* rec, unsigned long long* rec_cnt,
     end = base + kTcRecChunk;
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, uint32_t n_rt, uint32_t n_qt,
-                                                                 uint32_t G) {
+template <int QT, int EW>
+__global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs a, uint32_t n_rt, uint32_t n_qt,
+                                                                   uint32_t G) {
+    constexpr int kTcQueries = QT, kEpiWarps = EW;
+    constexpr int kEpiCols = kTcQueries / (kEpiWarps / 4);  // query columns per epilogue warp
+    constexpr int kEpiWords = kEpiCols / 32;                // candidate words per lane (columns per lane)
+    constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
     extern __shared__ __align__(1024) uint8_t sm[];
     // tfull/tempty per (accumulator, query part): the kQSplit query parts of a
     // tile are separate MMAs, so the epilogue warps of one part never wait for
@@ -188,11 +196,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
     __shared__ __align__(8) uint64_t full[6], empty[6], tfull[2][kQSplit], tempty[2][kQSplit];
     __shared__ uint32_t tslot, unit_s;
     const int R = a.R, kch = R / 16;
-    const uint32_t stages = tc_stages(R);
+    const bool chunked = R > 256;  // rows streamed in 256-byte K chunks
+    const uint32_t stages = chunked ? 2u : tc_stages(R);
     const uint32_t tile_bytes = static_cast<uint32_t>(kTcRows * R);
-    uint8_t* sB = sm;                                    // [256][R] core layout
-    uint8_t* sA = sB + kTcQueries * R;                   // [stages][128][R] core layout
-    int32_t* snh = reinterpret_cast<int32_t*>(sA + stages * tile_bytes);  // tau^2 - |q|^2
+    const uint32_t nkc = chunked ? static_cast<uint32_t>((kch + 15) / 16) : 1u;  // K chunks per row tile
+    const uint32_t stage_bytes = chunked ? kTcChunkBytes : tile_bytes;
+    uint8_t* sB = sm;                                    // [QT][R] core layout
+    uint8_t* sA = sB + kTcQueries * R;                   // [stages][128][R or 256] core layout
+    int32_t* snh = reinterpret_cast<int32_t*>(sA + stages * stage_bytes);  // tau^2 - |q|^2
     int32_t* sqn = snh + kTcQueries;
     uint32_t* sstash = reinterpret_cast<uint32_t*>(sqn + kTcQueries);  // [kEpiWarps][32 lanes][kTcStash]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -216,7 +227,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
     const uint32_t tmem = tslot;
     const uint32_t idesc = umma::idesc_u8_s32(kTcRows, kTcQueries / kQSplit);  // one query part per MMA
     const uint32_t units = n_qt * G;
-    uint32_t it = 0;  // tiles processed by this CTA so far (pipeline phases)
+    uint32_t it = 0;  // tiles processed by this CTA so far (accumulator phases)
+    uint32_t ic = 0;  // row-tile K chunks loaded so far (stage phases; == it unless chunked)
     uint32_t loaded_qt = 0xffffffffu;
     uint64_t res_next = 0, res_end = 0;  // this warp's reservation in a.rec
     for (;;) {
@@ -258,35 +270,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
         }
         if (warp == kProducerWarp) {
             if (lane == 0) {
-                for (uint32_t t = rt0, j = 0; t < rt1; ++t, ++j) {
-                    const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
-                    umma::mbar_wait_hint(&empty[s], ph ^ 1, kWaitHintNs);
-                    umma::mbar_arrive_expect_tx(&full[s], tile_bytes);
-                    umma::bulk_g2s(sA + s * tile_bytes, a.rows + static_cast<uint64_t>(t) * tile_bytes, tile_bytes,
-                                   &full[s]);
+                for (uint32_t t = rt0, j = 0; t < rt1; ++t) {
+                    for (uint32_t c = 0; c < nkc; ++c, ++j) {
+                        const uint32_t i = ic + j, s = i % stages, ph = (i / stages) & 1;
+                        // chunk c: 16-byte K columns [16 c, 16 c + 16) of the tile, contiguous
+                        const uint32_t bytes = chunked ? min(16u, static_cast<uint32_t>(kch) - 16u * c) * kTcRows * 16u
+                                                       : tile_bytes;
+                        umma::mbar_wait_hint(&empty[s], ph ^ 1, kWaitHintNs);
+                        umma::mbar_arrive_expect_tx(&full[s], bytes);
+                        umma::bulk_g2s(sA + s * stage_bytes,
+                                       a.rows + static_cast<uint64_t>(t) * tile_bytes + c * kTcChunkBytes, bytes,
+                                       &full[s]);
+                    }
                 }
             }
         } else if (warp == kMmaWarp) {
             if (lane == 0) {
-                for (uint32_t t = rt0, j = 0; t < rt1; ++t, ++j) {
-                    const uint32_t i = it + j, s = i % stages, ph = (i / stages) & 1;
+                for (uint32_t t = rt0, j = 0, jc = 0; t < rt1; ++t, ++j) {
+                    const uint32_t i = it + j;
                     const uint32_t acc = i & 1, aph = (i >> 1) & 1;
-                    umma::mbar_wait_hint(&full[s], ph, kWaitHintNs);
-                    const uint32_t a0 = umma::smem_u32(sA + s * tile_bytes), b0 = umma::smem_u32(sB);
-                    for (int h = 0; h < kQSplit; ++h) {
-                        umma::mbar_wait_hint(&tempty[acc][h], aph ^ 1, kWaitHintNs);
-                        umma::fence_after_sync();
-                        // part h's queries start (256 / kQSplit) / 8 eight-row groups in (K-major core layout)
-                        constexpr int kQP = kTcQueries / kQSplit;
-                        for (int k = 0; k < R / 32; ++k) {
-                            const uint64_t da = umma::smem_desc(a0 + 2 * k * kTcRows * 16, kTcRows * 16, 128);
-                            const uint64_t db = umma::smem_desc(b0 + 2 * k * kTcQueries * 16 + h * kQP * 16,
-                                                                kTcQueries * 16, 128);
-                            umma::mma_u8(tmem + acc * kTcQueries + h * kQP, da, db, idesc, k > 0 ? 1u : 0u);
+                    for (uint32_t c = 0; c < nkc; ++c, ++jc) {
+                        const uint32_t ii = ic + jc, s = ii % stages, ph = (ii / stages) & 1;
+                        const int ksteps = chunked ? static_cast<int>(min(16u, static_cast<uint32_t>(kch) - 16u * c)) / 2
+                                                   : R / 32;
+                        umma::mbar_wait_hint(&full[s], ph, kWaitHintNs);
+                        const uint32_t a0 = umma::smem_u32(sA + s * stage_bytes), b0 = umma::smem_u32(sB);
+                        for (int h = 0; h < kQSplit; ++h) {
+                            if (c == 0) umma::mbar_wait_hint(&tempty[acc][h], aph ^ 1, kWaitHintNs);
+                            umma::fence_after_sync();
+                            // part h's queries start (QT / kQSplit) / 8 eight-row groups in (K-major core layout)
+                            constexpr int kQP = kTcQueries / kQSplit;
+                            for (int k = 0; k < ksteps; ++k) {
+                                const int kg = static_cast<int>(8 * c) + k;  // K step within the whole row
+                                const uint64_t da = umma::smem_desc(a0 + 2 * k * kTcRows * 16, kTcRows * 16, 128);
+                                const uint64_t db = umma::smem_desc(b0 + 2 * kg * kTcQueries * 16 + h * kQP * 16,
+                                                                    kTcQueries * 16, 128);
+                                umma::mma_u8(tmem + acc * kTcQueries + h * kQP, da, db, idesc,
+                                             (c > 0 || k > 0) ? 1u : 0u);
+                            }
+                            if (c + 1 == nkc) umma::commit(&tfull[acc][h]);
                         }
-                        umma::commit(&tfull[acc][h]);
+                        umma::commit(&empty[s]);
                     }
-                    umma::commit(&empty[s]);
                 }
             }
         } else {
@@ -398,6 +423,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_score_kernel(TcScoreArgs a, 
             }
         }
         it += ntiles;
+        ic += ntiles * nkc;
         umma::fence_before_sync();
         __syncthreads();
         umma::fence_after_sync();
@@ -480,10 +506,15 @@ __global__ void __launch_bounds__(256) tc_finish_kernel(TcScoreArgs a, const uin
 }  // namespace
 
 size_t tc_score_smem(int R) {
-    const size_t need = static_cast<size_t>(kTcQueries + (R <= 128 ? 3 : 2) * kTcRows) * R + 2 * kTcQueries * 4 +
-                        kEpiWarps * 32 * kTcStash * 4 + 1024;
+    const bool chunked = R > 256;
+    const size_t qt = chunked ? 128 : kTcQueries, ew = chunked ? 8 : 16;
+    const size_t rows = chunked ? 2 * static_cast<size_t>(kTcChunkBytes)
+                                : static_cast<size_t>(tc_stages(R)) * kTcRows * R;
+    const size_t need = qt * R + rows + 2 * qt * 4 + ew * 32 * kTcStash * 4 + 1024;
     return std::max<size_t>(need, 120 * 1024);  // one CTA per SM: it owns all 512 TMEM columns
 }
+
+bool tc_score_fits(int R) { return R % 32 == 0 && tc_score_smem(R) <= 227 * 1024; }
 
 void launch_tc_pack_queries(const float* q, const uint32_t* order, uint64_t slot0, uint64_t m, int d,
                             int R, uint8_t* q8, int32_t* qn, cudaStream_t s) {
@@ -500,10 +531,13 @@ void launch_row_norms_u8(const uint8_t* rows, uint64_t n, int R, int32_t* xn, cu
 
 void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s) {
     const uint32_t n_rt = static_cast<uint32_t>((a.n + kTcRows - 1) / kTcRows);
-    const uint32_t n_qt = static_cast<uint32_t>((a.nq + kTcQueries - 1) / kTcQueries);
+    const bool chunked = a.R > 256;
+    const uint32_t qt = chunked ? 128u : static_cast<uint32_t>(kTcQueries);
+    const uint32_t n_qt = static_cast<uint32_t>((a.nq + qt - 1) / qt);
     const size_t smem = tc_score_smem(a.R);
-    DETLSH_CUDA(cudaFuncSetAttribute(tc_score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+    auto* const kern = chunked ? &tc_score_kernel<128, 8> : &tc_score_kernel<kTcQueries, 16>;
+    const int threads = chunked ? 32 * (8 + 2) : 32 * (16 + 2);
+    DETLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // persistent: one CTA per SM; work units = (query tile, row-tile range),
     // about 8 per CTA, handed out by an atomic counter
     const uint32_t sms = static_cast<uint32_t>(sm_count(device));
@@ -511,7 +545,7 @@ void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s) {
     const uint32_t grid = std::min<uint32_t>(sms, n_qt * G);
     {
         ProfScope ps("tc_score", s);
-        tc_score_kernel<<<grid, kTcThreads, smem, s>>>(a, n_rt, n_qt, G);
+        kern<<<grid, threads, smem, s>>>(a, n_rt, n_qt, G);
         DETLSH_LAUNCH_CHECK();
     }
     ProfScope ps("tc_collect", s);

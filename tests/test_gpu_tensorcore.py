@@ -34,7 +34,8 @@ def _sparse_u8(g, n, d):
 
 
 @pytest.mark.parametrize("d,k,nq,cap", [(128, 50, 5000, None), (100, 100, 600, None),
-                                        (256, 20, 1500, None), (64, 30, 800, 120)])
+                                        (256, 20, 1500, None), (64, 30, 800, 120),
+                                        (784, 50, 600, None), (300, 20, 700, None)])
 def test_tc_verification_equals_gather_path_and_oracle(gpu, port, monkeypatch, d, k, nq, cap):
     """Dataset-major tcgen05 verification (u8 rows, budget >= 8192) returns the
     same (position, distance) lists as the per-query gather path and as the
