@@ -473,6 +473,13 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             } else if (i == 0) {  // fp32 rows in leaf order: contiguous per-leaf candidate reads
                 Xp->data_leaf.alloc(n * static_cast<size_t>(Xp->d));
                 launch_pack_f32(Xp->data, Xp->trees[0]->perm.get(), n, Xp->d, Xp->data_leaf.get(), ts);
+                const int Rf = (6 * Xp->d + 31) / 32 * 32;  // [hi, lo, hi] bf16 along K
+                if (Rf > 256 && tc_score_fits(Rf)) {  // bf16x3 verification operand tiles
+                    Xp->row_f = Rf;
+                    Xp->data_tcf.alloc((n + 127) / 128 * 128 * static_cast<uint64_t>(Rf));
+                    Xp->xnf.alloc(n);
+                    launch_pack_tcf_tiles(Xp->data_leaf.get(), n, Xp->d, Rf, Xp->data_tcf.get(), Xp->xnf.get(), ts);
+                }
                 DETLSH_CUDA(cudaStreamSynchronize(ts));
             }
         });
@@ -775,6 +782,9 @@ void query_impl(GpuIndex& X, const float* queries, uint64_t nq, int k, uint32_t 
     P.xn_u8 = X.xn_u8.get();
     P.data_tc = X.data_tc.get();
     P.data_leaf = X.data_leaf.get();
+    P.data_tcf = X.data_tcf.get();
+    P.xnf = X.xnf.get();
+    P.row_f = X.row_f;
     P.trees_num_leaves0 = static_cast<uint32_t>(X.trees[0]->num_leaves);
     P.trees_leaf_begin0 = X.trees[0]->leaf_begin.get();
     P.trees_leaf_count0 = X.trees[0]->leaf_count.get();

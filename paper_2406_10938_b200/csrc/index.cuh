@@ -43,6 +43,9 @@ struct GpuIndex {
     DevBuf<int32_t> xn_u8;    // |x|^2 of those rows (tensor-core verification)
     DevBuf<uint8_t> data_tc;  // those rows as 128-row MMA operand tiles
     DevBuf<float> data_leaf;  // non-integral datasets: fp32 rows in tree-0 leaf order
+    DevBuf<uint8_t> data_tcf; // those rows as bf16-triple MMA tiles (bf16x3 verification)
+    DevBuf<float> xnf;        // (1 - kappa)|x|^2 of those rows, rounded down
+    int row_f = 0;            // bytes per bf16-triple row
     int row_u8 = 0, u8_lpr = 0;
     std::vector<std::unique_ptr<DevTree>> trees;
     // per tree: leaf indices in the reference's DFS order (range_query_exact), built on first use

@@ -932,6 +932,52 @@ __device__ int32_t kth_dist2(const QueryPlan& P, const FastSlot& F, const Smem& 
     return static_cast<int32_t>(prefix);
 }
 
+// Float data: the k-th smallest exact distance among the nt rows (fp64, the
+// reference's l2), each rounded UP to fp32 so the order statistic of the rounded
+// keys bounds the exact one from above; returns the float bits of tau^2, rounded up.
+__device__ int32_t kth_dist2_f32up(const QueryPlan& P, const FastSlot& F, const Smem& S, uint32_t nt, int k) {
+    if (nt < static_cast<uint32_t>(k)) return __float_as_int(3.0e38f);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(S.th);  // 4096 bins: top-k staging is idle here
+    int sh = 20;                                         // 12-bit digits of the 32-bit keys: 20, 8, 0
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (uint32_t c0 = 0; c0 < nt; c0 += kBatch) {
+        const uint32_t nb = min(static_cast<uint32_t>(kBatch), nt - c0);
+        score_batch(P, F, S, c0, nb, false);
+        __syncthreads();
+        for (uint32_t r = threadIdx.x; r < nb; r += blockDim.x) {
+            const double dist = __longlong_as_double(static_cast<long long>(S.bh[r]));
+            const uint32_t key = __float_as_uint(__double2float_ru(dist));  // positive: bits are monotone
+            F.cand[c0 + r] = key;
+            atomicAdd(&hist[key >> sh], 1u);
+        }
+        __syncthreads();
+    }
+    uint32_t cb, before;
+    select_count_bin(hist, 4096, static_cast<uint32_t>(k), S, cb, before);
+    uint32_t prefix = cb, need = static_cast<uint32_t>(k) - before;
+    while (sh > 0) {
+        const int nsh = sh > 12 ? sh - 12 : 0;
+        const int nb = 1 << (sh - nsh);
+        for (int i = threadIdx.x; i < 4096; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+            const uint32_t key = F.cand[i];
+            if ((key >> sh) == prefix) atomicAdd(&hist[(key >> nsh) & (nb - 1)], 1u);
+        }
+        __syncthreads();
+        uint32_t fb, before2;
+        select_count_bin(hist, nb >= static_cast<int>(blockDim.x) ? nb : static_cast<int>(blockDim.x), need, S, fb,
+                         before2);
+        prefix = (prefix << (sh - nsh)) | fb;
+        need -= before2;
+        sh = nsh;
+    }
+    const float tau = __uint_as_float(prefix);
+    return __float_as_int(__fmul_ru(tau, tau));
+}
+
+
 // MINB CTAs per SM: 5 for u8 rows (the plan / u8 scoring is load-latency bound
 // and gains from more CTAs), 3 for fp32 rows (the 32-float row chunks in
 // flight need the registers; at 48 registers they spill)
@@ -972,7 +1018,7 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
         const double r2_in = r2 * (1.0 - 1e-12), r2_out = r2 * (1.0 + 1e-12);
         bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30 && !P.force_exact;
         // tensor-core hand-off for this query (u8 rows, large budget)
-        const bool tc_eligible = P.tc_bm != nullptr && u8 && B32 >= kTcMinBudget;
+        const bool tc_eligible = P.tc_bm != nullptr && (u8 || P.tc_f32) && B32 >= kTcMinBudget;
         if (approx) build_pen_tables(P, S);
         else build_sq(P, 0, S);
         if (approx) build_half_tables(P, S);
@@ -1304,7 +1350,9 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             const uint32_t n_tau = S.u32s[12];
             __syncthreads();
             const uint32_t nt = min(emit_rows(F.tau, n_tau, T0, F.cand, B32, S), B32);
-            const int32_t tau2 = kth_dist2(P, F, S, nt, P.k);  // exact k-th smallest among those rows
+            // exact k-th smallest dist^2 among those rows (float data: an fp32
+            // upper bound of it, from the exact fp64 distances)
+            const int32_t tau2 = P.tc_f32 ? kth_dist2_f32up(P, F, S, nt, P.k) : kth_dist2(P, F, S, nt, P.k);
             phase(4);  // (profiling: tau rows + tau^2 apart from the bitmap)
             // candidate set: this query's row bitmap over tree-0 rows, written
             // here (zeroed, then each whole leaf's row range and the cut leaf's
@@ -1654,14 +1702,20 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // where the sample is a small part of the budget.
     const uint64_t tau_rows = std::max<uint64_t>(
         std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + kTcFinishCap - 1) / kTcFinishCap);
-    const bool tc_ok = P.tc_allowed && P.data_u8 && P.xn_u8 && P.data_tc && tc_score_fits(P.row_u8) && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
-                       2ULL * P.k <= kTcFinishCap && 8 * tau_rows <= P.budget && P.k <= kFastMaxK && !P.rc_mode;
+    const bool tc_any = P.tc_allowed && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
+                        2ULL * P.k <= kTcFinishCap && 8 * tau_rows <= P.budget && P.k <= kFastMaxK && !P.rc_mode;
+    // 8-bit rows: exact int8 scores; float rows: bf16x3 scores filtered with a
+    // rigorous slack, survivors rescored exactly in fp64 (tc_finish_f32)
+    const bool tc_u8 = tc_any && P.data_u8 && P.xn_u8 && P.data_tc && tc_score_fits(P.row_u8);
+    const bool tc_f32 = tc_any && !P.data_u8 && P.data_leaf && P.data_tcf && P.xnf && P.row_f > 256 &&
+                        tc_score_fits(P.row_f);
+    const bool tc_ok = tc_u8 || tc_f32;
     // plan-kernel occupancy: 5 CTAs/SM when it hands verification to the
     // tensor cores (load-latency bound plan), 3 when it verifies candidates
     // itself (the row chunks in flight need the registers); measured on C1-C4.
     // DETLSH_FAST_MINB=3|5 overrides (measurement hook).
     const char* minb_env = std::getenv("DETLSH_FAST_MINB");
-    const bool five = minb_env ? std::atoi(minb_env) == 5 : tc_ok;
+    const bool five = minb_env ? std::atoi(minb_env) == 5 : tc_u8;  // (float tau rows: fp64 chains, 3/SM)
     auto* const fast_kernel = five ? &query_fast_kernel<5> : &query_fast_kernel<3>;
     DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -1750,7 +1804,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         } else {
             // u8 rows with a large budget: the plan kernel hands each query's
             // candidate set to the tcgen05 dataset-major scorer (tc_score.cu)
-            const int R = P.row_u8;
+            const int R = tc_f32 ? P.row_f : P.row_u8;
+            Pp.tc_f32 = tc_f32 ? 1 : 0;
             const uint64_t W = ((P.n + 31) / 32 + 3) / 4 * 4;  // bitmap words per query, rows 16-B aligned
             // test hook: a smaller staging buffer forces the overflow re-run
             uint32_t tc_cap = kTcFinishCap;
@@ -1787,10 +1842,15 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 Pc.tc_W = W;
                 Pc.tc_tau2 = X.tc_tau2.get();
                 launch_fast(Pc);
-                launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, X.tc_q8.get(), X.tc_qn.get(), s);
+                if (tc_f32)
+                    launch_tc_pack_queries_f32(P.q, Pp.order, c0, m, P.d, R, X.tc_q8.get(),
+                                               reinterpret_cast<float*>(X.tc_qn.get()), s);
+                else
+                    launch_tc_pack_queries(P.q, Pp.order, c0, m, P.d, R, X.tc_q8.get(), X.tc_qn.get(), s);
                 TcScoreArgs a{};
-                a.rows = P.data_tc;
-                a.xn = P.xn_u8;
+                a.f32 = tc_f32 ? 1 : 0;
+                a.rows = tc_f32 ? P.data_tcf : P.data_tc;
+                a.xn = tc_f32 ? reinterpret_cast<const int32_t*>(P.xnf) : P.xn_u8;
                 a.q8 = X.tc_q8.get();
                 a.qn = X.tc_qn.get();
                 a.tau2 = X.tc_tau2.get();
@@ -1812,8 +1872,13 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 launch_tc_score(a, device, s);
                 // queries whose survivors overflowed (or whose chunk's pass
                 // records did) are listed for the gather path below
-                launch_tc_finish(a, P.perm0, P.k, P.r_min, P.budget, P.ids, P.dists, P.n_hits, P.radius,
-                                 P.cands, X.over_list.get(), X.counters.get() + kCntOver, s);
+                if (tc_f32)
+                    launch_tc_finish_f32(a, P.perm0, P.data_leaf, P.q, P.d, P.k, P.r_min, P.budget, P.ids, P.dists,
+                                         P.n_hits, P.radius, P.cands, X.over_list.get(), X.counters.get() + kCntOver,
+                                         s);
+                else
+                    launch_tc_finish(a, P.perm0, P.k, P.r_min, P.budget, P.ids, P.dists, P.n_hits, P.radius,
+                                     P.cands, X.over_list.get(), X.counters.get() + kCntOver, s);
             }
             // gather path for the listed queries: the count stays on the device
             QueryPlan Pc = Pp;

@@ -31,6 +31,10 @@ struct QueryPlan {
     const int32_t* xn_u8;    // |x|^2 of those rows
     const uint8_t* data_tc;  // the same rows in MMA tiles (launch_pack_tc_tiles)
     const float* data_leaf;  // fp32 rows in tree-0 leaf order (non-integral datasets), or null
+    const uint8_t* data_tcf; // those rows as bf16-triple MMA tiles (launch_pack_tcf_tiles), or null
+    const float* xnf;        // (1 - kTcF32Kappa)|x|^2 of those rows, rounded down
+    int row_f;               // bytes per bf16-triple row (round32(6 d))
+    int tc_f32;              // this batch hands float queries to the bf16x3 scorer
     int row_u8;              // bytes per u8 row (d rounded up to 16)
     int u8_lpr;              // lanes per u8 row (power of two <= 32)
     double eps, c, r_min;
@@ -130,11 +134,26 @@ struct TcScoreArgs {
     uint4* rec;            // threshold passes {row, slot, dist^2, 0}; row ~0u: padding
     unsigned long long* rec_cnt;  // reserved records (zeroed by the caller)
     uint64_t rec_cap;
+    // float datasets (f32 = 1): rows / queries are bf16 triples [hi, lo, hi] /
+    // [hi, hi, lo] of R bytes, xn / qn are the float bits of (1 - kTcF32Kappa)
+    // |x|^2 / |q|^2 rounded down, tau2 the float bits of an upper bound on the
+    // k-th smallest exact dist^2; survivors are rescored exactly in fp64
+    int f32;
 };
+constexpr float kTcF32Kappa = 1.0f / 4096.0f;  // relative slack of the bf16x3 dot product
 
 size_t tc_score_smem(int R);
 // rows of R bytes fit the scorer (R % 32 == 0; R > 256 takes the 128-query, K-chunked shape)
 bool tc_score_fits(int R);
+// float rows -> bf16-triple MMA tiles (R = round32(6 d) bytes) + (1 - kappa)|x|^2 (float, rounded down)
+void launch_pack_tcf_tiles(const float* rows_leaf, uint64_t n, int d, int R, uint8_t* tiles, float* xnf,
+                           cudaStream_t s);
+void launch_tc_pack_queries_f32(const float* q, const uint32_t* order, uint64_t slot0, uint64_t m, int d,
+                                int R, uint8_t* q16, float* qnf, cudaStream_t s);
+void launch_tc_finish_f32(const TcScoreArgs& a, const uint32_t* perm0, const float* rows_leaf, const float* q,
+                          int d, int k, double r_min, uint64_t budget, uint32_t* ids, double* dists,
+                          int32_t* n_hits, double* radius, uint64_t* cands, uint32_t* overflow_list,
+                          uint32_t* overflow_n, cudaStream_t s);
 void launch_tc_pack_queries(const float* q, const uint32_t* order, uint64_t slot0, uint64_t m, int d,
                             int R, uint8_t* q8, int32_t* qn, cudaStream_t s);
 void launch_row_norms_u8(const uint8_t* rows, uint64_t n, int R, int32_t* xn, cudaStream_t s);

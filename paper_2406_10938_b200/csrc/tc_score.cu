@@ -3,6 +3,8 @@
 // the descriptor / TMEM plumbing before it is used in the query path.
 #include <algorithm>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "query.cuh"
 #include "umma.cuh"
@@ -125,6 +127,162 @@ __global__ void row_norms_u8_kernel(const uint8_t* __restrict__ rows, uint64_t n
     }
 }
 
+// ---- float datasets: bf16-triple operands ------------------------------------
+// x = x_hi + x_lo + r with x_hi = bf16(x), x_lo = bf16(x - x_hi), |r| <= 2^-16 |x|.
+// Rows hold [x_hi, x_lo, x_hi] and queries [q_hi, q_hi, q_lo] along K, so one
+// kind::f16 accumulation gives q_hi.x_hi + q_hi.x_lo + q_lo.x_hi: within
+// ~2^-13.6 |q||x| of q.x (dropped lo.lo and residual terms, fp32 accumulation
+// of 3 d exact bf16 products), inside kTcF32Kappa = 2^-12.
+__device__ __forceinline__ uint16_t bf16_bits(float v) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+}
+__device__ __forceinline__ float bf16_hi(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+
+// element e of a float row in the triple layout (K-major, zero past 3 d)
+__device__ __forceinline__ uint16_t row_elem(const float* x, int d, int e) {
+    if (e < d) return bf16_bits(x[e]);
+    if (e < 2 * d) {
+        const float v = x[e - d];
+        return bf16_bits(__fsub_rn(v, bf16_hi(v)));  // exact: |v - hi| has fewer bits than v
+    }
+    if (e < 3 * d) return bf16_bits(x[e - 2 * d]);
+    return 0;
+}
+__device__ __forceinline__ uint16_t query_elem(const float* q, int d, int e) {
+    if (e < 2 * d) return bf16_bits(q[e < d ? e : e - d]);
+    if (e < 3 * d) {
+        const float v = q[e - 2 * d];
+        return bf16_bits(__fsub_rn(v, bf16_hi(v)));
+    }
+    return 0;
+}
+
+// rows (tree-0 leaf order) -> 128-row tiles, chunk kc (8 elements) of row r at
+// tile + kc * 2048 + r * 16; xnf[r] = (1 - kappa) |x_r|^2 rounded down
+__global__ void pack_tcf_tiles_kernel(const float* __restrict__ rows, uint64_t n, int d, int R,
+                                      uint8_t* __restrict__ tiles, float* __restrict__ xnf) {
+    const int kch = R / 16;
+    const uint64_t total = (n + kTcRows - 1) / kTcRows * kTcRows * kch;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t t = i / (static_cast<uint64_t>(kch) * kTcRows);
+        const uint32_t rem = static_cast<uint32_t>(i % (static_cast<uint64_t>(kch) * kTcRows));
+        const uint32_t kc = rem / kTcRows, r = rem % kTcRows;
+        const uint64_t row = t * kTcRows + r;
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (row < n) {
+            const float* x = rows + row * d;
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+                w[h] = row_elem(x, d, 8 * kc + 2 * h) | static_cast<uint32_t>(row_elem(x, d, 8 * kc + 2 * h + 1)) << 16;
+        }
+        reinterpret_cast<uint4*>(tiles)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    for (uint64_t row = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; row < n;
+         row += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const float* x = rows + row * d;
+        double s2 = 0.0;
+        for (int t = 0; t < d; ++t) s2 = __fma_rn(static_cast<double>(x[t]), static_cast<double>(x[t]), s2);
+        xnf[row] = __double2float_rd(s2 * (1.0 - static_cast<double>(kTcF32Kappa)) * (1.0 - 0x1p-40));
+    }
+}
+
+// Slot s <- query order[slot0 + s]: [q_hi, q_hi, q_lo] bf16 (R bytes) and
+// (1 - kappa)|q|^2 rounded down.
+__global__ void tc_pack_queries_f32_kernel(const float* __restrict__ q, const uint32_t* __restrict__ order,
+                                           uint64_t slot0, uint64_t m, int d, int R, uint8_t* __restrict__ q16,
+                                           float* __restrict__ qnf) {
+    const int lane = threadIdx.x & 31;  // one warp per slot
+    for (uint64_t i = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; i < m;
+         i += (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t qi = order ? order[slot0 + i] : slot0 + i;
+        const float* qv = q + qi * d;
+        uint16_t* out = reinterpret_cast<uint16_t*>(q16 + i * R);
+        for (int e = lane; e < R / 2; e += 32) out[e] = query_elem(qv, d, e);
+        if (lane == 0) {
+            double s2 = 0.0;
+            for (int t = 0; t < d; ++t) s2 = __fma_rn(static_cast<double>(qv[t]), static_cast<double>(qv[t]), s2);
+            qnf[i] = __double2float_rd(s2 * (1.0 - static_cast<double>(kTcF32Kappa)) * (1.0 - 0x1p-40));
+        }
+    }
+}
+
+// Exact top-k of each float query's survivors: the reference's fp64 distance
+// (dataset.hpp:23-34: sequential (q - x)^2 sums, sqrt) per survivor row, then a
+// bitonic sort by (distance, dataset position).
+__global__ void __launch_bounds__(256) tc_finish_f32_kernel(TcScoreArgs a, const uint32_t* __restrict__ perm0,
+                                                            const float* __restrict__ rows, const float* __restrict__ qs,
+                                                            int d, int k, double r_min, uint64_t budget,
+                                                            uint32_t* ids, double* dists, int32_t* n_hits,
+                                                            double* radius, uint64_t* cands, uint32_t* overflow_list,
+                                                            uint32_t* overflow_n) {
+    extern __shared__ uint64_t fkey[];  // [cap2] distance bits, then [cap2] u32 positions
+    uint32_t cap2 = 64;                 // the widest sort: a power of two >= cap
+    while (cap2 < a.cap) cap2 <<= 1;
+    uint32_t* fpos = reinterpret_cast<uint32_t*>(fkey + cap2);
+    const bool rec_over = *a.rec_cnt > a.rec_cap;
+    for (uint64_t slot = blockIdx.x; slot < a.nq; slot += gridDim.x) {
+        if (a.tau2[slot] < 0) continue;
+        const uint64_t q = a.order ? a.order[a.slot0 + slot] : a.slot0 + slot;
+        const uint32_t cnt = a.surv_cnt[slot];
+        if (rec_over || cnt > a.cap) {
+            if (threadIdx.x == 0) overflow_list[atomicAdd(overflow_n, 1u)] = static_cast<uint32_t>(q);
+            continue;
+        }
+        uint32_t n2 = 64;
+        while (n2 < cnt) n2 <<= 1;
+        const float* qv = qs + q * d;
+        for (uint32_t i = threadIdx.x; i < n2; i += blockDim.x) {
+            uint64_t kd = ~0ULL;
+            uint32_t kp = 0xffffffffu;
+            if (i < cnt) {
+                const uint32_t row = static_cast<uint32_t>(a.surv[slot * a.cap + i]);
+                const float* x = rows + static_cast<uint64_t>(row) * d;
+                double acc = 0.0;
+                for (int t = 0; t < d; ++t) {
+                    const double df = __dsub_rn(static_cast<double>(__ldg(qv + t)), static_cast<double>(__ldg(x + t)));
+                    acc = __dadd_rn(acc, __dmul_rn(df, df));
+                }
+                kd = static_cast<uint64_t>(__double_as_longlong(__dsqrt_rn(acc)));
+                kp = __ldg(perm0 + row);
+            }
+            fkey[i] = kd;
+            fpos[i] = kp;
+        }
+        __syncthreads();
+        for (uint32_t size = 2; size <= n2; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = threadIdx.x; i < n2 / 2; i += blockDim.x) {
+                    const int lo = 2 * i - (i & (stride - 1));
+                    const int hi = lo + stride;
+                    const bool asc = (lo & size) == 0;
+                    const uint64_t x = fkey[lo], y = fkey[hi];
+                    const uint32_t px = fpos[lo], py = fpos[hi];
+                    const bool y_less = y < x || (y == x && py < px);
+                    if (y_less == asc) {
+                        fkey[lo] = y;
+                        fkey[hi] = x;
+                        fpos[lo] = py;
+                        fpos[hi] = px;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        const uint32_t nh = min(cnt, static_cast<uint32_t>(k));
+        for (uint32_t t = threadIdx.x; t < nh; t += blockDim.x) {
+            if (ids) ids[q * k + t] = fpos[t];
+            if (dists) dists[q * k + t] = __longlong_as_double(static_cast<long long>(fkey[t]));
+        }
+        if (threadIdx.x == 0) {
+            if (n_hits) n_hits[q] = static_cast<int32_t>(nh);
+            if (radius) radius[q] = r_min;
+            if (cands) cands[q] = budget;
+        }
+        __syncthreads();
+    }
+}
+
 // Rows -> HBM tiles of 128 rows in the canonical no-swizzle K-major layout
 // (chunk kc of row r at kc * 2048 + r * 16), zero rows past n: one tile is one
 // contiguous 128 * R byte block, moved by a single bulk copy.
@@ -182,7 +340,7 @@ __device__ __noinline__ void tc_reserve(uint4* rec, unsigned long long* rec_cnt,
     end = base + kTcRecChunk;
 }
 
-template <int QT, int EW>
+template <int QT, int EW, bool F32>
 __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs a, uint32_t n_rt, uint32_t n_qt,
                                                                    uint32_t G) {
     constexpr int kTcQueries = QT, kEpiWarps = EW;
@@ -225,7 +383,8 @@ __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs 
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tmem = tslot;
-    const uint32_t idesc = umma::idesc_u8_s32(kTcRows, kTcQueries / kQSplit);  // one query part per MMA
+    const uint32_t idesc = F32 ? umma::idesc_bf16_f32(kTcRows, kTcQueries / kQSplit)  // one query part per MMA
+                               : umma::idesc_u8_s32(kTcRows, kTcQueries / kQSplit);
     const uint32_t units = n_qt * G;
     uint32_t it = 0;  // tiles processed by this CTA so far (accumulator phases)
     uint32_t ic = 0;  // row-tile K chunks loaded so far (stage phases; == it unless chunked)
@@ -260,7 +419,10 @@ __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs 
                 const int32_t t = qq < a.nq ? a.tau2[qq] : -1;
                 const int32_t qn = qq < a.nq ? a.qn[qq] : 0;
                 sqn[r] = qn;
-                snh[r] = t < 0 ? -0x20000000 : t - qn;  // -2^29: no row can pass
+                if (F32)  // tau^2 - (1 - kappa)|q|^2, rounded up (the filter only ever widens)
+                    snh[r] = __float_as_int(t < 0 ? -3.0e38f : __fsub_ru(__int_as_float(t), __int_as_float(qn)));
+                else
+                    snh[r] = t < 0 ? -0x20000000 : t - qn;  // -2^29: no row can pass
             }
             umma::fence_async_smem();
             umma::fence_before_sync();
@@ -305,8 +467,12 @@ __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs 
                                 const uint64_t da = umma::smem_desc(a0 + 2 * k * kTcRows * 16, kTcRows * 16, 128);
                                 const uint64_t db = umma::smem_desc(b0 + 2 * kg * kTcQueries * 16 + h * kQP * 16,
                                                                     kTcQueries * 16, 128);
-                                umma::mma_u8(tmem + acc * kTcQueries + h * kQP, da, db, idesc,
-                                             (c > 0 || k > 0) ? 1u : 0u);
+                                if (F32)
+                                    umma::mma_f16(tmem + acc * kTcQueries + h * kQP, da, db, idesc,
+                                                  (c > 0 || k > 0) ? 1u : 0u);
+                                else
+                                    umma::mma_u8(tmem + acc * kTcQueries + h * kQP, da, db, idesc,
+                                                 (c > 0 || k > 0) ? 1u : 0u);
                             }
                             if (c + 1 == nkc) umma::commit(&tfull[acc][h]);
                         }
@@ -344,8 +510,9 @@ __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs 
             for (uint32_t t = rt0, j = 0; t < rt1; ++t, ++j) {
                 const uint32_t i = it + j, acc = i & 1, aph = (i >> 1) & 1;
                 const uint64_t r = static_cast<uint64_t>(t) * kTcRows + row;
-                const int32_t xn = r < a.n ? __ldg(a.xn + r) : 0x40000000;  // padded rows never pass
-                const int32_t nxn = -xn;
+                // padded rows never pass (integers: 2^30; floats: +3e38)
+                const int32_t xn = r < a.n ? __ldg(a.xn + r) : (F32 ? __float_as_int(3.0e38f) : 0x40000000);
+                const int32_t nxn = F32 ? (xn ^ static_cast<int32_t>(0x80000000u)) : -xn;  // float: flip the sign
                 const uint32_t tn = t + 1;
                 if (tn < rt1) load_words(tn, nw);  // next tile's words, in flight during this one
                 umma::mbar_wait_hint(&tfull[acc][half], aph, kWaitHintNs);
@@ -371,8 +538,14 @@ __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs 
                     uint32_t fail[4] = {0, 0, 0, 0};
                     const int4* nh4 = reinterpret_cast<const int4*>(snh + c0);
                     auto step = [&](uint32_t& f, uint32_t vv, int32_t h) {
-                        const int32_t t = static_cast<int32_t>(vv) * two + h;
-                        f = __funnelshift_l(static_cast<uint32_t>(t * one + nxn), f, 1);
+                        if (F32) {  // 2 acc + h - (1 - kappa)|x|^2 < 0: sign bit
+                            const float t = __fadd_rn(__fmaf_rn(__uint_as_float(vv), 2.0f, __int_as_float(h)),
+                                                      __int_as_float(nxn));
+                            f = __funnelshift_l(__float_as_uint(t), f, 1);
+                        } else {
+                            const int32_t t = static_cast<int32_t>(vv) * two + h;
+                            f = __funnelshift_l(static_cast<uint32_t>(t * one + nxn), f, 1);
+                        }
                     };
 #pragma unroll
                     for (int e4 = 1; e4 >= 0; --e4) {
@@ -412,7 +585,8 @@ __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs 
                             if (((b >> lane) & 1u) && slot < a.rec_cap) {
                                 const int c = c0 + e;
                                 a.rec[slot] = make_uint4(static_cast<uint32_t>(r), static_cast<uint32_t>(q0 + c),
-                                                         static_cast<uint32_t>(sqn[c] + xn - 2 * static_cast<int32_t>(sv[e])), 0);
+                                                         F32 ? 0u : static_cast<uint32_t>(sqn[c] + xn - 2 * static_cast<int32_t>(sv[e])),
+                                                         0);
                             }
                         }
                         __syncwarp();
@@ -535,7 +709,9 @@ void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s) {
     const uint32_t qt = chunked ? 128u : static_cast<uint32_t>(kTcQueries);
     const uint32_t n_qt = static_cast<uint32_t>((a.nq + qt - 1) / qt);
     const size_t smem = tc_score_smem(a.R);
-    auto* const kern = chunked ? &tc_score_kernel<128, 8> : &tc_score_kernel<kTcQueries, 16>;
+    auto* const kern = a.f32 ? &tc_score_kernel<128, 8, true>
+                             : chunked ? &tc_score_kernel<128, 8, false> : &tc_score_kernel<kTcQueries, 16, false>;
+    if (a.f32 && !chunked) throw InvalidArgument("tc_score: float rows are bf16 triples of more than 256 bytes");
     const int threads = chunked ? 32 * (8 + 2) : 32 * (16 + 2);
     DETLSH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // persistent: one CTA per SM; work units = (query tile, row-tile range),
@@ -550,6 +726,41 @@ void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s) {
     }
     ProfScope ps("tc_collect", s);
     tc_collect_kernel<<<sms * 8, 256, 0, s>>>(a);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_pack_tcf_tiles(const float* rows_leaf, uint64_t n, int d, int R, uint8_t* tiles, float* xnf,
+                           cudaStream_t s) {
+    const uint64_t chunks = (n + kTcRows - 1) / kTcRows * kTcRows * (R / 16);
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((chunks + 255) / 256, 16384)));
+    pack_tcf_tiles_kernel<<<grid, 256, 0, s>>>(rows_leaf, n, d, R, tiles, xnf);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_tc_pack_queries_f32(const float* q, const uint32_t* order, uint64_t slot0, uint64_t m, int d, int R,
+                                uint8_t* q16, float* qnf, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((m * 32 + 255) / 256, 8192)));
+    tc_pack_queries_f32_kernel<<<grid, 256, 0, s>>>(q, order, slot0, m, d, R, q16, qnf);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_tc_finish_f32(const TcScoreArgs& a, const uint32_t* perm0, const float* rows_leaf, const float* q,
+                          int d, int k, double r_min, uint64_t budget, uint32_t* ids, double* dists,
+                          int32_t* n_hits, double* radius, uint64_t* cands, uint32_t* overflow_list,
+                          uint32_t* overflow_n, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(a.nq, 4096)));
+    uint32_t cap2 = 64;
+    while (cap2 < a.cap) cap2 <<= 1;
+    const size_t smem = static_cast<size_t>(cap2) * 12;
+    static bool attr = false;
+    if (!attr) {
+        DETLSH_CUDA(cudaFuncSetAttribute(tc_finish_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kTcFinishCap * 12)));
+        attr = true;
+    }
+    ProfScope ps("tc_finish", s);
+    tc_finish_f32_kernel<<<grid, 256, smem, s>>>(a, perm0, rows_leaf, q, d, k, r_min, budget, ids, dists, n_hits,
+                                                 radius, cands, overflow_list, overflow_n);
     DETLSH_LAUNCH_CHECK();
 }
 

@@ -34,6 +34,25 @@ __host__ __device__ constexpr uint32_t idesc_u8_s32(int M, int N) {
            | (static_cast<uint32_t>(M >> 4) << 24);   // m_dim
 }
 
+// Instruction descriptor: kind::f16, A/B bf16, K-major, D = f32.
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
+    return (1u << 4)                                  // c_format = F32
+           | (1u << 7) | (1u << 10)                   // a/b format = BF16
+           | (static_cast<uint32_t>(N >> 3) << 17)    // n_dim
+           | (static_cast<uint32_t>(M >> 4) << 24);   // m_dim
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+}
+
 __device__ __forceinline__ void mma_u8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
                                        uint32_t accumulate) {
     asm volatile(

@@ -96,3 +96,51 @@ def test_host_buffers_pinned_and_pageable_agree(gpu):
     assert np.array_equal(outs[2].numpy(), ref.n_hits)
     assert np.array_equal(outs[3].numpy().view(np.uint64), ref.radius_used.view(np.uint64))
     assert np.array_equal(outs[4].numpy().view(np.uint64), ref.candidates_seen.view(np.uint64))
+
+
+def _unit_gaussian(g, n, d):
+    x = g.normal(0, 1, (n, d))
+    return (x / np.linalg.norm(x, axis=1, keepdims=True)).astype(np.float32)
+
+
+@pytest.mark.parametrize("kind,d,k,nq,cap", [("unit", 96, 50, 1500, None), ("mixture", 128, 50, 600, None),
+                                             ("unit", 96, 20, 400, 100)])
+def test_bf16x3_verification_equals_gather_path_and_oracle(gpu, port, monkeypatch, kind, d, k, nq, cap):
+    """Float datasets: bf16-triple tcgen05 scores with a rigorous slack filter,
+    survivors rescored in fp64 — the same (position, distance) lists as the
+    fp64 gather path and the oracle (C4-like unit vectors; C1-like mixture
+    with large norms; a tiny survivor cap forcing the gather re-run)."""
+    from paper_2406_10938_b200 import LshParams
+    if cap is not None:
+        monkeypatch.setenv("DETLSH_TEST_TC_CAP", str(cap))
+    g = np.random.Generator(np.random.PCG64(d * 13 + k))
+    n = 120000
+    if kind == "unit":
+        data = _unit_gaussian(g, n + nq, d)
+    else:
+        centres = g.uniform(0, 100, (100, d))
+        data = (centres[g.integers(0, 100, n + nq)] + g.normal(0, 5, (n + nq, d))).astype(np.float32)
+    data, Q = np.ascontiguousarray(data[:n]), np.ascontiguousarray(data[n:])
+    data[n // 2: n // 2 + 300] = data[:300]  # exact duplicates -> distance ties
+    Q[:20] = data[g.integers(0, n, 20)]       # queries on data points (distance 0)
+    c = dict(K=16, L=4, n_regions=256, leaf_capacity=128, sample_fraction=0.1, beta=0.1, k=k)
+    idx = gpu.build_index(data, LshParams(**c), seed=5)
+    assert idx.row_u8() == 0
+    lib = gpu.load()
+    lib.detlsh_profile_enable(1)
+    ra = gpu.ck_ann_batch(idx, Q, k)
+    lib.detlsh_profile_enable(0)
+    assert "tc_score" in _scopes(lib), "bf16x3 tensor-core path not taken"
+    rb = gpu.ck_ann_batch(idx, Q, k, tensor_cores=False)
+    assert np.array_equal(ra.n_hits, rb.n_hits)
+    assert np.array_equal(ra.ids, rb.ids)
+    assert np.array_equal(ra.dists.view(np.uint64), rb.dists.view(np.uint64))
+    assert np.array_equal(ra.candidates_seen, rb.candidates_seen)
+    assert np.array_equal(ra.radius_used, rb.radius_used)
+    from oracle.bindings import make_params
+    oi = port.build_index(data, make_params(**c), 5)
+    for qi in list(range(0, nq, max(1, nq // 10))) + [3, nq - 1]:
+        ids, ds, rad, cs = oi.ck_ann(Q[qi], k)
+        assert np.array_equal(ra.ids[qi], ids), f"query {qi}"
+        assert np.array_equal(ra.dists[qi].view(np.uint64), np.asarray(ds).view(np.uint64)), f"query {qi}"
+        assert ra.radius_used[qi] == rad and int(ra.candidates_seen[qi]) == cs
