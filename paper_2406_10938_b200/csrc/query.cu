@@ -981,7 +981,9 @@ __device__ int32_t kth_dist2_f32up(const QueryPlan& P, const FastSlot& F, const 
 // MINB CTAs per SM: 5 for u8 rows (the plan / u8 scoring is load-latency bound
 // and gains from more CTAs), 3 for fp32 rows (the 32-float row chunks in
 // flight need the registers; at 48 registers they spill)
-template <int MINB>
+// F32TC: the float bf16x3 hand-off is compiled only into its own instance, so
+// the u8 instance keeps its register budget
+template <int MINB, bool F32TC>
 __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1018,7 +1020,7 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
         const double r2_in = r2 * (1.0 - 1e-12), r2_out = r2 * (1.0 + 1e-12);
         bool approx = P.K <= 16 && r2 > 1e-30 && r2 < 1e30 && !P.force_exact;
         // tensor-core hand-off for this query (u8 rows, large budget)
-        const bool tc_eligible = P.tc_bm != nullptr && (u8 || P.tc_f32) && B32 >= kTcMinBudget;
+        const bool tc_eligible = P.tc_bm != nullptr && (F32TC || u8) && B32 >= kTcMinBudget;
         if (approx) build_pen_tables(P, S);
         else build_sq(P, 0, S);
         if (approx) build_half_tables(P, S);
@@ -1352,7 +1354,9 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             const uint32_t nt = min(emit_rows(F.tau, n_tau, T0, F.cand, B32, S), B32);
             // exact k-th smallest dist^2 among those rows (float data: an fp32
             // upper bound of it, from the exact fp64 distances)
-            const int32_t tau2 = P.tc_f32 ? kth_dist2_f32up(P, F, S, nt, P.k) : kth_dist2(P, F, S, nt, P.k);
+            int32_t tau2;
+            if constexpr (F32TC) tau2 = kth_dist2_f32up(P, F, S, nt, P.k);
+            else tau2 = kth_dist2(P, F, S, nt, P.k);
             phase(4);  // (profiling: tau rows + tau^2 apart from the bitmap)
             // candidate set: this query's row bitmap over tree-0 rows, written
             // here (zeroed, then each whole leaf's row range and the cut leaf's
@@ -1700,15 +1704,18 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // do better than uniform; measured on C2, 2x this sample trades 1 ms
     // of plan for 2.5 ms of scoring), and keep the tensor-core path only
     // where the sample is a small part of the budget.
-    const uint64_t tau_rows = std::max<uint64_t>(
-        std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + kTcFinishCap - 1) / kTcFinishCap);
-    const bool tc_any = P.tc_allowed && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
-                        2ULL * P.k <= kTcFinishCap && 8 * tau_rows <= P.budget && P.k <= kFastMaxK && !P.rc_mode;
     // 8-bit rows: exact int8 scores; float rows: bf16x3 scores filtered with a
-    // rigorous slack, survivors rescored exactly in fp64 (tc_finish_f32)
+    // rigorous slack, survivors rescored exactly in fp64 (tc_finish_f32).  The
+    // float path stages 4x more survivors per query (kTcFinishCapF32): its tau
+    // rows are fp64 chains, so 4x fewer of them is the better trade.
+    const bool f32_rows = !P.data_u8 && P.data_leaf && P.data_tcf && P.xnf && P.row_f > 256 && tc_score_fits(P.row_f);
+    const uint32_t fin_cap = f32_rows ? kTcFinishCapF32 : kTcFinishCap;
+    const uint64_t tau_rows = std::max<uint64_t>(
+        std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + fin_cap - 1) / fin_cap);
+    const bool tc_any = P.tc_allowed && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
+                        2ULL * P.k <= fin_cap && 8 * tau_rows <= P.budget && P.k <= kFastMaxK && !P.rc_mode;
     const bool tc_u8 = tc_any && P.data_u8 && P.xn_u8 && P.data_tc && tc_score_fits(P.row_u8);
-    const bool tc_f32 = tc_any && !P.data_u8 && P.data_leaf && P.data_tcf && P.xnf && P.row_f > 256 &&
-                        tc_score_fits(P.row_f);
+    const bool tc_f32 = tc_any && f32_rows;
     const bool tc_ok = tc_u8 || tc_f32;
     // plan-kernel occupancy: 5 CTAs/SM when it hands verification to the
     // tensor cores (load-latency bound plan), 3 when it verifies candidates
@@ -1716,7 +1723,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // DETLSH_FAST_MINB=3|5 overrides (measurement hook).
     const char* minb_env = std::getenv("DETLSH_FAST_MINB");
     const bool five = minb_env ? std::atoi(minb_env) == 5 : tc_u8;  // (float tau rows: fp64 chains, 3/SM)
-    auto* const fast_kernel = five ? &query_fast_kernel<5> : &query_fast_kernel<3>;
+    auto* const fast_kernel = tc_f32 ? &query_fast_kernel<3, true>
+                              : five ? &query_fast_kernel<5, false> : &query_fast_kernel<3, false>;
     DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // Persistent scratch lives on the index's own stream (it outlives any
@@ -1808,17 +1816,17 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             Pp.tc_f32 = tc_f32 ? 1 : 0;
             const uint64_t W = ((P.n + 31) / 32 + 3) / 4 * 4;  // bitmap words per query, rows 16-B aligned
             // test hook: a smaller staging buffer forces the overflow re-run
-            uint32_t tc_cap = kTcFinishCap;
+            uint32_t tc_cap = fin_cap;
             if (const char* e = std::getenv("DETLSH_TEST_TC_CAP"))
-                tc_cap = static_cast<uint32_t>(std::max(1L, std::min<long>(std::atol(e), kTcFinishCap)));
-            // per processing slot: row bitmap (n/8 bytes), survivors (32 KB),
+                tc_cap = static_cast<uint32_t>(std::max(1L, std::min<long>(std::atol(e), fin_cap)));
+            // per processing slot: row bitmap (n/8 bytes), survivors (8 B each),
             // pass records (128 KB); a chunk stays under ~3 GB
-            uint64_t chunk = (3ULL << 30) / (W * 4 + 160 * 1024);
+            uint64_t chunk = (3ULL << 30) / (W * 4 + 8ULL * fin_cap + 128 * 1024);
             chunk = std::max<uint64_t>(256, chunk / 256 * 256);
             chunk = std::min<uint64_t>(chunk, (P.nq + 255) / 256 * 256);
             // pass records staged per chunk: ~8192 per query, plus the runs of
             // kTcRecChunk slots the scorer's warps reserve ahead of use
-            uint64_t rec_cap = chunk * 8192 + static_cast<uint64_t>(sms) * kTcRecReserve;
+            uint64_t rec_cap = chunk * 2ULL * fin_cap + static_cast<uint64_t>(sms) * kTcRecReserve;
             if (const char* e = std::getenv("DETLSH_TEST_REC_CAP"))  // test hook: force the overflow path
                 rec_cap = std::max<uint64_t>(1, std::min<uint64_t>(std::strtoull(e, nullptr, 10), rec_cap));
             grow_scratch(X.tc_bm, chunk * W);
@@ -1826,7 +1834,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             grow_scratch(X.tc_qn, chunk);
             grow_scratch(X.tc_surv_cnt, chunk);
             grow_scratch(X.tc_q8, chunk * R);
-            grow_scratch(X.tc_surv, chunk * kTcFinishCap);
+            grow_scratch(X.tc_surv, chunk * fin_cap);
             grow_scratch(X.tc_rec, rec_cap);
             grow_scratch(X.tc_rec_cnt, 1);
             grow_scratch(X.over_list, P.nq);

@@ -110,6 +110,7 @@ struct QueryScratch {
 
 // ---- tensor-core exact verification (tc_score.cu) ----
 constexpr uint32_t kTcFinishCap = 4096;  // survivors staged per query
+constexpr uint32_t kTcFinishCapF32 = 16384;  // the same for float rows (tc_finish_f32 sorts in dynamic smem)
 // pass-record slots one tc_score CTA may hold reserved ahead of use
 // (epilogue warps x the run each reserves; checked in tc_score.cu)
 constexpr uint64_t kTcRecReserve = 16 * 1024;

@@ -324,9 +324,19 @@ static_assert(kTcRecReserve >= static_cast<uint64_t>(kEpiWarps) * kTcRecChunk, "
 constexpr uint32_t kTcChunkBytes = kTcRows * 256;  // one 256-byte K chunk of a 128-row tile
 constexpr int kTcStash = 36;             // words per lane of the rare-path stash (bank spread)
 constexpr uint32_t kWaitHintNs = 20000;  // mbarrier try_wait suspend hint (woken on completion)
-constexpr int kQSplit = 2;               // MMAs (and accumulator barriers) per tile, one per query part (4: slower)
+#ifndef DETLSH_TC_QSPLIT
+#define DETLSH_TC_QSPLIT 2
+#endif
+constexpr int kQSplitMax = 2;            // MMAs (and accumulator barriers) per tile, one per query part (4: slower)
 
 __host__ __device__ __forceinline__ uint32_t tc_stages(int R) { return R <= 128 ? 3u : 2u; }
+// the K-chunked shape (R > 256, 128-query tiles, 8 epilogue warps): three
+// 32 KB row-chunk stages when they fit beside the query tile, else two
+__host__ __device__ __forceinline__ uint32_t tc_chunk_stages(int R) {
+    const uint32_t fixed = 128u * static_cast<uint32_t>(R) + 2u * 128u * 4u + 8u * 32u * static_cast<uint32_t>(kTcStash) * 4u +
+                           1024u + 2048u;  // (+ static smem, alignment)
+    return fixed + 3u * kTcChunkBytes <= 227u * 1024u ? 3u : 2u;
+}
 
 // A warp's next run of kTcRecChunk record slots; the unused tail of the old
 // run becomes padding.  (Called warp-uniformly.)
@@ -344,6 +354,10 @@ template <int QT, int EW, bool F32>
 __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs a, uint32_t n_rt, uint32_t n_qt,
                                                                    uint32_t G) {
     constexpr int kTcQueries = QT, kEpiWarps = EW;
+    // one MMA per query part: two 128-query parts for 256-query tiles (each
+    // part's epilogue warps wait only for their own MMA); one 128-wide MMA for
+    // 128-query tiles (N = 64 halves measured ~2x slower on the bf16 path)
+    constexpr int kQSplit = QT >= 256 ? DETLSH_TC_QSPLIT : 1;
     constexpr int kEpiCols = kTcQueries / (kEpiWarps / 4);  // query columns per epilogue warp
     constexpr int kEpiWords = kEpiCols / 32;                // candidate words per lane (columns per lane)
     constexpr int kProducerWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
@@ -351,11 +365,11 @@ __global__ void __launch_bounds__(32 * (EW + 2), 1) tc_score_kernel(TcScoreArgs 
     // tfull/tempty per (accumulator, query part): the kQSplit query parts of a
     // tile are separate MMAs, so the epilogue warps of one part never wait for
     // another part's stragglers
-    __shared__ __align__(8) uint64_t full[6], empty[6], tfull[2][kQSplit], tempty[2][kQSplit];
+    __shared__ __align__(8) uint64_t full[6], empty[6], tfull[2][kQSplitMax], tempty[2][kQSplitMax];
     __shared__ uint32_t tslot, unit_s;
     const int R = a.R, kch = R / 16;
     const bool chunked = R > 256;  // rows streamed in 256-byte K chunks
-    const uint32_t stages = chunked ? 2u : tc_stages(R);
+    const uint32_t stages = chunked ? tc_chunk_stages(R) : tc_stages(R);
     const uint32_t tile_bytes = static_cast<uint32_t>(kTcRows * R);
     const uint32_t nkc = chunked ? static_cast<uint32_t>((kch + 15) / 16) : 1u;  // K chunks per row tile
     const uint32_t stage_bytes = chunked ? kTcChunkBytes : tile_bytes;
@@ -682,7 +696,7 @@ __global__ void __launch_bounds__(256) tc_finish_kernel(TcScoreArgs a, const uin
 size_t tc_score_smem(int R) {
     const bool chunked = R > 256;
     const size_t qt = chunked ? 128 : kTcQueries, ew = chunked ? 8 : 16;
-    const size_t rows = chunked ? 2 * static_cast<size_t>(kTcChunkBytes)
+    const size_t rows = chunked ? static_cast<size_t>(tc_chunk_stages(R)) * kTcChunkBytes
                                 : static_cast<size_t>(tc_stages(R)) * kTcRows * R;
     const size_t need = qt * R + rows + 2 * qt * 4 + ew * 32 * kTcStash * 4 + 1024;
     return std::max<size_t>(need, 120 * 1024);  // one CTA per SM: it owns all 512 TMEM columns
@@ -717,7 +731,13 @@ void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s) {
     // persistent: one CTA per SM; work units = (query tile, row-tile range),
     // about 8 per CTA, handed out by an atomic counter
     const uint32_t sms = static_cast<uint32_t>(sm_count(device));
-    const uint32_t G = std::max<uint32_t>(1, std::min<uint32_t>((n_rt + 7) / 8, (8 * sms + n_qt - 1) / n_qt));
+    // row ranges of at most ~8 MB: the CTAs working on one range at the same
+    // time (one per query tile) then read it from L2, not each from HBM
+    // (C4's 5.8 GB of bf16 rows; C2's 128 MB of u8 rows fit L2 whole)
+    const uint64_t row_bytes_all = static_cast<uint64_t>(n_rt) * kTcRows * a.R;
+    const uint32_t g_l2 = static_cast<uint32_t>(std::min<uint64_t>(n_rt, (row_bytes_all + (8u << 20) - 1) >> 23));
+    const uint32_t G = std::max<uint32_t>(
+        std::max<uint32_t>(1, std::min<uint32_t>((n_rt + 7) / 8, (8 * sms + n_qt - 1) / n_qt)), g_l2);
     const uint32_t grid = std::min<uint32_t>(sms, n_qt * G);
     {
         ProfScope ps("tc_score", s);
@@ -755,7 +775,7 @@ void launch_tc_finish_f32(const TcScoreArgs& a, const uint32_t* perm0, const flo
     static bool attr = false;
     if (!attr) {
         DETLSH_CUDA(cudaFuncSetAttribute(tc_finish_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kTcFinishCap * 12)));
+                                         static_cast<int>(kTcFinishCapF32 * 12)));
         attr = true;
     }
     ProfScope ps("tc_finish", s);
