@@ -48,9 +48,11 @@ def main(rep, pattern, units, out_txt, config=None):
                 except ValueError:
                     x = v
                 rec[w] = x
-        short = re.sub(r"\(.*", "", name).split("::")[-1]
+        short = re.sub(r"<.*", "", re.sub(r"\(.*", "", name).split("::")[-1])  # template args dropped
         lines.append(f"{short}: " + ", ".join(f"{k}={v}" for k, v in rec.items()))
         dram = rec.get("dram__bytes_read.sum", 0) + rec.get("dram__bytes_write.sum", 0)
+        if short in summary and summary[short]["duration_ms"] >= rec.get("gpu__time_duration.sum", 0):
+            continue  # several launches of one kernel: keep the longest (the full-size one)
         summary[short] = {"dram_bytes": dram, "duration_ms": rec.get("gpu__time_duration.sum"),
                           "dram_bytes_per_unit": dram / float(units),
                           "source": os.path.basename(out_txt), "config": config}
