@@ -338,7 +338,7 @@ __device__ __forceinline__ double l2_exact(const float* q, const float* x, int d
 
 // Warp-aggregated append of `item` to list (counter in smem).
 __device__ __forceinline__ void warp_append(bool ok, const LeafItem& it, LeafItem* list,
-                                            uint32_t* counter) {
+                                            uint32_t* counter, uint32_t cap = 0xffffffffu) {
     const uint32_t m = __ballot_sync(0xffffffffu, ok);
     if (!m) return;
     const int lane = threadIdx.x & 31;
@@ -346,7 +346,8 @@ __device__ __forceinline__ void warp_append(bool ok, const LeafItem& it, LeafIte
     uint32_t base = 0;
     if (lane == leader) base = atomicAdd(counter, static_cast<uint32_t>(__popc(m)));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (ok) list[base + __popc(m & ((1u << lane) - 1u))] = it;
+    const uint32_t at = base + __popc(m & ((1u << lane) - 1u));
+    if (ok && at < cap) list[at] = it;
 }
 
 // Scan every leaf of tree `tree`, appending those with mindist <= radius.
@@ -629,14 +630,23 @@ struct FastSlot {
     uint32_t* cand;       // candidate rows as tree-0 permutation indices
 };
 
+// The bin-b* item lists (and the select's ping-pong buffers) hold the leaves of
+// the crossing bins only — a few hundred per query; they are capped at
+// kItemCap so the per-CTA slots of a 1e8-point index (6.7 M leaves per tree)
+// stay small enough for many CTAs.  A query that overflows them takes the
+// general path.
+constexpr uint32_t kItemCap = 1u << 20;
+__host__ __device__ __forceinline__ uint32_t item_cap(uint32_t maxl) { return maxl < kItemCap ? maxl : kItemCap; }
+
 __device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl,
                                               uint64_t budget) {
     uint8_t* p = base + static_cast<size_t>(blockIdx.x) * slot_bytes;
+    const uint32_t ic = item_cap(maxl);
     FastSlot f;
     f.A = reinterpret_cast<LeafItem*>(p);
-    f.B = f.A + maxl;
-    f.C = f.B + maxl;
-    f.full = reinterpret_cast<uint32_t*>(f.C + maxl);
+    f.B = f.A + ic;
+    f.C = f.B + ic;
+    f.full = reinterpret_cast<uint32_t*>(f.C + ic);
     f.tau = f.full + maxl;
     f.cand = f.tau + maxl;
     f.bin16 = reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(f.cand + budget) + 15) & ~uintptr_t(15));
@@ -655,7 +665,7 @@ size_t fast_scratch_limit() { return scratch_limit_env("DETLSH_FAST_SCRATCH_MB",
 size_t slow_scratch_limit() { return scratch_limit_env("DETLSH_SLOW_SCRATCH_MB", 512); }
 
 size_t fast_slot_bytes(uint32_t maxl, uint64_t budget) {
-    const size_t b = 3 * static_cast<size_t>(maxl) * sizeof(LeafItem) + 8 * static_cast<size_t>(maxl) +
+    const size_t b = 3 * static_cast<size_t>(item_cap(maxl)) * sizeof(LeafItem) + 8 * static_cast<size_t>(maxl) +
                      4 * budget + 2 * (static_cast<size_t>(maxl) + 8) + 16;
     return (b + 255) / 256 * 256;
 }
@@ -1188,6 +1198,7 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             {
                 unsigned long long w_margin = 0, wm = 0;
                 uint32_t* amb_list = reinterpret_cast<uint32_t*>(F.C);  // free until the select
+                const uint32_t amb_cap = item_cap(P.max_leaves) * static_cast<uint32_t>(sizeof(LeafItem) / 4);
                 // 32 leaf bins per thread per step: four 16-byte loads in flight
                 const uint32_t nv = (nl + 7) / 8, nv4 = (nv + 3) / 4;
                 for (uint32_t vb = 0; vb < nv4; vb += blockDim.x) {
@@ -1254,10 +1265,15 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
                     uint32_t a0 = 0;
                     if (lane == 31 && atot) a0 = atomicAdd(&S.u32s[15], atot);
                     a0 = __shfl_sync(0xffffffffu, a0, 31) + ainc - acnt;
-                    for (uint32_t m = amask; m; m &= m - 1) amb_list[a0++] = v * 8 + __ffs(m) - 1;
+                    for (uint32_t m = amask; m; m &= m - 1, ++a0)
+                        if (a0 < amb_cap) amb_list[a0] = v * 8 + __ffs(m) - 1;
                 }
                 __syncthreads();
                 const uint32_t n_amb = S.u32s[15];
+                if (n_amb > amb_cap) {  // (uniform) far more ambiguous leaves than the lists hold
+                    to_slow = true;
+                    break;
+                }
                 for (uint32_t base = 0; base < n_amb; base += blockDim.x) {
                     const uint32_t i = base + threadIdx.x;
                     bool ok = false;
@@ -1275,7 +1291,7 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
                         it.pad = 0;
                         if (ok) wm += w;
                     }
-                    warp_append(ok, it, F.B, &S.u32s[1]);
+                    warp_append(ok, it, F.B, &S.u32s[1], item_cap(P.max_leaves));
                 }
                 for (int o = 16; o; o >>= 1) {
                     w_margin += __shfl_xor_sync(0xffffffffu, w_margin, o);
@@ -1286,6 +1302,10 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             }
             __syncthreads();
             const uint32_t n_bin = S.u32s[1];  // weighted_select reuses this counter
+            if (n_bin > item_cap(P.max_leaves)) {  // (uniform) list overflow: the general path
+                to_slow = true;
+                break;
+            }
             // approximate round: weight taken whole = histogram weight below b*
             // minus the margin leaves of bin b*-1 that turned out ambiguous
             const uint64_t need = approx ? S.u64s[1] + S.u64s[2] : S.u64s[1];
