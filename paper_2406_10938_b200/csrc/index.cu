@@ -9,6 +9,7 @@
 //   side[L]     : r_min order statistics (needs projections only; own thread)
 // so the trees and r_min overlap the sequential host replay of later spaces.
 #include <algorithm>
+#include <cstdio>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -188,6 +189,17 @@ void validate_params(const detlsh_params& p, uint64_t n, int d) {
     sample_size_for(p.sample_fraction, n, p.n_regions);
 }
 
+// Device-side alias of a page-locked host pointer (UVA), or null for pageable memory.
+static const float* mapped_host_ptr(const float* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost || at.devicePointer == nullptr) return nullptr;
+    return static_cast<const float*>(at.devicePointer);
+}
+
 std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int d,
                                            detlsh_params* params, const float* coeffs_host,
                                            uint64_t family_seed, uint64_t seed, int device,
@@ -332,7 +344,10 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         cudaStream_t s2 = X->side[L]->s;  // free until the r_min worker starts
         {
             StreamScope sc(s2);
+            const bool zero_copy_sample = !dev_in && mapped_host_ptr(points) != nullptr;
             const auto& idx0 = sampler_ptr->next_space_indices();
+            const bool dbg = std::getenv("DETLSH_DEBUG_BUILD") != nullptr;
+            if (dbg) fprintf(stderr, "[build] fy %.2f ms mapped=%d\n", ms_since(t0), zero_copy_sample ? 1 : 0);
             DevBuf<float> dG(n_s * static_cast<size_t>(d)), dGp(static_cast<size_t>(L) * n_s * K);
             DevBuf<uint32_t> iota(n_s);
             std::vector<uint32_t> h_iota(n_s);
@@ -342,6 +357,12 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                 DETLSH_CUDA(cudaMemcpyAsync(d_idx0.get(), idx0.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
                 DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
                 launch_pack_f32(X->data, d_idx0.get(), n_s, d, dG.get(), s2);  // rows idx0[t]
+            } else if (const float* mapped = zero_copy_sample ? mapped_host_ptr(points) : nullptr) {
+                // page-locked host input: the GPU gathers the sample rows over the
+                // bus itself (zero-copy), no host-side gather on the critical path
+                DevBuf<uint32_t> d_idx0(n_s);
+                DETLSH_CUDA(cudaMemcpyAsync(d_idx0.get(), idx0.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
+                launch_pack_f32(mapped, d_idx0.get(), n_s, d, dG.get(), s2);
             } else {
                 float* G = pinned_scratch(n_s * static_cast<size_t>(d) * sizeof(float), 1);
                 const int nt = 8;
@@ -366,6 +387,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             cudaEvent_t copied0;
             DETLSH_CUDA(cudaEventCreateWithFlags(&copied0, cudaEventDisableTiming));
             DETLSH_CUDA(cudaEventRecord(copied0, s2));
+            if (dbg) fprintf(stderr, "[build] enqueued %.2f ms\n", ms_since(t0));
             gpu_order_stat_table(d_sample0.get(), K, n_s, NR, X->table.get(), s2, /*sync=*/false);
             DETLSH_CUDA(cudaEventCreateWithFlags(&table0, cudaEventDisableTiming));
             DETLSH_CUDA(cudaEventRecord(table0, s2));
@@ -377,6 +399,9 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                 try {
                     DETLSH_CUDA(cudaSetDevice(device));
                     StreamScope sc(s);
+                    // the sample rows first: with page-locked input the GPU gathers
+                    // them over the bus, which the bulk upload would otherwise share
+                    if (zero_copy_sample) DETLSH_CUDA(cudaStreamWaitEvent(s, copied0, 0));
                     DETLSH_CUDA(cudaMemcpyAsync(X->data_buf.get(), points, n * static_cast<size_t>(d) * 4,
                                                 cudaMemcpyHostToDevice, s));
                     project_all();
@@ -391,14 +416,16 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                 }
             } joiner{uploader};
             DETLSH_CUDA(cudaEventSynchronize(copied0));
-            cudaEventDestroy(copied0);
+            if (dbg) fprintf(stderr, "[build] sample on host %.2f ms\n", ms_since(t0));
             X->timings.emplace_back("bp_space0_sample", ms_since(t0));
             const auto tr = Clock::now();
             if (L > 1)
                 for (int j = 0; j < K; ++j)
                     sampler_ptr->select_row(h_sample + static_cast<size_t>(j) * n_s, h_rows.data() + j * W);
             X->timings.emplace_back("bp_space0_replay", ms_since(tr));
+            if (dbg) fprintf(stderr, "[build] space-0 replay done %.2f ms\n", ms_since(t0));
             uploader.join();
+            cudaEventDestroy(copied0);  // (after the uploader's wait on it)
             if (up_err) std::rethrow_exception(up_err);
         }
         cudaEventDestroy(coeffs_ready);
