@@ -630,13 +630,16 @@ struct FastSlot {
     uint32_t* cand;       // candidate rows as tree-0 permutation indices
 };
 
-// The bin-b* item lists (and the select's ping-pong buffers) hold the leaves of
-// the crossing bins only — a few hundred per query; they are capped at
-// kItemCap so the per-CTA slots of a 1e8-point index (6.7 M leaves per tree)
-// stay small enough for many CTAs.  A query that overflows them takes the
-// general path.
-constexpr uint32_t kItemCap = 1u << 20;
+// The per-CTA leaf lists are capped (bin-b* items and the select's ping-pong
+// buffers: a few hundred per query; whole leaves; tau leaves) so the slots of a
+// 1e8-point index (6.7 M leaves per tree) stay small enough for many CTAs.  A
+// query that overflows one takes the general path.
+constexpr uint32_t kItemCap = 1u << 20;   // bin-b* items (C5: up to ~10^5 in the crossing bins)
+constexpr uint32_t kFullCap = 0xffffffffu; // whole leaves: not capped (up to budget leaves at C5)
+constexpr uint32_t kTauCap = 1u << 20;    // tau leaves (<= tau rows: C5 ~33 K per query)
 __host__ __device__ __forceinline__ uint32_t item_cap(uint32_t maxl) { return maxl < kItemCap ? maxl : kItemCap; }
+__host__ __device__ __forceinline__ uint32_t full_cap(uint32_t maxl) { return maxl < kFullCap ? maxl : kFullCap; }
+__host__ __device__ __forceinline__ uint32_t tau_cap(uint32_t maxl) { return maxl < kTauCap ? maxl : kTauCap; }
 
 __device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl,
                                               uint64_t budget) {
@@ -647,8 +650,8 @@ __device__ __forceinline__ FastSlot fast_slot(uint8_t* base, size_t slot_bytes, 
     f.B = f.A + ic;
     f.C = f.B + ic;
     f.full = reinterpret_cast<uint32_t*>(f.C + ic);
-    f.tau = f.full + maxl;
-    f.cand = f.tau + maxl;
+    f.tau = f.full + full_cap(maxl);
+    f.cand = f.tau + tau_cap(maxl);
     f.bin16 = reinterpret_cast<uint16_t*>((reinterpret_cast<uintptr_t>(f.cand + budget) + 15) & ~uintptr_t(15));
     return f;
 }
@@ -661,12 +664,36 @@ size_t scratch_limit_env(const char* name, size_t dflt_mb) {
     const size_t mb = e ? static_cast<size_t>(std::max(1L, std::atol(e))) : dflt_mb;
     return mb << 20;
 }
-size_t fast_scratch_limit() { return scratch_limit_env("DETLSH_FAST_SCRATCH_MB", 8192); }
-size_t slow_scratch_limit() { return scratch_limit_env("DETLSH_SLOW_SCRATCH_MB", 512); }
+// Memory the query scratch may take: the free device memory plus what the
+// stream-ordered pool holds but does not use (freed build temporaries).
+size_t device_memory_available(int device) {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t reserved = 0, used = 0;
+        if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+            cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+            fr += static_cast<size_t>(reserved - used);
+    }
+    cudaGetLastError();
+    return fr;
+}
+// 8 GB, or up to a third of the available memory for large indexes (C5's
+// slots are ~150 MB each: more of them keep more SMs busy)
+size_t fast_scratch_limit(int device) {
+    if (std::getenv("DETLSH_FAST_SCRATCH_MB")) return scratch_limit_env("DETLSH_FAST_SCRATCH_MB", 8192);
+    return std::max<size_t>(size_t(8192) << 20, std::min<size_t>(size_t(32768) << 20, device_memory_available(device) / 3));
+}
+size_t slow_scratch_limit() { return scratch_limit_env("DETLSH_SLOW_SCRATCH_MB", 2048); }
 
 size_t fast_slot_bytes(uint32_t maxl, uint64_t budget) {
-    const size_t b = 3 * static_cast<size_t>(item_cap(maxl)) * sizeof(LeafItem) + 8 * static_cast<size_t>(maxl) +
-                     4 * budget + 2 * (static_cast<size_t>(maxl) + 8) + 16;
+    const size_t b = 3 * static_cast<size_t>(item_cap(maxl)) * sizeof(LeafItem) +
+                     4 * (static_cast<size_t>(full_cap(maxl)) + tau_cap(maxl)) + 4 * budget +
+                     2 * (static_cast<size_t>(maxl) + 8) + 16;
     return (b + 255) / 256 * 256;
 }
 
@@ -1239,7 +1266,8 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
                     uint32_t b0 = 0;
                     if (lane == 31 && tot) b0 = atomicAdd(&S.u32s[0], tot);
                     b0 = __shfl_sync(0xffffffffu, b0, 31) + incl - cnt;
-                    for (uint32_t m = wmask; m; m &= m - 1) F.full[b0++] = v * 8 + __ffs(m) - 1;
+                    for (uint32_t m = wmask; m; m &= m - 1, ++b0)
+                        if (b0 < full_cap(P.max_leaves)) F.full[b0] = v * 8 + __ffs(m) - 1;
                     if (__any_sync(0xffffffffu, tmask != 0)) {  // tau leaves (nearest bins)
                         const uint32_t tcnt = __popc(tmask);
                         uint32_t tinc = tcnt;
@@ -1251,7 +1279,8 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
                         uint32_t t0 = 0;
                         if (lane == 31) t0 = atomicAdd(&S.u32s[12], ttot);
                         t0 = __shfl_sync(0xffffffffu, t0, 31) + tinc - tcnt;
-                        for (uint32_t m = tmask; m; m &= m - 1) F.tau[t0++] = v * 8 + __ffs(m) - 1;
+                        for (uint32_t m = tmask; m; m &= m - 1, ++t0)
+                            if (t0 < tau_cap(P.max_leaves)) F.tau[t0] = v * 8 + __ffs(m) - 1;
                     }
                     // ambiguous leaves (a few hundred per query): listed, then
                     // scored exactly below, one per thread
@@ -1350,11 +1379,16 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
                     uint32_t b0 = 0;
                     if (lane == leader) b0 = atomicAdd(&S.u32s[0], static_cast<uint32_t>(__popc(m)));
                     b0 = __shfl_sync(0xffffffffu, b0, leader);
-                    if (before) F.full[b0 + __popc(m & ((1u << lane) - 1u))] = li;
+                    const uint32_t at = b0 + __popc(m & ((1u << lane) - 1u));
+                    if (before && at < full_cap(P.max_leaves)) F.full[at] = li;
                 }
             }
             __syncthreads();
             n_full = S.u32s[0];
+            if (n_full > full_cap(P.max_leaves) || S.u32s[12] > tau_cap(P.max_leaves)) {  // (uniform) lists full
+                to_slow = true;
+                break;
+            }
             cut_li = S.u32s[10];
 
             break;
@@ -1814,7 +1848,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         // processing slots: a CTA each, bounded by the scratch they need
         // (fast_bytes grows with the budget: 4 B per candidate)
         size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
-        slots = std::max<size_t>(1, std::min<size_t>(slots, fast_scratch_limit() / fast_bytes));
+        slots = std::max<size_t>(1, std::min<size_t>(slots, fast_scratch_limit(device) / fast_bytes));
         grow_scratch(X.fast, slots * fast_bytes);
         auto launch_fast = [&](const QueryPlan& Pc) {
             const uint64_t m = Pc.q_end - Pc.q_begin;
