@@ -1848,7 +1848,10 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         // processing slots: a CTA each, bounded by the scratch they need
         // (fast_bytes grows with the budget: 4 B per candidate)
         size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
-        slots = std::max<size_t>(1, std::min<size_t>(slots, fast_scratch_limit(device) / fast_bytes));
+        // (under stream capture no memory query: the scratch an earlier,
+        // uncaptured batch of this shape sized is what the slots get)
+        const size_t lim = capturing ? std::max<size_t>(X.fast.size(), fast_bytes) : fast_scratch_limit(device);
+        slots = std::max<size_t>(1, std::min<size_t>(slots, lim / fast_bytes));
         grow_scratch(X.fast, slots * fast_bytes);
         auto launch_fast = [&](const QueryPlan& Pc) {
             const uint64_t m = Pc.q_end - Pc.q_begin;
