@@ -115,17 +115,18 @@ double estimate_rmin_gpu(GpuIndex& X, const float* d_proj, uint64_t seed, cudaSt
     std::vector<uint64_t> pos(np);
     for (int p = 0; p < np; ++p) pos[p] = rng.bounded(n);
     DevBuf<float> probe(static_cast<size_t>(np) * L * K);
-    for (int p = 0; p < np; ++p)
-        for (int i = 0; i < L; ++i)
-            DETLSH_CUDA(cudaMemcpyAsync(probe.get() + (static_cast<size_t>(p) * L + i) * K,
-                                        d_proj + (static_cast<size_t>(i) * n + pos[p]) * K,
-                                        K * sizeof(float), cudaMemcpyDeviceToDevice, s));
-    // initial guess: median pairwise distance of 32 strided points (space 0)
+    // initial guess: median pairwise distance of 32 strided points (space 0);
+    // the probes' and those points' projected rows come over in two gathers
     const uint64_t m = std::min<uint64_t>(32, n);
+    std::vector<uint64_t> gpos(pos.begin(), pos.end());
+    for (uint64_t t = 0; t < m; ++t) gpos.push_back(t * n / m);
+    DevBuf<uint64_t> d_gpos(gpos.size());
+    DevBuf<float> d_sc(m * K);
+    DETLSH_CUDA(cudaMemcpyAsync(d_gpos.get(), gpos.data(), gpos.size() * 8, cudaMemcpyHostToDevice, s));
+    launch_gather_proj_rows(d_proj, n, K, L, d_gpos.get(), np, probe.get(), s);
+    launch_gather_proj_rows(d_proj, n, K, 1, d_gpos.get() + np, static_cast<int>(m), d_sc.get(), s);
     std::vector<float> sc_rows(m * K);
-    for (uint64_t t = 0; t < m; ++t)
-        DETLSH_CUDA(cudaMemcpyAsync(sc_rows.data() + t * K, d_proj + (t * n / m) * K,
-                                    K * sizeof(float), cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaMemcpyAsync(sc_rows.data(), d_sc.get(), m * K * 4, cudaMemcpyDeviceToHost, s));
     const uint64_t budget = candidate_budget(X.params.beta, n, X.params.k);
     DevBuf<double> D(static_cast<size_t>(np) * n);
     DevBuf<uint32_t> hist(static_cast<size_t>(np) * 65536);

@@ -131,6 +131,17 @@ __global__ void project_paa_kernel(const float* __restrict__ pts, uint64_t n, in
     }
 }
 
+// out[(r * Lg + i) * K + j] = proj[(i * n + pos[r]) * K + j]: whole projected
+// rows of a few points (r_min probes, the initial-guess points), one launch.
+__global__ void gather_proj_rows_kernel(const float* __restrict__ proj, uint64_t n, int K, int Lg,
+                                        const uint64_t* __restrict__ pos, int m, float* __restrict__ out) {
+    const int total = m * Lg * K;
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const int r = t / (Lg * K), i = (t / K) % Lg, j = t % K;
+        out[t] = proj[(static_cast<uint64_t>(i) * n + pos[r]) * K + j];
+    }
+}
+
 __global__ void gather_sample_kernel(const float* __restrict__ proj, const uint32_t* __restrict__ idx,
                                      uint64_t n_s, int K, float* __restrict__ out) {
     for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < n_s;
@@ -484,6 +495,13 @@ void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* 
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n * K + 255) / 256, 65535)));
     ProfScope ps(prof, s);
     project_paa_kernel<<<grid, 256, 0, s>>>(d_points, n, d, K, d_out);
+    DETLSH_LAUNCH_CHECK();
+}
+
+void launch_gather_proj_rows(const float* d_proj, uint64_t n, int K, int Lg, const uint64_t* d_pos, int m,
+                             float* d_out, cudaStream_t s) {
+    if (m <= 0) return;
+    gather_proj_rows_kernel<<<(m * Lg * K + 255) / 256, 256, 0, s>>>(d_proj, n, K, Lg, d_pos, m, d_out);
     DETLSH_LAUNCH_CHECK();
 }
 

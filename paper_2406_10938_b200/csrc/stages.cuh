@@ -55,6 +55,9 @@ void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* 
                         const char* prof = "project_paa");
 
 // sample values: out[j][t] = proj[space][idx[t]][j]  (j < K, t < n_s)
+// out[(r Lg + i) K + j] = proj[(i n + pos[r]) K + j] for r < m, i < Lg (device positions)
+void launch_gather_proj_rows(const float* d_proj, uint64_t n, int K, int Lg, const uint64_t* d_pos, int m,
+                             float* d_out, cudaStream_t s);
 void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
                           float* d_out, cudaStream_t s);
 
