@@ -336,7 +336,7 @@ def run_reference(args, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(build_rate, 6), "unit": "Mpoints/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(build_s * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(build_s * 1e3, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg}: n={n}, d={d}, nq={Q.shape[0]}, K=16, L=4, N_r=256, "
                                f"leaf=128, k={args.k}, c=1.5, beta={args.beta}",
