@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "primitives.cuh"
 #include "query.cuh"
@@ -42,6 +43,11 @@ constexpr int kFine = kBins * 32;               // approximate round: fine bins 
 constexpr uint32_t kTcMinBudget = 8192;         // tensor-core hand-off from this budget on
 constexpr int kMergeMaxShards = 1024;           // merge_topk: shards per call
 constexpr uint32_t kTauRows = 512;              // min rows scored exactly to set tau^2
+// max rows scored for tau^2: the nearest leaves beat a uniform sample by far
+// at large budgets (C5, budget 1e7: 131072 rows leave 857 survivors at the
+// median and 2574 at most against the 4096 staged; the uniform estimate asks
+// for 488 K rows, 4x the plan time).  Overflowing queries take the gather path.
+constexpr uint64_t kTauRowsMax = 1u << 17;
 static_assert(kFastMaxK == kTopCap - kBatch, "fast-path k bound");
 
 struct LeafItem {
@@ -682,13 +688,19 @@ size_t device_memory_available(int device) {
     cudaGetLastError();
     return fr;
 }
-// 8 GB, or up to a third of the available memory for large indexes (C5's
-// slots are ~150 MB each: more of them keep more SMs busy)
-size_t fast_scratch_limit(int device) {
+// `avail`: the available memory plus the query scratch already held (it is
+// reused).  Fast path: 8 GB, or up to a third of it for large indexes (C5's
+// slots are ~150 MB each: more of them keep more SMs busy).
+size_t fast_scratch_limit(size_t avail) {
     if (std::getenv("DETLSH_FAST_SCRATCH_MB")) return scratch_limit_env("DETLSH_FAST_SCRATCH_MB", 8192);
-    return std::max<size_t>(size_t(8192) << 20, std::min<size_t>(size_t(32768) << 20, device_memory_available(device) / 3));
+    return std::max<size_t>(size_t(8192) << 20, std::min<size_t>(size_t(32768) << 20, avail / 3));
 }
-size_t slow_scratch_limit() { return scratch_limit_env("DETLSH_SLOW_SCRATCH_MB", 2048); }
+// general path: 2 GB, or up to a fifth for large indexes (C5: ~210 MB per
+// slot; 2 GB kept it to 9 CTAs)
+size_t slow_scratch_limit(size_t avail) {
+    if (std::getenv("DETLSH_SLOW_SCRATCH_MB")) return scratch_limit_env("DETLSH_SLOW_SCRATCH_MB", 2048);
+    return std::max<size_t>(size_t(2048) << 20, std::min<size_t>(size_t(24576) << 20, avail / 5));
+}
 
 size_t fast_slot_bytes(uint32_t maxl, uint64_t budget) {
     const size_t b = 3 * static_cast<size_t>(item_cap(maxl)) * sizeof(LeafItem) +
@@ -1479,6 +1491,16 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
 // ---------------------------------------------------------------------------
 // General path: every tree, every round, bitmap dedup (CandidateSet).
 // ---------------------------------------------------------------------------
+// A deferred general-path query (query_slow_kernel -> slow_score_kernel ->
+// slow_topk_kernel), one per slot.
+struct SlowRec {
+    uint32_t q, msz, scored, done;
+    double r;
+};
+constexpr uint32_t kNoQuery = 0xffffffffu;
+// budget from which the general path defers member distances (C5: 10^7)
+constexpr uint64_t kSlowDeferMinBudget = 1u << 18;
+
 struct SlowSlot {
     LeafItem *A, *B, *C;
     uint32_t* bitmap;  // n bits
@@ -1486,16 +1508,20 @@ struct SlowSlot {
     double* mdist;
 };
 
+// The slot's bitmap lives apart (`bitmaps`, bm_words per slot, zeroed once
+// and cleared by each query): the rest of a slot is laid out by the budget,
+// which changes with k from one batch to the next.
 __device__ __forceinline__ SlowSlot slow_slot(uint8_t* base, size_t slot_bytes, uint32_t maxl,
-                                              uint64_t budget) {
-    uint8_t* p = base + static_cast<size_t>(blockIdx.x) * slot_bytes;
+                                              uint64_t budget, uint32_t slot, uint32_t* bitmaps = nullptr,
+                                              uint64_t bm_words = 0) {
+    uint8_t* p = base + static_cast<size_t>(slot) * slot_bytes;
     SlowSlot s;
     s.A = reinterpret_cast<LeafItem*>(p);
     s.B = s.A + maxl;
     s.C = s.B + maxl;
     s.mdist = reinterpret_cast<double*>(s.C + maxl);
     s.mpos = reinterpret_cast<uint32_t*>(s.mdist + budget);
-    s.bitmap = s.mpos + budget;
+    s.bitmap = bitmaps ? bitmaps + static_cast<uint64_t>(slot) * bm_words : nullptr;
     return s;
 }
 
@@ -1503,7 +1529,7 @@ __device__ __forceinline__ SlowSlot slow_slot(uint8_t* base, size_t slot_bytes, 
 // new ones of the cut leaf) into the member list.
 __device__ void emit_members(const QueryPlan& P, int tree, const LeafItem* A, uint32_t nA,
                              bool select, uint64_t kmdb, uint32_t kid, uint64_t take_cut,
-                             const SlowSlot& L, const Smem& S) {
+                             const SlowSlot& L, const Smem& S, bool score) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const QTree T = P.trees[tree];
     for (uint32_t i = warp; i < nA; i += blockDim.x / 32) {
@@ -1537,7 +1563,7 @@ __device__ void emit_members(const QueryPlan& P, int tree, const LeafItem* A, ui
                     atomicOr(&L.bitmap[pos >> 5], 1u << (pos & 31));
                     const uint32_t slot = slot0 + __popc(tm & ((1u << lane) - 1u));
                     L.mpos[slot] = pos;
-                    L.mdist[slot] = l2_exact(S.qv, P.data + static_cast<uint64_t>(pos) * P.d, P.d);
+                    if (score) L.mdist[slot] = l2_exact(S.qv, P.data + static_cast<uint64_t>(pos) * P.d, P.d);
                 }
             }
             emitted += __popc(tm);
@@ -1546,20 +1572,112 @@ __device__ void emit_members(const QueryPlan& P, int tree, const LeafItem* A, ui
     __syncthreads();
 }
 
+// Top-k of a general-path query's members (extracted kFastMaxK at a time,
+// any k) and its outputs.
+__device__ void slow_finish(const QueryPlan& P, const Smem& S, const SlowSlot& L, uint64_t q, uint32_t msz,
+                            double r, bool done) {
+    uint32_t want = min(msz, static_cast<uint32_t>(P.k));
+    uint32_t out = 0;
+    uint64_t lbh = 0;
+    uint32_t lbl = 0;
+    bool have_lb = false;
+    while (out < want) {
+        const int kk = static_cast<int>(min(want - out, static_cast<uint32_t>(kFastMaxK)));
+        topk_init(S);
+        for (uint32_t c0 = 0; c0 < msz; c0 += kBatch) {
+            const uint32_t nb = min(static_cast<uint32_t>(kBatch), msz - c0);
+            for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+                const uint64_t h = static_cast<uint64_t>(__double_as_longlong(L.mdist[c0 + i]));
+                const uint32_t l = L.mpos[c0 + i];
+                const bool above = !have_lb || key_less(lbh, lbl, h, l);
+                S.bh[i] = above ? h : ~0ULL;  // sentinels never beat a real key
+                S.bl[i] = above ? l : 0xffffffffu;
+            }
+            __syncthreads();
+            topk_absorb(S, nb, kk, nullptr);
+        }
+        uint32_t got = topk_finish(S, kk);
+        // drop sentinel entries (only possible when fewer than kk remain)
+        while (got > 0 && S.th[got - 1] == ~0ULL && S.tl[got - 1] == 0xffffffffu) --got;
+        for (uint32_t t = threadIdx.x; t < got; t += blockDim.x) {
+            if (P.ids) P.ids[q * P.k + out + t] = S.tl[t];
+            if (P.dists) P.dists[q * P.k + out + t] = __longlong_as_double(static_cast<long long>(S.th[t]));
+        }
+        lbh = S.th[got - 1];
+        lbl = S.tl[got - 1];
+        have_lb = true;
+        out += got;
+        __syncthreads();
+    }
+    // rc_ann: without the budget reached, the closest counts only within c * r
+    if (P.rc_mode && !done && want > 0 && !(__longlong_as_double(static_cast<long long>(lbh)) <= __dmul_rn(P.c, r)))
+        want = 0;
+    if (threadIdx.x == 0) {
+        if (P.n_hits) P.n_hits[q] = static_cast<int32_t>(want);
+        if (P.radius) P.radius[q] = r;
+        if (P.cands) P.cands[q] = msz;
+    }
+}
+
+// Exact distances of members [from, msz) by the whole block.
+__device__ void score_members(const QueryPlan& P, const float* qv, const SlowSlot& L, uint32_t from, uint32_t msz) {
+    for (uint32_t i = from + threadIdx.x; i < msz; i += blockDim.x)
+        L.mdist[i] = l2_exact(qv, P.data + static_cast<uint64_t>(L.mpos[i]) * P.d, P.d);
+    __syncthreads();
+}
+
+// The listed queries are claimed one at a time through `taken` (never past
+// `count`): a slot that finishes early takes the next one.
+//
+// Deferred mode (recs != null and no more listed queries than slots): a
+// query with a large budget is ~10^7 members, and one CTA computing their
+// distances and top-k leaves the GPU idle (C5: ~0.5 s per query).  Each CTA
+// then takes at most one query and records its member list (rec); the
+// distances are computed grid-wide (slow_score_kernel) and the top-k by
+// slow_topk_kernel.  Distances a round's count_within needs are computed
+// here as before.
 __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
-    QueryPlan P, const uint32_t* list, uint32_t count, const uint32_t* count_dev, uint8_t* scratch,
-    size_t slot_bytes) {
+    QueryPlan P, const uint32_t* list, uint32_t count, const uint32_t* count_dev, uint32_t* taken,
+    uint8_t* scratch, size_t slot_bytes, uint32_t* bitmaps, uint64_t bm_words, SlowRec* recs) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
+    __shared__ uint32_t s_qi;
     const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
-    const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.budget);
+    const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.budget, blockIdx.x, bitmaps, bm_words);
     if (count_dev) count = min(count, *count_dev);
-    for (uint32_t qi = blockIdx.x; qi < count; qi += gridDim.x) {
+    const bool defer = recs != nullptr && count <= gridDim.x;
+    if (recs && threadIdx.x == 0) recs[blockIdx.x].q = kNoQuery;
+    long long t_prev = clock64();
+    auto phase = [&](int i, unsigned long long add = 0) {  // profiling: slots 8.. of the phase array
+        if (P.phase_cycles && threadIdx.x == 0) {
+            const long long t = clock64();
+            atomicAdd(P.phase_cycles + 8 + i, add ? add : static_cast<unsigned long long>(t - t_prev));
+            t_prev = t;
+        }
+    };
+    for (;;) {
+        if (threadIdx.x == 0) {
+            uint32_t cur = *static_cast<volatile uint32_t*>(taken), got = count;
+            while (cur < count) {
+                const uint32_t prev = atomicCAS(taken, cur, cur + 1);
+                if (prev == cur) {
+                    got = cur;
+                    break;
+                }
+                cur = prev;
+            }
+            s_qi = got;
+        }
+        __syncthreads();
+        const uint32_t qi = s_qi;
+        __syncthreads();
+        if (qi >= count) break;
         const uint64_t q = list ? list[qi] : qi;
         if (threadIdx.x == 0) S.u32s[7] = 0;  // |S|
         __syncthreads();
         load_query_vec(P, q, S);
         double r = P.r_min;
         bool done = false;
+        uint32_t scored = 0;  // members [0, scored) have distances
         for (;;) {
             for (int tree = 0; tree < P.L && !done; ++tree) {
                 load_query_proj(P, q, tree, S);
@@ -1569,21 +1687,28 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
                 uint32_t nA;
                 uint64_t W;
                 scan_leaves(P, tree, radius, S, L.A, have ? L.bitmap : nullptr, nA, W);
+                phase(0);
                 const uint64_t need = P.budget - have;
                 if (W >= need) {
                     uint64_t kmdb, take_cut;
                     uint32_t kid;
                     weighted_select(L.A, nA, need, L.B, L.C, S, kmdb, kid, take_cut);
-                    emit_members(P, tree, L.A, nA, true, kmdb, kid, take_cut, L, S);
+                    phase(1);
+                    emit_members(P, tree, L.A, nA, true, kmdb, kid, take_cut, L, S, !defer);
                     done = true;
                 } else {
-                    emit_members(P, tree, L.A, nA, false, 0, 0, 0, L, S);
+                    emit_members(P, tree, L.A, nA, false, 0, 0, 0, L, S, !defer);
                 }
+                if (!defer) scored = S.u32s[7];
+                phase(2);
+                phase(5, nA);
             }
             if (done || P.rc_mode) break;  // rc_ann: a single pass (index.cpp:278-289)
             // count_within(c * r) (index.cpp:244-249, 328)
             const double lim = __dmul_rn(P.c, r);
             const uint32_t msz = S.u32s[7];
+            if (scored < msz) score_members(P, S.qv, L, scored, msz);
+            scored = msz;
             uint32_t mine = 0;
             for (uint32_t i = threadIdx.x; i < msz; i += blockDim.x) mine += L.mdist[i] <= lim ? 1u : 0u;
             for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
@@ -1593,57 +1718,65 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
             __syncthreads();
             const bool enough = S.u32s[8] >= static_cast<uint32_t>(P.k);
             __syncthreads();
+            phase(3);
+            phase(6, 1);
             if (enough) break;
             r = __dmul_rn(r, P.c);
         }
-        // top-k of the members, extracted kFastMaxK at a time (any k)
         const uint32_t msz = S.u32s[7];
-        uint32_t want = min(msz, static_cast<uint32_t>(P.k));
-        uint32_t out = 0;
-        uint64_t lbh = 0;
-        uint32_t lbl = 0;
-        bool have_lb = false;
-        while (out < want) {
-            const int kk = static_cast<int>(min(want - out, static_cast<uint32_t>(kFastMaxK)));
-            topk_init(S);
-            for (uint32_t c0 = 0; c0 < msz; c0 += kBatch) {
-                const uint32_t nb = min(static_cast<uint32_t>(kBatch), msz - c0);
-                for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) {
-                    const uint64_t h = static_cast<uint64_t>(__double_as_longlong(L.mdist[c0 + i]));
-                    const uint32_t l = L.mpos[c0 + i];
-                    const bool above = !have_lb || key_less(lbh, lbl, h, l);
-                    S.bh[i] = above ? h : ~0ULL;  // sentinels never beat a real key
-                    S.bl[i] = above ? l : 0xffffffffu;
-                }
-                __syncthreads();
-                topk_absorb(S, nb, kk, nullptr);
-            }
-            uint32_t got = topk_finish(S, kk);
-            // drop sentinel entries (only possible when fewer than kk remain)
-            while (got > 0 && S.th[got - 1] == ~0ULL && S.tl[got - 1] == 0xffffffffu) --got;
-            for (uint32_t t = threadIdx.x; t < got; t += blockDim.x) {
-                if (P.ids) P.ids[q * P.k + out + t] = S.tl[t];
-                if (P.dists) P.dists[q * P.k + out + t] = __longlong_as_double(static_cast<long long>(S.th[t]));
-            }
-            lbh = S.th[got - 1];
-            lbl = S.tl[got - 1];
-            have_lb = true;
-            out += got;
-            __syncthreads();
-        }
-        // rc_ann: without the budget reached, the closest counts only within c * r
-        if (P.rc_mode && !done && want > 0 &&
-            !(__longlong_as_double(static_cast<long long>(lbh)) <= __dmul_rn(P.c, r)))
-            want = 0;
-        if (threadIdx.x == 0) {
-            if (P.n_hits) P.n_hits[q] = static_cast<int32_t>(want);
-            if (P.radius) P.radius[q] = r;
-            if (P.cands) P.cands[q] = msz;
-        }
+        if (!defer) slow_finish(P, S, L, q, msz, r, done);
         // clear the bitmap words we touched
         for (uint32_t i = threadIdx.x; i < msz; i += blockDim.x) L.bitmap[L.mpos[i] >> 5] = 0;
         __syncthreads();
+        phase(4);
+        phase(7, msz + 1);
+        if (defer) {
+            if (threadIdx.x == 0) {
+                SlowRec rc;
+                rc.q = static_cast<uint32_t>(q);
+                rc.msz = msz;
+                rc.scored = scored;
+                rc.done = done ? 1u : 0u;
+                rc.r = r;
+                recs[blockIdx.x] = rc;
+            }
+            break;  // the slot's members wait for slow_score_kernel
+        }
     }
+}
+
+// Deferred members' exact distances: blockIdx.y = slot, blockIdx.x strides
+// over its members (one thread per member, the same fp64 chain as above).
+__global__ void __launch_bounds__(256) slow_score_kernel(QueryPlan P, const SlowRec* recs, uint8_t* scratch,
+                                                        size_t slot_bytes) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const SlowRec rc = recs[blockIdx.y];
+    if (rc.q == kNoQuery || rc.scored >= rc.msz) return;
+    float* qv = reinterpret_cast<float*>(smem_raw);
+    for (int t = threadIdx.x; t < P.d; t += blockDim.x) qv[t] = P.q[static_cast<uint64_t>(rc.q) * P.d + t];
+    __syncthreads();
+    const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.budget, blockIdx.y);
+    const uint32_t stride = gridDim.x * blockDim.x;
+    uint32_t i = rc.scored + blockIdx.x * blockDim.x + threadIdx.x;
+    // two members in flight per thread (independent fp64 chains)
+    for (; i + stride < rc.msz; i += 2 * stride) {
+        const double a = l2_exact(qv, P.data + static_cast<uint64_t>(L.mpos[i]) * P.d, P.d);
+        const double b = l2_exact(qv, P.data + static_cast<uint64_t>(L.mpos[i + stride]) * P.d, P.d);
+        L.mdist[i] = a;
+        L.mdist[i + stride] = b;
+    }
+    if (i < rc.msz) L.mdist[i] = l2_exact(qv, P.data + static_cast<uint64_t>(L.mpos[i]) * P.d, P.d);
+}
+
+// Deferred queries' top-k and outputs: one CTA per slot.
+__global__ void __launch_bounds__(kQueryThreads) slow_topk_kernel(QueryPlan P, const SlowRec* recs, uint8_t* scratch,
+                                                                 size_t slot_bytes) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    const SlowRec rc = recs[blockIdx.x];
+    if (rc.q == kNoQuery) return;
+    const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
+    const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.budget, blockIdx.x);
+    slow_finish(P, S, L, rc.q, rc.msz, rc.r, rc.done != 0);
 }
 
 // One warp per query: lane l owns shards l, l+32, ...; every step the warp
@@ -1764,8 +1897,11 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // rows are fp64 chains, so 4x fewer of them is the better trade.
     const bool f32_rows = !P.data_u8 && P.data_leaf && P.data_tcf && P.xnf && P.row_f > 256 && tc_score_fits(P.row_f);
     const uint32_t fin_cap = f32_rows ? kTcFinishCapF32 : kTcFinishCap;
-    const uint64_t tau_rows = std::max<uint64_t>(
-        std::max<uint64_t>(kTauRows, 2ULL * P.k), (4ULL * P.k * P.budget + fin_cap - 1) / fin_cap);
+    uint64_t tau_rows = std::max<uint64_t>(
+        std::max<uint64_t>(kTauRows, 2ULL * P.k),
+        std::min<uint64_t>(kTauRowsMax, (4ULL * P.k * P.budget + fin_cap - 1) / fin_cap));
+    if (const char* e = std::getenv("DETLSH_TAU_ROWS"))  // measurement hook
+        tau_rows = std::max<uint64_t>(2ULL * P.k, std::strtoull(e, nullptr, 10));
     const bool tc_any = P.tc_allowed && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
                         2ULL * P.k <= fin_cap && 8 * tau_rows <= P.budget && P.k <= kFastMaxK && !P.rc_mode;
     const bool tc_u8 = tc_any && P.data_u8 && P.xn_u8 && P.data_tc && tc_score_fits(P.row_u8);
@@ -1781,6 +1917,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                               : five ? &query_fast_kernel<5, false> : &query_fast_kernel<3, false>;
     DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    DETLSH_CUDA(cudaFuncSetAttribute(slow_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // Persistent scratch lives on the index's own stream (it outlives any
     // caller stream).  Growing it is the one host wait of a batch, and only
     // happens when a batch needs more scratch than every earlier one.
@@ -1804,19 +1941,20 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     };
     if (!X.done) DETLSH_CUDA(cudaEventCreateWithFlags(&X.done, cudaEventDisableTiming));
     else if (!capturing) DETLSH_CUDA(cudaStreamWaitEvent(s, X.done, 0));
-    if (X.counters.size() < 4) {
-        grow_scratch(X.counters, 4);
-        DETLSH_CUDA(cudaMemsetAsync(X.counters.get(), 0, 16, s));  // incl. the sticky invariant flag
+    if (X.counters.size() < 8) {
+        grow_scratch(X.counters, 8);
+        DETLSH_CUDA(cudaMemsetAsync(X.counters.get(), 0, 32, s));  // incl. the sticky invariant flag
     }
     grow_scratch(X.slow_list, P.nq);
     // counters: slow-path and overflow counts reset per batch; the invariant flag is sticky
     DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntSlow, 0, 4, s));
     DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntOver, 0, 4, s));
+    DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntTaken, 0, 8, s));  // general-path claims + published count
     QueryPlan Pp = P;
     Pp.q_count = nullptr;
     if (profiling_enabled()) {
-        grow_scratch(X.phases, 8);
-        DETLSH_CUDA(cudaMemsetAsync(X.phases.get(), 0, 8 * sizeof(unsigned long long), s));
+        grow_scratch(X.phases, 16);
+        DETLSH_CUDA(cudaMemsetAsync(X.phases.get(), 0, 16 * sizeof(unsigned long long), s));
         Pp.phase_cycles = X.phases.get();
     }
     // locality-aware processing order for large batches (results are written
@@ -1839,7 +1977,31 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         Pp.order = flip ? ov1.get() : ov0.get();
     }
     const size_t items = 3 * static_cast<size_t>(P.max_leaves) * sizeof(LeafItem);
+    // memory the scratch may be sized against (no query under capture)
+    const size_t avail = capturing ? 0
+                                   : device_memory_available(device) + X.fast.size() + X.slow.size() +
+                                         (X.slow_bm.size() + X.tc_bm.size()) * sizeof(uint32_t);
     const bool fast_path = P.k <= kFastMaxK && !P.rc_mode;
+    // general path: the queries the fast path listed (count on the device), or
+    // every query (k beyond the fast path, rc_ann).  A fixed number of slots,
+    // each looping over the list; a slot's bitmap is cleared by the kernel.
+    const uint64_t n_list = P.nq;
+    const size_t slow_bytes = (items + 12 * P.budget + 255) / 256 * 256;
+    const uint64_t bm_words = ((P.n + 31) / 32 + 3) / 4 * 4;  // per-slot bitmap (n bits), kept zero
+    size_t gslots = std::min<size_t>(n_list, static_cast<size_t>(sms));
+    const size_t slow_lim = capturing ? std::max<size_t>(X.slow.size(), slow_bytes) : slow_scratch_limit(avail);
+    gslots = std::max<size_t>(1, std::min<size_t>(gslots, slow_lim / (slow_bytes + 4 * bm_words)));
+    if (std::getenv("DETLSH_DEBUG_QUERY"))
+        std::fprintf(stderr, "[query] general path: slots=%zu bytes/slot=%zu\n", gslots, slow_bytes);
+    grow_scratch(X.slow, gslots * slow_bytes);
+    if (X.slow_slots < gslots || X.slow_bm.size() < gslots * bm_words) {
+        if (capturing) throw InvalidArgument("ck_ann: the first batch of a shape cannot be captured (scratch grows)");
+        if (X.done) DETLSH_CUDA(cudaEventSynchronize(X.done));
+        X.slow_bm.release();
+        grow_scratch(X.slow_bm, gslots * bm_words);
+        DETLSH_CUDA(cudaMemsetAsync(X.slow_bm.get(), 0, gslots * bm_words * 4, s));
+        X.slow_slots = gslots;
+    }
     if (fast_path) {
         int per_sm = 0;
         DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast_kernel, kQueryThreads, smem));
@@ -1850,7 +2012,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         size_t slots = std::min<size_t>(P.nq, static_cast<size_t>(sms) * per_sm);
         // (under stream capture no memory query: the scratch an earlier,
         // uncaptured batch of this shape sized is what the slots get)
-        const size_t lim = capturing ? std::max<size_t>(X.fast.size(), fast_bytes) : fast_scratch_limit(device);
+        const size_t lim = capturing ? std::max<size_t>(X.fast.size(), fast_bytes) : fast_scratch_limit(avail);
         slots = std::max<size_t>(1, std::min<size_t>(slots, lim / fast_bytes));
         grow_scratch(X.fast, slots * fast_bytes);
         auto launch_fast = [&](const QueryPlan& Pc) {
@@ -1878,9 +2040,20 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 tc_cap = static_cast<uint32_t>(std::max(1L, std::min<long>(std::atol(e), fin_cap)));
             // per processing slot: row bitmap (n/8 bytes), survivors (8 B each),
             // pass records (128 KB); a chunk stays under ~3 GB
-            uint64_t chunk = (3ULL << 30) / (W * 4 + 8ULL * fin_cap + 128 * 1024);
-            chunk = std::max<uint64_t>(256, chunk / 256 * 256);
-            chunk = std::min<uint64_t>(chunk, (P.nq + 255) / 256 * 256);
+            // pass records (128 KB); a chunk stays under ~3 GB, or up to an
+            // eighth of the memory (12 GB) when the bitmaps are large
+            const uint64_t per_q = W * 4 + 8ULL * fin_cap + 128 * 1024;
+            const uint64_t chunk_bytes =
+                capturing ? (3ULL << 30)
+                          : std::max<uint64_t>(3ULL << 30, std::min<uint64_t>(12ULL << 30, avail / 8));
+            uint64_t chunk = chunk_bytes / per_q;
+            if (chunk >= P.nq) {
+                chunk = (P.nq + 255) / 256 * 256;
+            } else if (chunk >= slots) {
+                chunk = chunk / slots * slots;  // whole rounds of the plan kernel's CTAs (no tail round)
+            } else {
+                chunk = std::max<uint64_t>(256, chunk / 256 * 256);
+            }
             // pass records staged per chunk: ~8192 per query, plus the runs of
             // kTcRecChunk slots the scorer's warps reserve ahead of use
             uint64_t rec_cap = chunk * 2ULL * fin_cap + static_cast<uint64_t>(sms) * kTcRecReserve;
@@ -1944,6 +2117,20 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 else
                     launch_tc_finish(a, P.perm0, P.k, P.r_min, P.budget, P.ids, P.dists, P.n_hits, P.radius,
                                      P.cands, X.over_list.get(), X.counters.get() + kCntOver, s);
+                if (std::getenv("DETLSH_DEBUG_QUERY")) {  // survivor-count spread per chunk (syncs)
+                    std::vector<uint32_t> sc(m);
+                    uint32_t over = 0, slow = 0;
+                    DETLSH_CUDA(cudaMemcpyAsync(sc.data(), X.tc_surv_cnt.get(), m * 4, cudaMemcpyDeviceToHost, s));
+                    DETLSH_CUDA(cudaMemcpyAsync(&over, X.counters.get() + kCntOver, 4, cudaMemcpyDeviceToHost, s));
+                    DETLSH_CUDA(cudaMemcpyAsync(&slow, X.counters.get() + kCntSlow, 4, cudaMemcpyDeviceToHost, s));
+                    DETLSH_CUDA(cudaStreamSynchronize(s));
+                    std::sort(sc.begin(), sc.end());
+                    std::fprintf(stderr,
+                                 "[query] chunk %llu+%llu slots=%zu chunk=%llu tau_rows=%llu cap=%u surv p50=%u p90=%u "
+                                 "max=%u over_total=%u slow_total=%u\n",
+                                 (unsigned long long)c0, (unsigned long long)m, slots, (unsigned long long)chunk,
+                                 (unsigned long long)tau_rows, tc_cap, sc[m / 2], sc[m * 9 / 10], sc[m - 1], over, slow);
+                }
             }
             // gather path for the listed queries: the count stays on the device
             QueryPlan Pc = Pp;
@@ -1961,27 +2148,47 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             for (int i = 0; i < 8; ++i) g_phase[i] = static_cast<double>(ph[i]);
         }
     }
-    // general path: the queries the fast path listed (count on the device), or
-    // every query (k beyond the fast path, rc_ann).  A fixed number of slots,
-    // each looping over the list; a slot's bitmap is cleared by the kernel.
-    const uint64_t n_list = fast_path ? P.nq : P.nq;
-    const size_t slow_bytes = (items + 12 * P.budget + ((P.n + 31) / 32) * 4 + 255) / 256 * 256;
-    size_t slots = std::min<size_t>(n_list, static_cast<size_t>(sms));
-    slots = std::max<size_t>(1, std::min<size_t>(slots, slow_scratch_limit() / slow_bytes));
-    if (X.slow_slots < slots || X.slow.size() < slots * slow_bytes) {
-        if (capturing) throw InvalidArgument("ck_ann: the first batch of a shape cannot be captured (scratch grows)");
-        if (X.done) DETLSH_CUDA(cudaEventSynchronize(X.done));
-        X.slow.release();
-        grow_scratch(X.slow, slots * slow_bytes);
-        DETLSH_CUDA(cudaMemsetAsync(X.slow.get(), 0, slots * slow_bytes, s));
-        X.slow_slots = slots;
-    }
     {
-        ProfScope ps("query_slow", s);
-        query_slow_kernel<<<static_cast<unsigned>(slots), kQueryThreads, smem, s>>>(
-            P, fast_path ? X.slow_list.get() : nullptr, static_cast<uint32_t>(n_list),
-            fast_path ? X.counters.get() + kCntSlow : nullptr, X.slow.get(), slow_bytes);
-        DETLSH_LAUNCH_CHECK();
+        // deferred mode for large budgets (the member distances grid-wide);
+        // DETLSH_SLOW_DEFER_MIN sets the budget threshold (test hook)
+        uint64_t defer_min = kSlowDeferMinBudget;
+        if (const char* e = std::getenv("DETLSH_SLOW_DEFER_MIN")) defer_min = std::strtoull(e, nullptr, 10);
+        const bool defer = P.budget >= defer_min;
+        static_assert(sizeof(SlowRec) == 3 * sizeof(uint64_t), "SlowRec layout");
+        if (defer) grow_scratch(X.slow_rec, 3 * X.slow_slots);
+        SlowRec* recs = defer ? reinterpret_cast<SlowRec*>(X.slow_rec.get()) : nullptr;
+        QueryPlan Ps = P;
+        Ps.phase_cycles = profiling_enabled() ? X.phases.get() : nullptr;
+        {
+            ProfScope ps("query_slow", s);
+            query_slow_kernel<<<static_cast<unsigned>(gslots), kQueryThreads, smem, s>>>(
+                Ps, fast_path ? X.slow_list.get() : nullptr, static_cast<uint32_t>(n_list),
+                fast_path ? X.counters.get() + kCntSlow : nullptr, X.counters.get() + kCntTaken, X.slow.get(),
+                slow_bytes, X.slow_bm.get(), bm_words, recs);
+            DETLSH_LAUNCH_CHECK();
+        }
+        if (defer) {
+            {
+                ProfScope ps("query_slow_score", s);
+                const unsigned gx = static_cast<unsigned>(std::max<int>(1, 4 * sms));
+                slow_score_kernel<<<dim3(gx, static_cast<unsigned>(gslots)), 256, static_cast<size_t>(P.d) * 4, s>>>(
+                    P, recs, X.slow.get(), slow_bytes);
+                DETLSH_LAUNCH_CHECK();
+            }
+            ProfScope ps("query_slow_topk", s);
+            slow_topk_kernel<<<static_cast<unsigned>(gslots), kQueryThreads, smem, s>>>(P, recs, X.slow.get(),
+                                                                                    slow_bytes);
+            DETLSH_LAUNCH_CHECK();
+        }
+    }
+    if (profiling_enabled() && !capturing && std::getenv("DETLSH_DEBUG_QUERY")) {  // general-path phase split
+        unsigned long long ph[8];
+        DETLSH_CUDA(cudaMemcpyAsync(ph, X.phases.get() + 8, sizeof(ph), cudaMemcpyDeviceToHost, s));
+        DETLSH_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr,
+                     "[query] general path cycles: scan %llu select %llu emit %llu count %llu topk %llu | "
+                     "leaf items %llu rounds %llu members+queries %llu\n",
+                     ph[0], ph[1], ph[2], ph[3], ph[4], ph[5], ph[6], ph[7]);
     }
     if (!capturing) DETLSH_CUDA(cudaEventRecord(X.done, s));
 }

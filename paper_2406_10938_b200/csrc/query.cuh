@@ -84,8 +84,10 @@ constexpr int kFastMaxK = 1024;  // k handled by the fast path (larger k: genera
 // owned by the caller-provided QueryScratch (grown on demand).
 struct QueryScratch {
     DevBuf<uint8_t> fast;  // per-CTA leaf item lists + candidate positions
-    DevBuf<uint8_t> slow;  // per-slot bitmap + members
+    DevBuf<uint8_t> slow;  // per-slot leaf items + members
+    DevBuf<uint32_t> slow_bm;  // per-slot n-bit member bitmaps (zero between queries)
     DevBuf<uint32_t> slow_list;
+    DevBuf<uint64_t> slow_rec;  // [slots] deferred general-path queries (SlowRec)
     DevBuf<uint32_t> counters;
     DevBuf<unsigned long long> phases;  // [6] fast-path phase cycles (profiling only)
     size_t fast_slots = 0, slow_slots = 0;
@@ -166,7 +168,7 @@ void launch_tc_finish(const TcScoreArgs& a, const uint32_t* perm0, int k, double
                       uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, cudaStream_t s);
 // counters[] of QueryScratch: [0] slow-path queries, [1] sticky internal-invariant
 // flag, [2] tensor-core overflow queries, [3] tc_score work counter
-constexpr int kCntSlow = 0, kCntInvariant = 1, kCntOver = 2, kCntWork = 3;
+constexpr int kCntSlow = 0, kCntInvariant = 1, kCntOver = 2, kCntWork = 3, kCntTaken = 4;
 
 // tcgen05 kind::i8 self-test (tc_score.cu): C[128][N] = A[128][K] . B[N][K]^T.
 void tc_gemm_u8_test(const uint8_t* hA, const uint8_t* hB, int N, int K, int32_t* hC);

@@ -106,3 +106,56 @@ def test_device_mode_is_stream_ordered_and_capturable(gpu, u8_index):
         graph.replay()
         torch.cuda.synchronize()
         same(o3)
+
+
+def _same(got, want):
+    assert np.array_equal(got.n_hits, want.n_hits)
+    assert np.array_equal(got.ids, want.ids)
+    assert np.array_equal(got.dists.view(np.uint64), want.dists.view(np.uint64))
+    assert np.array_equal(got.radius_used, want.radius_used)
+    assert np.array_equal(got.candidates_seen, want.candidates_seen)
+
+
+@pytest.mark.parametrize("k", [20, 1100])
+def test_deferred_general_path(gpu, u8_index, monkeypatch, k):
+    """With a large budget the general path defers the member distances to a
+    grid-wide kernel and the top-k to one CTA per query (C5).  Forced here on
+    a small index (DETLSH_SLOW_DEFER_MIN=0): far queries that need several
+    rounds (count_within scored in the kernel) and, with k above the fast
+    path's bound, a whole batch on the general path.  Results must equal the
+    in-kernel general path bit for bit."""
+    data, idx, g = u8_index
+    d = data.shape[1]
+    Q = np.concatenate([_far_queries(g, 24, d), _sparse_u8(g, 40, d)])
+    monkeypatch.setenv("DETLSH_SLOW_DEFER_MIN", str(2**62))
+    want = gpu.ck_ann_batch(idx, Q, k)
+    assert (want.radius_used > idx.params.r_min).sum() >= 20, "multi-round general path not exercised"
+    monkeypatch.setenv("DETLSH_SLOW_DEFER_MIN", "0")
+    _same(gpu.ck_ann_batch(idx, Q, k), want)
+
+
+def test_deferred_general_path_rc_ann(gpu, u8_index, monkeypatch):
+    """rc_ann (a single pass; the c*r check on the k-th member) through the
+    deferred general path equals the in-kernel one."""
+    data, idx, g = u8_index
+    d = data.shape[1]
+    Q = np.concatenate([_far_queries(g, 8, d), _sparse_u8(g, 40, d)])
+    r = idx.params.r_min
+    monkeypatch.setenv("DETLSH_SLOW_DEFER_MIN", str(2**62))
+    want = gpu.rc_ann_batch(idx, Q, r, 1.5)
+    monkeypatch.setenv("DETLSH_SLOW_DEFER_MIN", "0")
+    got = gpu.rc_ann_batch(idx, Q, r, 1.5)
+    for a, b in zip(got, want):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+def test_general_path_after_budget_change(gpu, u8_index):
+    """The budget (beta*n + k) lays out the general path's per-slot scratch; a
+    batch with another k must not read an earlier batch's members as bitmap
+    bits (the member bitmaps live apart and stay zero between queries)."""
+    data, idx, g = u8_index
+    d = data.shape[1]
+    Q = np.concatenate([_far_queries(g, 24, d), _sparse_u8(g, 40, d)])
+    first = gpu.ck_ann_batch(idx, Q, 600)
+    gpu.ck_ann_batch(idx, Q, 1100)  # every query on the general path, larger budget
+    _same(gpu.ck_ann_batch(idx, Q, 600), first)
