@@ -215,7 +215,7 @@ def recall_ratio(res_ids, res_d, n_hits, gt_ids, gt_d, k):
 
 def tc_tau_rows(k, budget):
     """Rows the plan kernel scores exactly for tau^2 (query.cu run_query_batch)."""
-    return max(512, 2 * k, -(-4 * k * budget // 4096))
+    return max(512, 2 * k, min(1 << 17, -(-4 * k * budget // 4096)))  # kTauRowsMax
 
 
 # algorithmic bytes per launch (DESIGN.md §5); kernels without a model get null
@@ -248,8 +248,9 @@ def ncu_traffic(kernel, units, cfg_key):
     try:
         with open(path) as f:
             table = json.load(f)
-        rec = table.get(kernel) or table[kernel + "_kernel"]
-        if rec.get("config") != cfg_key:
+        recs = table.get(kernel) or table[kernel + "_kernel"]  # {config: record}
+        rec = recs.get(cfg_key)
+        if rec is None:
             return None, None
         return rec["dram_bytes_per_unit"] * units, rec["source"]
     except Exception:

@@ -56,6 +56,7 @@ def main(rep, pattern, units, out_txt, config=None):
         summary[short] = {"dram_bytes": dram, "duration_ms": rec.get("gpu__time_duration.sum"),
                           "dram_bytes_per_unit": dram / float(units),
                           "source": os.path.basename(out_txt), "config": config}
+    # records are kept per (kernel, workload): {kernel: {config: record}}
     with open(out_txt, "w") as f:
         f.write(f"# ncu summary of {os.path.basename(rep)} (units per launch = {units})\n")
         f.write("\n".join(lines) + "\n")
@@ -63,7 +64,8 @@ def main(rep, pattern, units, out_txt, config=None):
     cur = {}
     if os.path.exists(latest):
         cur = json.load(open(latest))
-    cur.update(summary)
+    for kname, rec in summary.items():
+        cur.setdefault(kname, {})[str(rec["config"])] = rec
     json.dump(cur, open(latest, "w"), indent=1)
     print("\n".join(lines))
 
