@@ -342,6 +342,33 @@ __device__ __forceinline__ double l2_exact(const float* q, const float* x, int d
     return __dsqrt_rn(l2sq_exact(q, x, d));
 }
 
+// The same distance when the row and the query hold integers in [0, 255]
+// (a u8 index and a u8-exact query): every partial sum of l2sq_exact is then
+// an integer below 2^53, so integer arithmetic in any order gives the same
+// double.  No dependent fp64 chain: ~10x the rows per SM.
+__device__ __forceinline__ double l2_exact_u8(const float* __restrict__ q, const float* __restrict__ x, int d) {
+    unsigned long long acc = 0;
+    if ((d & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+#pragma unroll 8
+        for (int t = 0; t < d / 4; ++t) {
+            const float4 xv = __ldg(x4 + t);
+            const float* qq = q + 4 * t;
+            const int a = static_cast<int>(qq[0]) - static_cast<int>(xv.x);
+            const int b = static_cast<int>(qq[1]) - static_cast<int>(xv.y);
+            const int c = static_cast<int>(qq[2]) - static_cast<int>(xv.z);
+            const int e = static_cast<int>(qq[3]) - static_cast<int>(xv.w);
+            acc += static_cast<unsigned>(a * a + b * b + c * c + e * e);
+        }
+    } else {
+        for (int t = 0; t < d; ++t) {
+            const int a = static_cast<int>(q[t]) - static_cast<int>(__ldg(x + t));
+            acc += static_cast<unsigned>(a * a);
+        }
+    }
+    return __dsqrt_rn(static_cast<double>(acc));
+}
+
 // Warp-aggregated append of `item` to list (counter in smem).
 __device__ __forceinline__ void warp_append(bool ok, const LeafItem& it, LeafItem* list,
                                             uint32_t* counter, uint32_t cap = 0xffffffffu) {
@@ -858,8 +885,8 @@ __device__ uint32_t emit_rows(const uint32_t* list, uint32_t n, const QTree& T0,
     if (threadIdx.x == 0) S.u32s[3] = 0;
     __syncthreads();
     uint32_t* st_dst = S.tl;  // the top-k staging area is free outside verification
-    uint32_t* st_src = S.tl + kQueryThreads;
-    uint32_t* st_take = S.tl + 2 * kQueryThreads;
+    uint32_t* st_src = S.tl + blockDim.x;  // (3 x blockDim.x <= kTopCap)
+    uint32_t* st_take = S.tl + 2 * blockDim.x;
     for (uint32_t base = 0; base < n; base += blockDim.x) {
         const uint32_t i = base + threadIdx.x;
         uint32_t take = 0, src = 0;
@@ -877,7 +904,7 @@ __device__ uint32_t emit_rows(const uint32_t* list, uint32_t n, const QTree& T0,
         if (lane == 31) wt[warp] = incl;
         __syncthreads();
         uint32_t wpre = 0, tot = 0;
-        for (int w = 0; w < kQueryThreads / 32; ++w) {
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
             if (w < warp) wpre += wt[w];
             tot += wt[w];
         }
@@ -1031,9 +1058,10 @@ __device__ int32_t kth_dist2_f32up(const QueryPlan& P, const FastSlot& F, const 
 // and gains from more CTAs), 3 for fp32 rows (the 32-float row chunks in
 // flight need the registers; at 48 registers they spill)
 // F32TC: the float bf16x3 hand-off is compiled only into its own instance, so
-// the u8 instance keeps its register budget
-template <int MINB, bool F32TC>
-__global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
+// the u8 instance keeps its register budget.  NT: threads per CTA (512 for
+// indexes with ~10^6 leaves per tree, whose slots are few: memory-bound)
+template <int MINB, bool F32TC, int NT = kQueryThreads>
+__global__ void __launch_bounds__(NT, MINB) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const Smem S = carve(smem_raw, P.K, P.NR, P.d, P.row_u8);
@@ -1112,8 +1140,10 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
             // monotone in mindist; the per-leaf key is kept for pass 2
             {
                 unsigned long long wsum = 0;
+                uint32_t nin = 0;  // (profiling) leaves not certainly outside
                 auto record = [&](uint32_t li, uint32_t b, uint32_t cnt) {
                     if (b != 0xffffu) {
+                        ++nin;
                         wsum += cnt;
                         atomicAdd(&S.bins[approx ? b >> 5 : b], cnt);
                     }
@@ -1162,6 +1192,11 @@ __global__ void __launch_bounds__(kQueryThreads, MINB) query_fast_kernel(
                 }
                 for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
                 if (lane == 0 && wsum) atomicAdd(&S.u64s[0], wsum);
+                if (P.phase_cycles) {
+                    for (int o = 16; o; o >>= 1) nin += __shfl_xor_sync(0xffffffffu, nin, o);
+                    if (lane == 0) atomicAdd(P.phase_cycles + 16, static_cast<unsigned long long>(nin));
+                    if (threadIdx.x == 0) atomicAdd(P.phase_cycles + 17, static_cast<unsigned long long>(nl));
+                }
             }
             __syncthreads();
             const uint64_t W = S.u64s[0];  // approximate round: an upper bound
@@ -1529,7 +1564,7 @@ __device__ __forceinline__ SlowSlot slow_slot(uint8_t* base, size_t slot_bytes, 
 // new ones of the cut leaf) into the member list.
 __device__ void emit_members(const QueryPlan& P, int tree, const LeafItem* A, uint32_t nA,
                              bool select, uint64_t kmdb, uint32_t kid, uint64_t take_cut,
-                             const SlowSlot& L, const Smem& S, bool score) {
+                             const SlowSlot& L, const Smem& S, bool score, bool u8q) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const QTree T = P.trees[tree];
     for (uint32_t i = warp; i < nA; i += blockDim.x / 32) {
@@ -1563,7 +1598,10 @@ __device__ void emit_members(const QueryPlan& P, int tree, const LeafItem* A, ui
                     atomicOr(&L.bitmap[pos >> 5], 1u << (pos & 31));
                     const uint32_t slot = slot0 + __popc(tm & ((1u << lane) - 1u));
                     L.mpos[slot] = pos;
-                    if (score) L.mdist[slot] = l2_exact(S.qv, P.data + static_cast<uint64_t>(pos) * P.d, P.d);
+                    if (score) {
+                        const float* x = P.data + static_cast<uint64_t>(pos) * P.d;
+                        L.mdist[slot] = u8q ? l2_exact_u8(S.qv, x, P.d) : l2_exact(S.qv, x, P.d);
+                    }
                 }
             }
             emitted += __popc(tm);
@@ -1620,9 +1658,12 @@ __device__ void slow_finish(const QueryPlan& P, const Smem& S, const SlowSlot& L
 }
 
 // Exact distances of members [from, msz) by the whole block.
-__device__ void score_members(const QueryPlan& P, const float* qv, const SlowSlot& L, uint32_t from, uint32_t msz) {
-    for (uint32_t i = from + threadIdx.x; i < msz; i += blockDim.x)
-        L.mdist[i] = l2_exact(qv, P.data + static_cast<uint64_t>(L.mpos[i]) * P.d, P.d);
+__device__ void score_members(const QueryPlan& P, const float* qv, const SlowSlot& L, uint32_t from, uint32_t msz,
+                              bool u8q) {
+    for (uint32_t i = from + threadIdx.x; i < msz; i += blockDim.x) {
+        const float* x = P.data + static_cast<uint64_t>(L.mpos[i]) * P.d;
+        L.mdist[i] = u8q ? l2_exact_u8(qv, x, P.d) : l2_exact(qv, x, P.d);
+    }
     __syncthreads();
 }
 
@@ -1636,7 +1677,8 @@ __device__ void score_members(const QueryPlan& P, const float* qv, const SlowSlo
 // distances are computed grid-wide (slow_score_kernel) and the top-k by
 // slow_topk_kernel.  Distances a round's count_within needs are computed
 // here as before.
-__global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
+template <int NT>
+__global__ void __launch_bounds__(NT) query_slow_kernel(
     QueryPlan P, const uint32_t* list, uint32_t count, const uint32_t* count_dev, uint32_t* taken,
     uint8_t* scratch, size_t slot_bytes, uint32_t* bitmaps, uint64_t bm_words, SlowRec* recs) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1674,7 +1716,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
         const uint64_t q = list ? list[qi] : qi;
         if (threadIdx.x == 0) S.u32s[7] = 0;  // |S|
         __syncthreads();
-        load_query_vec(P, q, S);
+        const bool u8q = load_query_vec(P, q, S);  // u8 index and u8-exact query: integer distances
         double r = P.r_min;
         bool done = false;
         uint32_t scored = 0;  // members [0, scored) have distances
@@ -1694,10 +1736,10 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
                     uint32_t kid;
                     weighted_select(L.A, nA, need, L.B, L.C, S, kmdb, kid, take_cut);
                     phase(1);
-                    emit_members(P, tree, L.A, nA, true, kmdb, kid, take_cut, L, S, !defer);
+                    emit_members(P, tree, L.A, nA, true, kmdb, kid, take_cut, L, S, !defer, u8q);
                     done = true;
                 } else {
-                    emit_members(P, tree, L.A, nA, false, 0, 0, 0, L, S, !defer);
+                    emit_members(P, tree, L.A, nA, false, 0, 0, 0, L, S, !defer, u8q);
                 }
                 if (!defer) scored = S.u32s[7];
                 phase(2);
@@ -1707,7 +1749,7 @@ __global__ void __launch_bounds__(kQueryThreads) query_slow_kernel(
             // count_within(c * r) (index.cpp:244-249, 328)
             const double lim = __dmul_rn(P.c, r);
             const uint32_t msz = S.u32s[7];
-            if (scored < msz) score_members(P, S.qv, L, scored, msz);
+            if (scored < msz) score_members(P, S.qv, L, scored, msz, u8q);
             scored = msz;
             uint32_t mine = 0;
             for (uint32_t i = threadIdx.x; i < msz; i += blockDim.x) mine += L.mdist[i] <= lim ? 1u : 0u;
@@ -1753,11 +1795,57 @@ __global__ void __launch_bounds__(256) slow_score_kernel(QueryPlan P, const Slow
     const SlowRec rc = recs[blockIdx.y];
     if (rc.q == kNoQuery || rc.scored >= rc.msz) return;
     float* qv = reinterpret_cast<float*>(smem_raw);
-    for (int t = threadIdx.x; t < P.d; t += blockDim.x) qv[t] = P.q[static_cast<uint64_t>(rc.q) * P.d + t];
+    __shared__ int s_nonint;
+    if (threadIdx.x == 0) s_nonint = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < P.d; t += blockDim.x) {
+        const float v = P.q[static_cast<uint64_t>(rc.q) * P.d + t];
+        qv[t] = v;
+        if (!(v >= 0.0f && v <= 255.0f && v == floorf(v))) s_nonint = 1;
+    }
     __syncthreads();
     const SlowSlot L = slow_slot(scratch, slot_bytes, P.max_leaves, P.budget, blockIdx.y);
     const uint32_t stride = gridDim.x * blockDim.x;
     uint32_t i = rc.scored + blockIdx.x * blockDim.x + threadIdx.x;
+    if (P.data_u8 && !s_nonint) {
+        // u8 index, u8-exact query: integer sums (the same doubles), so a warp
+        // reads a member's row as whole 128-byte lines and reduces across
+        // lanes; four rows in flight per warp
+        const int lane = threadIdx.x & 31;
+        const uint32_t wstride = gridDim.x * (blockDim.x / 32);
+        const int d4 = (P.d & 3) == 0 ? P.d / 4 : 0;
+        for (uint32_t j = rc.scored + (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * 4; j < rc.msz;
+             j += wstride * 4) {
+            unsigned acc[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (j + u >= rc.msz) break;
+                const float* x = P.data + static_cast<uint64_t>(L.mpos[j + u]) * P.d;
+                if (d4) {
+                    for (int t = lane; t < d4; t += 32) {
+                        const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + t);
+                        const int a = static_cast<int>(qv[4 * t]) - static_cast<int>(xv.x);
+                        const int b = static_cast<int>(qv[4 * t + 1]) - static_cast<int>(xv.y);
+                        const int c = static_cast<int>(qv[4 * t + 2]) - static_cast<int>(xv.z);
+                        const int e = static_cast<int>(qv[4 * t + 3]) - static_cast<int>(xv.w);
+                        acc[u] += static_cast<unsigned>(a * a + b * b + c * c + e * e);
+                    }
+                } else {
+                    for (int t = lane; t < P.d; t += 32) {
+                        const int a = static_cast<int>(qv[t]) - static_cast<int>(__ldg(x + t));
+                        acc[u] += static_cast<unsigned>(a * a);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                unsigned long long v = acc[u];
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == u && j + u < rc.msz) L.mdist[j + u] = __dsqrt_rn(static_cast<double>(v));
+            }
+        }
+        return;
+    }
     // two members in flight per thread (independent fp64 chains)
     for (; i + stride < rc.msz; i += 2 * stride) {
         const double a = l2_exact(qv, P.data + static_cast<uint64_t>(L.mpos[i]) * P.d, P.d);
@@ -1769,7 +1857,8 @@ __global__ void __launch_bounds__(256) slow_score_kernel(QueryPlan P, const Slow
 }
 
 // Deferred queries' top-k and outputs: one CTA per slot.
-__global__ void __launch_bounds__(kQueryThreads) slow_topk_kernel(QueryPlan P, const SlowRec* recs, uint8_t* scratch,
+template <int NT>
+__global__ void __launch_bounds__(NT) slow_topk_kernel(QueryPlan P, const SlowRec* recs, uint8_t* scratch,
                                                                  size_t slot_bytes) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     const SlowRec rc = recs[blockIdx.x];
@@ -1913,11 +2002,25 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // DETLSH_FAST_MINB=3|5 overrides (measurement hook).
     const char* minb_env = std::getenv("DETLSH_FAST_MINB");
     const bool five = minb_env ? std::atoi(minb_env) == 5 : tc_u8;  // (float tau rows: fp64 chains, 3/SM)
+    // Indexes with ~10^6 leaves per tree (C5): a slot's scratch is ~100 MB,
+    // so memory, not occupancy, bounds the CTAs in flight; 512 threads per CTA
+    // halve each query's scan.  DETLSH_FAST_THREADS=256|512 overrides.
+    const char* nt_env = std::getenv("DETLSH_FAST_THREADS");
+    const bool wide = nt_env ? std::atoi(nt_env) == 512 : (tc_u8 && P.max_leaves >= (1u << 19));
+    const int fast_nt = wide && !tc_f32 ? 512 : kQueryThreads;
     auto* const fast_kernel = tc_f32 ? &query_fast_kernel<3, true>
+                              : fast_nt == 512 ? &query_fast_kernel<2, false, 512>
                               : five ? &query_fast_kernel<5, false> : &query_fast_kernel<3, false>;
     DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    DETLSH_CUDA(cudaFuncSetAttribute(query_slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    DETLSH_CUDA(cudaFuncSetAttribute(slow_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    // general path: 1024 threads per query for large budgets (few slots, each
+    // query's scans and member lists ~10^6-10^7 long), 256 otherwise
+    const char* snt_env = std::getenv("DETLSH_SLOW_THREADS");  // 256|1024 (test hook)
+    const bool slow_wide = snt_env ? std::atoi(snt_env) == 1024 : P.budget >= kSlowDeferMinBudget;
+    const int slow_nt = slow_wide ? 1024 : kQueryThreads;
+    auto* const slow_kernel = slow_wide ? &query_slow_kernel<1024> : &query_slow_kernel<kQueryThreads>;
+    auto* const slow_topk = slow_wide ? &slow_topk_kernel<1024> : &slow_topk_kernel<kQueryThreads>;
+    DETLSH_CUDA(cudaFuncSetAttribute(slow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    DETLSH_CUDA(cudaFuncSetAttribute(slow_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // Persistent scratch lives on the index's own stream (it outlives any
     // caller stream).  Growing it is the one host wait of a batch, and only
     // happens when a batch needs more scratch than every earlier one.
@@ -1953,8 +2056,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     QueryPlan Pp = P;
     Pp.q_count = nullptr;
     if (profiling_enabled()) {
-        grow_scratch(X.phases, 16);
-        DETLSH_CUDA(cudaMemsetAsync(X.phases.get(), 0, 16 * sizeof(unsigned long long), s));
+        grow_scratch(X.phases, 24);
+        DETLSH_CUDA(cudaMemsetAsync(X.phases.get(), 0, 24 * sizeof(unsigned long long), s));
         Pp.phase_cycles = X.phases.get();
     }
     // locality-aware processing order for large batches (results are written
@@ -2004,7 +2107,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     }
     if (fast_path) {
         int per_sm = 0;
-        DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast_kernel, kQueryThreads, smem));
+        DETLSH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast_kernel, fast_nt, smem));
         per_sm = std::max(1, std::min(per_sm, 6));
         const size_t fast_bytes = fast_slot_bytes(P.max_leaves, P.budget);
         // processing slots: a CTA each, bounded by the scratch they need
@@ -2019,7 +2122,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             const uint64_t m = Pc.q_end - Pc.q_begin;
             if (m == 0) return;
             ProfScope ps("query_fast", s);
-            fast_kernel<<<static_cast<unsigned>(std::min<uint64_t>(slots, m)), kQueryThreads, smem, s>>>(
+            fast_kernel<<<static_cast<unsigned>(std::min<uint64_t>(slots, m)), fast_nt, smem, s>>>(
                 Pc, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
             DETLSH_LAUNCH_CHECK();
         };
@@ -2161,7 +2264,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         Ps.phase_cycles = profiling_enabled() ? X.phases.get() : nullptr;
         {
             ProfScope ps("query_slow", s);
-            query_slow_kernel<<<static_cast<unsigned>(gslots), kQueryThreads, smem, s>>>(
+            slow_kernel<<<static_cast<unsigned>(gslots), slow_nt, smem, s>>>(
                 Ps, fast_path ? X.slow_list.get() : nullptr, static_cast<uint32_t>(n_list),
                 fast_path ? X.counters.get() + kCntSlow : nullptr, X.counters.get() + kCntTaken, X.slow.get(),
                 slow_bytes, X.slow_bm.get(), bm_words, recs);
@@ -2176,15 +2279,16 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 DETLSH_LAUNCH_CHECK();
             }
             ProfScope ps("query_slow_topk", s);
-            slow_topk_kernel<<<static_cast<unsigned>(gslots), kQueryThreads, smem, s>>>(P, recs, X.slow.get(),
+            slow_topk<<<static_cast<unsigned>(gslots), slow_nt, smem, s>>>(P, recs, X.slow.get(),
                                                                                     slow_bytes);
             DETLSH_LAUNCH_CHECK();
         }
     }
     if (profiling_enabled() && !capturing && std::getenv("DETLSH_DEBUG_QUERY")) {  // general-path phase split
-        unsigned long long ph[8];
+        unsigned long long ph[10];
         DETLSH_CUDA(cudaMemcpyAsync(ph, X.phases.get() + 8, sizeof(ph), cudaMemcpyDeviceToHost, s));
         DETLSH_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[query] fast-path leaf scan: %llu of %llu leaves not certainly outside\n", ph[8], ph[9]);
         std::fprintf(stderr,
                      "[query] general path cycles: scan %llu select %llu emit %llu count %llu topk %llu | "
                      "leaf items %llu rounds %llu members+queries %llu\n",

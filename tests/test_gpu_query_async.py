@@ -159,3 +159,45 @@ def test_general_path_after_budget_change(gpu, u8_index):
     first = gpu.ck_ann_batch(idx, Q, 600)
     gpu.ck_ann_batch(idx, Q, 1100)  # every query on the general path, larger budget
     _same(gpu.ck_ann_batch(idx, Q, 600), first)
+
+
+@pytest.mark.parametrize("defer", [False, True])
+def test_wide_ctas_equal(gpu, u8_index, monkeypatch, defer):
+    """The C5 shapes (512-thread plan CTAs, 1024-thread general-path CTAs,
+    chosen by index size) forced on a small index give the same results as
+    the default 256-thread CTAs, with and without deferred member scoring."""
+    data, idx, g = u8_index
+    d = data.shape[1]
+    Q = np.concatenate([_far_queries(g, 20, d), _sparse_u8(g, 300, d)])
+    monkeypatch.setenv("DETLSH_SLOW_DEFER_MIN", "0" if defer else str(2**62))
+    want = gpu.ck_ann_batch(idx, Q, 20)
+    monkeypatch.setenv("DETLSH_FAST_THREADS", "512")
+    monkeypatch.setenv("DETLSH_SLOW_THREADS", "1024")
+    _same(gpu.ck_ann_batch(idx, Q, 20), want)
+    _same(gpu.ck_ann_batch(idx, Q, 1100), gpu.ck_ann_batch(idx, Q, 1100, tensor_cores=False))
+
+
+@pytest.mark.parametrize("defer", [False, True])
+def test_general_path_u8_matches_oracle(gpu, port, monkeypatch, defer):
+    """u8 index and u8-exact queries on the general path (integer member
+    distances, in the kernel or deferred) equal the oracle bit for bit,
+    including far queries that need several rounds."""
+    from oracle.bindings import make_params
+    g = np.random.Generator(np.random.PCG64(91))
+    n, d, k = 20000, 64, 20
+    data = _sparse_u8(g, n, d)
+    idx = gpu.build_index(data, gpu.LshParams(beta=0.2, k=k), seed=5)
+    oi = port.build_index(data, make_params(beta=0.2, k=k), 5)
+    Q = np.concatenate([_far_queries(g, 12, d), _sparse_u8(g, 12, d)])
+    monkeypatch.setenv("DETLSH_SLOW_DEFER_MIN", "0" if defer else str(2**62))
+    monkeypatch.setenv("DETLSH_SLOW_THREADS", "1024" if defer else "256")
+    res = gpu.ck_ann_batch(idx, Q, k)
+    assert (res.radius_used > idx.params.r_min).sum() >= 10
+    for qi in range(Q.shape[0]):
+        ids, ds, rad, cs = oi.ck_ann(Q[qi], k)
+        m = int(res.n_hits[qi])
+        assert m == len(ids)
+        assert np.array_equal(res.ids[qi, :m], ids), f"query {qi} ids"
+        assert np.array_equal(res.dists[qi, :m].view(np.uint64), np.asarray(ds).view(np.uint64)), f"query {qi}"
+        assert res.radius_used[qi] == rad
+        assert int(res.candidates_seen[qi]) == cs
