@@ -388,7 +388,7 @@ __device__ __forceinline__ void warp_append(bool ok, const LeafItem& it, LeafIte
 // Each appended item also records its histogram bin floor(md * kBins / radius)
 // (monotone in md) in `pad`, and its weight is added to S.bins.
 __device__ void scan_leaves(const QueryPlan& P, int tree, double radius, const Smem& S,
-                            LeafItem* A, const uint32_t* bitmap, uint32_t& nA, uint64_t& W) {
+                            LeafItem* A, const uint32_t* bitmap, uint32_t& nA, uint64_t& W, LeafItem* tmp) {
     const QTree T = P.trees[tree];
     if (threadIdx.x == 0) {
         S.u32s[0] = 0;
@@ -399,6 +399,12 @@ __device__ void scan_leaves(const QueryPlan& P, int tree, double radius, const S
     __syncthreads();
     unsigned long long wsum = 0;
     const uint32_t nl = T.num_leaves;
+    auto add_weight = [&](const LeafItem& it) {
+        wsum += it.w;
+        atomicAdd(&S.bins[it.pad], it.w);
+    };
+    // pass A: every leaf's exact mindist; leaves within the radius are listed
+    // (weight = leaf size; with a bitmap, corrected in pass B)
     for (uint32_t base = 0; base < nl; base += blockDim.x) {
         const uint32_t li = base + threadIdx.x;
         bool ok = false;
@@ -406,16 +412,7 @@ __device__ void scan_leaves(const QueryPlan& P, int tree, double radius, const S
         if (li < nl) {
             const double md = leaf_mindist(P, T, li, S);
             if (md <= radius) {
-                uint32_t w = T.leaf_count[li];
-                if (bitmap) {
-                    const uint32_t b0 = T.leaf_begin[li];
-                    uint32_t nw = 0;
-                    for (uint32_t e = 0; e < w; ++e) {
-                        const uint32_t pos = T.perm[b0 + e];
-                        nw += ((bitmap[pos >> 5] >> (pos & 31)) & 1u) ? 0u : 1u;
-                    }
-                    w = nw;
-                }
+                const uint32_t w = T.leaf_count[li];
                 if (w > 0) {
                     ok = true;
                     it.mdb = static_cast<uint64_t>(__double_as_longlong(md));
@@ -424,12 +421,44 @@ __device__ void scan_leaves(const QueryPlan& P, int tree, double radius, const S
                     it.li = li;
                     const double fb = __dmul_rn(md, scale);
                     it.pad = fb >= static_cast<double>(kBins - 1) ? kBins - 1 : static_cast<uint32_t>(fb);
-                    wsum += w;
-                    atomicAdd(&S.bins[it.pad], w);
+                    if (!bitmap) add_weight(it);
                 }
             }
         }
-        warp_append(ok, it, A, &S.u32s[0]);
+        warp_append(ok, it, bitmap ? tmp : A, &S.u32s[0]);
+    }
+    if (bitmap) {
+        // pass B: each listed leaf's entries not yet in S, one leaf per thread
+        // with every lane busy and eight rows' loads in flight.  (C5: ~4x10^7
+        // random bitmap reads per query and tree, bound by one SM's L1 request
+        // rate: ~75% of the general path's scan time.)
+        __syncthreads();
+        const uint32_t n0 = S.u32s[0];
+        __syncthreads();
+        if (threadIdx.x == 0) S.u32s[0] = 0;
+        __syncthreads();
+        for (uint32_t base = 0; base < n0; base += blockDim.x) {
+            const uint32_t i = base + threadIdx.x;
+            bool ok = false;
+            LeafItem it;
+            if (i < n0) {
+                it = tmp[i];
+                const uint32_t b0 = T.leaf_begin[it.li], w = it.w;
+                uint32_t nw = 0;
+                for (uint32_t e0 = 0; e0 < w; e0 += 8) {
+                    uint32_t pos[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) pos[u] = e0 + u < w ? __ldg(T.perm + b0 + e0 + u) : 0xffffffffu;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (pos[u] != 0xffffffffu) nw += ((bitmap[pos[u] >> 5] >> (pos[u] & 31)) & 1u) ? 0u : 1u;
+                }
+                it.w = nw;
+                ok = nw > 0;
+                if (ok) add_weight(it);
+            }
+            warp_append(ok, it, A, &S.u32s[0]);
+        }
     }
     for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
     if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(&S.u64s[0], wsum);
@@ -1728,7 +1757,7 @@ __global__ void __launch_bounds__(NT) query_slow_kernel(
                 const uint32_t have = S.u32s[7];
                 uint32_t nA;
                 uint64_t W;
-                scan_leaves(P, tree, radius, S, L.A, have ? L.bitmap : nullptr, nA, W);
+                scan_leaves(P, tree, radius, S, L.A, have ? L.bitmap : nullptr, nA, W, L.C);
                 phase(0);
                 const uint64_t need = P.budget - have;
                 if (W >= need) {
