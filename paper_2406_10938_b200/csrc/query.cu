@@ -2173,19 +2173,16 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             // per processing slot: row bitmap (n/8 bytes), survivors (8 B each),
             // pass records (128 KB); a chunk stays under ~3 GB
             // pass records (128 KB); a chunk stays under ~3 GB, or up to an
-            // eighth of the memory (12 GB) when the bitmaps are large
+            // eighth of the memory (16 GB) when the bitmaps are large.  Whole
+            // 256-query tiles of tc_score (C5: 1024 queries per chunk, 3.8
+            // rounds of the plan kernel's 271 CTAs; 813 = 3 whole rounds left
+            // a 45-query tile per chunk)
             const uint64_t per_q = W * 4 + 8ULL * fin_cap + 128 * 1024;
             const uint64_t chunk_bytes =
                 capturing ? (3ULL << 30)
-                          : std::max<uint64_t>(3ULL << 30, std::min<uint64_t>(12ULL << 30, avail / 8));
+                          : std::max<uint64_t>(3ULL << 30, std::min<uint64_t>(16ULL << 30, avail / 8));
             uint64_t chunk = chunk_bytes / per_q;
-            if (chunk >= P.nq) {
-                chunk = (P.nq + 255) / 256 * 256;
-            } else if (chunk >= slots) {
-                chunk = chunk / slots * slots;  // whole rounds of the plan kernel's CTAs (no tail round)
-            } else {
-                chunk = std::max<uint64_t>(256, chunk / 256 * 256);
-            }
+            chunk = chunk >= P.nq ? (P.nq + 255) / 256 * 256 : std::max<uint64_t>(256, chunk / 256 * 256);
             // pass records staged per chunk: ~8192 per query, plus the runs of
             // kTcRecChunk slots the scorer's warps reserve ahead of use
             uint64_t rec_cap = chunk * 2ULL * fin_cap + static_cast<uint64_t>(sms) * kTcRecReserve;
