@@ -175,18 +175,32 @@ __global__ void radix_upsweep(const KeyT* __restrict__ keys, size_t n, int shift
     hist[static_cast<size_t>(threadIdx.x) * num_tiles + blockIdx.x] = h[threadIdx.x];
 }
 
+// Stable downsweep: each 256-key round is ranked (warp match + per-warp digit
+// counts) into a shared-memory copy of the tile ordered by digit; the tile is
+// then written out in that order, so consecutive threads store consecutive
+// positions of a digit's run (coalesced) instead of one scattered key each.
 template <typename KeyT>
 __global__ void radix_downsweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                 KeyT* __restrict__ kout, uint32_t* __restrict__ vout, size_t n,
                                 int shift, const uint32_t* __restrict__ offsets,
-                                uint32_t num_tiles, int rounds) {
+                                const uint32_t* __restrict__ hist, uint32_t num_tiles, int rounds) {
+    extern __shared__ __align__(16) uint8_t radix_smem[];
+    KeyT* sk = reinterpret_cast<KeyT*>(radix_smem);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + static_cast<size_t>(rounds) * kRadixThreads);
     __shared__ uint32_t wh[kRadixThreads / 32][256];
-    __shared__ uint32_t running[256];
     __shared__ uint32_t gbase[256];
+    __shared__ uint32_t toff[256];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    running[tid] = 0;
+    {
+        uint32_t ex;
+        block_excl_scan(hist[static_cast<size_t>(tid) * num_tiles + blockIdx.x], ex);
+        toff[tid] = ex;  // this digit's first slot in the tile
+    }
     gbase[tid] = offsets[static_cast<size_t>(tid) * num_tiles + blockIdx.x];
+    uint32_t running = 0;  // keys of digit `tid` in the earlier rounds
     const size_t base = static_cast<size_t>(blockIdx.x) * kRadixThreads * rounds;
+    const size_t tile_cap = static_cast<size_t>(kRadixThreads) * rounds;
+    const uint32_t tile_n = static_cast<uint32_t>(n - base < tile_cap ? n - base : tile_cap);
     const uint32_t lt_mask = (1u << lane) - 1u;
     for (int r = 0; r < rounds; ++r) {
         const size_t idx = base + static_cast<size_t>(r) * kRadixThreads + tid;
@@ -208,22 +222,30 @@ __global__ void radix_downsweep(const KeyT* __restrict__ kin, const uint32_t* __
         if (valid && rank == 0) wh[warp][d] = __popc(peers);
         __syncthreads();
         {
-            uint32_t run = running[tid];
+            uint32_t run = toff[tid] + running;
 #pragma unroll
             for (int w = 0; w < kRadixThreads / 32; ++w) {
                 const uint32_t c = wh[w][tid];
                 wh[w][tid] = run;
                 run += c;
             }
-            running[tid] = run;
+            running = run - toff[tid];
         }
         __syncthreads();
         if (valid) {
-            const uint32_t pos = gbase[d] + wh[warp][d] + rank;
-            kout[pos] = key;
-            vout[pos] = val;
+            const uint32_t at = wh[warp][d] + rank;
+            sk[at] = key;
+            sv[at] = val;
         }
-        __syncthreads();
+        __syncthreads();  // wh is reset by the next round
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < tile_n; i += kRadixThreads) {
+        const KeyT key = sk[i];
+        const uint32_t d = static_cast<uint32_t>((key >> shift) & 0xff);
+        const size_t pos = static_cast<size_t>(gbase[d]) + (i - toff[d]);
+        kout[pos] = key;
+        vout[pos] = sv[i];
     }
 }
 
@@ -245,6 +267,10 @@ bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, 
     uint32_t* hist = tmp;
     uint32_t* offs = tmp + 256 * static_cast<size_t>(tiles);
     uint32_t* stmp = offs + 256 * static_cast<size_t>(tiles);
+    const size_t smem = tile * (sizeof(KeyT) + sizeof(uint32_t));  // the tile, digit-ordered
+    // (per device: set on every call, a host-side attribute write)
+    DETLSH_CUDA(cudaFuncSetAttribute(radix_downsweep<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kRadixThreads * kRadixMaxRounds * (sizeof(KeyT) + 4))));
     bool flipped = false;
     for (int bit = begin_bit; bit < end_bit; bit += 8) {
         KeyT* ki = flipped ? k1 : k0;
@@ -254,7 +280,7 @@ bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, 
         radix_upsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, n, bit, hist, tiles, rounds);
         DETLSH_LAUNCH_CHECK();
         exclusive_scan_u32(hist, offs, 256 * static_cast<size_t>(tiles), stmp, nullptr, s);
-        radix_downsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, vi, ko, vo, n, bit, offs, tiles, rounds);
+        radix_downsweep<KeyT><<<tiles, kRadixThreads, smem, s>>>(ki, vi, ko, vo, n, bit, offs, hist, tiles, rounds);
         DETLSH_LAUNCH_CHECK();
         flipped = !flipped;
     }
