@@ -161,8 +161,9 @@ int radix_rounds(size_t n) {
 
 template <typename KeyT>
 __global__ void radix_upsweep(const KeyT* __restrict__ keys, size_t n, int shift,
-                              uint32_t* __restrict__ hist, uint32_t num_tiles, int rounds) {
+                              uint32_t* __restrict__ hist, uint32_t num_tiles, int rounds, const uint32_t* d_n) {
     __shared__ uint32_t h[256];
+    if (d_n && *d_n < n) n = *d_n;
     h[threadIdx.x] = 0;
     __syncthreads();
     const size_t base = static_cast<size_t>(blockIdx.x) * kRadixThreads * rounds;
@@ -183,8 +184,10 @@ template <typename KeyT>
 __global__ void radix_downsweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                 KeyT* __restrict__ kout, uint32_t* __restrict__ vout, size_t n,
                                 int shift, const uint32_t* __restrict__ offsets,
-                                const uint32_t* __restrict__ hist, uint32_t num_tiles, int rounds) {
+                                const uint32_t* __restrict__ hist, uint32_t num_tiles, int rounds,
+                                const uint32_t* d_n) {
     extern __shared__ __align__(16) uint8_t radix_smem[];
+    if (d_n && *d_n < n) n = *d_n;
     KeyT* sk = reinterpret_cast<KeyT*>(radix_smem);
     uint32_t* sv = reinterpret_cast<uint32_t*>(sk + static_cast<size_t>(rounds) * kRadixThreads);
     __shared__ uint32_t wh[kRadixThreads / 32][256];
@@ -199,6 +202,7 @@ __global__ void radix_downsweep(const KeyT* __restrict__ kin, const uint32_t* __
     gbase[tid] = offsets[static_cast<size_t>(tid) * num_tiles + blockIdx.x];
     uint32_t running = 0;  // keys of digit `tid` in the earlier rounds
     const size_t base = static_cast<size_t>(blockIdx.x) * kRadixThreads * rounds;
+    if (base >= n) return;  // (a tile past a device-side count; uniform)
     const size_t tile_cap = static_cast<size_t>(kRadixThreads) * rounds;
     const uint32_t tile_n = static_cast<uint32_t>(n - base < tile_cap ? n - base : tile_cap);
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -259,7 +263,7 @@ size_t radix_temp_elems(size_t n) {
 
 template <typename KeyT>
 bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, int begin_bit,
-                      int end_bit, uint32_t* tmp, cudaStream_t s) {
+                      int end_bit, uint32_t* tmp, cudaStream_t s, const uint32_t* d_n) {
     if (n <= 1) return false;
     const int rounds = radix_rounds(n);
     const size_t tile = static_cast<size_t>(kRadixThreads) * rounds;
@@ -277,10 +281,10 @@ bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, 
         uint32_t* vi = flipped ? v1 : v0;
         KeyT* ko = flipped ? k0 : k1;
         uint32_t* vo = flipped ? v0 : v1;
-        radix_upsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, n, bit, hist, tiles, rounds);
+        radix_upsweep<KeyT><<<tiles, kRadixThreads, 0, s>>>(ki, n, bit, hist, tiles, rounds, d_n);
         DETLSH_LAUNCH_CHECK();
         exclusive_scan_u32(hist, offs, 256 * static_cast<size_t>(tiles), stmp, nullptr, s);
-        radix_downsweep<KeyT><<<tiles, kRadixThreads, smem, s>>>(ki, vi, ko, vo, n, bit, offs, hist, tiles, rounds);
+        radix_downsweep<KeyT><<<tiles, kRadixThreads, smem, s>>>(ki, vi, ko, vo, n, bit, offs, hist, tiles, rounds, d_n);
         DETLSH_LAUNCH_CHECK();
         flipped = !flipped;
     }
@@ -288,8 +292,8 @@ bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, 
 }
 
 template bool radix_sort_pairs<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, size_t, int,
-                                         int, uint32_t*, cudaStream_t);
+                                         int, uint32_t*, cudaStream_t, const uint32_t*);
 template bool radix_sort_pairs<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, size_t, int,
-                                         int, uint32_t*, cudaStream_t);
+                                         int, uint32_t*, cudaStream_t, const uint32_t*);
 
 }  // namespace detlsh_b200

@@ -22,8 +22,10 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, size_t n, uint32_t* t
 // ping-ponged between (k0,v0) and (k1,v1); returns true if the result ended in
 // (k1,v1).  `tmp` must hold radix_temp_elems(n) u32.
 size_t radix_temp_elems(size_t n);
+// d_n (optional): the pair count on the device (<= n, the capacity the tiles
+// are laid out for), so a count produced by an earlier kernel needs no host read.
 template <typename KeyT>
 bool radix_sort_pairs(KeyT* k0, uint32_t* v0, KeyT* k1, uint32_t* v1, size_t n, int begin_bit,
-                      int end_bit, uint32_t* tmp, cudaStream_t s);
+                      int end_bit, uint32_t* tmp, cudaStream_t s, const uint32_t* d_n = nullptr);
 
 }  // namespace detlsh_b200

@@ -7,6 +7,8 @@
 #include "primitives.cuh"
 #include "stages.cuh"
 
+#include <cstdlib>
+
 namespace detlsh_b200 {
 
 int lk_padded(int LK) { return (LK + 63) / 64 * 64; }
@@ -210,6 +212,241 @@ __global__ void order_pick_kernel(const uint64_t* __restrict__ sorted, int R, ui
         else rank = span * b - 1;
         table[static_cast<uint64_t>(r) * (NR + 1) + b] =
             fval(static_cast<uint32_t>(sorted[static_cast<uint64_t>(r) * n_s + rank]));
+    }
+}
+
+// ---- order statistics by binning (gpu_order_stat_table, large samples) ----
+constexpr int kOsBins = 16384;
+
+__global__ void os_minmax_kernel(const float* __restrict__ rows, uint64_t n_s, uint32_t* kmin, uint32_t* kmax) {
+    const float* row = rows + static_cast<uint64_t>(blockIdx.y) * n_s;
+    uint32_t lo = 0xffffffffu, hi = 0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_s;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t k = fkey(row[i]);
+        lo = min(lo, k);
+        hi = max(hi, k);
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(kmin + blockIdx.y, lo);
+        atomicMax(kmax + blockIdx.y, hi);
+    }
+}
+
+// Monotone bin of a key: linear in the value between the row's min and max
+// (exact double difference, rounded product: non-decreasing in the value;
+// -0 and +0 share a bin).  Non-finite extremes: one bin.
+struct OsGrid {
+    double vmin, scale;
+    __device__ OsGrid(uint32_t kmin, uint32_t kmax) {
+        const float a = fval(kmin), b = fval(kmax);
+        vmin = a;
+        scale = (isfinite(a) && isfinite(b) && b > a) ? static_cast<double>(kOsBins - 1) / (static_cast<double>(b) - a) : 0.0;
+    }
+    __device__ uint32_t bin(uint32_t k) const {
+        if (scale == 0.0) return 0;
+        const double x = (static_cast<double>(fval(k)) - vmin) * scale;
+        return x <= 0.0 ? 0u : (x >= kOsBins - 1 ? kOsBins - 1 : static_cast<uint32_t>(x));
+    }
+};
+
+__global__ void os_hist_kernel(const float* __restrict__ rows, uint64_t n_s, const uint32_t* kmin,
+                               const uint32_t* kmax, uint32_t* __restrict__ hist) {
+    extern __shared__ uint32_t h[];
+    for (int b = threadIdx.x; b < kOsBins; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    const OsGrid G(kmin[blockIdx.y], kmax[blockIdx.y]);
+    const float* row = rows + static_cast<uint64_t>(blockIdx.y) * n_s;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_s;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(&h[G.bin(fkey(row[i]))], 1u);
+    __syncthreads();
+    uint32_t* g = hist + static_cast<uint64_t>(blockIdx.y) * kOsBins;
+    if (gridDim.x == 1) {
+        for (int b = threadIdx.x; b < kOsBins; b += blockDim.x) g[b] = h[b];
+    } else {
+        for (int b = threadIdx.x; b < kOsBins; b += blockDim.x)
+            if (h[b]) atomicAdd(g + b, h[b]);
+    }
+}
+
+// Exclusive scan of kOsBins counts in shared memory by a 1024-thread block
+// (16 consecutive bins per thread); returns the total.
+__device__ uint32_t os_block_scan(const uint32_t* in, uint32_t* out) {
+    __shared__ uint32_t wsum[32];
+    constexpr int per = kOsBins / 1024;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    uint32_t loc = 0;
+    for (int j = 0; j < per; ++j) loc += in[t * per + j];
+    uint32_t inc = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = wsum[lane];
+        uint32_t wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += v;
+        }
+        wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    uint32_t run = wsum[warp] + inc - loc;
+    for (int j = 0; j < per; ++j) {
+        const uint32_t c = in[t * per + j];
+        out[t * per + j] = run;
+        run += c;
+    }
+    __syncthreads();
+    const uint32_t total = out[kOsBins - 1] + in[kOsBins - 1];
+    __syncthreads();
+    return total;
+}
+
+// rank b of a table row (order_pick_kernel's ranks)
+__device__ __forceinline__ uint64_t os_rank(int b, uint64_t n_s, int NR) {
+    return b == 0 ? 0 : (b == NR ? n_s - 1 : (n_s / NR) * b - 1);
+}
+
+// the bin holding rank rho: the last bin with pre[bin] <= rho (non-empty)
+__device__ __forceinline__ uint32_t os_find(const uint32_t* pre, const uint32_t* h, uint64_t rho) {
+    uint32_t lo = 0, hi = kOsBins - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (pre[mid] <= rho) lo = mid;
+        else hi = mid - 1;
+    }
+    while (h[lo] == 0) --lo;  // (empty bins share the next bin's prefix)
+    return lo;
+}
+
+__global__ void __launch_bounds__(1024) os_mark_kernel(const uint32_t* __restrict__ hist, uint64_t n_s, int NR,
+                                                       uint8_t* __restrict__ flags, uint32_t* __restrict__ tcount) {
+    extern __shared__ __align__(16) uint8_t os_smem[];
+    uint32_t* pre = reinterpret_cast<uint32_t*>(os_smem);
+    uint8_t* fl = os_smem + kOsBins * 4;
+    const uint32_t* hr = hist + static_cast<uint64_t>(blockIdx.x) * kOsBins;
+    for (int b = threadIdx.x; b < kOsBins; b += blockDim.x) fl[b] = 0;
+    os_block_scan(hr, pre);
+    for (int b = threadIdx.x; b <= NR; b += blockDim.x) fl[os_find(pre, hr, os_rank(b, n_s, NR))] = 1;
+    __syncthreads();
+    uint32_t t = 0;
+    uint8_t* fo = flags + static_cast<uint64_t>(blockIdx.x) * kOsBins;
+    for (int b = threadIdx.x; b < kOsBins; b += blockDim.x) {
+        fo[b] = fl[b];
+        if (fl[b]) t += hr[b];
+    }
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0 && t) atomicAdd(tcount + blockIdx.x, t);
+}
+
+__global__ void os_compact_kernel(const float* __restrict__ rows, uint64_t n_s, const uint32_t* kmin,
+                                  const uint32_t* kmax, const uint8_t* __restrict__ flags, uint64_t* __restrict__ keys,
+                                  uint32_t* __restrict__ vals, uint32_t* count) {
+    // one counter reservation per block step (warp counts -> block prefix)
+    __shared__ uint32_t wcnt[32];
+    __shared__ uint32_t bbase;
+    const OsGrid G(kmin[blockIdx.y], kmax[blockIdx.y]);
+    const float* row = rows + static_cast<uint64_t>(blockIdx.y) * n_s;
+    const uint8_t* fr = flags + static_cast<uint64_t>(blockIdx.y) * kOsBins;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t base = blockIdx.x * static_cast<uint64_t>(blockDim.x); base < n_s; base += stride) {
+        const uint64_t i = base + threadIdx.x;
+        uint32_t k = 0;
+        bool keep = false;
+        if (i < n_s) {
+            k = fkey(row[i]);
+            keep = fr[G.bin(k)] != 0;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wcnt[warp] = __popc(m);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < nw; ++w) {
+                const uint32_t c = wcnt[w];
+                wcnt[w] = t;
+                t += c;
+            }
+            bbase = t ? atomicAdd(count, t) : 0u;
+        }
+        __syncthreads();
+        if (keep) {
+            const uint32_t at = bbase + wcnt[warp] + __popc(m & ((1u << lane) - 1u));
+            keys[at] = (static_cast<uint64_t>(blockIdx.y) << 32) | k;
+            vals[at] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) os_pick_kernel(const uint32_t* __restrict__ hist, const uint8_t* __restrict__ flags,
+                                                       const uint32_t* __restrict__ tcount,
+                                                       const uint64_t* __restrict__ sorted, uint64_t n_s, int NR,
+                                                       float* __restrict__ table) {
+    extern __shared__ __align__(16) uint8_t os_smem[];
+    uint32_t* pre = reinterpret_cast<uint32_t*>(os_smem);
+    uint32_t* tpre = pre + kOsBins;
+    const int r = blockIdx.x;
+    const uint32_t* hr = hist + static_cast<uint64_t>(r) * kOsBins;
+    const uint8_t* fr = flags + static_cast<uint64_t>(r) * kOsBins;
+    __shared__ uint64_t rowstart;
+    if (threadIdx.x == 0) {
+        uint64_t a = 0;
+        for (int q = 0; q < r; ++q) a += tcount[q];
+        rowstart = a;
+    }
+    os_block_scan(hr, pre);
+    // flagged-only prefix: scan of (flag ? count : 0), staged in tpre first
+    for (int b = threadIdx.x; b < kOsBins; b += blockDim.x) tpre[b] = fr[b] ? hr[b] : 0u;
+    __syncthreads();
+    {
+        constexpr int per = kOsBins / 1024;
+        uint32_t v[per];
+        for (int j = 0; j < per; ++j) v[j] = tpre[threadIdx.x * per + j];
+        __syncthreads();
+        uint32_t loc = 0;
+        for (int j = 0; j < per; ++j) loc += v[j];
+        __shared__ uint32_t wsum[32];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        uint32_t inc = loc;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += x;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t w = wsum[lane];
+            uint32_t wi = w;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t x = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += x;
+            }
+            wsum[lane] = wi - w;
+        }
+        __syncthreads();
+        uint32_t run = wsum[warp] + inc - loc;
+        for (int j = 0; j < per; ++j) {
+            tpre[threadIdx.x * per + j] = run;
+            run += v[j];
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b <= NR; b += blockDim.x) {
+        const uint64_t rho = os_rank(b, n_s, NR);
+        const uint32_t b1 = os_find(pre, hr, rho);
+        const uint64_t pos = rho - pre[b1] + tpre[b1];
+        table[static_cast<uint64_t>(r) * (NR + 1) + b] = fval(static_cast<uint32_t>(sorted[rowstart + pos]));
     }
 }
 
@@ -527,17 +764,58 @@ void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_region
                           float* d_table, cudaStream_t s, bool sync) {
     StreamScope scope(s);
     const uint64_t total = static_cast<uint64_t>(R) * n_s;
-    DevBuf<uint64_t> k0(total), k1(total);
-    DevBuf<uint32_t> v0(total), v1(total), tmp(radix_temp_elems(total));
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 65535));
-    order_keys_kernel<<<grid, 256, 0, s>>>(d_rows, total, n_s, k0.get(), v0.get());
-    DETLSH_LAUNCH_CHECK();
     int rbits = 0;
     while ((1 << rbits) < R) ++rbits;
-    const bool flip = radix_sort_pairs<uint64_t>(k0.get(), v0.get(), k1.get(), v1.get(), total, 0,
-                                                 32 + ((rbits + 7) / 8) * 8, tmp.get(), s);
-    order_pick_kernel<<<R, 256, 0, s>>>(flip ? k1.get() : k0.get(), R, n_s, n_regions, d_table);
-    DETLSH_LAUNCH_CHECK();
+    const int end_bit = 32 + ((rbits + 7) / 8) * 8;
+    if (n_s < 4 * static_cast<uint64_t>(kOsBins) || std::getenv("DETLSH_TEST_FULL_ORDER_SORT")) {
+        // small samples: sort everything
+        DevBuf<uint64_t> k0(total), k1(total);
+        DevBuf<uint32_t> v0(total), v1(total), tmp(radix_temp_elems(total));
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 65535));
+        order_keys_kernel<<<grid, 256, 0, s>>>(d_rows, total, n_s, k0.get(), v0.get());
+        DETLSH_LAUNCH_CHECK();
+        const bool flip = radix_sort_pairs<uint64_t>(k0.get(), v0.get(), k1.get(), v1.get(), total, 0, end_bit,
+                                                     tmp.get(), s);
+        order_pick_kernel<<<R, 256, 0, s>>>(flip ? k1.get() : k0.get(), R, n_s, n_regions, d_table);
+        DETLSH_LAUNCH_CHECK();
+    } else {
+        // Only the N_r + 1 ranks are needed: bin each row's values on a
+        // monotone (linear in value, between the row's min and max) 16 K-bin
+        // grid, keep just the values of the bins that hold a wanted rank, sort
+        // those, and read the ranks off with the bins' prefix counts.  Same
+        // order (the order-preserving key), so the same values as a full sort.
+        DevBuf<uint32_t> kmin(R), kmax(R), hist(static_cast<size_t>(R) * kOsBins), tcount(R), count(1);
+        DevBuf<uint8_t> flags(static_cast<size_t>(R) * kOsBins);
+        DETLSH_CUDA(cudaMemsetAsync(kmin.get(), 0xff, R * 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(kmax.get(), 0, R * 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(hist.get(), 0, static_cast<size_t>(R) * kOsBins * 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(count.get(), 0, 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(tcount.get(), 0, R * 4, s));
+        const unsigned gx = static_cast<unsigned>(std::min<uint64_t>((n_s + 16383) / 16384, 1024));
+        os_minmax_kernel<<<dim3(gx, R), 256, 0, s>>>(d_rows, n_s, kmin.get(), kmax.get());
+        DETLSH_LAUNCH_CHECK();
+        DETLSH_CUDA(cudaFuncSetAttribute(os_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOsBins * 4));
+        // (a few blocks per row: each flushes its whole histogram)
+        const unsigned gh = static_cast<unsigned>(std::min<uint64_t>((n_s + 262143) / 262144, 256));
+        os_hist_kernel<<<dim3(gh, R), 1024, kOsBins * 4, s>>>(d_rows, n_s, kmin.get(), kmax.get(), hist.get());
+        DETLSH_LAUNCH_CHECK();
+        DETLSH_CUDA(cudaFuncSetAttribute(os_mark_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kOsBins * 4 + kOsBins));
+        os_mark_kernel<<<R, 1024, kOsBins * 4 + kOsBins, s>>>(hist.get(), n_s, n_regions, flags.get(), tcount.get());
+        DETLSH_LAUNCH_CHECK();
+        DevBuf<uint64_t> k0(total), k1(total);
+        DevBuf<uint32_t> v0(total), v1(total), tmp(radix_temp_elems(total));
+        os_compact_kernel<<<dim3(gx, R), 256, 0, s>>>(d_rows, n_s, kmin.get(), kmax.get(), flags.get(), k0.get(),
+                                                     v0.get(), count.get());
+        DETLSH_LAUNCH_CHECK();
+        const bool flip = radix_sort_pairs<uint64_t>(k0.get(), v0.get(), k1.get(), v1.get(), total, 0, end_bit,
+                                                     tmp.get(), s, count.get());
+        DETLSH_CUDA(cudaFuncSetAttribute(os_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kOsBins * 4 * 2));
+        os_pick_kernel<<<R, 1024, kOsBins * 4 * 2, s>>>(hist.get(), flags.get(), tcount.get(),
+                                                                flip ? k1.get() : k0.get(), n_s, n_regions, d_table);
+        DETLSH_LAUNCH_CHECK();
+    }
     if (sync) DETLSH_CUDA(cudaStreamSynchronize(s));
 }
 

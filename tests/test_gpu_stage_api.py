@@ -76,3 +76,28 @@ def test_range_queries_match_reference(gpu, pair):
                 got = gpu.range_query_exact(gi, tree, P[q], radius)
                 want = ri.range_query(tree, P[q], radius, exact=True)
                 assert np.array_equal(got, want), (tree, q, scale, "exact")
+
+
+def test_order_statistics_by_binning_equal_full_sort(gpu, monkeypatch):
+    """Large samples take the boundary order statistics from a 16 K-bin
+    monotone binning plus a sort of the wanted bins only; the table must equal
+    the full sort's bit for bit, on rows with heavy duplicates, signed zeros,
+    a constant row, a row holding +inf and a Gaussian row (n_s = 140 K)."""
+    g = np.random.Generator(np.random.PCG64(11))
+    L, n, K = 2, 700_000, 4
+    pr = np.empty((L, n, K), np.float32)
+    pr[0, :, 0] = g.standard_normal(n) * 3.0
+    pr[0, :, 1] = g.integers(-3, 4, n).astype(np.float32)             # heavy duplicates
+    pr[0, :, 2] = np.where(g.random(n) < 0.5, -0.0, 0.0) * (g.random(n) < 0.7) + (g.random(n) < 0.3) * g.standard_normal(n)
+    pr[0, :, 3] = 1.25                                                 # constant
+    pr[1, :, 0] = g.standard_normal(n).astype(np.float32)
+    pr[1, :50, 0] = np.inf                                             # non-finite max
+    pr[1, :, 1] = np.exp(g.standard_normal(n) * 6).astype(np.float32)  # wide dynamic range
+    pr[1, :, 2] = -np.abs(g.standard_normal(n)).astype(np.float32)
+    pr[1, :, 3] = (g.random(n) < 0.999) * 7.0
+    for sample in ("gpu",):
+        got = gpu.select_breakpoints(pr, 256, 0.2, 5, sample=sample)
+        monkeypatch.setenv("DETLSH_TEST_FULL_ORDER_SORT", "1")
+        want = gpu.select_breakpoints(pr, 256, 0.2, 5, sample=sample)
+        monkeypatch.delenv("DETLSH_TEST_FULL_ORDER_SORT")
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), sample
