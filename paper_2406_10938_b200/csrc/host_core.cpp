@@ -2,9 +2,11 @@
 #include "host_core.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <numeric>
 #include <stdexcept>
+#include <thread>
 
 #include <immintrin.h>
 
@@ -628,25 +630,73 @@ void select_row_breakpoints(float* a, uint64_t n_s, int n_regions, Rng& rng, flo
     if (draws) *draws += nd;
 }
 
+namespace {
+// Runs f(begin, end) over [0, n) on up to 8 threads (one when n is small).
+template <typename F>
+void parallel_ranges(uint64_t n, uint64_t min_per_thread, F&& f) {
+    const uint64_t want = std::min<uint64_t>(8, std::max<uint64_t>(1, n / min_per_thread));
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint64_t nt = std::min<uint64_t>(want, hw);
+    if (nt <= 1) {
+        f(uint64_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (uint64_t w = 0; w < nt; ++w)
+        th.emplace_back([&, w]() { f(n * w / nt, n * (w + 1) / nt); });
+    for (auto& t : th) t.join();
+}
+}  // namespace
+
 RefSampler::RefSampler(uint64_t n, uint64_t n_s, int n_regions, uint64_t seed)
-    : n_(n), n_s_(n_s), n_regions_(n_regions), rng_(seed), idx_(n), sample_idx_(n_s) {
-    std::iota(idx_.begin(), idx_.end(), 0u);
+    : n_(n), n_s_(n_s), n_regions_(n_regions), rng_(seed), idx_(new uint32_t[n]), sample_idx_(n_s) {
+    uint32_t* idx = idx_.get();
+    parallel_ranges(n, uint64_t{1} << 22, [idx](uint64_t a, uint64_t b) {
+        for (uint64_t t = a; t < b; ++t) idx[t] = static_cast<uint32_t>(t);
+    });
 }
 
 const std::vector<uint32_t>& RefSampler::next_space_indices() {
     // Partial Fisher-Yates (encoder.cpp:133-134).  The swap targets depend only
     // on the RNG stream, so they are drawn first (same draws, same order) and
     // the random-access swaps then run with the targets prefetched ahead.
+    // bounded() takes one raw draw unless r < bound and r < 2^64 mod bound
+    // (probability < n / 2^64): the raw draws are taken in order, the 64-bit
+    // remainders (the costly part) computed on several threads, and in the
+    // rejection case the space is redrawn exactly from the saved state.
     constexpr uint64_t kAhead = 16;
     std::vector<uint32_t>& tgt = targets_;
     tgt.resize(n_s_);
-    for (uint64_t t = 0; t < n_s_; ++t) tgt[t] = static_cast<uint32_t>(t + rng_.bounded(n_ - t));
-    uint32_t* idx = idx_.data();
+    if (n_s_ >= (uint64_t{1} << 20)) {  // (below: thread start-up outweighs the remainders)
+        const Rng saved = rng_;
+        raw_.resize(n_s_);
+        for (uint64_t t = 0; t < n_s_; ++t) raw_[t] = rng_.next_u64();
+        std::atomic<bool> rejected{false};
+        const uint64_t n = n_;
+        const uint64_t* raw = raw_.data();
+        uint32_t* tg = tgt.data();
+        parallel_ranges(n_s_, uint64_t{1} << 15, [&rejected, n, raw, tg](uint64_t a, uint64_t b) {
+            bool rej = false;
+            for (uint64_t t = a; t < b; ++t) {
+                const uint64_t bound = n - t, r = raw[t];
+                if (r < bound && r < (0 - bound) % bound) rej = true;
+                tg[t] = static_cast<uint32_t>(t + r % bound);
+            }
+            if (rej) rejected = true;
+        });
+        if (rejected) {
+            rng_ = saved;
+            for (uint64_t t = 0; t < n_s_; ++t) tgt[t] = static_cast<uint32_t>(t + rng_.bounded(n_ - t));
+        }
+    } else {
+        for (uint64_t t = 0; t < n_s_; ++t) tgt[t] = static_cast<uint32_t>(t + rng_.bounded(n_ - t));
+    }
+    uint32_t* idx = idx_.get();
     for (uint64_t t = 0; t < n_s_; ++t) {
         if (t + kAhead < n_s_) __builtin_prefetch(idx + tgt[t + kAhead], 1);
         std::swap(idx[t], idx[tgt[t]]);
     }
-    std::copy(idx_.begin(), idx_.begin() + static_cast<ptrdiff_t>(n_s_), sample_idx_.begin());
+    std::copy(idx, idx + n_s_, sample_idx_.begin());
     return sample_idx_;
 }
 

@@ -10,6 +10,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <random>
 #include <vector>
 
@@ -72,9 +73,10 @@ private:
     uint64_t n_, n_s_;
     int n_regions_;
     Rng rng_;
-    std::vector<uint32_t> idx_;
+    std::unique_ptr<uint32_t[]> idx_;  // [n] (filled in parallel: no serial first touch)
     std::vector<uint32_t> sample_idx_;
     std::vector<uint32_t> targets_;
+    std::vector<uint64_t> raw_;  // one space's raw draws
     uint64_t draws_ = 0;
 };
 
