@@ -2012,9 +2012,12 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // 8-bit rows: exact int8 scores; float rows: bf16x3 scores filtered with a
     // rigorous slack, survivors rescored exactly in fp64 (tc_finish_f32).  The
     // float path stages 4x more survivors per query (kTcFinishCapF32): its tau
-    // rows are fp64 chains, so 4x fewer of them is the better trade.
+    // rows are fp64 chains, so 4x fewer of them is the better trade.  So do
+    // 8-bit rows wider than 256 B (C3, d = 784): there the tau rows are read
+    // from HBM (the rows exceed L2) and were ~2/3 of the plan kernel's time.
     const bool f32_rows = !P.data_u8 && P.data_leaf && P.data_tcf && P.xnf && P.row_f > 256 && tc_score_fits(P.row_f);
-    const uint32_t fin_cap = f32_rows ? kTcFinishCapF32 : kTcFinishCap;
+    const bool wide_u8 = P.data_u8 && P.row_u8 > 256 && !std::getenv("DETLSH_TEST_NARROW_FIN_CAP");
+    const uint32_t fin_cap = (f32_rows || wide_u8) ? kTcFinishCapF32 : kTcFinishCap;
     uint64_t tau_rows = std::max<uint64_t>(
         std::max<uint64_t>(kTauRows, 2ULL * P.k),
         std::min<uint64_t>(kTauRowsMax, (4ULL * P.k * P.budget + fin_cap - 1) / fin_cap));
@@ -2177,7 +2180,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             // 256-query tiles of tc_score (C5: 1024 queries per chunk, 3.8
             // rounds of the plan kernel's 271 CTAs; 813 = 3 whole rounds left
             // a 45-query tile per chunk)
-            const uint64_t per_q = W * 4 + 8ULL * fin_cap + 128 * 1024;
+            const uint64_t per_q = W * 4 + 8ULL * fin_cap + 2ULL * fin_cap * sizeof(uint4);
             const uint64_t chunk_bytes =
                 capturing ? (3ULL << 30)
                           : std::max<uint64_t>(3ULL << 30, std::min<uint64_t>(16ULL << 30, avail / 8));
@@ -2197,11 +2200,13 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
             grow_scratch(X.tc_rec, rec_cap);
             grow_scratch(X.tc_rec_cnt, 1);
             grow_scratch(X.over_list, P.nq);
+            grow_scratch(X.tc_big, chunk);
             for (uint64_t c0 = 0; c0 < P.nq; c0 += chunk) {
                 const uint64_t m = std::min<uint64_t>(chunk, P.nq - c0);
                 DETLSH_CUDA(cudaMemsetAsync(X.tc_tau2.get(), 0xff, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(X.tc_surv_cnt.get(), 0, m * 4, s));
                 DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntWork, 0, 4, s));
+                DETLSH_CUDA(cudaMemsetAsync(X.counters.get() + kCntBig, 0, 4, s));
                 QueryPlan Pc = Pp;
                 Pc.q_begin = c0;
                 Pc.q_end = c0 + m;
@@ -2245,7 +2250,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                                          s);
                 else
                     launch_tc_finish(a, P.perm0, P.k, P.r_min, P.budget, P.ids, P.dists, P.n_hits, P.radius,
-                                     P.cands, X.over_list.get(), X.counters.get() + kCntOver, s);
+                                     P.cands, X.over_list.get(), X.counters.get() + kCntOver, X.tc_big.get(),
+                                     X.counters.get() + kCntBig, s);
                 if (std::getenv("DETLSH_DEBUG_QUERY")) {  // survivor-count spread per chunk (syncs)
                     std::vector<uint32_t> sc(m);
                     uint32_t over = 0, slow = 0;

@@ -102,6 +102,7 @@ struct QueryScratch {
     DevBuf<uint4> tc_rec;
     DevBuf<unsigned long long> tc_rec_cnt;
     DevBuf<uint32_t> over_list;
+    DevBuf<uint32_t> tc_big;  // [chunk] slots whose survivors need the wide tc_finish
     // completion of the last batch that used this scratch: a batch on another
     // stream waits for it (the enqueue is serialised by the index mutex)
     cudaEvent_t done = nullptr;
@@ -163,12 +164,15 @@ void launch_row_norms_u8(const uint8_t* rows, uint64_t n, int R, int32_t* xn, cu
 // u8 rows -> 128-row tiles in the MMA operand layout ([ceil(n/128)][R/16][128][16] bytes)
 void launch_pack_tc_tiles(const uint8_t* rows, uint64_t n, int R, uint8_t* tiles, cudaStream_t s);
 void launch_tc_score(const TcScoreArgs& a, int device, cudaStream_t s);
+// big_list [a.nq] / big_n (zeroed by the caller): the queries with more
+// survivors than the first launch's sort width, finished by a second launch
 void launch_tc_finish(const TcScoreArgs& a, const uint32_t* perm0, int k, double r_min,
                       uint64_t budget, uint32_t* ids, double* dists, int32_t* n_hits, double* radius,
-                      uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, cudaStream_t s);
+                      uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, uint32_t* big_list,
+                      uint32_t* big_n, cudaStream_t s);
 // counters[] of QueryScratch: [0] slow-path queries, [1] sticky internal-invariant
 // flag, [2] tensor-core overflow queries, [3] tc_score work counter
-constexpr int kCntSlow = 0, kCntInvariant = 1, kCntOver = 2, kCntWork = 3, kCntTaken = 4;
+constexpr int kCntSlow = 0, kCntInvariant = 1, kCntOver = 2, kCntWork = 3, kCntTaken = 4, kCntBig = 6;
 
 // tcgen05 kind::i8 self-test (tc_score.cu): C[128][N] = A[128][K] . B[N][K]^T.
 void tc_gemm_u8_test(const uint8_t* hA, const uint8_t* hB, int N, int K, int32_t* hC);

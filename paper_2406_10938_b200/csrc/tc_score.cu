@@ -633,21 +633,32 @@ __global__ void tc_collect_kernel(TcScoreArgs a) {
 }
 
 // Exact top-k of each TC query's survivors by (dist^2, dataset position).
+// Two launches: the first sorts up to `width` survivors per query (small
+// shared memory, many CTAs per SM) and lists the queries with more in
+// big_list; the second (width = the staging cap) takes only those.
 __global__ void __launch_bounds__(256) tc_finish_kernel(TcScoreArgs a, const uint32_t* __restrict__ perm0,
                                                         int k, double r_min, uint64_t budget,
                                                         uint32_t* ids, double* dists, int32_t* n_hits,
                                                         double* radius, uint64_t* cands,
-                                                        uint32_t* overflow_list, uint32_t* overflow_n) {
-    __shared__ uint64_t key[kTcFinishCap];  // (d2 << 32) | position, sorted ascending
+                                                        uint32_t* overflow_list, uint32_t* overflow_n,
+                                                        uint32_t width, uint32_t* big_list, uint32_t* big_n,
+                                                        const uint32_t* only_list, const uint32_t* only_n) {
+    extern __shared__ uint64_t key[];  // [width] (d2 << 32) | position, sorted ascending
     // the pass-record list overflowed: no survivor list of this chunk is
     // complete, so every tensor-core query of the chunk takes the gather path
     const bool rec_over = *a.rec_cnt > a.rec_cap;
-    for (uint64_t slot = blockIdx.x; slot < a.nq; slot += gridDim.x) {
+    const uint64_t nslots = only_list ? *only_n : a.nq;
+    for (uint64_t it = blockIdx.x; it < nslots; it += gridDim.x) {
+        const uint64_t slot = only_list ? only_list[it] : it;
         if (a.tau2[slot] < 0) continue;
         const uint64_t q = a.order ? a.order[a.slot0 + slot] : a.slot0 + slot;
         const uint32_t cnt = a.surv_cnt[slot];
         if (rec_over || cnt > a.cap) {  // threshold too loose for the staging: rerun on the gather path
             if (threadIdx.x == 0) overflow_list[atomicAdd(overflow_n, 1u)] = static_cast<uint32_t>(q);
+            continue;
+        }
+        if (cnt > width) {  // (first launch only: width < cap)
+            if (threadIdx.x == 0) big_list[atomicAdd(big_n, 1u)] = static_cast<uint32_t>(slot);
             continue;
         }
         uint32_t n2 = 64;  // sort width: power of two >= cnt
@@ -793,11 +804,29 @@ void launch_pack_tc_tiles(const uint8_t* rows, uint64_t n, int R, uint8_t* tiles
 
 void launch_tc_finish(const TcScoreArgs& a, const uint32_t* perm0, int k, double r_min,
                       uint64_t budget, uint32_t* ids, double* dists, int32_t* n_hits, double* radius,
-                      uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, cudaStream_t s) {
+                      uint64_t* cands, uint32_t* overflow_list, uint32_t* overflow_n, uint32_t* big_list,
+                      uint32_t* big_n, cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>(a.nq, 4096)));
+    uint32_t cap2 = 64;  // the sort width for a full staging list
+    while (cap2 < a.cap) cap2 <<= 1;
+    const uint32_t w1 = std::min<uint32_t>(cap2, kTcFinishCap);  // 32 KB: several CTAs per SM
+    DETLSH_CUDA(cudaFuncSetAttribute(tc_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(cap2 * sizeof(uint64_t))));
     ProfScope ps("tc_finish", s);
-    tc_finish_kernel<<<grid, 256, 0, s>>>(a, perm0, k, r_min, budget, ids, dists, n_hits, radius, cands,
-                                          overflow_list, overflow_n);
+    tc_finish_kernel<<<grid, 256, w1 * sizeof(uint64_t), s>>>(a, perm0, k, r_min, budget, ids, dists, n_hits,
+                                                              radius, cands, overflow_list, overflow_n, w1, big_list,
+                                                              big_n, nullptr, nullptr);
+    DETLSH_LAUNCH_CHECK();
+    if (cap2 > w1) {
+        int sms = 148;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        tc_finish_kernel<<<static_cast<unsigned>(sms), 256, cap2 * sizeof(uint64_t), s>>>(
+            a, perm0, k, r_min, budget, ids, dists, n_hits, radius, cands, overflow_list, overflow_n, cap2, nullptr,
+            nullptr, big_list, big_n);
+        DETLSH_LAUNCH_CHECK();
+    }
     DETLSH_LAUNCH_CHECK();
 }
 
