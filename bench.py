@@ -574,8 +574,16 @@ def main():
         del ix2
     Qpin = torch.from_numpy(Q).pin_memory().numpy()
 
+    # page-locked result arrays, reused across steps (what a serving loop does)
+    def pinned(shape, dt):
+        return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+
+    res_pin = D.BatchResult(pinned((nq, k), torch.int32).view(np.uint32), pinned((nq, k), torch.float64),
+                            pinned((nq,), torch.int32), pinned((nq,), torch.float64),
+                            pinned((nq,), torch.int64).view(np.uint64))
+
     def e2e_query():
-        res = D.ck_ann_batch(idx, Qpin, k)
+        res = D.ck_ann_batch(idx, Qpin, k, out=res_pin)
         if world > 1:
             t = torch.from_numpy(res.ids.astype(np.int64) + s0).cuda()
             td = torch.from_numpy(res.dists).cuda()

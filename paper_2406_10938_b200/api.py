@@ -335,17 +335,26 @@ class BatchResult:
 
 
 def ck_ann_batch(index: DetIndex, queries, k: int, *, stream=None,
-                 tensor_cores: bool = True) -> BatchResult:
+                 tensor_cores: bool = True, out: BatchResult | None = None) -> BatchResult:
     """Batched ck_ann over host queries [nq][d] (outputs on the host).
 
     tensor_cores=False keeps verification on the per-query gather path (no
-    tcgen05 dataset-major scoring); the results are identical either way."""
+    tcgen05 dataset-major scoring); the results are identical either way.
+    `out`: caller-owned result arrays (e.g. page-locked, reused across
+    batches); shapes [nq][k] / [nq], dtypes as in BatchResult."""
     Q = _as_host_f32(queries)
     if Q.shape[1] != index.d():
         raise ValueError("ck_ann: query dimension mismatch")
     nq = Q.shape[0]
-    out = BatchResult(np.zeros((nq, k), np.uint32), np.zeros((nq, k), np.float64),
-                      np.zeros(nq, np.int32), np.zeros(nq, np.float64), np.zeros(nq, np.uint64))
+    if out is None:
+        out = BatchResult(np.zeros((nq, k), np.uint32), np.zeros((nq, k), np.float64),
+                          np.zeros(nq, np.int32), np.zeros(nq, np.float64), np.zeros(nq, np.uint64))
+    else:
+        want = ((out.ids, np.uint32, (nq, k)), (out.dists, np.float64, (nq, k)), (out.n_hits, np.int32, (nq,)),
+                (out.radius_used, np.float64, (nq,)), (out.candidates_seen, np.uint64, (nq,)))
+        for arr, dt, shape in want:
+            if arr.dtype != dt or arr.shape != shape or not arr.flags["C_CONTIGUOUS"]:
+                raise ValueError(f"ck_ann: out array must be {np.dtype(dt).name} {shape} C-contiguous")
     flags = 0 if tensor_cores else F_NO_TC
     check(_lib.load().detlsh_gpu_query(index.handle, _ptr(Q), nq, k, flags, _ptr(out.ids),
                                        _ptr(out.dists), _ptr(out.n_hits), _ptr(out.radius_used),
