@@ -201,3 +201,21 @@ def test_general_path_u8_matches_oracle(gpu, port, monkeypatch, defer):
         assert np.array_equal(res.dists[qi, :m].view(np.uint64), np.asarray(ds).view(np.uint64)), f"query {qi}"
         assert res.radius_used[qi] == rad
         assert int(res.candidates_seen[qi]) == cs
+
+
+def test_batch_into_caller_arrays(gpu, u8_index):
+    """ck_ann_batch(out=...) fills caller-owned (here page-locked) arrays with
+    the same results, and rejects a wrongly typed one."""
+    import torch
+    data, idx, g = u8_index
+    Q = _sparse_u8(g, 64, data.shape[1])
+    want = gpu.ck_ann_batch(idx, Q, 20)
+    pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()  # noqa: E731
+    out = gpu.BatchResult(pin((64, 20), torch.int32).view(np.uint32), pin((64, 20), torch.float64),
+                          pin((64,), torch.int32), pin((64,), torch.float64), pin((64,), torch.int64).view(np.uint64))
+    got = gpu.ck_ann_batch(idx, Q, 20, out=out)
+    assert got is out
+    _same(got, want)
+    bad = gpu.BatchResult(np.zeros((64, 20), np.int64), out.dists, out.n_hits, out.radius_used, out.candidates_seen)
+    with pytest.raises(ValueError):
+        gpu.ck_ann_batch(idx, Q, 20, out=bad)
