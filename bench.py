@@ -213,9 +213,11 @@ def recall_ratio(res_ids, res_d, n_hits, gt_ids, gt_d, k):
     return float(np.mean(rec)), float(np.mean(rat))
 
 
-def tc_tau_rows(k, budget):
-    """Rows the plan kernel scores exactly for tau^2 (query.cu run_query_batch)."""
-    return max(512, 2 * k, min(1 << 17, -(-4 * k * budget // 4096)))  # kTauRowsMax
+def tc_tau_rows(k, budget, R=128):
+    """Rows the plan kernel scores exactly for tau^2 (query.cu run_query_batch):
+    the staging cap is 16 K for rows wider than 256 B or budgets of 2^20+, else 4 K."""
+    cap = 16384 if (R > 256 or budget >= (1 << 20)) else 4096
+    return max(512, 2 * k, min((1 << 17) * 4096 // cap, -(-4 * k * budget // cap)))  # kTauRowsMax
 
 
 # algorithmic bytes per launch (DESIGN.md §5); kernels without a model get null
@@ -663,7 +665,7 @@ def main():
                                          else "2x measured bf16 burst"),
                            "frac": round(ops / (pms / 1e3) / 1e12 / pk, 4), "launch_ms": round(pms, 4),
                            "note": "the projection of 8-bit data is HBM/epilogue bound; see roofline"}
-    plan = {"leaves": int(idx.tree(0).is_leaf.sum()), "tau_rows": tc_tau_rows(k, budget)}
+    plan = {"leaves": int(idx.tree(0).is_leaf.sum()), "tau_rows": tc_tau_rows(k, budget, idx.row_u8())}
     query_roof = roofline(prof_query, args.steps, n_loc, d, nq, budget, 16, 4, hbm, peak_kind,
                           only=("query_fast",), row_u8=idx.row_u8(), plan=plan, cfg_key=cfg_key)
     query_roof_tc = roofline_tc(prof_query, args.steps, n_loc, nq, idx.row_u8(), peak_bf16())

@@ -2016,11 +2016,16 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // 8-bit rows wider than 256 B (C3, d = 784): there the tau rows are read
     // from HBM (the rows exceed L2) and were ~2/3 of the plan kernel's time.
     const bool f32_rows = !P.data_u8 && P.data_leaf && P.data_tcf && P.xnf && P.row_f > 256 && tc_score_fits(P.row_f);
-    const bool wide_u8 = P.data_u8 && P.row_u8 > 256 && !std::getenv("DETLSH_TEST_NARROW_FIN_CAP");
+    // Likewise for budgets of 10^6+ (C5: 4x fewer tau rows, 32 K instead of
+    // 131 K, which were ~half the plan kernel's HBM reads; the survivors,
+    // 3.3 K at the median and 11 K at most, fit the wider staging).
+    const bool wide_u8 = P.data_u8 && (P.row_u8 > 256 || P.budget >= (1u << 20)) &&
+                         !std::getenv("DETLSH_TEST_NARROW_FIN_CAP");
     const uint32_t fin_cap = (f32_rows || wide_u8) ? kTcFinishCapF32 : kTcFinishCap;
+    const uint64_t tau_max = kTauRowsMax * kTcFinishCap / fin_cap;  // the same survivor margin
     uint64_t tau_rows = std::max<uint64_t>(
         std::max<uint64_t>(kTauRows, 2ULL * P.k),
-        std::min<uint64_t>(kTauRowsMax, (4ULL * P.k * P.budget + fin_cap - 1) / fin_cap));
+        std::min<uint64_t>(tau_max, (4ULL * P.k * P.budget + fin_cap - 1) / fin_cap));
     if (const char* e = std::getenv("DETLSH_TAU_ROWS"))  // measurement hook
         tau_rows = std::max<uint64_t>(2ULL * P.k, std::strtoull(e, nullptr, 10));
     const bool tc_any = P.tc_allowed && P.budget >= kTcMinBudget && P.budget <= 0xffffffffULL &&
