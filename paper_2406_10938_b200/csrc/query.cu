@@ -2019,7 +2019,7 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     // Likewise for budgets of 10^6+ (C5: 4x fewer tau rows, 32 K instead of
     // 131 K, which were ~half the plan kernel's HBM reads; the survivors,
     // 3.3 K at the median and 11 K at most, fit the wider staging).
-    const bool wide_u8 = P.data_u8 && (P.row_u8 > 256 || P.budget >= (1u << 20)) &&
+    const bool wide_u8 = P.data_u8 && (P.row_u8 > 256 || P.budget >= (1u << 20) || std::getenv("DETLSH_TEST_WIDE_FIN_CAP")) &&
                          !std::getenv("DETLSH_TEST_NARROW_FIN_CAP");
     const uint32_t fin_cap = (f32_rows || wide_u8) ? kTcFinishCapF32 : kTcFinishCap;
     const uint64_t tau_max = kTauRowsMax * kTcFinishCap / fin_cap;  // the same survivor margin
