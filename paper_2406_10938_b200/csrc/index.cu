@@ -238,6 +238,36 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     const int K = p.K, L = p.L, NR = p.n_regions;
     const int LK = K * L;
     const size_t W = static_cast<size_t>(NR) + 1;
+    // reference-compatible sample (encoder.cpp:105-143): one RNG stream picks
+    // every space's sample and pivots, so the host replay is sequential.  Space
+    // 0's indices depend on the seed alone: drawn on a helper thread while the
+    // hash family and the device set-up proceed.
+    X->sample_size = sample_size_for(p.sample_fraction, n, NR);
+    std::unique_ptr<RefSampler> sampler_ptr;
+    const std::vector<uint32_t>* idx0_early = nullptr;
+    std::exception_ptr fy_err;
+    std::thread fy_thread;
+    if (!X->sample_gpu) {
+        const uint64_t ns0 = X->sample_size;
+        fy_thread = std::thread([&sampler_ptr, &idx0_early, &fy_err, n, ns0, NR, seed]() {
+            try {
+                sampler_ptr = std::make_unique<RefSampler>(n, ns0, NR, mix_seed(seed, kStreamBreakpoints));
+                idx0_early = &sampler_ptr->next_space_indices();
+            } catch (...) {
+                fy_err = std::current_exception();
+            }
+        });
+    }
+    struct FyJoin {
+        std::thread& t;
+        ~FyJoin() {
+            if (t.joinable()) t.join();
+        }
+    } fy_join{fy_thread};
+    auto join_fy = [&]() {
+        if (fy_thread.joinable()) fy_thread.join();
+        if (fy_err) std::rethrow_exception(fy_err);
+    };
     for (int i = 0; i <= L; ++i) {
         X->side.push_back(std::make_unique<OwnedStream>());
         X->side.back()->create();
@@ -270,7 +300,6 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         prepare_proj_tc(X->coeffs.get(), LK, d, X->proj_tc, s);
     }
     DevBuf<float> proj(static_cast<size_t>(L) * n * K);
-    X->sample_size = sample_size_for(p.sample_fraction, n, NR);
     const uint64_t n_s = X->sample_size;
     X->table.alloc(static_cast<size_t>(L) * K * W);
     X->codes.alloc(static_cast<size_t>(L) * n * K);
@@ -293,11 +322,6 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         launch_project_exact(X->data, n, d, X->coeffs_t.get(), K, L, proj.get(), s, "project_exact",
                              try_tc ? &X->proj_tc : nullptr, nonint.get());
     };
-    // reference-compatible sample (encoder.cpp:105-143): one RNG stream picks
-    // every space's sample and pivots, so the host replay is sequential
-    std::unique_ptr<RefSampler> sampler_ptr;
-    if (!X->sample_gpu)
-        sampler_ptr = std::make_unique<RefSampler>(n, n_s, NR, mix_seed(seed, kStreamBreakpoints));
     std::vector<float> h_rows;  // replayed boundary rows [L][K][W]
     if (!X->sample_gpu) h_rows.assign(static_cast<size_t>(L) * K * W, 0.0f);
     // Host input in reference mode: space 0's sample positions depend on the
@@ -346,7 +370,8 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         {
             StreamScope sc(s2);
             const bool zero_copy_sample = !dev_in && mapped_host_ptr(points) != nullptr;
-            const auto& idx0 = sampler_ptr->next_space_indices();
+            join_fy();
+            const auto& idx0 = *idx0_early;
             const bool dbg = std::getenv("DETLSH_DEBUG_BUILD") != nullptr;
             if (dbg) fprintf(stderr, "[build] fy %.2f ms mapped=%d\n", ms_since(t0), zero_copy_sample ? 1 : 0);
             DevBuf<float> dG(n_s * static_cast<size_t>(d)), dGp(static_cast<size_t>(L) * n_s * K);
