@@ -446,7 +446,11 @@ def main():
     k = args.k
     dev_shard = base_d[s0:s1] if devgen else torch.from_numpy(shard).cuda()
     dev_Q = Q_d if devgen else torch.from_numpy(Q).cuda()
-    stream = torch.cuda.current_stream()
+    # a stream of our own: the queries are enqueued on it (device mode returns
+    # at once) and the timing events are recorded on it, so they bracket the
+    # kernels (the legacy default stream would not order the library's streams)
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
@@ -500,24 +504,20 @@ def main():
     del other_idx
     other_ms = max_over_ranks(other_ms)
 
-    # warm-ups run with the event profile on (then discarded) so the timed steps
-    # reuse pooled CUDA events instead of creating them
-    lib.detlsh_profile_enable(1)
+    # The timed steps run without the per-kernel event profile (its phase
+    # read-backs are host waits that would open gaps between batches); the
+    # profile comes from as many extra steps of the same workload right after.
     for _ in range(args.warmup):
         idx = build()
-    lib.detlsh_profile_enable(0)
-    collect_profile(lib)
     del idx
     clocks = ClockSampler(local)
     clocks.start()
     lc0 = lib.detlsh_launch_count()
-    lib.detlsh_profile_enable(1)
     build_ms, idx = timed(build, args.steps)
-    lib.detlsh_profile_enable(0)
     build_launches = (lib.detlsh_launch_count() - lc0) / args.steps
-    prof_build = collect_profile(lib)
     build_ms = max_over_ranks(build_ms)
     stage_ms = idx.build_timings()
+    prof_build = profiled_steps(lib, build, args.steps)
 
     # ---------------- queries ----------------
     ids = torch.empty((nq, k), dtype=torch.int32, device="cuda")
@@ -537,24 +537,20 @@ def main():
         D.ck_ann_device(idx, dev_Q, k, ids, dists, hits, rad, cands, stream=stream.cuda_stream)
         if world == 1:
             return ids, dists, hits
-        gid = ids.to(torch.int64) + s0  # global positions
-        gather_topk(dists, gid, hits, g_d, g_i, g_h)
-        D.merge_topk_device(g_d, g_i, g_h, k, m_d, m_i, m_h, stream=stream.cuda_stream)
+        with torch.cuda.stream(stream):  # the exchange is ordered after the batch
+            gid = ids.to(torch.int64) + s0  # global positions
+            gather_topk(dists, gid, hits, g_d, g_i, g_h)
+            D.merge_topk_device(g_d, g_i, g_h, k, m_d, m_i, m_h, stream=stream.cuda_stream)
         return m_i, m_d, m_h
 
-    lib.detlsh_profile_enable(1)
     for _ in range(args.warmup):
         query()
-    lib.detlsh_profile_enable(0)
-    collect_profile(lib)
     lc0 = lib.detlsh_launch_count()
-    lib.detlsh_profile_enable(1)
     query_ms, (r_ids, r_d, r_h) = timed(query, args.steps)
-    lib.detlsh_profile_enable(0)
     query_launches = (lib.detlsh_launch_count() - lc0) / args.steps
-    prof_query = collect_profile(lib)
     query_ms = max_over_ranks(query_ms)
     clk = clocks.stop()
+    prof_query = profiled_steps(lib, query, args.steps)
 
     # ---------------- end to end through the public API, host buffers ----------------
     shard_pinned = None if devgen else torch.from_numpy(shard).pin_memory().numpy()  # host input, pinned
@@ -790,6 +786,20 @@ def plumbing(args, rank, world):
                           "shards": bounds, "gathered_ids": gi[:, 0, 0].tolist()}), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def profiled_steps(lib, fn, steps):
+    """Per-kernel CUDA-event profile over `steps` extra (untimed) steps; the
+    index returned by a build step is dropped right away."""
+    import torch
+    collect_profile(lib)
+    lib.detlsh_profile_enable(1)
+    for _ in range(steps):
+        out = fn()
+        del out
+    torch.cuda.synchronize()
+    lib.detlsh_profile_enable(0)
+    return collect_profile(lib)
 
 
 def collect_profile(lib):

@@ -2073,6 +2073,8 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         if (capturing) throw InvalidArgument("ck_ann: the first batch of a shape cannot be captured (scratch grows)");
         if (!grew && X.done) DETLSH_CUDA(cudaEventSynchronize(X.done));  // earlier batches still read it
         grew = true;
+        if (std::getenv("DETLSH_DEBUG_GROW"))
+            std::fprintf(stderr, "[query] scratch grows %zu -> %zu elements\n", buf.size(), count);
         {
             StreamScope sc(alloc_s);
             buf.alloc(count);
