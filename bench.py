@@ -14,6 +14,7 @@ indexes, NCCL all-gather of per-shard top-k + GPU merge.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -464,6 +465,16 @@ def main():
         return float(t.item())
 
     def timed(fn, steps):
+        # no garbage collection inside the timed region: an index freed there
+        # by the collector would release its device memory mid-step
+        gc.collect()
+        gc.disable()
+        try:
+            return _timed(fn, steps)
+        finally:
+            gc.enable()
+
+    def _timed(fn, steps):
         barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
