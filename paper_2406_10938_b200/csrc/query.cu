@@ -2119,10 +2119,20 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         Pp.order = flip ? ov1.get() : ov0.get();
     }
     const size_t items = 3 * static_cast<size_t>(P.max_leaves) * sizeof(LeafItem);
-    // memory the scratch may be sized against (no query under capture)
-    const size_t avail = capturing ? 0
-                                   : device_memory_available(device) + X.fast.size() + X.slow.size() +
-                                         (X.slow_bm.size() + X.tc_bm.size()) * sizeof(uint32_t);
+    // memory the scratch may be sized against (no query under capture).  Asked
+    // of the driver once per batch shape: cudaMemGetInfo on every batch was a
+    // host stall of up to ~100 ms whenever another thread was in the driver
+    // (an NVML clock sampler), leaving the GPU idle between device-mode batches.
+    size_t avail = 0;
+    if (!capturing) {
+        if (X.avail_nq != P.nq || X.avail_budget != P.budget) {
+            X.avail_bytes = device_memory_available(device) + X.fast.size() + X.slow.size() +
+                            (X.slow_bm.size() + X.tc_bm.size()) * sizeof(uint32_t);
+            X.avail_nq = P.nq;
+            X.avail_budget = P.budget;
+        }
+        avail = X.avail_bytes;
+    }
     const bool fast_path = P.k <= kFastMaxK && !P.rc_mode;
     // general path: the queries the fast path listed (count on the device), or
     // every query (k beyond the fast path, rc_ann).  A fixed number of slots,

@@ -91,6 +91,9 @@ struct QueryScratch {
     DevBuf<uint32_t> counters;
     DevBuf<unsigned long long> phases;  // [6] fast-path phase cycles (profiling only)
     size_t fast_slots = 0, slow_slots = 0;
+    // the memory figure the scratch was sized against, per batch shape
+    uint64_t avail_nq = 0, avail_budget = 0;
+    size_t avail_bytes = 0;
     // tensor-core hand-off staging (per chunk of queries), kept across calls:
     // several of these are GB-sized and re-allocating them from the pool per
     // batch costs fresh mappings whenever the pool is fragmented.  Nothing reads
