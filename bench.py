@@ -465,14 +465,8 @@ def main():
         return float(t.item())
 
     def timed(fn, steps):
-        # no garbage collection inside the timed region: an index freed there
-        # by the collector would release its device memory mid-step
-        gc.collect()
-        gc.disable()
-        try:
-            return _timed(fn, steps)
-        finally:
-            gc.enable()
+        gc.collect()  # indexes left in reference cycles by earlier phases
+        return _timed(fn, steps)
 
     def _timed(fn, steps):
         barrier()
