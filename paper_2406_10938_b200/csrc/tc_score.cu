@@ -303,15 +303,18 @@ __global__ void pack_tc_tiles_kernel(const uint8_t* __restrict__ rows, uint64_t 
     }
 }
 
-// Warp-specialised, persistent: warp 8 streams the occupied row tiles
+// Warp-specialised, persistent: warp EW (the producer) streams row tiles
 // (pre-tiled in HBM in the canonical no-swizzle K-major layout, one 1-D bulk
-// copy per tile) into a kTcStages ring; warp 9 issues the tcgen05 MMAs into one
-// of two TMEM accumulators (2 x 256 columns); warps 0-7 drain the other one.
-// Work units (query tile, row-tile range) are handed out dynamically; row
-// tiles holding no candidate of the query tile are skipped.  The epilogue is
-// branch-free: 2 q.x - (|q|^2 - tau^2) >= |x|^2 per element (IMAD + compare
-// into a mask); only columns where some lane passes are revisited, with
-// single-column TMEM loads, to consult the candidate bitmap.
+// copy per tile, or per 256-byte K chunk) into a staging ring; warp EW + 1
+// issues the tcgen05 MMAs into one of two TMEM accumulators (2 x 256 columns,
+// one MMA per query half); warps 0 .. EW-1 drain the other one.  Work units
+// (query tile, row-tile range) are handed out dynamically; every row tile of
+// a unit is scored (the candidate sets of a locality-ordered 256-query tile
+// reach almost every tile).  The epilogue is branch-free: 2 q.x + (tau^2 -
+// |q|^2) - |x|^2 >= 0 per element (IMAD, IMAD, funnel shift of the sign into
+// a fail mask); only columns where some lane passes and whose query has a
+// candidate in these 32 rows are revisited, from a shared-memory stash of the
+// loaded values, to write pass records.
 // Two shapes of the same kernel: QT queries per tile, EW epilogue warps (4 per
 // TMEM lane quarter per 4-warp group).  Rows of R <= 256 bytes: 256-query
 // tiles, 16 epilogue warps, whole row tiles per stage.  Wider rows (C3,
