@@ -5,6 +5,9 @@
 #include <atomic>
 #include <cmath>
 #include <numeric>
+#include <mutex>
+#include <functional>
+#include <condition_variable>
 #include <stdexcept>
 #include <thread>
 
@@ -549,6 +552,266 @@ bool have_avx2() {
     return v;
 }
 
+// ---- the closed form on several threads (segments of kParMin+ values) ----
+// A small persistent pool: workers spin briefly, then sleep on a condition
+// variable; run(n, f) executes f(0..n-1) across the workers and the caller.
+class ParPool {
+public:
+    static ParPool& get() {
+        static ParPool pool;
+        return pool;
+    }
+    int threads() const { return static_cast<int>(workers_.size()) + 1; }
+    template <typename F>
+    void run(int n, F&& f) {
+        if (workers_.empty() || n <= 1) {
+            for (int i = 0; i < n; ++i) f(i);
+            return;
+        }
+        std::lock_guard<std::mutex> one_caller(call_mu_);  // (builds on several threads share the pool)
+        std::function<void(int)> job(std::forward<F>(f));
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &job;
+            ntasks_ = n;
+            done_.store(0, std::memory_order_relaxed);
+            gen_.fetch_add(1, std::memory_order_release);
+        }
+        cv_.notify_all();
+        work(0);
+        while (done_.load(std::memory_order_acquire) < n) _mm_pause();
+        std::lock_guard<std::mutex> lk(mu_);
+        job_ = nullptr;
+    }
+
+private:
+    ParPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned nw = std::min(7u, hw > 1 ? hw - 1 : 0u);  // (16 on the 16-core box: no faster, bandwidth-bound)
+        for (unsigned w = 0; w < nw; ++w) workers_.emplace_back([this, w]() { loop(static_cast<int>(w) + 1); });
+    }
+    ~ParPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            gen_.fetch_add(1);
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    // static assignment: participant `me` (0 = the caller) runs tasks me,
+    // me + P, ... (a chunk index stays on one core from pass to pass)
+    void work(int me) {
+        const int P = threads();
+        for (int t = me; t < ntasks_; t += P) {
+            (*job_)(t);
+            done_.fetch_add(1, std::memory_order_acq_rel);
+        }
+    }
+    void loop(int me) {
+        uint64_t seen = 0;  // (a worker starting late still takes a job posted before it ran)
+        for (;;) {
+            for (int spin = 0; gen_.load(std::memory_order_acquire) == seen; ++spin) {
+                if (spin < 200000) {  // (~5 ms: the next partition of the replay usually comes sooner)
+                    _mm_pause();
+                    continue;
+                }
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&]() { return gen_.load() != seen; });
+            }
+            seen = gen_.load(std::memory_order_acquire);
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (stop_) return;
+                if (!job_) continue;
+            }
+            work(me);
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_, call_mu_;
+    std::condition_variable cv_;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<int> done_{0};
+    int ntasks_ = 0;
+    std::function<void(int)>* job_ = nullptr;
+    bool stop_ = false;
+};
+
+// Chunk kernels of the closed form (AVX-512, masked tails).
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512dq,popcnt,bmi,bmi2")))
+void par_count(const float* a, int64_t x0, int64_t x1, float pv, uint64_t* lt, uint64_t* eq, uint64_t* gt) {
+    const __m512 vp = _mm512_set1_ps(pv);
+    uint64_t l = 0, e = 0, g = 0;
+    int64_t x = x0;
+    for (; x + 16 <= x1; x += 16) {
+        const __m512 v = _mm512_loadu_ps(a + x);
+        l += _mm_popcnt_u32(_mm512_cmp_ps_mask(v, vp, _CMP_LT_OQ));
+        e += _mm_popcnt_u32(_mm512_cmp_ps_mask(v, vp, _CMP_EQ_OQ));
+        g += _mm_popcnt_u32(_mm512_cmp_ps_mask(v, vp, _CMP_GT_OQ));
+    }
+    for (; x < x1; ++x) {
+        l += a[x] < pv;
+        e += a[x] == pv;
+        g += a[x] > pv;
+    }
+    *lt = l;
+    *eq = e;
+    *gt = g;
+}
+
+// values > pv of [x0, x1), ascending position, into out
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512dq,popcnt,bmi,bmi2")))
+void par_collect_gt(const float* a, int64_t x0, int64_t x1, float pv, float* out) {
+    const __m512 vp = _mm512_set1_ps(pv);
+    int64_t n = 0, x = x0;
+    for (; x + 16 <= x1; x += 16) {
+        const __m512 v = _mm512_loadu_ps(a + x);
+        const __mmask16 m = _mm512_cmp_ps_mask(v, vp, _CMP_GT_OQ);
+        _mm512_mask_compressstoreu_ps(out + n, m, v);
+        n += _mm_popcnt_u32(m);
+    }
+    for (; x < x1; ++x)
+        if (a[x] > pv) out[n++] = a[x];
+}
+
+// values < pv of [x0, x1), descending position, into out
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512dq,popcnt,bmi,bmi2")))
+void par_collect_lt_desc(const float* a, int64_t x0, int64_t x1, float pv, float* out) {
+    const __m512 vp = _mm512_set1_ps(pv);
+    const __m512i rev = _mm512_setr_epi32(15, 14, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0);
+    int64_t n = 0, y = x1;
+    for (; y - 16 >= x0; y -= 16) {
+        const __m512 v = _mm512_permutexvar_ps(rev, _mm512_loadu_ps(a + y - 16));
+        const __mmask16 m = _mm512_cmp_ps_mask(v, vp, _CMP_LT_OQ);
+        _mm512_mask_compressstoreu_ps(out + n, m, v);
+        n += _mm_popcnt_u32(m);
+    }
+    for (int64_t t = y - 1; t >= x0; --t)
+        if (a[t] < pv) out[n++] = a[t];
+}
+
+// the i-th position of [x0, x1) holding a value > pv (ascending) takes src[i]
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512dq,popcnt,bmi,bmi2")))
+void par_fill_gt(float* a, int64_t x0, int64_t x1, float pv, const float* src) {
+    const __m512 vp = _mm512_set1_ps(pv);
+    int64_t u = 0, x = x0;
+    for (; x + 16 <= x1; x += 16) {
+        const __m512 v = _mm512_loadu_ps(a + x);
+        const __mmask16 m = _mm512_cmp_ps_mask(v, vp, _CMP_GT_OQ);
+        if (m) {
+            _mm512_storeu_ps(a + x, _mm512_mask_expandloadu_ps(v, m, src + u));
+            u += _mm_popcnt_u32(m);
+        }
+    }
+    for (; x < x1; ++x)
+        if (a[x] > pv) a[x] = src[u++];
+}
+
+// the i-th position of [x0, x1) holding a value < pv (descending) takes src[i]
+__attribute__((target("avx512f,avx512vl,avx512bw,avx512dq,popcnt,bmi,bmi2")))
+void par_fill_lt_desc(float* a, int64_t x0, int64_t x1, float pv, const float* src) {
+    const __m512 vp = _mm512_set1_ps(pv);
+    const __m512i rev = _mm512_setr_epi32(15, 14, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0);
+    int64_t u = 0, y = x1;
+    for (; y - 16 >= x0; y -= 16) {
+        const __m512 v = _mm512_permutexvar_ps(rev, _mm512_loadu_ps(a + y - 16));
+        const __mmask16 m = _mm512_cmp_ps_mask(v, vp, _CMP_LT_OQ);
+        if (m) {
+            _mm512_storeu_ps(a + y - 16, _mm512_permutexvar_ps(rev, _mm512_mask_expandloadu_ps(v, m, src + u)));
+            u += _mm_popcnt_u32(m);
+        }
+    }
+    for (int64_t t = y - 1; t >= x0; --t)
+        if (a[t] < pv) a[t] = src[u++];
+}
+
+size_t kParMin = size_t{1} << 18;  // segment length from which the closed form runs on the pool
+
+// hoare_rewrite_avx512's closed form with every pass split over the pool:
+// counts (p), per-chunk stopper counts and their prefix sums, the stoppers
+// gathered into buf (left region's large values ascending, right region's
+// small values descending), then written back crosswise.  Same result.
+bool hoare_rewrite_par(float* a, size_t lo, size_t hi, float pv, float* buf, size_t* p_out) {
+    if (!(a[lo] < pv) || !(a[hi - 1] > pv)) return false;
+    ParPool& pool = ParPool::get();
+    const int T = pool.threads();
+    const int64_t s0 = static_cast<int64_t>(lo) + 2, s1 = static_cast<int64_t>(hi) - 1;  // scan region
+    // one chunking of the scan region for every pass (chunk t stays on one core)
+    std::vector<int64_t> cb(T + 1);
+    for (int t = 0; t <= T; ++t) cb[t] = s0 + (s1 - s0) * t / T;
+    std::vector<uint64_t> lt(T), eq(T), gt(T);
+    pool.run(T, [&](int t) { par_count(a, cb[t], cb[t + 1], pv, &lt[t], &eq[t], &gt[t]); });
+    uint64_t nlt = 0, neq = 0;
+    for (int t = 0; t < T; ++t) {
+        nlt += lt[t];
+        neq += eq[t];
+    }
+    if (neq) return false;
+    const int64_t p = static_cast<int64_t>(lo) + 1 + static_cast<int64_t>(nlt);
+    // left region [s0, p], right region [p+1, s1): chunk t's part of each
+    auto lpart = [&](int t, int64_t& x0, int64_t& x1) {
+        x0 = cb[t];
+        x1 = std::min(cb[t + 1], p + 1);
+    };
+    auto rpart = [&](int t, int64_t& x0, int64_t& x1) {
+        x0 = std::max(cb[t], p + 1);
+        x1 = cb[t + 1];
+    };
+    // stopper counts per chunk: large values in its left part, small in its
+    // right part; only the chunk holding p needs a recount
+    std::vector<uint64_t> cl(T), cr(T);
+    int tb = -1;
+    for (int t = 0; t < T; ++t) {
+        if (cb[t + 1] <= p + 1) {
+            cl[t] = gt[t];
+            cr[t] = 0;
+        } else if (cb[t] >= p + 1) {
+            cl[t] = 0;
+            cr[t] = lt[t];
+        } else {
+            tb = t;
+        }
+    }
+    if (tb >= 0) {
+        uint64_t a1, a2, a3, b1, b2, b3;
+        par_count(a, cb[tb], p + 1, pv, &a1, &a2, &a3);
+        par_count(a, p + 1, cb[tb + 1], pv, &b1, &b2, &b3);
+        cl[tb] = a3;
+        cr[tb] = b1;
+    }
+    std::vector<uint64_t> offl(T), offr(T);
+    uint64_t m = 0, mr = 0;
+    for (int t = 0; t < T; ++t) {
+        offl[t] = m;
+        m += cl[t];
+    }
+    for (int t = T - 1; t >= 0; --t) {  // the right region is taken top-down
+        offr[t] = mr;
+        mr += cr[t];
+    }
+    if (m != mr) throw std::logic_error("hoare_rewrite: stopper counts differ");  // rank balance
+    float* bl = buf;                   // left region's large values, ascending
+    float* br = buf + (hi - lo) + 16;  // right region's small values, descending position
+    pool.run(T, [&](int t) {
+        int64_t x0, x1;
+        lpart(t, x0, x1);
+        if (x0 < x1) par_collect_gt(a, x0, x1, pv, bl + offl[t]);
+        rpart(t, x0, x1);
+        if (x0 < x1) par_collect_lt_desc(a, x0, x1, pv, br + offr[t]);
+    });
+    pool.run(T, [&](int t) {
+        int64_t x0, x1;
+        lpart(t, x0, x1);
+        if (x0 < x1) par_fill_gt(a, x0, x1, pv, br + offl[t]);
+        rpart(t, x0, x1);
+        if (x0 < x1) par_fill_lt_desc(a, x0, x1, pv, bl + offr[t]);
+    });
+    std::swap(a[lo + 1], a[p]);
+    *p_out = static_cast<size_t>(p);
+    return true;
+}
+
 size_t kRewriteMin = 64;  // >= 32 (buffer layout);  // segment length from which the closed-form rewrite pays (measured)
 
 // Median-of-three around a seeded pick, sentinel Hoare scan; one bounded()
@@ -563,6 +826,9 @@ size_t hoare_partition(float* a, size_t lo, size_t hi, Rng& rng, float* buf = nu
     std::swap(a[mid], a[lo + 1]);
     const float pv = a[lo + 1];
     size_t pr;
+    if (buf && len >= kParMin && have_avx512() && ParPool::get().threads() > 1 &&
+        hoare_rewrite_par(a, lo, hi, pv, buf, &pr))
+        return pr;
     if (buf && len >= kRewriteMin && have_avx512() && hoare_rewrite_avx512(a, lo, hi, pv, buf, &pr)) return pr;
     const size_t j = len < 12        ? hoare_scan_simple(a, lo, hi, pv)  // (measured crossover)
                      : have_avx512() ? hoare_scan_avx512(a, lo, hi, pv)
