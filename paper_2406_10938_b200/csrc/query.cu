@@ -1089,7 +1089,7 @@ __device__ int32_t kth_dist2_f32up(const QueryPlan& P, const FastSlot& F, const 
 // F32TC: the float bf16x3 hand-off is compiled only into its own instance, so
 // the u8 instance keeps its register budget.  NT: threads per CTA (512 for
 // indexes with ~10^6 leaves per tree, whose slots are few: memory-bound)
-template <int MINB, bool F32TC, int NT = kQueryThreads>
+template <int MINB, bool F32TC, int NT = kQueryThreads, bool TCO = false>
 __global__ void __launch_bounds__(NT, MINB) query_fast_kernel(
     QueryPlan P, uint8_t* scratch, size_t slot_bytes, uint32_t* slow_list, uint32_t* slow_n) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1508,6 +1508,11 @@ __global__ void __launch_bounds__(NT, MINB) query_fast_kernel(
             if (threadIdx.x == 0) P.tc_tau2[qs - P.q_begin] = tau2;
             __syncthreads();
             phase(3);
+            continue;
+        }
+        if constexpr (TCO) {  // (tensor-core-only instance: the gather re-run verifies it)
+            if (threadIdx.x == 0) P.tc_over_list[atomicAdd(P.tc_over_n, 1u)] = static_cast<uint32_t>(q);
+            __syncthreads();
             continue;
         }
         // emission: whole leaves (block prefix of their sizes, then one warp per
@@ -2048,7 +2053,14 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
     auto* const fast_kernel = tc_f32 ? &query_fast_kernel<3, true>
                               : fast_nt == 512 ? &query_fast_kernel<2, false, 512>
                               : five ? &query_fast_kernel<5, false> : &query_fast_kernel<3, false>;
+    // the same plan kernel without the gather verification, for the
+    // tensor-core launches (smaller code and register footprint)
+    auto* const tco_kernel = tc_f32 ? &query_fast_kernel<3, true, kQueryThreads, true>
+                             : fast_nt == 512 ? &query_fast_kernel<2, false, 512, true>
+                             : five ? &query_fast_kernel<5, false, kQueryThreads, true>
+                                    : &query_fast_kernel<3, false, kQueryThreads, true>;
     DETLSH_CUDA(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    DETLSH_CUDA(cudaFuncSetAttribute(tco_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // general path: 1024 threads per query for large budgets (few slots, each
     // query's scans and member lists ~10^6-10^7 long), 256 otherwise
     const char* snt_env = std::getenv("DETLSH_SLOW_THREADS");  // 256|1024 (test hook)
@@ -2167,11 +2179,11 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
         const size_t lim = capturing ? std::max<size_t>(X.fast.size(), fast_bytes) : fast_scratch_limit(avail);
         slots = std::max<size_t>(1, std::min<size_t>(slots, lim / fast_bytes));
         grow_scratch(X.fast, slots * fast_bytes);
-        auto launch_fast = [&](const QueryPlan& Pc) {
+        auto launch_fast = [&](const QueryPlan& Pc, bool tco = false) {
             const uint64_t m = Pc.q_end - Pc.q_begin;
             if (m == 0) return;
             ProfScope ps("query_fast", s);
-            fast_kernel<<<static_cast<unsigned>(std::min<uint64_t>(slots, m)), fast_nt, smem, s>>>(
+            (tco ? tco_kernel : fast_kernel)<<<static_cast<unsigned>(std::min<uint64_t>(slots, m)), fast_nt, smem, s>>>(
                 Pc, X.fast.get(), fast_bytes, X.slow_list.get(), X.counters.get());
             DETLSH_LAUNCH_CHECK();
         };
@@ -2230,7 +2242,9 @@ void run_query_batch(const QueryPlan& P, QueryScratch& X, int device, cudaStream
                 Pc.tc_bm = X.tc_bm.get();
                 Pc.tc_W = W;
                 Pc.tc_tau2 = X.tc_tau2.get();
-                launch_fast(Pc);
+                Pc.tc_over_list = X.over_list.get();
+                Pc.tc_over_n = X.counters.get() + kCntOver;
+                launch_fast(Pc, !std::getenv("DETLSH_TEST_NO_TCO"));
                 if (tc_f32)
                     launch_tc_pack_queries_f32(P.q, Pp.order, c0, m, P.d, R, X.tc_q8.get(),
                                                reinterpret_cast<float*>(X.tc_qn.get()), s);

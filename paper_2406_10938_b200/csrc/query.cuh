@@ -74,6 +74,11 @@ struct QueryPlan {
     int force_exact;  // test hook: skip the approximate leaf scan
     int rc_mode;      // rc_ann: one pass at radius eps * r_min (= r), k = 1, c * r acceptance
     uint32_t tc_tau_rows;  // rows of the nearest leaves scored exactly for tau^2
+    // tensor-core launches of the plan kernel compiled without the gather
+    // verification: a query that cannot hand off is listed here instead and
+    // verified by the gather re-run
+    uint32_t* tc_over_list;
+    uint32_t* tc_over_n;
 };
 
 constexpr int kQueryThreads = 256;
