@@ -7,7 +7,7 @@
 #include <cstdio>
 #include <cstring>
 using namespace detlsh_b200;
-int main() {
+int main(int argc, char** argv) {
     std::mt19937_64 g(11);
     std::normal_distribution<float> nd(0.f, 300.f);
     int bad = 0, tried = 0, done = 0;
@@ -35,22 +35,23 @@ int main() {
     }
     printf("segments %d (closed form taken %d): mismatches %d\n", tried, done, bad);
     // whole rows
-    const size_t ns = 10000000;
+    const size_t ns = argc > 1 ? static_cast<size_t>(atol(argv[1])) : 10000000;
+    const int lo_shift = argc > 2 ? atoi(argv[2]) : 15;
     std::vector<float> base(ns), work(ns), row(257);
     for (auto& v : base) v = nd(g);
     for (int mode = 0; mode < 4; ++mode) {
-        kParMin = mode ? (size_t{1} << (15 + mode)) : ~size_t{0};
+        kParMin = mode ? (size_t{1} << (lo_shift + mode)) : ~size_t{0};
         Rng rng(5);
         uint64_t draws = 0;
         double t = 0;
-        std::vector<float> out(257 * 4);
-        for (int r = 0; r < 4; ++r) {
+        std::vector<float> out(257 * 48);
+        for (int r = 0; r < (ns < 1000000 ? 48 : 4); ++r) {
             work = base;
             const auto t0 = std::chrono::steady_clock::now();
             select_row_breakpoints(work.data(), ns, 256, rng, out.data() + r * 257, &draws);
             t += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         }
-        printf("%s (par from 2^%d): %.1f ms/row, draws %llu, row0[128] %.6f\n", mode ? "pool" : "single", 15 + mode, t / 4,
+        printf("%s (par from 2^%d): %.1f ms/row, draws %llu, row0[128] %.6f\n", mode ? "pool" : "single", lo_shift + mode, t / (ns < 1000000 ? 48 : 4),
                (unsigned long long)draws, out[128]);
     }
     return bad != 0;
