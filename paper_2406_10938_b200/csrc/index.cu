@@ -663,6 +663,11 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
     X->timings.emplace_back("trees_sum", tree_ms);
     X->timings.emplace_back("rmin", rmin_ms);
     X->timings.emplace_back("total", ms_since(t_all));
+    if (std::getenv("DETLSH_DEBUG_BUILD")) {
+        fprintf(stderr, "[build] stages");
+        for (const auto& t : X->timings) fprintf(stderr, " %s=%.2f", t.first.c_str(), t.second);
+        fprintf(stderr, "\n");
+    }
     *params = X->params;
     return X;
 }
