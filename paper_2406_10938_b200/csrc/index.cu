@@ -74,7 +74,9 @@ struct PinnedBuf {
 };
 
 float* pinned_scratch(size_t bytes, int slot = 0) {
-    thread_local PinnedBuf bufs[4];  // 0: build samples, 1: sample rows, 2: query results, 3: query upload
+    // 0: build samples, 1: sample rows, 2: query results, 3: query upload,
+    // 4: sample indices, 5: space-0 sample indices
+    thread_local PinnedBuf bufs[6];
     PinnedBuf& buf = bufs[slot];
     if (buf.bytes < bytes) {
         if (buf.p) cudaFreeHost(buf.p);
@@ -376,18 +378,23 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             if (dbg) fprintf(stderr, "[build] fy %.2f ms mapped=%d\n", ms_since(t0), zero_copy_sample ? 1 : 0);
             DevBuf<float> dG(n_s * static_cast<size_t>(d)), dGp(static_cast<size_t>(L) * n_s * K);
             DevBuf<uint32_t> iota(n_s);
-            std::vector<uint32_t> h_iota(n_s);
-            std::iota(h_iota.begin(), h_iota.end(), 0u);
+            // host arrays go over through page-locked staging (a pageable copy
+            // is staged by the driver and could wait behind other threads' copies)
+            auto staged_idx0 = [&]() {
+                uint32_t* h = reinterpret_cast<uint32_t*>(pinned_scratch(n_s * 4, 5));
+                std::memcpy(h, idx0.data(), n_s * 4);
+                return h;
+            };
             if (dev_in) {
                 DevBuf<uint32_t> d_idx0(n_s);
-                DETLSH_CUDA(cudaMemcpyAsync(d_idx0.get(), idx0.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
+                DETLSH_CUDA(cudaMemcpyAsync(d_idx0.get(), staged_idx0(), n_s * 4, cudaMemcpyHostToDevice, s2));
                 DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
                 launch_pack_f32(X->data, d_idx0.get(), n_s, d, dG.get(), s2);  // rows idx0[t]
             } else if (const float* mapped = zero_copy_sample ? mapped_host_ptr(points) : nullptr) {
                 // page-locked host input: the GPU gathers the sample rows over the
                 // bus itself (zero-copy), no host-side gather on the critical path
                 DevBuf<uint32_t> d_idx0(n_s);
-                DETLSH_CUDA(cudaMemcpyAsync(d_idx0.get(), idx0.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
+                DETLSH_CUDA(cudaMemcpyAsync(d_idx0.get(), staged_idx0(), n_s * 4, cudaMemcpyHostToDevice, s2));
                 launch_pack_f32(mapped, d_idx0.get(), n_s, d, dG.get(), s2);
             } else {
                 float* G = pinned_scratch(n_s * static_cast<size_t>(d) * sizeof(float), 1);
@@ -401,7 +408,7 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
                 for (auto& th : gth) th.join();
                 DETLSH_CUDA(cudaMemcpyAsync(dG.get(), G, n_s * static_cast<size_t>(d) * 4, cudaMemcpyHostToDevice, s2));
             }
-            DETLSH_CUDA(cudaMemcpyAsync(iota.get(), h_iota.data(), n_s * 4, cudaMemcpyHostToDevice, s2));
+            launch_iota_u32(iota.get(), n_s, s2);
             DETLSH_CUDA(cudaStreamWaitEvent(s2, coeffs_ready, 0));
             if (paa) launch_project_paa(dG.get(), n_s, d, K, dGp.get(), s2, "project_sample");
             else launch_project_exact(dG.get(), n_s, d, X->coeffs_t.get(), K, L, dGp.get(), s2, "project_sample", &X->proj_tc);
@@ -556,6 +563,11 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         RefSampler& sampler = *sampler_ptr;
         DevBuf<uint32_t> d_idx(n_s);
         DevBuf<float> d_sample(static_cast<size_t>(K) * n_s);
+        // the per-space order statistics' temporaries, reserved before the tree
+        // workers start (their GB-sized allocations would hold this thread --
+        // the replay's -- in the allocator for up to hundreds of ms at C4)
+        OrderStatWork os_work;
+        os_work.reserve(K, n_s, s);
         float* h_sample = pinned_scratch(static_cast<size_t>(K) * n_s * sizeof(float));
         cudaEvent_t copied;
         DETLSH_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
@@ -568,7 +580,8 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             for (int j = 0; j < rows_needed; ++j)
                 sampler.select_row(h_sample + static_cast<size_t>(j) * n_s, rows + j * W);
         };
-        double t_idx = 0.0, t_wait = 0.0, t_replay = 0.0;
+        double t_idx = 0.0, t_wait = 0.0, t_replay = 0.0, t_enq = 0.0;
+        const bool dbg_loop = std::getenv("DETLSH_DEBUG_BUILD") != nullptr;
         const auto t_loop = Clock::now();
         for (int i = 0; i < L; ++i) {
             if (i == 0 && early0) {
@@ -578,18 +591,32 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
             auto tq = Clock::now();
             const auto& idx = sampler.next_space_indices();
             t_idx += ms_since(tq);
-            DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), idx.data(), n_s * 4, cudaMemcpyHostToDevice, s));
+            const auto te = Clock::now();
+            // (through page-locked staging: a pageable copy is staged by the
+            // driver and could wait behind the tree workers' transfers)
+            uint32_t* h_idx = reinterpret_cast<uint32_t*>(pinned_scratch(n_s * 4, 4));
+            std::memcpy(h_idx, idx.data(), n_s * 4);
+            const double e0 = ms_since(te);
+            DETLSH_CUDA(cudaMemcpyAsync(d_idx.get(), h_idx, n_s * 4, cudaMemcpyHostToDevice, s));
             launch_gather_sample(d_proj + static_cast<size_t>(i) * n * K, d_idx.get(), n_s, K,
                                  d_sample.get(), s);
+            const double e1 = ms_since(te);
             const bool replay = i + 1 < L;
             if (replay) {
                 DETLSH_CUDA(cudaMemcpyAsync(h_sample, d_sample.get(), static_cast<size_t>(K) * n_s * 4,
                                             cudaMemcpyDeviceToHost, s));
                 DETLSH_CUDA(cudaEventRecord(copied, s));
             }
+            const double e2 = ms_since(te);
             gpu_order_stat_table(d_sample.get(), K, n_s, NR, X->table.get() + static_cast<size_t>(i) * K * W,
-                                 s, /*sync=*/false);
+                                 s, /*sync=*/false, &os_work);
+            const double e3 = ms_since(te);
             launch_space(i);
+            t_enq += ms_since(te);
+            if (dbg_loop)
+                fprintf(stderr, "[build] space %d enqueue: staged %.2f copy+gather %.2f d2h %.2f os %.2f launch %.2f ms\n",
+                        i, e0, e1 - e0, e2 - e1, e3 - e2, ms_since(te) - e3);
+            if (dbg_loop) fprintf(stderr, "[build] space %d enqueued %.2f ms into the loop\n", i, ms_since(t_loop));
             if (replay) {
                 tq = Clock::now();
                 DETLSH_CUDA(cudaEventSynchronize(copied));
@@ -602,11 +629,15 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         X->timings.emplace_back("bp_sample_indices", t_idx);
         X->timings.emplace_back("bp_sample_wait", t_wait);
         X->timings.emplace_back("bp_replay", t_replay);
+        X->timings.emplace_back("bp_enqueue", t_enq);
         X->timings.emplace_back("bp_loop", ms_since(t_loop));
         X->h_table.assign(static_cast<size_t>(L) * K * W, 0.0f);
-        DETLSH_CUDA(cudaMemcpyAsync(X->h_table.data(), X->table.get(), X->h_table.size() * 4,
-                                    cudaMemcpyDeviceToHost, s));
-        DETLSH_CUDA(cudaStreamSynchronize(s));
+        {  // (page-locked staging, like the index copies above)
+            float* h_tab = pinned_scratch(X->h_table.size() * 4, 4);
+            DETLSH_CUDA(cudaMemcpyAsync(h_tab, X->table.get(), X->h_table.size() * 4, cudaMemcpyDeviceToHost, s));
+            DETLSH_CUDA(cudaStreamSynchronize(s));
+            std::memcpy(X->h_table.data(), h_tab, X->h_table.size() * 4);
+        }
         // last space: replay only up to its last row holding a zero boundary
         int last_zero = -1;
         const size_t base = static_cast<size_t>(L - 1) * K * W;

@@ -742,6 +742,17 @@ void launch_gather_proj_rows(const float* d_proj, uint64_t n, int K, int Lg, con
     DETLSH_LAUNCH_CHECK();
 }
 
+__global__ void iota_u32_kernel(uint32_t* v, uint64_t n) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        v[i] = static_cast<uint32_t>(i);
+}
+void launch_iota_u32(uint32_t* v, uint64_t n, cudaStream_t s) {
+    const unsigned grid = static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 4096)));
+    iota_u32_kernel<<<grid, 256, 0, s>>>(v, n);
+    DETLSH_LAUNCH_CHECK();
+}
+
 void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
                           float* d_out, cudaStream_t s) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n_s + 255) / 256, 65535));
@@ -760,23 +771,39 @@ void launch_feistel_sample(uint64_t n, uint64_t n_s, uint64_t key, uint32_t* d_i
     DETLSH_LAUNCH_CHECK();
 }
 
+void OrderStatWork::reserve(int R, uint64_t n_s, cudaStream_t s) {
+    const uint64_t total = static_cast<uint64_t>(R) * n_s;
+    kmin.grow(R, 0, s);
+    kmax.grow(R, 0, s);
+    tcount.grow(R, 0, s);
+    count.grow(1, 0, s);
+    hist.grow(static_cast<size_t>(R) * kOsBins, 0, s);
+    flags.grow(static_cast<size_t>(R) * kOsBins, 0, s);
+    k0.grow(total, 0, s);
+    k1.grow(total, 0, s);
+    v0.grow(total, 0, s);
+    v1.grow(total, 0, s);
+    tmp.grow(radix_temp_elems(total), 0, s);
+}
+
 void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_regions,
-                          float* d_table, cudaStream_t s, bool sync) {
+                          float* d_table, cudaStream_t s, bool sync, OrderStatWork* work) {
     StreamScope scope(s);
     const uint64_t total = static_cast<uint64_t>(R) * n_s;
     int rbits = 0;
     while ((1 << rbits) < R) ++rbits;
     const int end_bit = 32 + ((rbits + 7) / 8) * 8;
+    OrderStatWork local;
+    OrderStatWork& w = work ? *work : local;
+    w.reserve(R, n_s, s);  // (no-op when the caller reserved enough)
     if (n_s < 4 * static_cast<uint64_t>(kOsBins) || std::getenv("DETLSH_TEST_FULL_ORDER_SORT")) {
         // small samples: sort everything
-        DevBuf<uint64_t> k0(total), k1(total);
-        DevBuf<uint32_t> v0(total), v1(total), tmp(radix_temp_elems(total));
         const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 65535));
-        order_keys_kernel<<<grid, 256, 0, s>>>(d_rows, total, n_s, k0.get(), v0.get());
+        order_keys_kernel<<<grid, 256, 0, s>>>(d_rows, total, n_s, w.k0.get(), w.v0.get());
         DETLSH_LAUNCH_CHECK();
-        const bool flip = radix_sort_pairs<uint64_t>(k0.get(), v0.get(), k1.get(), v1.get(), total, 0, end_bit,
-                                                     tmp.get(), s);
-        order_pick_kernel<<<R, 256, 0, s>>>(flip ? k1.get() : k0.get(), R, n_s, n_regions, d_table);
+        const bool flip = radix_sort_pairs<uint64_t>(w.k0.get(), w.v0.get(), w.k1.get(), w.v1.get(), total, 0,
+                                                     end_bit, w.tmp.get(), s);
+        order_pick_kernel<<<R, 256, 0, s>>>(flip ? w.k1.get() : w.k0.get(), R, n_s, n_regions, d_table);
         DETLSH_LAUNCH_CHECK();
     } else {
         // Only the N_r + 1 ranks are needed: bin each row's values on a
@@ -784,36 +811,33 @@ void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_region
         // grid, keep just the values of the bins that hold a wanted rank, sort
         // those, and read the ranks off with the bins' prefix counts.  Same
         // order (the order-preserving key), so the same values as a full sort.
-        DevBuf<uint32_t> kmin(R), kmax(R), hist(static_cast<size_t>(R) * kOsBins), tcount(R), count(1);
-        DevBuf<uint8_t> flags(static_cast<size_t>(R) * kOsBins);
-        DETLSH_CUDA(cudaMemsetAsync(kmin.get(), 0xff, R * 4, s));
-        DETLSH_CUDA(cudaMemsetAsync(kmax.get(), 0, R * 4, s));
-        DETLSH_CUDA(cudaMemsetAsync(hist.get(), 0, static_cast<size_t>(R) * kOsBins * 4, s));
-        DETLSH_CUDA(cudaMemsetAsync(count.get(), 0, 4, s));
-        DETLSH_CUDA(cudaMemsetAsync(tcount.get(), 0, R * 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(w.kmin.get(), 0xff, R * 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(w.kmax.get(), 0, R * 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(w.hist.get(), 0, static_cast<size_t>(R) * kOsBins * 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(w.count.get(), 0, 4, s));
+        DETLSH_CUDA(cudaMemsetAsync(w.tcount.get(), 0, R * 4, s));
         const unsigned gx = static_cast<unsigned>(std::min<uint64_t>((n_s + 16383) / 16384, 1024));
-        os_minmax_kernel<<<dim3(gx, R), 256, 0, s>>>(d_rows, n_s, kmin.get(), kmax.get());
+        os_minmax_kernel<<<dim3(gx, R), 256, 0, s>>>(d_rows, n_s, w.kmin.get(), w.kmax.get());
         DETLSH_LAUNCH_CHECK();
         DETLSH_CUDA(cudaFuncSetAttribute(os_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kOsBins * 4));
         // (a few blocks per row: each flushes its whole histogram)
         const unsigned gh = static_cast<unsigned>(std::min<uint64_t>((n_s + 262143) / 262144, 256));
-        os_hist_kernel<<<dim3(gh, R), 1024, kOsBins * 4, s>>>(d_rows, n_s, kmin.get(), kmax.get(), hist.get());
+        os_hist_kernel<<<dim3(gh, R), 1024, kOsBins * 4, s>>>(d_rows, n_s, w.kmin.get(), w.kmax.get(), w.hist.get());
         DETLSH_LAUNCH_CHECK();
         DETLSH_CUDA(cudaFuncSetAttribute(os_mark_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kOsBins * 4 + kOsBins));
-        os_mark_kernel<<<R, 1024, kOsBins * 4 + kOsBins, s>>>(hist.get(), n_s, n_regions, flags.get(), tcount.get());
+        os_mark_kernel<<<R, 1024, kOsBins * 4 + kOsBins, s>>>(w.hist.get(), n_s, n_regions, w.flags.get(),
+                                                              w.tcount.get());
         DETLSH_LAUNCH_CHECK();
-        DevBuf<uint64_t> k0(total), k1(total);
-        DevBuf<uint32_t> v0(total), v1(total), tmp(radix_temp_elems(total));
-        os_compact_kernel<<<dim3(gx, R), 256, 0, s>>>(d_rows, n_s, kmin.get(), kmax.get(), flags.get(), k0.get(),
-                                                     v0.get(), count.get());
+        os_compact_kernel<<<dim3(gx, R), 256, 0, s>>>(d_rows, n_s, w.kmin.get(), w.kmax.get(), w.flags.get(),
+                                                     w.k0.get(), w.v0.get(), w.count.get());
         DETLSH_LAUNCH_CHECK();
-        const bool flip = radix_sort_pairs<uint64_t>(k0.get(), v0.get(), k1.get(), v1.get(), total, 0, end_bit,
-                                                     tmp.get(), s, count.get());
+        const bool flip = radix_sort_pairs<uint64_t>(w.k0.get(), w.v0.get(), w.k1.get(), w.v1.get(), total, 0,
+                                                     end_bit, w.tmp.get(), s, w.count.get());
         DETLSH_CUDA(cudaFuncSetAttribute(os_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          kOsBins * 4 * 2));
-        os_pick_kernel<<<R, 1024, kOsBins * 4 * 2, s>>>(hist.get(), flags.get(), tcount.get(),
-                                                                flip ? k1.get() : k0.get(), n_s, n_regions, d_table);
+        os_pick_kernel<<<R, 1024, kOsBins * 4 * 2, s>>>(w.hist.get(), w.flags.get(), w.tcount.get(),
+                                                        flip ? w.k1.get() : w.k0.get(), n_s, n_regions, d_table);
         DETLSH_LAUNCH_CHECK();
     }
     if (sync) DETLSH_CUDA(cudaStreamSynchronize(s));

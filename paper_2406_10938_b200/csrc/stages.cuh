@@ -58,6 +58,8 @@ void launch_project_paa(const float* d_points, uint64_t n, int d, int K, float* 
 // out[(r Lg + i) K + j] = proj[(i n + pos[r]) K + j] for r < m, i < Lg (device positions)
 void launch_gather_proj_rows(const float* d_proj, uint64_t n, int K, int Lg, const uint64_t* d_pos, int m,
                              float* d_out, cudaStream_t s);
+// v[i] = i for i < n
+void launch_iota_u32(uint32_t* v, uint64_t n, cudaStream_t s);
 void launch_gather_sample(const float* d_proj_space, const uint32_t* d_idx, uint64_t n_s, int K,
                           float* d_out, cudaStream_t s);
 
@@ -69,8 +71,17 @@ void launch_feistel_sample(uint64_t n, uint64_t n_s, uint64_t key, uint32_t* d_i
 // Exact order statistics per row (GPU sample mode): rows [R][n_s] (fp32),
 // writes table rows [R][NR+1]: row[0]=min, row[t]=sorted[span*t-1], row[NR]=max.
 // `sync` = false leaves the work queued on s (temporaries are stream-ordered).
+// `work` (optional): temporaries kept by the caller across calls -- the
+// build's breakpoint loop reserves them before its tree workers start, whose
+// GB-sized allocations would otherwise hold this thread in the allocator.
+struct OrderStatWork {
+    DevBuf<uint32_t> kmin, kmax, hist, tcount, count, v0, v1, tmp;
+    DevBuf<uint8_t> flags;
+    DevBuf<uint64_t> k0, k1;
+    void reserve(int R, uint64_t n_s, cudaStream_t s);
+};
 void gpu_order_stat_table(const float* d_rows, int R, uint64_t n_s, int n_regions,
-                          float* d_table, cudaStream_t s, bool sync = true);
+                          float* d_table, cudaStream_t s, bool sync = true, OrderStatWork* work = nullptr);
 
 // encode_dataset (encoder.cpp:155-176): branchless lower_bound over the
 // N_r+1 boundaries staged in shared memory; out [L][n][K] u8.

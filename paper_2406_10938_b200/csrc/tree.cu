@@ -19,6 +19,7 @@
 // GPU form: root-slot keys -> stable radix sort -> level-synchronous segmented
 // splitting (one CTA per splitting node) -> node-id radix sort -> flatten.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <optional>
 
@@ -341,6 +342,26 @@ unsigned grid_for(uint64_t n, int threads = 256) {
 
 }  // namespace
 
+// Counter reads through page-locked words: a pageable device-to-host copy is
+// staged by the driver, and the trees are built on several threads at once
+// next to the breakpoint loop's own transfers.  One process-wide block of
+// slots handed out round-robin (the tree threads live for one build, so a
+// per-thread buffer would be a cudaMallocHost/cudaFreeHost pair per build,
+// and cudaFreeHost synchronises the device).
+uint32_t read_word(const uint32_t* d, cudaStream_t s) {
+    constexpr uint32_t kSlots = 1024, kStride = 16;  // one 64-B line per slot
+    static uint32_t* block = []() {
+        uint32_t* p = nullptr;
+        DETLSH_CUDA(cudaMallocHost(&p, kSlots * kStride * sizeof(uint32_t)));
+        return p;  // process lifetime
+    }();
+    static std::atomic<uint32_t> next{0};
+    uint32_t* w = block + (next.fetch_add(1, std::memory_order_relaxed) % kSlots) * kStride;
+    DETLSH_CUDA(cudaMemcpyAsync(w, d, 4, cudaMemcpyDeviceToHost, s));
+    DETLSH_CUDA(cudaStreamSynchronize(s));
+    return *w;
+}
+
 void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, int space,
                     int max_size, DevTree& T, cudaStream_t s) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -386,9 +407,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
         DETLSH_CUDA(cudaMemsetAsync(counters.get(), 0, 4 * sizeof(uint32_t), s));
         exclusive_scan_u32(flags.get(), ridx.get(), n, rtmp.get(), counters.get(), s);
     }
-    uint32_t R = 0;
-    DETLSH_CUDA(cudaMemcpyAsync(&R, counters.get(), 4, cudaMemcpyDeviceToHost, s));
-    DETLSH_CUDA(cudaStreamSynchronize(s));
+    const uint32_t R = read_word(counters.get(), s);
 
     BuildNodes B;
     B.grow(std::max<size_t>(R + 2 * (n / (cap + 1)) + 64, 1024), 0, K, s);
@@ -409,9 +428,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
                                                       actA.get(), d_act_n);
         DETLSH_LAUNCH_CHECK();
     }
-    uint32_t A = 0;
-    DETLSH_CUDA(cudaMemcpyAsync(&A, d_act_n, 4, cudaMemcpyDeviceToHost, s));
-    DETLSH_CUDA(cudaStreamSynchronize(s));
+    uint32_t A = read_word(d_act_n, s);
 
     // 5. level-synchronous splitting
     uint64_t total = R;
@@ -431,14 +448,11 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
             DETLSH_LAUNCH_CHECK();
         }
         total += 2 * static_cast<uint64_t>(A);
-        DETLSH_CUDA(cudaMemcpyAsync(&A, d_next_n, 4, cudaMemcpyDeviceToHost, s));
-        DETLSH_CUDA(cudaStreamSynchronize(s));
+        A = read_word(d_next_n, s);
         std::swap(actA, actB);
         ++levels;
     }
-    uint32_t invalid = 0;
-    DETLSH_CUDA(cudaMemcpyAsync(&invalid, d_invalid, 4, cudaMemcpyDeviceToHost, s));
-    DETLSH_CUDA(cudaStreamSynchronize(s));
+    const uint32_t invalid = read_word(d_invalid, s);
     const uint64_t valid = total - invalid;
 
     // 6. node ids = rank of (z, depth, side)
@@ -487,9 +501,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
     DETLSH_CUDA(cudaMemsetAsync(counters.get(), 0, 8, s));
     exclusive_scan_u32(leaf_flag.get(), leaf_idx.get(), valid, stmp.get(), counters.get(), s);
     ps_ids.reset();
-    uint32_t nl = 0;
-    DETLSH_CUDA(cudaMemcpyAsync(&nl, counters.get(), 4, cudaMemcpyDeviceToHost, s));
-    DETLSH_CUDA(cudaStreamSynchronize(s));
+    const uint32_t nl = read_word(counters.get(), s);
     T.num_leaves = nl;
     T.leaf_node.alloc(nl);
     T.leaf_begin.alloc(nl);
@@ -505,9 +517,7 @@ void build_tree_gpu(const uint8_t* d_codes, uint64_t n, int K, int n_regions, in
                                                       T.leaf_box.get(), T.leaf_cr.get(), counters.get() + 1);
         DETLSH_LAUNCH_CHECK();
     }
-    uint32_t mx = 0;
-    DETLSH_CUDA(cudaMemcpyAsync(&mx, counters.get() + 1, 4, cudaMemcpyDeviceToHost, s));
-    DETLSH_CUDA(cudaStreamSynchronize(s));
+    const uint32_t mx = read_word(counters.get() + 1, s);
     T.max_leaf_count = mx;
     T.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     (void)levels;
