@@ -483,6 +483,13 @@ std::unique_ptr<GpuIndex> build_index_impl(const float* points, uint64_t n, int 
         int lpr = 1;
         while (lpr < chunks && lpr < 32) lpr <<= 1;
         X->u8_lpr = lpr;
+    } else {
+        // float rows in tree-0 leaf order and their bf16-triple tiles: the pool
+        // grows for them here, on this thread, before the tree workers start
+        // (grown from the tree-0 worker during the replay, the mappings held the
+        // replay's stream for up to 0.3 s at C4)
+        const size_t Rf = (6 * static_cast<size_t>(d) + 31) / 32 * 32;
+        reserve_mempool(device, n * (4 * static_cast<size_t>(d) + Rf + 4), s);
     }
     X->timings.emplace_back("u8_check", ms_since(t0));
 
