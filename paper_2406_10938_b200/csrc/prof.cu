@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -98,6 +99,13 @@ void ensure_mempool(int device) {
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t thr = ~0ULL;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        if (const char* e = std::getenv("DETLSH_POOL_RESERVE_GB")) {  // measurement hook: pre-grow the pool
+            void* p = nullptr;
+            const size_t bytes = static_cast<size_t>(std::atof(e) * 1073741824.0);
+            if (bytes && cudaMallocAsync(&p, bytes, 0) == cudaSuccess) cudaFreeAsync(p, 0);
+            cudaGetLastError();
+            cudaDeviceSynchronize();
+        }
     }
     done[device] = true;
 }
